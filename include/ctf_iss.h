@@ -1,0 +1,207 @@
+/*
+ * ctf_iss.h — C ABI of the B200-native ISS+NMF hot path of CTF-MNMF-ISS
+ * (arXiv 2510.02382). Plain pointers and sizes only; no C++ or torch types.
+ *
+ * The reference (/root/reference/proj) is a C++ library with no FFI; its
+ * hot-path entry points and what replaces them here:
+ *
+ *   SeparationResult run(const CtfConfig&, const MixtureSpectrogram&,
+ *                        const CheckOptions& = {})
+ *       proj/include/ctfmnmf/estimator.hpp:122-123, body estimator.cpp:513-657
+ *       -> ctf_run()            (one call, host buffers in and out), or
+ *          ctf_setup() + ctf_iterate() + ctf_download()   (device-resident)
+ *   the per-iteration loop body, estimator.cpp:548-654 ("iterate")
+ *       -> ctf_iterate(ctx, n)  (n iterations + the trailing rescale/objective)
+ *   std::vector<MixtureSpectrogram> reconstruct_images(W, factors, x, config)
+ *       proj/include/ctfmnmf/wiener.hpp:18-20, body wiener.cpp:11-49
+ *       -> ctf_project_back()
+ *   CtfConfig (model.hpp:21-35) + the stacked observation of BASELINE (a)
+ *       -> ctf_problem
+ *   ConfigError / IoError / DegeneracyError{iteration,bin,row}
+ *       (errors.hpp:11-35) and CLI exit codes 2/3/4 (ctfmnmf_main.cpp:38-40)
+ *       -> ctf_status codes + ctf_err
+ *
+ * The host C++ mirror of the reference API (same names, argument meaning and
+ * exceptions) is paper_2510_02382_b200/csrc/ctfmnmf_b200.hpp; the Python mirror
+ * is paper_2510_02382_b200/api.py. INTEGRATION.md shows the binding a
+ * reference maintainer would add.
+ *
+ * Layouts (complex numbers are interleaved re,im pairs):
+ *   x (input)  : [mixture][bin][frame][channel], i.e. per mixture the
+ *                reference Spectrogram layout (i*frames + j)*channels + c
+ *                (types.hpp:32) == one column-major channels x frames Eigen
+ *                matrix per bin (model.hpp:55-66). channel count = num_mics.
+ *   W (output) : [mixture][bin] column-major R x D (Eigen MatrixXcd layout).
+ *   B (output) : [mixture][source] column-major F x K_n (Eigen MatrixXd).
+ *   V (output) : [mixture][source] column-major K_n x T.
+ *   objective  : [mixture][iteration].
+ *   images     : [source][mixture][bin] column-major Dout x T, where Dout = D
+ *                (full stacked observation, as reconstruct_images returns) or
+ *                num_mics when CTF_IMAGES_CURRENT_FRAME is requested.
+ *
+ * Stacked observation (BASELINE (a)): with stack_taps = L > 1
+ * the observation is x~(c = m*L + l, t) = x_m(t - l) (zero for t < l), built
+ * virtually inside the kernels (never materialised in HBM); D = num_mics*L.
+ * With stack_taps = 1 the input already is the D-channel observation.
+ *
+ * Threading: a context is single-owner; calls are
+ * stream-ordered on the context's stream. Multi-GPU: one process per GPU,
+ * each with one context; ctf_comm_init() joins the contexts into one
+ * frequency-sharded job (contiguous bin ranges, one NCCL all-reduce of the
+ * packed MU-V numerator/denominator + row powers + objective per iteration).
+ */
+#ifndef CTF_ISS_H_
+#define CTF_ISS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CTF_ABI_VERSION 1
+#define CTF_MAX_SOURCES 16
+#define CTF_MAX_ROWS 64
+
+/* Status codes mirror the reference CLI exit codes (ctfmnmf_main.cpp:38-40). */
+typedef enum ctf_status {
+  CTF_OK = 0,
+  CTF_ERR_CONFIG = 2,     /* ConfigError */
+  CTF_ERR_IO = 3,         /* IoError */
+  CTF_ERR_DEGENERACY = 4, /* DegeneracyError */
+  CTF_ERR_CUDA = 5,       /* device / runtime failure (no reference analogue) */
+  CTF_ERR_UNSUPPORTED = 6 /* shape outside the compiled kernel set */
+} ctf_status;
+
+typedef enum ctf_precision { CTF_F64 = 0, CTF_F32 = 1 } ctf_precision;
+typedef enum ctf_rule { CTF_RULE_IP = 0, CTF_RULE_ISS = 1 } ctf_rule;
+
+/* Degeneracy kinds carried in ctf_err.kind. */
+typedef enum ctf_err_kind {
+  CTF_KIND_NONE = 0,
+  CTF_KIND_STEERING_DENOM = 1,  /* estimator.cpp:451-454 */
+  CTF_KIND_NONFINITE_W = 2,     /* estimator.cpp:494-496 */
+  CTF_KIND_NONFINITE_Y = 3,     /* estimator.cpp:497-499 */
+  CTF_KIND_ZERO_PIVOT = 4,      /* estimator.cpp:46-47 */
+  CTF_KIND_TINY_DET = 5,        /* estimator.cpp:50-51 */
+  CTF_KIND_NONFINITE_OBJ = 6,   /* estimator.cpp:647-648 */
+  CTF_KIND_NONFINITE_X = 7,     /* estimator.cpp:521-522 */
+  CTF_KIND_ZERO_X = 8,          /* estimator.cpp:523-524 (ConfigError) */
+  CTF_KIND_SINGULAR_IMAGE = 9   /* wiener.cpp:38-40 */
+} ctf_err_kind;
+
+typedef struct ctf_err {
+  int32_t code;      /* ctf_status */
+  int32_t kind;      /* ctf_err_kind */
+  int32_t iteration; /* 1-based, -1 when absent (DegeneracyError::iteration) */
+  int32_t mixture;   /* batch index, -1 when absent */
+  int32_t bin;       /* global bin, -1 when absent (DegeneracyError::bin) */
+  int32_t row;       /* demixing row, -1 when absent (DegeneracyError::row) */
+  char msg[256];     /* reference-compatible message text */
+} ctf_err;
+
+/* CtfConfig (model.hpp:21-35) + batch/shape + the stacked observation. */
+typedef struct ctf_problem {
+  int32_t num_mixtures;                        /* B, independent mixtures */
+  int32_t num_bins;                            /* F */
+  int32_t num_frames;                          /* T */
+  int32_t num_mics;                            /* channels of x as supplied */
+  int32_t stack_taps;                          /* L of the virtual stack; 1 = x already stacked */
+  int32_t num_sources;                         /* N */
+  int32_t taps_per_source[CTF_MAX_SOURCES];    /* L_n, sum = D = num_mics*stack_taps */
+  int32_t bases_per_source[CTF_MAX_SOURCES];   /* K_n */
+  int32_t iterations;
+  int32_t update_rule;                         /* ctf_rule; IP is rejected (scope) */
+  int32_t precision;                           /* ctf_precision of the compute path */
+  int32_t x_precision;                         /* ctf_precision of the host x buffer */
+  double psd_floor;                            /* relative floor, model.hpp:29 */
+  uint64_t seed;                               /* mixture b is seeded with seed + b */
+  int32_t threads;                             /* accepted and ignored (GPU path) */
+  int32_t reserved[7];
+} ctf_problem;
+
+/* Per-phase device times of the last ctf_iterate()/ctf_run(), CUDA events. */
+typedef struct ctf_timing {
+  double sweep_ms;      /* fused demix+ISS sweep+demix+MU-B kernel */
+  double mu_ms;         /* MU-V partial/reduce/apply (+ all-reduce) */
+  double finalize_ms;   /* trailing rescale + objective pass */
+  int64_t sweep_launches;
+  int64_t launches;     /* all kernels launched by the library */
+} ctf_timing;
+
+typedef struct ctf_ctx ctf_ctx;
+
+int ctf_abi_version(void);
+
+/* Context on one CUDA device (one process per GPU). */
+int ctf_open(int device, ctf_ctx** out, ctf_err* err);
+void ctf_close(ctf_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t) so callers can time with events. */
+void* ctf_stream(ctf_ctx* ctx);
+
+/* Multi-GPU: rank 0 calls ctf_comm_unique_id, broadcasts the 128 bytes,
+ * every rank calls ctf_comm_init before ctf_setup. Bins are split into
+ * contiguous ranges by rank. NCCL is loaded lazily (dlopen). */
+int ctf_comm_unique_id(uint8_t id[128], ctf_err* err);
+int ctf_comm_init(ctf_ctx* ctx, int world_size, int rank, const uint8_t id[128], ctf_err* err);
+/* Local bin range [lo, hi) of this rank for a problem with num_bins bins. */
+void ctf_shard_range(int num_bins, int world_size, int rank, int* lo, int* hi);
+
+/* Validates the problem (CtfConfig::validate, model.cpp:32-50), allocates
+ * device state, uploads x (this rank's bins), computes mean power and the
+ * absolute PSD floor (estimator.cpp:520-529), draws the initial NMF factors
+ * with mt19937_64(seed+b) exactly as random_factors (model.cpp:189-208),
+ * and sets W = I (model.cpp:221-227). x is the full [B][F][T][num_mics]
+ * host array (pinned or pageable). */
+int ctf_setup(ctf_ctx* ctx, const ctf_problem* prob, const void* x_host, ctf_err* err);
+/* Replaces the state (for one-step parity): W [B][F] R x D col-major complex
+ * (full F, this rank's bins are read), B [B][N] F x K_n, V [B][N] K_n x T,
+ * host doubles. Any argument may be NULL to keep the current value. */
+int ctf_set_state(ctf_ctx* ctx, const double* W, const double* B, const double* V, ctf_err* err);
+/* Runs n iterations of estimator.cpp:548-654 followed by the trailing
+ * rescale+objective, so the state is exactly the reference's after n more
+ * iterations. Degeneracies are reported like the reference (first failing
+ * iteration, phase, lowest bin). */
+int ctf_iterate(ctf_ctx* ctx, int n, ctf_err* err);
+/* Device-resident benchmark form: n loop bodies without the trailing
+ * finalize (call ctf_finalize before ctf_download). No host sync. */
+int ctf_iterate_async(ctf_ctx* ctx, int n, ctf_err* err);
+int ctf_finalize(ctf_ctx* ctx, ctf_err* err);
+/* Copies the state to host doubles (layouts above). W/B cover this rank's
+ * bins (other bins untouched); V and the objective trace are replicated.
+ * objective receives [B][iterations_done]. Any pointer may be NULL. */
+int ctf_download(ctf_ctx* ctx, double* W, double* B, double* V, double* objective, ctf_err* err);
+int ctf_iterations_done(ctf_ctx* ctx);
+/* Absolute PSD floor per mixture (factors.floor, estimator.cpp:529). */
+int ctf_psd_floor(ctf_ctx* ctx, double* floor_out /* [B] */);
+/* Per-iteration phase times (OptimizationTrace demix_ms / mu_ms /
+ * rescale_ms, estimator.hpp:25-40) from CUDA events; rescale is fused into
+ * the next sweep and reported as 0. Arrays of ctf_iterations_done() entries. */
+int ctf_trace_ms(ctf_ctx* ctx, double* demix_ms, double* mu_ms, double* rescale_ms);
+int ctf_get_timing(ctf_ctx* ctx, ctf_timing* out);
+int ctf_reset_timing(ctf_ctx* ctx);
+
+/* One call end to end (== reference run() over a batch): setup, iterate
+ * prob->iterations times, download. */
+int ctf_run(ctf_ctx* ctx, const ctf_problem* prob, const void* x_host, double* W_out,
+            double* B_out, double* V_out, double* objective_out, ctf_err* err);
+
+/* Projection-back (wiener.cpp:11-49, collapsed form c_n = H_n y_n with
+ * H = W^-1) from the current state. images as documented above, host
+ * doubles, this rank's bins. */
+#define CTF_IMAGES_FULL 0
+#define CTF_IMAGES_CURRENT_FRAME 1
+int ctf_project_back(ctf_ctx* ctx, int mode, double* images, ctf_err* err);
+
+/* Synthetic generator of BASELINE.json configs (host code, no GPU):
+ * mixture b uses mt19937_64(base_seed + b); see DESIGN.md for draw order.
+ * x_out: [B][F][T][M] complex (double if out_precision == CTF_F64, float
+ * otherwise). threads <= 0 means hardware concurrency. */
+int ctf_synth_mixtures(int num_mixtures, int F, int T, int M, int N, int L, int K, double tap_decay,
+                       uint64_t base_seed, int out_precision, void* x_out, int threads, ctf_err* err);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CTF_ISS_H_ */

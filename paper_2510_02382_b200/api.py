@@ -1,0 +1,344 @@
+"""Python mirror of the reference estimator API over the C ABI.
+
+Names, argument meaning and errors follow /root/reference/proj:
+  CtfConfig            model.hpp:21-35 (validate: model.cpp:32-50)
+  run(config, x)       estimator.hpp:122-123 / estimator.cpp:513-657
+  reconstruct_images   wiener.hpp:18-20 / wiener.cpp:11-49
+  ConfigError, IoError, DegeneracyError{iteration, bin, row}   errors.hpp:11-35
+The array forms are numpy: a MixtureSpectrogram is a complex array of shape
+(F, channels, T) (one channels x frames matrix per bin, model.hpp:55-66),
+demixing matrices are (F, R, D), B_n is (F, K_n), V_n is (K_n, T).
+
+``Session`` is the batched, device-resident form used by the benchmark: a
+batch of independent mixtures in the reference Spectrogram layout
+[B][F][T][M], optionally stacked on the GPU into the M*L-channel CTF
+observation (BASELINE (a)).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import _lib as L
+
+
+class ConfigError(Exception):
+    """Invalid configuration (errors.hpp:19-22). CLI exit 2."""
+
+
+class IoError(Exception):
+    """File/format failure (errors.hpp:24-27). CLI exit 3."""
+
+
+class DegeneracyError(Exception):
+    """Numerical degeneracy (errors.hpp:29-35). CLI exit 4."""
+
+    def __init__(self, msg, iteration=-1, bin=-1, row=-1, mixture=-1, kind=0):
+        super().__init__(msg)
+        self.iteration, self.bin, self.row, self.mixture, self.kind = iteration, bin, row, mixture, kind
+
+
+class DeviceError(RuntimeError):
+    """CUDA / runtime failure, or a shape outside the compiled kernel set."""
+
+
+def _raise(rc: int, err: L.CtfErr):
+    msg = err.msg.decode(errors="replace")
+    if rc == L.CTF_ERR_CONFIG:
+        raise ConfigError(msg)
+    if rc == L.CTF_ERR_IO:
+        raise IoError(msg)
+    if rc == L.CTF_ERR_DEGENERACY:
+        raise DegeneracyError(msg, err.iteration, err.bin, err.row, err.mixture, err.kind)
+    raise DeviceError(f"[{rc}] {msg}")
+
+
+def _check(rc: int, err: L.CtfErr):
+    if rc != L.CTF_OK:
+        _raise(rc, err)
+
+
+@dataclass
+class CtfConfig:
+    """model.hpp:21-35."""
+    num_sources: int = 2
+    num_channels: int = 4
+    taps_per_source: List[int] = field(default_factory=list)
+    bases_per_source: List[int] = field(default_factory=list)
+    iterations: int = 100
+    update_rule: str = "iss"
+    psd_floor: float = 1e-10
+    seed: int = 0
+    threads: int = 1
+
+    def total_taps(self) -> int:
+        return int(sum(self.taps_per_source))
+
+    def row_offset(self, source: int) -> int:
+        return int(sum(self.taps_per_source[:source]))
+
+    def validate(self):
+        """model.cpp:32-50 (same messages)."""
+        if self.num_sources < 1:
+            raise ConfigError("n_sources must be >= 1")
+        if self.num_channels < 1:
+            raise ConfigError("n_channels must be >= 1")
+        if len(self.taps_per_source) != self.num_sources:
+            raise ConfigError("taps list must have one entry per source")
+        if len(self.bases_per_source) != self.num_sources:
+            raise ConfigError("bases list must have one entry per source")
+        if any(l < 1 for l in self.taps_per_source):
+            raise ConfigError("every tap count must be >= 1")
+        if any(k < 1 for k in self.bases_per_source):
+            raise ConfigError("every basis count must be >= 1")
+        if self.total_taps() != self.num_channels:
+            raise ConfigError(f"sum of taps ({self.total_taps()}) must equal n_channels ({self.num_channels}): "
+                              "the demixing system must be square")
+        if self.iterations < 0:
+            raise ConfigError("iters must be >= 0")
+        if not self.psd_floor > 0.0:
+            raise ConfigError("floor must be > 0")
+        if self.threads < 1:
+            raise ConfigError("threads must be >= 1")
+        if self.update_rule not in ("iss", "ISS", "ip", "IP"):
+            raise ConfigError(f"unknown update rule '{self.update_rule}' (expected ip or iss)")
+
+
+@dataclass
+class OptimizationTrace:
+    """estimator.hpp:25-40."""
+    objective: List[float]
+    demix_ms: List[float]
+    mu_ms: List[float]
+    rescale_ms: List[float]
+
+    def to_csv(self) -> str:
+        out = ["iter,objective,t_demix_ms,t_mu_ms,t_rescale_ms"]
+        for t, o in enumerate(self.objective):
+            out.append(f"{t + 1},{o:.12g},{self.demix_ms[t]:.12g},{self.mu_ms[t]:.12g},{self.rescale_ms[t]:.12g}")
+        return "\n".join(out) + "\n"
+
+
+@dataclass
+class SeparationResult:
+    """estimator.hpp:50-54 (factors flattened into bases/activations/floor)."""
+    demixing: np.ndarray            # (F, R, D) complex128
+    bases: List[np.ndarray]         # B_n (F, K_n)
+    activations: List[np.ndarray]   # V_n (K_n, T)
+    floor: float
+    trace: OptimizationTrace
+
+
+def _problem(num_mixtures, F, T, num_mics, stack_taps, taps, bases, iterations, precision, x_precision,
+             psd_floor, seed, threads=1, rule=L.CTF_RULE_ISS) -> L.CtfProblem:
+    p = L.CtfProblem()
+    p.num_mixtures, p.num_bins, p.num_frames = num_mixtures, F, T
+    p.num_mics, p.stack_taps, p.num_sources = num_mics, stack_taps, len(taps)
+    if len(taps) > L.CTF_MAX_SOURCES or len(bases) > L.CTF_MAX_SOURCES:
+        raise ConfigError("too many sources")
+    for n, (l, k) in enumerate(zip(taps, bases)):
+        p.taps_per_source[n] = l
+        p.bases_per_source[n] = k
+    p.iterations, p.update_rule = iterations, rule
+    p.precision = L.CTF_F32 if precision in ("f32", "float32") else L.CTF_F64
+    p.x_precision = L.CTF_F32 if x_precision in ("f32", "float32", "complex64") else L.CTF_F64
+    p.psd_floor, p.seed, p.threads = psd_floor, seed, threads
+    return p
+
+
+class Session:
+    """Device-resident batch of mixtures on one GPU (or one frequency shard).
+
+    x: complex array [B, F, T, M] (reference Spectrogram layout per mixture),
+    complex128 or complex64. With stack_taps = L > 1, D = M*L and the stacked
+    observation is built inside the kernels; otherwise x already holds the
+    D-channel observation.
+    """
+
+    def __init__(self, x: np.ndarray, taps, bases, *, stack_taps=1, iterations=100, precision="f64",
+                 psd_floor=1e-10, seed=0, device=0, world_size=1, rank=0, comm_id: Optional[bytes] = None):
+        self.lib = L.load()
+        if x.ndim != 4:
+            raise ConfigError("x must have shape [B, F, T, M]")
+        xprec = "f32" if x.dtype == np.complex64 else "f64"
+        x = np.ascontiguousarray(x, dtype=np.complex64 if xprec == "f32" else np.complex128)
+        B, F, T, M = x.shape
+        self.shape = (B, F, T, M)
+        self.taps, self.bases = list(taps), list(bases)
+        self.stack_taps = stack_taps
+        self.D = M * stack_taps
+        self.R = sum(self.taps)
+        self.precision = precision
+        self._ctx = C.c_void_p()
+        err = L.CtfErr()
+        _check(self.lib.ctf_open(device, C.byref(self._ctx), C.byref(err)), err)
+        if world_size > 1:
+            buf = (C.c_uint8 * 128).from_buffer_copy(comm_id)
+            _check(self.lib.ctf_comm_init(self._ctx, world_size, rank, buf, C.byref(err)), err)
+        self.world_size, self.rank = world_size, rank
+        lo, hi = C.c_int(), C.c_int()
+        self.lib.ctf_shard_range(F, world_size, rank, C.byref(lo), C.byref(hi))
+        self.bin_range = (lo.value, hi.value)
+        self.problem = _problem(B, F, T, M, stack_taps, self.taps, self.bases, iterations, precision, xprec,
+                                psd_floor, seed)
+        _check(self.lib.ctf_setup(self._ctx, C.byref(self.problem), L.vptr(x), C.byref(err)), err)
+
+    # -- state -----------------------------------------------------------
+    def iterate(self, n: int):
+        err = L.CtfErr()
+        _check(self.lib.ctf_iterate(self._ctx, n, C.byref(err)), err)
+
+    def iterate_async(self, n: int):
+        err = L.CtfErr()
+        _check(self.lib.ctf_iterate_async(self._ctx, n, C.byref(err)), err)
+
+    def finalize(self):
+        err = L.CtfErr()
+        _check(self.lib.ctf_finalize(self._ctx, C.byref(err)), err)
+
+    @property
+    def iterations_done(self) -> int:
+        return self.lib.ctf_iterations_done(self._ctx)
+
+    def set_state(self, W=None, B=None, V=None):
+        """W: [B, F, R*D*2] doubles in column-major per bin (see download)."""
+        err = L.CtfErr()
+        arrs = [None if a is None else np.ascontiguousarray(a, dtype=np.float64) for a in (W, B, V)]
+        _check(self.lib.ctf_set_state(self._ctx, *[L.dptr(a) for a in arrs], C.byref(err)), err)
+
+    def download_raw(self):
+        """Flat arrays in the C-ABI layouts: W [B][F][R x D col-major] complex,
+        B [B][sum_n F*K_n], V [B][sum_n K_n*T], objective [B][iters]."""
+        B, F, T, M = self.shape
+        SK = sum(self.bases)
+        W = np.zeros((B, F, self.R * self.D), np.complex128)
+        Bf = np.zeros((B, F * SK))
+        V = np.zeros((B, SK * T))
+        it = self.iterations_done
+        obj = np.zeros((B, max(it, 1)))
+        err = L.CtfErr()
+        _check(self.lib.ctf_download(self._ctx, W.ctypes.data_as(L._D), L.dptr(Bf), L.dptr(V), L.dptr(obj),
+                                     C.byref(err)), err)
+        return W, Bf, V, obj[:, :it]
+
+    def download(self):
+        """Per mixture: demixing (F, R, D), bases [(F, K_n)], activations [(K_n, T)], objective (iters,)."""
+        B, F, T, M = self.shape
+        W, Bf, V, obj = self.download_raw()
+        out = []
+        for b in range(B):
+            dem = W[b].reshape(F, self.D, self.R).transpose(0, 2, 1)
+            bases, acts, ob, ov = [], [], 0, 0
+            for K in self.bases:
+                bases.append(Bf[b, ob:ob + F * K].reshape(K, F).T.copy())
+                acts.append(V[b, ov:ov + K * T].reshape(T, K).T.copy())
+                ob += F * K
+                ov += K * T
+            out.append((dem, bases, acts, obj[b]))
+        return out
+
+    def psd_floor(self) -> np.ndarray:
+        out = np.zeros(self.shape[0])
+        self.lib.ctf_psd_floor(self._ctx, L.dptr(out))
+        return out
+
+    def trace_ms(self):
+        n = self.iterations_done
+        a, b, c = np.zeros(max(n, 1)), np.zeros(max(n, 1)), np.zeros(max(n, 1))
+        self.lib.ctf_trace_ms(self._ctx, L.dptr(a), L.dptr(b), L.dptr(c))
+        return a[:n], b[:n], c[:n]
+
+    def timing(self) -> L.CtfTiming:
+        t = L.CtfTiming()
+        self.lib.ctf_get_timing(self._ctx, C.byref(t))
+        return t
+
+    def reset_timing(self):
+        self.lib.ctf_reset_timing(self._ctx)
+
+    def stream_ptr(self) -> int:
+        return self.lib.ctf_stream(self._ctx) or 0
+
+    def project_back(self, current_frame_only=False) -> np.ndarray:
+        """images [N, B, F, T, Dout] complex (wiener.cpp:11-49)."""
+        B, F, T, M = self.shape
+        dout = M if current_frame_only else self.D
+        img = np.zeros((len(self.taps), B, F, T, dout), np.complex128)
+        err = L.CtfErr()
+        mode = L.CTF_IMAGES_CURRENT_FRAME if current_frame_only else L.CTF_IMAGES_FULL
+        _check(self.lib.ctf_project_back(self._ctx, mode, img.ctypes.data_as(L._D), C.byref(err)), err)
+        return img
+
+    def close(self):
+        if self._ctx:
+            self.lib.ctf_close(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _spectrogram_to_abi(x: np.ndarray) -> np.ndarray:
+    """(F, D, T) MixtureSpectrogram -> [1, F, T, D] (reference Spectrogram layout)."""
+    if x.ndim != 3:
+        raise ConfigError("mixture must have shape (F, channels, T)")
+    return np.ascontiguousarray(np.transpose(x, (0, 2, 1)))[None].astype(np.complex128)
+
+
+def run(config: CtfConfig, x: np.ndarray, precision: str = "f64", device: int = 0,
+        stack_taps: int = 1) -> SeparationResult:
+    """estimator.hpp:122-123 on the GPU. x: (F, channels, T) complex; with
+    stack_taps = L > 1, x holds num_channels / L microphones and the
+    stacked observation is built on the GPU."""
+    config.validate()
+    if config.update_rule.lower() != "iss":
+        raise ConfigError("update rule 'ip' is not implemented on the GPU path (ISS only)")
+    if x.shape[1] * stack_taps != config.num_channels:
+        raise ConfigError(f"mixture has {x.shape[1] * stack_taps} channels but config expects {config.num_channels}")
+    xa = _spectrogram_to_abi(x)
+    s = Session(xa, config.taps_per_source, config.bases_per_source, stack_taps=stack_taps,
+                iterations=config.iterations, precision=precision, psd_floor=config.psd_floor,
+                seed=config.seed, device=device)
+    try:
+        s.iterate(config.iterations)
+        dem, bases, acts, obj = s.download()[0]
+        d, m, r = s.trace_ms()
+        return SeparationResult(dem, bases, acts, float(s.psd_floor()[0]),
+                                OptimizationTrace(list(obj), list(d), list(m), list(r)))
+    finally:
+        s.close()
+
+
+def reconstruct_images(demixing: np.ndarray, config: CtfConfig, x: np.ndarray, precision="f64", device=0,
+                       stack_taps: int = 1) -> np.ndarray:
+    """wiener.cpp:11-49: images (N, F, D, T) complex for the given (F, R, D) demixing."""
+    config.validate()
+    xa = _spectrogram_to_abi(x)
+    F = x.shape[0]
+    s = Session(xa, config.taps_per_source, config.bases_per_source, stack_taps=stack_taps, iterations=0,
+                precision=precision, psd_floor=config.psd_floor, seed=config.seed, device=device)
+    try:
+        W = np.ascontiguousarray(np.transpose(demixing, (0, 2, 1))).reshape(1, F, -1)
+        s.set_state(W=W.view(np.float64))
+        img = s.project_back()
+        return np.transpose(img[:, 0], (0, 1, 3, 2))
+    finally:
+        s.close()
+
+
+def synth_mixtures(num_mixtures, F, T, M, N, L_taps, K, decay, seed, precision="f64", threads=0) -> np.ndarray:
+    """BASELINE.json configs[0] generator (host code): [B, F, T, M] complex."""
+    lib = L.load()
+    dt = np.complex64 if precision == "f32" else np.complex128
+    x = np.empty((num_mixtures, F, T, M), dt)
+    err = L.CtfErr()
+    rc = lib.ctf_synth_mixtures(num_mixtures, F, T, M, N, L_taps, K, decay, seed,
+                                L.CTF_F32 if precision == "f32" else L.CTF_F64, L.vptr(x), threads, C.byref(err))
+    _check(rc, err)
+    return x

@@ -1,0 +1,1033 @@
+// ctf_capi.cu — C ABI (include/ctf_iss.h) over the sm_100a kernels.
+//
+// Owns the device state of one frequency shard of a batch of mixtures and
+// drives one iteration of proj/src/estimator.cpp:548-654 as
+//   sweep_kernel          (per bin: rescale, lambda, demix, objective of the
+//                          previous iteration, ISS sweep, demix, E, row
+//                          powers, MU-B)
+//   muv_partial_kernel    (MU-V numerator/denominator over bin chunks)
+//   [ncclAllReduce]       (world > 1: packed V sums + row powers + objective)
+//   reduce_apply_kernel   (V update, mu, objective trace)
+// with no host synchronisation inside the loop.
+#include "ctf_kernels.cuh"
+#include "../../include/ctf_iss.h"
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+using ctf::kMaxRows;
+using ctf::kMaxSources;
+
+// ---------------------------------------------------------------------------
+// Kernel variant registry (instantiated in ctf_sweep_*.cu).
+namespace ctf {
+struct SweepVariant {
+  int prec, rmax, ft, rreg, maxt;
+  void (*fn)(SweepParams);
+};
+const std::vector<SweepVariant>& sweep_variants_f32();
+const std::vector<SweepVariant>& sweep_variants_f64();
+}  // namespace ctf
+
+namespace {
+
+// Minimal NCCL surface, resolved with dlopen so the library has no link-time
+// NCCL dependency (torch ships its own libnccl.so.2; whichever is loaded
+// first in the process is reused).
+typedef struct {
+  char internal[128];
+} NcclUid;
+typedef void* NcclComm;
+struct NcclApi {
+  void* h = nullptr;
+  int (*GetUniqueId)(NcclUid*) = nullptr;
+  int (*CommInitRank)(NcclComm*, int, NcclUid, int) = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+  int (*CommDestroy)(NcclComm) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+  bool load() {
+    if (h) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) return false;
+    GetUniqueId = (decltype(GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    CommInitRank = (decltype(CommInitRank))dlsym(h, "ncclCommInitRank");
+    AllReduce = (decltype(AllReduce))dlsym(h, "ncclAllReduce");
+    CommDestroy = (decltype(CommDestroy))dlsym(h, "ncclCommDestroy");
+    GetErrorString = (decltype(GetErrorString))dlsym(h, "ncclGetErrorString");
+    return GetUniqueId && CommInitRank && AllReduce && CommDestroy;
+  }
+};
+NcclApi g_nccl;
+enum { kNcclFloat = 7, kNcclDouble = 8, kNcclUint64 = 5, kNcclSum = 0, kNcclMin = 3 };
+
+struct CtfError : std::runtime_error {
+  int code, kind, iteration, mixture, bin, row;
+  CtfError(int c, const std::string& m, int k = 0, int it = -1, int mix = -1, int b = -1, int r = -1)
+      : std::runtime_error(m), code(c), kind(k), iteration(it), mixture(mix), bin(b), row(r) {}
+};
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CtfError(CTF_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void alloc(size_t count) {
+    free();
+    n = count;
+    if (count) CK(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void free() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { free(); }
+};
+
+size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
+
+}  // namespace
+
+struct ctf_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  // multi-GPU
+  int world = 1, rank = 0;
+  NcclComm comm = nullptr;
+  // problem
+  bool ready = false;
+  ctf_problem prob{};
+  int F = 0, T = 0, Mx = 0, Ls = 1, D = 0, R = 0, N = 0, SK = 0, B = 0;
+  int lo = 0, hi = 0, FL = 0;
+  int real_size = 8;
+  int taps[kMaxSources]{}, bases[kMaxSources]{}, row0[kMaxSources]{}, koff[kMaxSources + 1]{};
+  int max_iters = 0;
+  int done = 0;       // iterations completed
+  bool pending = false;  // the last iteration's rescale/objective are not yet applied
+  // kernel choice
+  ctf::SweepVariant sv{};
+  int NT = 0, TP = 0;
+  size_t sweep_smem = 0;
+  ctf::SweepParams sp{};
+  int kmax = 0, chunk_bins = 0, nchunk = 0;
+  // device buffers
+  DevBuf<unsigned char> x, W, Bf, V, E, part, packed;
+  DevBuf<double> rowpow, objbin, packed_d, mu, floor_abs, objective, mp_part;
+  DevBuf<unsigned long long> err;
+  // timing
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_sweep, ev_mu, ev_fin;
+  std::vector<cudaEvent_t> ev_pool;
+  ctf_timing timing{};
+  std::vector<double> it_sweep_ms, it_mu_ms;  // per completed iteration
+  std::vector<double> floors;
+};
+
+namespace {
+
+void set_err(ctf_err* e, int code, const std::string& msg, int kind = 0, int it = -1, int mix = -1, int bin = -1,
+             int row = -1) {
+  if (!e) return;
+  e->code = code;
+  e->kind = kind;
+  e->iteration = it;
+  e->mixture = mix;
+  e->bin = bin;
+  e->row = row;
+  std::snprintf(e->msg, sizeof(e->msg), "%s", msg.c_str());
+}
+
+template <class Fn>
+int guarded(ctf_err* err, Fn&& fn) {
+  set_err(err, CTF_OK, "");
+  try {
+    fn();
+    return CTF_OK;
+  } catch (const CtfError& e) {
+    set_err(err, e.code, e.what(), e.kind, e.iteration, e.mixture, e.bin, e.row);
+    return e.code;
+  } catch (const std::exception& e) {
+    set_err(err, CTF_ERR_CUDA, e.what());
+    return CTF_ERR_CUDA;
+  }
+}
+
+cudaEvent_t take_event(ctf_ctx* c) {
+  cudaEvent_t e;
+  if (!c->ev_pool.empty()) {
+    e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+  } else {
+    CK(cudaEventCreate(&e));
+  }
+  return e;
+}
+
+// CtfConfig::validate (model.cpp:32-50) plus the GPU path's own limits.
+void validate(const ctf_problem& p) {
+  if (p.num_sources < 1) throw CtfError(CTF_ERR_CONFIG, "n_sources must be >= 1");
+  if (p.num_sources > CTF_MAX_SOURCES) throw CtfError(CTF_ERR_CONFIG, "n_sources exceeds CTF_MAX_SOURCES");
+  if (p.num_mics < 1 || p.stack_taps < 1) throw CtfError(CTF_ERR_CONFIG, "n_channels must be >= 1");
+  int sum = 0;
+  for (int n = 0; n < p.num_sources; ++n) {
+    if (p.taps_per_source[n] < 1) throw CtfError(CTF_ERR_CONFIG, "every tap count must be >= 1");
+    if (p.bases_per_source[n] < 1) throw CtfError(CTF_ERR_CONFIG, "every basis count must be >= 1");
+    sum += p.taps_per_source[n];
+  }
+  const int D = p.num_mics * p.stack_taps;
+  if (sum != D)
+    throw CtfError(CTF_ERR_CONFIG, "sum of taps (" + std::to_string(sum) + ") must equal n_channels (" +
+                                       std::to_string(D) + "): the demixing system must be square");
+  if (p.iterations < 0) throw CtfError(CTF_ERR_CONFIG, "iters must be >= 0");
+  if (!(p.psd_floor > 0.0)) throw CtfError(CTF_ERR_CONFIG, "floor must be > 0");
+  if (p.threads < 1) throw CtfError(CTF_ERR_CONFIG, "threads must be >= 1");
+  if (p.update_rule != CTF_RULE_ISS)
+    throw CtfError(CTF_ERR_CONFIG, "update rule 'ip' is not implemented on the GPU path (ISS only)");
+  if (p.num_mixtures < 1 || p.num_bins < 1 || p.num_frames < 1)
+    throw CtfError(CTF_ERR_CONFIG, "empty problem (mixtures, bins and frames must be >= 1)");
+  if (p.precision != CTF_F32 && p.precision != CTF_F64) throw CtfError(CTF_ERR_CONFIG, "unknown precision");
+  if (p.x_precision != CTF_F32 && p.x_precision != CTF_F64) throw CtfError(CTF_ERR_CONFIG, "unknown x precision");
+  if (D > 32) throw CtfError(CTF_ERR_UNSUPPORTED, "D > 32 rows is not in the compiled kernel set yet");
+  if (p.num_bins >= (1 << 20)) throw CtfError(CTF_ERR_UNSUPPORTED, "too many bins");
+}
+
+// Chooses the sweep variant and lays out its shared memory.
+void plan_sweep(ctf_ctx* c) {
+  const auto& vars = c->prob.precision == CTF_F32 ? ctf::sweep_variants_f32() : ctf::sweep_variants_f64();
+  int max_smem = 0;
+  CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+  const size_t rs = c->real_size, cs = 2 * rs;
+  bool found = false;
+  ctf::SweepVariant best{};
+  size_t best_smem = 0;
+  int best_nt = 0;
+  for (const auto& v : vars) {
+    if (v.rmax < c->R) continue;
+    int nt = (c->T + v.ft - 1) / v.ft;
+    nt = std::max(32, (nt + 31) / 32 * 32);
+    if (nt > v.maxt) continue;
+    const int TP = nt * v.ft;
+    const int NW = nt / 32;
+    const int VP = ((3 * v.rmax + 31) / 32) * 32;
+    const int xoff = c->Ls - 1, xp = xoff + TP;
+    const int loff = ((std::max(1, *std::max_element(c->taps, c->taps + c->N)) + 3) / 4) * 4, lp = loff + TP;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+      const size_t o = off;
+      off = align16(off + bytes);
+      return o;
+    };
+    ctf::SweepParams& sp = c->sp;
+    ctf::SweepParams cand = sp;
+    cand.off_y = (int)take((size_t)(v.rmax - v.rreg) * TP * cs);
+    const size_t xbytes = std::max((size_t)c->Mx * xp * cs, align16((size_t)v.rreg * TP * rs) + (size_t)c->N * TP * rs);
+    cand.off_x = (int)take(xbytes);
+    cand.off_e = cand.off_x + (int)align16((size_t)v.rreg * TP * rs);
+    cand.off_l = (int)take((size_t)c->N * lp * rs);
+    cand.off_w = (int)take((size_t)c->R * c->D * cs);
+    cand.off_lu = (int)take((size_t)c->R * c->D * cs);
+    cand.off_red = (int)take((size_t)2 * NW * VP * rs);
+    cand.off_z = (int)take((size_t)NW * v.rmax * cs);
+    cand.off_b = (int)take((size_t)c->SK * rs);
+    cand.off_d = (int)take((size_t)NW * 4 * sizeof(double));
+    if (off > (size_t)max_smem) continue;
+    // prefer the smallest rmax, then the most register-resident rows, then fewer threads
+    const bool better = !found || v.rmax < best.rmax ||
+                        (v.rmax == best.rmax && (v.rreg > best.rreg || (v.rreg == best.rreg && nt < best_nt)));
+    if (better) {
+      found = true;
+      best = v;
+      best_smem = off;
+      best_nt = nt;
+      cand.xoff = xoff;
+      cand.xp = xp;
+      cand.loff = loff;
+      cand.lp = lp;
+      c->TP = TP;
+      sp = cand;
+    }
+  }
+  if (!found)
+    throw CtfError(CTF_ERR_UNSUPPORTED, "no compiled sweep kernel for R=" + std::to_string(c->R) +
+                                            " T=" + std::to_string(c->T));
+  c->sv = best;
+  c->NT = best_nt;
+  c->sweep_smem = best_smem;
+  CK(cudaFuncSetAttribute((const void*)best.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)best_smem));
+  ctf::SweepParams& sp = c->sp;
+  sp.FL = c->FL;
+  sp.bin_lo = c->lo;
+  sp.T = c->T;
+  sp.TP = c->TP;
+  sp.Mx = c->Mx;
+  sp.Ls = c->Ls;
+  sp.D = c->D;
+  sp.R = c->R;
+  sp.N = c->N;
+  sp.SK = c->SK;
+  int r = 0;
+  for (int n = 0; n < c->N; ++n) {
+    sp.row0[n] = c->row0[n];
+    sp.ntaps[n] = c->taps[n];
+    for (int l = 0; l < c->taps[n]; ++l, ++r) sp.woff[r] = n * sp.lp + sp.loff - l;
+  }
+  for (int n = 0; n <= c->N; ++n) sp.koff[n] = c->koff[n];
+}
+
+template <class Real>
+__global__ void convert_kernel(const double* in, Real* out, size_t n) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    out[i] = (Real)in[i];
+}
+template <class Real>
+__global__ void convert_f32_kernel(const float* in, Real* out, size_t n) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    out[i] = (Real)in[i];
+}
+template <class Real>
+__global__ void identity_kernel(Real* W, size_t nbins, int R, int D) {
+  // W per bin: column-major R x D complex (2 reals per entry)
+  const size_t per = (size_t)R * D * 2;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nbins * per; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t e = (i % per) / 2;
+    const int r = (int)(e % R), col = (int)(e / R);
+    W[i] = (Real)((r == col && (i & 1) == 0) ? 1.0 : 0.0);
+  }
+}
+
+void upload_real(ctf_ctx* c, void* dst, const double* src, size_t n) {
+  // host doubles -> device Real
+  if (c->real_size == 8) {
+    CK(cudaMemcpyAsync(dst, src, n * 8, cudaMemcpyHostToDevice, c->stream));
+    return;
+  }
+  DevBuf<double> tmp;
+  tmp.alloc(n);
+  CK(cudaMemcpyAsync(tmp.p, src, n * 8, cudaMemcpyHostToDevice, c->stream));
+  convert_kernel<float><<<std::min<size_t>((n + 255) / 256, 4096), 256, 0, c->stream>>>(tmp.p, (float*)dst, n);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(c->stream));
+}
+
+void download_real(ctf_ctx* c, double* dst, const void* src, size_t n) {
+  if (c->real_size == 8) {
+    CK(cudaMemcpyAsync(dst, src, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return;
+  }
+  DevBuf<double> tmp;
+  tmp.alloc(n);
+  convert_f32_kernel<double><<<std::min<size_t>((n + 255) / 256, 4096), 256, 0, c->stream>>>((const float*)src, tmp.p, n);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(dst, tmp.p, n * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+}
+
+void allreduce(ctf_ctx* c, void* buf, size_t count, int dtype, int op) {
+  if (c->world <= 1 || count == 0) return;
+  const int rc = g_nccl.AllReduce(buf, buf, count, dtype, op, c->comm, c->stream);
+  if (rc != 0)
+    throw CtfError(CTF_ERR_CUDA, std::string("ncclAllReduce failed: ") +
+                                     (g_nccl.GetErrorString ? g_nccl.GetErrorString(rc) : "?"));
+}
+
+// Decodes the per-mixture error keys into the reference's exception text.
+void check_errors(ctf_ctx* c) {
+  std::vector<unsigned long long> keys((size_t)c->B);
+  if (c->world > 1) allreduce(c, c->err.p, (size_t)c->B, kNcclUint64, kNcclMin);
+  CK(cudaMemcpyAsync(keys.data(), c->err.p, keys.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (int b = 0; b < c->B; ++b) {
+    const unsigned long long k = keys[(size_t)b];
+    if (k == ctf::kNoErr) continue;
+    const int it = (int)(k >> 44), ph = (int)((k >> 40) & 0xF), bin = (int)((k >> 20) & 0xFFFFF),
+              row = (int)((k >> 8) & 0xFFF), code = (int)(k & 0xFF);
+    const std::string its = " (iteration " + std::to_string(it) + ")";
+    switch (ph) {
+      case ctf::kPhSweep:
+        throw CtfError(CTF_ERR_DEGENERACY,
+                       "steering update: nonpositive denominator for rows (" + std::to_string(row) + ", " +
+                           std::to_string(code) + ")" + its,
+                       CTF_KIND_STEERING_DENOM, it, b, bin, row);
+      case ctf::kPhFinite:
+        if (code == 1)
+          throw CtfError(CTF_ERR_DEGENERACY, "non-finite demixing matrix", CTF_KIND_NONFINITE_W, it, b, bin, -1);
+        throw CtfError(CTF_ERR_DEGENERACY, "non-finite source estimates", CTF_KIND_NONFINITE_Y, it, b, bin, -1);
+      case ctf::kPhDet:
+        if (code == 4)
+          throw CtfError(CTF_ERR_DEGENERACY, "singular demixing matrix (zero pivot)" + its, CTF_KIND_ZERO_PIVOT, it,
+                         b, bin, -1);
+        throw CtfError(CTF_ERR_DEGENERACY, "demixing determinant magnitude below 1e-300" + its, CTF_KIND_TINY_DET,
+                       it, b, bin, -1);
+      case ctf::kPhObj:
+        throw CtfError(CTF_ERR_DEGENERACY, "non-finite objective", CTF_KIND_NONFINITE_OBJ, it, b, -1, -1);
+      default:
+        throw CtfError(CTF_ERR_DEGENERACY, "degeneracy", 0, it, b, bin, row);
+    }
+  }
+}
+
+template <class Real>
+void launch_muv(ctf_ctx* c) {
+  ctf::MuvParams mp{};
+  mp.Bf = c->Bf.p;
+  mp.V = c->V.p;
+  mp.E = c->E.p;
+  mp.part = c->part.p;
+  mp.floor_abs = c->floor_abs.p;
+  mp.FL = c->FL;
+  mp.T = c->T;
+  mp.N = c->N;
+  mp.SK = c->SK;
+  mp.nmix = c->B;
+  mp.chunk_bins = c->chunk_bins;
+  for (int n = 0; n <= c->N; ++n) mp.koff[n] = c->koff[n];
+  for (int n = 0; n < c->N; ++n) mp.ntaps[n] = c->taps[n];
+  dim3 grid((c->T + 127) / 128, c->B * c->N, c->nchunk);
+  const size_t smem = (size_t)c->chunk_bins * c->kmax * sizeof(Real);
+  switch (c->kmax) {
+    case 8: ctf::muv_partial_kernel<Real, 8><<<grid, 128, smem, c->stream>>>(mp); break;
+    case 16: ctf::muv_partial_kernel<Real, 16><<<grid, 128, smem, c->stream>>>(mp); break;
+    case 24: ctf::muv_partial_kernel<Real, 24><<<grid, 128, smem, c->stream>>>(mp); break;
+    default: ctf::muv_partial_kernel<Real, 32><<<grid, 128, smem, c->stream>>>(mp); break;
+  }
+  CK(cudaGetLastError());
+}
+
+template <class Real>
+void launch_apply(ctf_ctx* c, int mode, int obj_slot, int do_v) {
+  ctf::ApplyParams ap{};
+  ap.part = c->part.p;
+  ap.packed = c->packed.p;
+  ap.V = c->V.p;
+  ap.rowpow = c->rowpow.p;
+  ap.objbin = c->objbin.p;
+  ap.packed_d = c->packed_d.p;
+  ap.mu = c->mu.p;
+  ap.objective = c->objective.p;
+  ap.floor_abs = c->floor_abs.p;
+  ap.err = c->err.p;
+  ap.nchunk = c->nchunk;
+  ap.nmix = c->B;
+  ap.SK = c->SK;
+  ap.T = c->T;
+  ap.FL = c->FL;
+  ap.R = c->R;
+  ap.F_total = c->F;
+  ap.max_iters = c->max_iters;
+  ap.obj_slot = obj_slot;
+  ap.mode = mode;
+  ap.do_v = do_v;
+  const size_t plane = (size_t)c->SK * c->T;
+  const int bx = do_v ? (int)std::min<size_t>((plane + 255) / 256, 64) : 1;
+  ctf::reduce_apply_kernel<Real><<<dim3(bx, c->B), 256, 0, c->stream>>>(ap);
+  CK(cudaGetLastError());
+}
+
+// One loop body (estimator.cpp:553-654) or, with do_sweep = false, the
+// trailing rescale + objective of the last completed iteration.
+template <class Real>
+void run_body(ctf_ctx* c, bool do_sweep) {
+  ctf::SweepParams sp = c->sp;
+  sp.x = c->x.p;
+  sp.W = c->W.p;
+  sp.Bf = c->Bf.p;
+  sp.V = c->V.p;
+  sp.E = c->E.p;
+  sp.rowpow = c->rowpow.p;
+  sp.objbin = c->objbin.p;
+  sp.mu = c->pending ? c->mu.p : nullptr;
+  sp.floor_abs = c->floor_abs.p;
+  sp.err = c->err.p;
+  sp.iteration = c->done + 1;
+  sp.do_sweep = do_sweep ? 1 : 0;
+  sp.has_prev = c->pending ? 1 : 0;
+  const int obj_slot = c->pending ? c->done - 1 : -1;
+
+  cudaEvent_t e0 = take_event(c), e1 = take_event(c), e2 = take_event(c);
+  CK(cudaEventRecord(e0, c->stream));
+  c->sv.fn<<<dim3(c->FL, c->B), c->NT, c->sweep_smem, c->stream>>>(sp);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(e1, c->stream));
+  c->timing.sweep_launches += 1;
+  c->timing.launches += 1;
+  if (do_sweep) {
+    launch_muv<Real>(c);
+    c->timing.launches += 1;
+  }
+  if (c->world > 1) {
+    launch_apply<Real>(c, 0, obj_slot, do_sweep ? 1 : 0);
+    if (do_sweep) allreduce(c, c->packed.p, (size_t)c->B * 2 * c->SK * c->T, sizeof(Real) == 4 ? kNcclFloat : kNcclDouble, kNcclSum);
+    allreduce(c, c->packed_d.p, (size_t)c->B * (c->R + 1), kNcclDouble, kNcclSum);
+    launch_apply<Real>(c, 1, obj_slot, do_sweep ? 1 : 0);
+    c->timing.launches += 2;
+  } else {
+    launch_apply<Real>(c, 2, obj_slot, do_sweep ? 1 : 0);
+    c->timing.launches += 1;
+  }
+  CK(cudaEventRecord(e2, c->stream));
+  if (do_sweep) {
+    c->ev_sweep.push_back({e0, e1});
+    c->ev_mu.push_back({e1, e2});
+    c->done += 1;
+    c->pending = true;
+  } else {
+    c->ev_fin.push_back({e0, e2});
+    c->ev_pool.push_back(e1);
+    c->pending = false;
+  }
+}
+
+void collect_timing(ctf_ctx* c) {
+  CK(cudaStreamSynchronize(c->stream));
+  auto drain = [&](std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v, double& acc) {
+    for (auto& pr : v) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, pr.first, pr.second));
+      acc += ms;
+      c->ev_pool.push_back(pr.first);
+      c->ev_pool.push_back(pr.second);
+    }
+    v.clear();
+  };
+  // ev_sweep and ev_mu share events; collect times first, then recycle once
+  for (size_t i = 0; i < c->ev_sweep.size(); ++i) {
+    float a = 0.f, b = 0.f;
+    CK(cudaEventElapsedTime(&a, c->ev_sweep[i].first, c->ev_sweep[i].second));
+    CK(cudaEventElapsedTime(&b, c->ev_mu[i].first, c->ev_mu[i].second));
+    c->timing.sweep_ms += a;
+    c->timing.mu_ms += b;
+    c->it_sweep_ms.push_back(a);
+    c->it_mu_ms.push_back(b);
+    c->ev_pool.push_back(c->ev_sweep[i].first);
+    c->ev_pool.push_back(c->ev_sweep[i].second);
+    c->ev_pool.push_back(c->ev_mu[i].second);
+  }
+  c->ev_sweep.clear();
+  c->ev_mu.clear();
+  drain(c->ev_fin, c->timing.finalize_ms);
+}
+
+void iterate_impl(ctf_ctx* c, int n, bool finalize) {
+  if (!c->ready) throw CtfError(CTF_ERR_CONFIG, "ctf_setup has not been called");
+  if (n < 0) throw CtfError(CTF_ERR_CONFIG, "iteration count must be >= 0");
+  CK(cudaSetDevice(c->device));
+  if (c->done + n > c->max_iters) {
+    // grow the objective trace
+    const int new_max = std::max(c->done + n, 2 * c->max_iters);
+    DevBuf<double> nt;
+    nt.alloc((size_t)c->B * new_max);
+    CK(cudaMemsetAsync(nt.p, 0, nt.n * 8, c->stream));
+    if (c->max_iters > 0)
+      CK(cudaMemcpy2DAsync(nt.p, (size_t)new_max * 8, c->objective.p, (size_t)c->max_iters * 8,
+                           (size_t)c->max_iters * 8, c->B, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    std::swap(c->objective.p, nt.p);
+    std::swap(c->objective.n, nt.n);
+    c->max_iters = new_max;
+  }
+  for (int i = 0; i < n; ++i) {
+    if (c->real_size == 4) run_body<float>(c, true);
+    else run_body<double>(c, true);
+  }
+  if (finalize && c->pending) {
+    if (c->real_size == 4) run_body<float>(c, false);
+    else run_body<double>(c, false);
+  }
+  if (finalize) {
+    collect_timing(c);
+    check_errors(c);
+  }
+}
+
+size_t plane_stride(const ctf_ctx* c) { return (size_t)c->FL * c->R * c->D; }
+
+void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host) {
+  if (!prob) throw CtfError(CTF_ERR_CONFIG, "null problem");
+  validate(*prob);
+  if (!x_host) throw CtfError(CTF_ERR_CONFIG, "null mixture");
+  CK(cudaSetDevice(c->device));
+  c->ready = false;
+  c->prob = *prob;
+  c->B = prob->num_mixtures;
+  c->F = prob->num_bins;
+  c->T = prob->num_frames;
+  c->Mx = prob->num_mics;
+  c->Ls = prob->stack_taps;
+  c->D = c->Mx * c->Ls;
+  c->R = c->D;
+  c->N = prob->num_sources;
+  c->real_size = prob->precision == CTF_F32 ? 4 : 8;
+  ctf_shard_range(c->F, c->world, c->rank, &c->lo, &c->hi);
+  c->FL = c->hi - c->lo;
+  if (c->FL < 1) throw CtfError(CTF_ERR_CONFIG, "more ranks than frequency bins");
+  int r0 = 0, k0 = 0, kmax = 0;
+  for (int n = 0; n < c->N; ++n) {
+    c->taps[n] = prob->taps_per_source[n];
+    c->bases[n] = prob->bases_per_source[n];
+    c->row0[n] = r0;
+    c->koff[n] = k0;
+    r0 += c->taps[n];
+    k0 += c->bases[n];
+    kmax = std::max(kmax, c->bases[n]);
+  }
+  c->koff[c->N] = k0;
+  c->SK = k0;
+  if (kmax > 32) throw CtfError(CTF_ERR_UNSUPPORTED, "more than 32 bases per source");
+  c->kmax = kmax <= 8 ? 8 : kmax <= 16 ? 16 : kmax <= 24 ? 24 : 32;
+  plan_sweep(c);
+  // MU-V bin chunks: enough CTAs to fill the GPU, deterministic fixed-order combine
+  const int ctas_per_chunk = ((c->T + 127) / 128) * c->B * c->N;
+  int nchunk = std::max(1, std::min(c->FL, (4 * 148 + ctas_per_chunk - 1) / ctas_per_chunk));
+  c->chunk_bins = (c->FL + nchunk - 1) / nchunk;
+  c->nchunk = (c->FL + c->chunk_bins - 1) / c->chunk_bins;
+
+  const size_t rs = c->real_size, cs = 2 * rs;
+  const size_t xcount = (size_t)c->B * c->FL * c->T * c->Mx;  // complex
+  c->x.alloc(xcount * cs);
+  c->W.alloc((size_t)c->B * plane_stride(c) * cs);
+  c->Bf.alloc((size_t)c->B * c->FL * c->SK * rs);
+  c->V.alloc((size_t)c->B * c->SK * c->T * rs);
+  c->E.alloc((size_t)c->B * c->N * c->FL * c->T * rs);
+  c->part.alloc((size_t)c->nchunk * c->B * 2 * c->SK * c->T * rs);
+  c->packed.alloc(c->world > 1 ? (size_t)c->B * 2 * c->SK * c->T * rs : 16);
+  c->rowpow.alloc((size_t)c->B * c->FL * c->R);
+  c->objbin.alloc((size_t)c->B * c->FL);
+  c->packed_d.alloc((size_t)c->B * (c->R + 1));
+  c->mu.alloc((size_t)c->B * c->R);
+  c->floor_abs.alloc((size_t)c->B);
+  c->mp_part.alloc((size_t)c->B * c->FL);
+  c->err.alloc((size_t)c->B);
+  c->max_iters = std::max(1, prob->iterations);
+  c->objective.alloc((size_t)c->B * c->max_iters);
+  CK(cudaMemsetAsync(c->objective.p, 0, c->objective.n * 8, c->stream));
+  CK(cudaMemsetAsync(c->err.p, 0xFF, c->err.n * 8, c->stream));
+  CK(cudaMemsetAsync(c->E.p, 0, c->E.n, c->stream));
+
+  // x: this rank's bins of every mixture, converted to the compute precision
+  const size_t xs_in = prob->x_precision == CTF_F32 ? 8 : 16;
+  const size_t per_mix = (size_t)c->FL * c->T * c->Mx;  // complex per mixture (local)
+  const bool same = (xs_in == cs);
+  DevBuf<unsigned char> stage;
+  if (!same) stage.alloc(per_mix * xs_in);
+  for (int b = 0; b < c->B; ++b) {
+    const unsigned char* src =
+        static_cast<const unsigned char*>(x_host) + ((size_t)b * c->F + c->lo) * c->T * c->Mx * xs_in;
+    unsigned char* dst = c->x.p + (size_t)b * per_mix * cs;
+    if (same) {
+      CK(cudaMemcpyAsync(dst, src, per_mix * xs_in, cudaMemcpyHostToDevice, c->stream));
+    } else {
+      CK(cudaMemcpyAsync(stage.p, src, per_mix * xs_in, cudaMemcpyHostToDevice, c->stream));
+      const size_t n = per_mix * 2;
+      const int g = (int)std::min<size_t>((n + 255) / 256, 8192);
+      if (xs_in == 16)
+        convert_kernel<float><<<g, 256, 0, c->stream>>>((const double*)stage.p, (float*)dst, n);
+      else
+        convert_f32_kernel<double><<<g, 256, 0, c->stream>>>((const float*)stage.p, (double*)dst, n);
+      CK(cudaGetLastError());
+      CK(cudaStreamSynchronize(c->stream));  // stage is reused
+    }
+  }
+  // mean power of x~ and the absolute PSD floor (estimator.cpp:520-529)
+  if (rs == 4)
+    ctf::mean_power_kernel<float><<<dim3(c->FL, c->B), 256, 0, c->stream>>>(c->x.p, c->mp_part.p, c->FL, c->T, c->Mx, c->Ls);
+  else
+    ctf::mean_power_kernel<double><<<dim3(c->FL, c->B), 256, 0, c->stream>>>(c->x.p, c->mp_part.p, c->FL, c->T, c->Mx, c->Ls);
+  CK(cudaGetLastError());
+  std::vector<double> mp_part((size_t)c->B * c->FL), sums((size_t)c->B, 0.0);
+  CK(cudaMemcpyAsync(mp_part.data(), c->mp_part.p, mp_part.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (int b = 0; b < c->B; ++b)
+    for (int i = 0; i < c->FL; ++i) sums[(size_t)b] += mp_part[(size_t)b * c->FL + i];
+  if (c->world > 1) {
+    CK(cudaMemcpyAsync(c->mp_part.p, sums.data(), sums.size() * 8, cudaMemcpyHostToDevice, c->stream));
+    allreduce(c, c->mp_part.p, sums.size(), kNcclDouble, kNcclSum);
+    CK(cudaMemcpyAsync(sums.data(), c->mp_part.p, sums.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  std::vector<double> floors((size_t)c->B);
+  const double count = (double)c->F * c->D * c->T;
+  for (int b = 0; b < c->B; ++b) {
+    const double mp = sums[(size_t)b] / count;
+    if (!std::isfinite(mp))
+      throw CtfError(CTF_ERR_DEGENERACY, "mixture spectrogram contains non-finite values", CTF_KIND_NONFINITE_X, -1, b);
+    if (!(mp > 0.0))
+      throw CtfError(CTF_ERR_CONFIG, "mixture spectrogram is identically zero", CTF_KIND_ZERO_X, -1, b);
+    floors[(size_t)b] = prob->psd_floor * mp;
+  }
+  CK(cudaMemcpyAsync(c->floor_abs.p, floors.data(), floors.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  c->floors = floors;
+  c->it_sweep_ms.clear();
+  c->it_mu_ms.clear();
+
+  // random_factors with mt19937_64(seed + b) (model.cpp:189-208, estimator.cpp:532-533)
+  std::vector<double> hb((size_t)c->B * c->FL * c->SK), hv((size_t)c->B * c->SK * c->T);
+  for (int b = 0; b < c->B; ++b) {
+    std::mt19937_64 rng(prob->seed + (uint64_t)b);
+    std::uniform_real_distribution<double> uni(0.1, 1.0);
+    for (int n = 0; n < c->N; ++n) {
+      const int K = c->bases[n];
+      for (int i = 0; i < c->F; ++i)
+        for (int k = 0; k < K; ++k) {
+          const double v = uni(rng);
+          if (i >= c->lo && i < c->hi) hb[((size_t)b * c->FL + (i - c->lo)) * c->SK + c->koff[n] + k] = v;
+        }
+      for (int k = 0; k < K; ++k)
+        for (int j = 0; j < c->T; ++j) hv[((size_t)b * c->SK + c->koff[n] + k) * c->T + j] = uni(rng);
+    }
+  }
+  upload_real(c, c->Bf.p, hb.data(), hb.size());
+  upload_real(c, c->V.p, hv.data(), hv.size());
+  // W = I (model.cpp:221-227)
+  {
+    const size_t n = (size_t)c->B * plane_stride(c) * 2;
+    const int g = (int)std::min<size_t>((n + 255) / 256, 8192);
+    if (rs == 4) identity_kernel<float><<<g, 256, 0, c->stream>>>((float*)c->W.p, (size_t)c->B * c->FL, c->R, c->D);
+    else identity_kernel<double><<<g, 256, 0, c->stream>>>((double*)c->W.p, (size_t)c->B * c->FL, c->R, c->D);
+    CK(cudaGetLastError());
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  c->done = 0;
+  c->pending = false;
+  c->timing = ctf_timing{};
+  c->ready = true;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int ctf_abi_version(void) { return CTF_ABI_VERSION; }
+
+void ctf_shard_range(int num_bins, int world_size, int rank, int* lo, int* hi) {
+  // contiguous ranges, sizes differ by at most one
+  const int w = std::max(1, world_size);
+  const int base = num_bins / w, rem = num_bins % w;
+  const int l = rank * base + std::min(rank, rem);
+  *lo = l;
+  *hi = l + base + (rank < rem ? 1 : 0);
+}
+
+int ctf_open(int device, ctf_ctx** out, ctf_err* err) {
+  return guarded(err, [&] {
+    if (!out) throw CtfError(CTF_ERR_CONFIG, "null output");
+    int count = 0;
+    CK(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) throw CtfError(CTF_ERR_CUDA, "no such CUDA device");
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) throw CtfError(CTF_ERR_CUDA, "the kernels are built for sm_100a (B200) only");
+    auto* c = new ctf_ctx();
+    c->device = device;
+    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      delete c;
+      cuda_check(e, "cudaStreamCreate");
+    }
+    *out = c;
+  });
+}
+
+void ctf_close(ctf_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& pr : c->ev_sweep) c->ev_pool.push_back(pr.first), c->ev_pool.push_back(pr.second);
+  for (auto& pr : c->ev_mu) c->ev_pool.push_back(pr.second);
+  for (auto& pr : c->ev_fin) c->ev_pool.push_back(pr.first), c->ev_pool.push_back(pr.second);
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+void* ctf_stream(ctf_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int ctf_comm_unique_id(uint8_t id[128], ctf_err* err) {
+  return guarded(err, [&] {
+    if (!g_nccl.load()) throw CtfError(CTF_ERR_CUDA, "libnccl.so.2 could not be loaded");
+    NcclUid u;
+    if (g_nccl.GetUniqueId(&u) != 0) throw CtfError(CTF_ERR_CUDA, "ncclGetUniqueId failed");
+    std::memcpy(id, u.internal, 128);
+  });
+}
+
+int ctf_comm_init(ctf_ctx* c, int world, int rank, const uint8_t id[128], ctf_err* err) {
+  return guarded(err, [&] {
+    if (!c) throw CtfError(CTF_ERR_CONFIG, "null context");
+    if (world < 1 || rank < 0 || rank >= world) throw CtfError(CTF_ERR_CONFIG, "bad world/rank");
+    c->world = world;
+    c->rank = rank;
+    if (world == 1) return;
+    if (!g_nccl.load()) throw CtfError(CTF_ERR_CUDA, "libnccl.so.2 could not be loaded");
+    CK(cudaSetDevice(c->device));
+    NcclUid u;
+    std::memcpy(u.internal, id, 128);
+    const int rc = g_nccl.CommInitRank(&c->comm, world, u, rank);
+    if (rc != 0) throw CtfError(CTF_ERR_CUDA, "ncclCommInitRank failed");
+  });
+}
+
+int ctf_setup(ctf_ctx* c, const ctf_problem* prob, const void* x_host, ctf_err* err) {
+  return guarded(err, [&] {
+    if (!c) throw CtfError(CTF_ERR_CONFIG, "null context");
+    setup_impl(c, prob, x_host);
+  });
+}
+
+int ctf_set_state(ctf_ctx* c, const double* W, const double* Bh, const double* Vh, ctf_err* err) {
+  return guarded(err, [&] {
+    if (!c || !c->ready) throw CtfError(CTF_ERR_CONFIG, "ctf_setup has not been called");
+    CK(cudaSetDevice(c->device));
+    if (W) {
+      std::vector<double> w((size_t)c->B * plane_stride(c) * 2);
+      const size_t per = (size_t)c->R * c->D * 2;
+      for (int b = 0; b < c->B; ++b)
+        std::memcpy(w.data() + (size_t)b * c->FL * per, W + ((size_t)b * c->F + c->lo) * per, c->FL * per * 8);
+      upload_real(c, c->W.p, w.data(), w.size());
+    }
+    if (Bh) {  // [B][N] F x K_n column-major -> [B][FL][SK]
+      std::vector<double> hb((size_t)c->B * c->FL * c->SK);
+      for (int b = 0; b < c->B; ++b) {
+        size_t off = (size_t)b * c->F * c->SK;
+        for (int n = 0; n < c->N; ++n) {
+          const int K = c->bases[n];
+          for (int k = 0; k < K; ++k)
+            for (int i = c->lo; i < c->hi; ++i)
+              hb[((size_t)b * c->FL + (i - c->lo)) * c->SK + c->koff[n] + k] = Bh[off + (size_t)i + (size_t)k * c->F];
+          off += (size_t)c->F * K;
+        }
+      }
+      upload_real(c, c->Bf.p, hb.data(), hb.size());
+    }
+    if (Vh) {  // [B][N] K_n x T column-major -> [B][SK][T]
+      std::vector<double> hv((size_t)c->B * c->SK * c->T);
+      for (int b = 0; b < c->B; ++b) {
+        size_t off = (size_t)b * c->SK * c->T;
+        for (int n = 0; n < c->N; ++n) {
+          const int K = c->bases[n];
+          for (int j = 0; j < c->T; ++j)
+            for (int k = 0; k < K; ++k)
+              hv[((size_t)b * c->SK + c->koff[n] + k) * c->T + j] = Vh[off + (size_t)k + (size_t)j * K];
+          off += (size_t)K * c->T;
+        }
+      }
+      upload_real(c, c->V.p, hv.data(), hv.size());
+    }
+    c->pending = false;
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int ctf_iterate(ctf_ctx* c, int n, ctf_err* err) {
+  return guarded(err, [&] {
+    if (!c) throw CtfError(CTF_ERR_CONFIG, "null context");
+    iterate_impl(c, n, true);
+  });
+}
+
+int ctf_iterate_async(ctf_ctx* c, int n, ctf_err* err) {
+  return guarded(err, [&] {
+    if (!c) throw CtfError(CTF_ERR_CONFIG, "null context");
+    iterate_impl(c, n, false);
+  });
+}
+
+int ctf_finalize(ctf_ctx* c, ctf_err* err) {
+  return guarded(err, [&] {
+    if (!c) throw CtfError(CTF_ERR_CONFIG, "null context");
+    iterate_impl(c, 0, true);
+  });
+}
+
+int ctf_iterations_done(ctf_ctx* c) { return c ? c->done : 0; }
+
+int ctf_psd_floor(ctf_ctx* c, double* out) {
+  if (!c || !c->ready || !out) return CTF_ERR_CONFIG;
+  for (int b = 0; b < c->B; ++b) out[b] = c->floors[(size_t)b];
+  return CTF_OK;
+}
+
+int ctf_trace_ms(ctf_ctx* c, double* demix_ms, double* mu_ms, double* rescale_ms) {
+  if (!c) return CTF_ERR_CONFIG;
+  try {
+    collect_timing(c);
+  } catch (...) {
+    return CTF_ERR_CUDA;
+  }
+  const size_t n = std::min<size_t>(c->it_sweep_ms.size(), (size_t)c->done);
+  const size_t off = c->it_sweep_ms.size() - n;
+  for (size_t i = 0; i < n; ++i) {
+    if (demix_ms) demix_ms[i] = c->it_sweep_ms[off + i];
+    if (mu_ms) mu_ms[i] = c->it_mu_ms[off + i];
+    if (rescale_ms) rescale_ms[i] = 0.0;
+  }
+  return CTF_OK;
+}
+
+int ctf_get_timing(ctf_ctx* c, ctf_timing* out) {
+  if (!c || !out) return CTF_ERR_CONFIG;
+  try {
+    collect_timing(c);
+  } catch (...) {
+    return CTF_ERR_CUDA;
+  }
+  *out = c->timing;
+  return CTF_OK;
+}
+
+int ctf_reset_timing(ctf_ctx* c) {
+  if (!c) return CTF_ERR_CONFIG;
+  try {
+    collect_timing(c);
+  } catch (...) {
+    return CTF_ERR_CUDA;
+  }
+  c->timing = ctf_timing{};
+  return CTF_OK;
+}
+
+int ctf_download(ctf_ctx* c, double* W, double* Bh, double* Vh, double* objective, ctf_err* err) {
+  return guarded(err, [&] {
+    if (!c || !c->ready) throw CtfError(CTF_ERR_CONFIG, "ctf_setup has not been called");
+    if (c->pending) throw CtfError(CTF_ERR_CONFIG, "call ctf_finalize before ctf_download");
+    CK(cudaSetDevice(c->device));
+    if (W) {
+      std::vector<double> w((size_t)c->B * plane_stride(c) * 2);
+      download_real(c, w.data(), c->W.p, w.size());
+      const size_t per = (size_t)c->R * c->D * 2;
+      for (int b = 0; b < c->B; ++b)
+        std::memcpy(W + ((size_t)b * c->F + c->lo) * per, w.data() + (size_t)b * c->FL * per, c->FL * per * 8);
+    }
+    if (Bh) {
+      std::vector<double> hb((size_t)c->B * c->FL * c->SK);
+      download_real(c, hb.data(), c->Bf.p, hb.size());
+      for (int b = 0; b < c->B; ++b) {
+        size_t off = (size_t)b * c->F * c->SK;
+        for (int n = 0; n < c->N; ++n) {
+          const int K = c->bases[n];
+          for (int k = 0; k < K; ++k)
+            for (int i = c->lo; i < c->hi; ++i)
+              Bh[off + (size_t)i + (size_t)k * c->F] = hb[((size_t)b * c->FL + (i - c->lo)) * c->SK + c->koff[n] + k];
+          off += (size_t)c->F * K;
+        }
+      }
+    }
+    if (Vh) {
+      std::vector<double> hv((size_t)c->B * c->SK * c->T);
+      download_real(c, hv.data(), c->V.p, hv.size());
+      for (int b = 0; b < c->B; ++b) {
+        size_t off = (size_t)b * c->SK * c->T;
+        for (int n = 0; n < c->N; ++n) {
+          const int K = c->bases[n];
+          for (int j = 0; j < c->T; ++j)
+            for (int k = 0; k < K; ++k)
+              Vh[off + (size_t)k + (size_t)j * K] = hv[((size_t)b * c->SK + c->koff[n] + k) * c->T + j];
+          off += (size_t)K * c->T;
+        }
+      }
+    }
+    if (objective && c->done > 0) {
+      std::vector<double> o((size_t)c->B * c->max_iters);
+      CK(cudaMemcpyAsync(o.data(), c->objective.p, o.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      for (int b = 0; b < c->B; ++b)
+        for (int it = 0; it < c->done; ++it) objective[(size_t)b * c->done + it] = o[(size_t)b * c->max_iters + it];
+    }
+  });
+}
+
+int ctf_run(ctf_ctx* c, const ctf_problem* prob, const void* x_host, double* W_out, double* B_out, double* V_out,
+            double* objective_out, ctf_err* err) {
+  return guarded(err, [&] {
+    if (!c) throw CtfError(CTF_ERR_CONFIG, "null context");
+    setup_impl(c, prob, x_host);
+    iterate_impl(c, prob->iterations, true);
+    ctf_err e2{};
+    const int rc = ctf_download(c, W_out, B_out, V_out, objective_out, &e2);
+    if (rc != CTF_OK) throw CtfError(rc, e2.msg);
+  });
+}
+
+int ctf_project_back(ctf_ctx* c, int mode, double* images, ctf_err* err) {
+  return guarded(err, [&] {
+    if (!c || !c->ready) throw CtfError(CTF_ERR_CONFIG, "ctf_setup has not been called");
+    if (c->pending) throw CtfError(CTF_ERR_CONFIG, "call ctf_finalize before ctf_project_back");
+    if (!images) throw CtfError(CTF_ERR_CONFIG, "null output");
+    CK(cudaSetDevice(c->device));
+    const int Dout = mode == CTF_IMAGES_CURRENT_FRAME ? c->Mx : c->D;
+    // local bins of every mixture, per source: [n][mix][FL][T][Dout]
+    const size_t per_bin = (size_t)c->T * Dout;
+    DevBuf<double> out;
+    out.alloc((size_t)c->N * c->B * c->FL * per_bin * 2);
+    ctf::ImageParams ip{};
+    ip.x = c->x.p;
+    ip.W = c->W.p;
+    ip.out = out.p;
+    ip.err = c->err.p;
+    ip.FL = c->FL;
+    ip.bin_lo = c->lo;
+    ip.T = c->T;
+    ip.Mx = c->Mx;
+    ip.Ls = c->Ls;
+    ip.D = c->D;
+    ip.R = c->R;
+    ip.N = c->N;
+    ip.nmix = c->B;
+    ip.current_only = mode == CTF_IMAGES_CURRENT_FRAME ? 1 : 0;
+    for (int n = 0; n < c->N; ++n) {
+      ip.row0[n] = c->row0[n];
+      ip.ntaps[n] = c->taps[n];
+    }
+    const size_t cs = 2 * (size_t)c->real_size;
+    const size_t smem = (size_t)(2 * c->R * c->R + c->R * c->D) * cs + (size_t)c->Mx * (c->Ls - 1 + c->T) * cs;
+    int max_smem = 0;
+    CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+    if (smem > (size_t)max_smem) throw CtfError(CTF_ERR_UNSUPPORTED, "projection-back tile exceeds shared memory");
+    CK(cudaMemsetAsync(c->err.p, 0xFF, c->err.n * 8, c->stream));
+    if (c->real_size == 4) {
+      CK(cudaFuncSetAttribute((const void*)ctf::image_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      ctf::image_kernel<float><<<dim3(c->FL, c->B), 256, smem, c->stream>>>(ip);
+    } else {
+      CK(cudaFuncSetAttribute((const void*)ctf::image_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      ctf::image_kernel<double><<<dim3(c->FL, c->B), 256, smem, c->stream>>>(ip);
+    }
+    CK(cudaGetLastError());
+    c->timing.launches += 1;
+    std::vector<unsigned long long> keys((size_t)c->B);
+    CK(cudaMemcpyAsync(keys.data(), c->err.p, keys.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int b = 0; b < c->B; ++b)
+      if (keys[(size_t)b] != ctf::kNoErr)
+        throw CtfError(CTF_ERR_DEGENERACY, "image reconstruction: demixing matrix not invertible",
+                       CTF_KIND_SINGULAR_IMAGE, -1, b, (int)((keys[(size_t)b] >> 20) & 0xFFFFF), -1);
+    // scatter the local bins into the full-F host layout
+    for (int n = 0; n < c->N; ++n)
+      for (int b = 0; b < c->B; ++b) {
+        double* dst = images + ((((size_t)n * c->B + b) * c->F + c->lo) * per_bin) * 2;
+        const double* src = out.p + ((((size_t)n * c->B + b) * c->FL) * per_bin) * 2;
+        CK(cudaMemcpyAsync(dst, src, (size_t)c->FL * per_bin * 16, cudaMemcpyDeviceToHost, c->stream));
+      }
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+}  // extern "C"

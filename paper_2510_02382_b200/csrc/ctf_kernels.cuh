@@ -1,0 +1,884 @@
+// ctf_kernels.cuh — sm_100a kernels for the ISS+NMF hot path of CTF-MNMF-ISS.
+//
+// One CTA per (mixture, frequency bin) runs the whole bin-local part of one
+// iteration of proj/src/estimator.cpp:548-654:
+//   prologue : rescale of the previous iteration (W rows /= mu_r, B /= mu0^2,
+//              estimator.cpp:399-411), PSD refresh lambda = max(B V, floor)
+//              (model.cpp:210-215), Y = W x~ (estimator.cpp:555), finite
+//              check (:491-501) and the previous iteration's objective
+//              contribution (:55-77) incl. log|det W| by pivoted LU (:41-53).
+//   sweep    : R steps of iss_step (estimator.cpp:434-484): weighted
+//              reductions over frames with warp reduce-scatter trees, the
+//              steering vector z, rank-1 updates of Y (registers/smem) and W.
+//   epilogue : Y = W' x~ (:607), delayed energies E (:321-332), row powers
+//              (:391-397), and MU-B for this bin (:313-346).
+// Frames are owned by threads (frame j = tid + k*NT), so every per-frame
+// update is thread-private; the only cross-thread traffic is the 3R-value
+// reduction per step, done as a warp reduce-scatter plus a fixed-order
+// cross-warp sum (deterministic, run-to-run bit-identical).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include <type_traits>
+
+namespace ctf {
+
+constexpr int kMaxRows = 64;
+constexpr int kMaxSources = 16;
+constexpr unsigned kFull = 0xffffffffu;
+
+template <typename Real> struct Cplx;
+template <> struct Cplx<float> { using T = float2; };
+template <> struct Cplx<double> { using T = double2; };
+
+// Error keys: atomicMin over (iteration, phase, bin, row, code) reproduces the
+// reference's "first failing iteration, phase in program order, lowest bin".
+enum Phase : uint64_t { kPhSetup = 0, kPhSweep = 1, kPhFinite = 2, kPhDet = 3, kPhObj = 4, kPhImage = 5 };
+__host__ __device__ inline unsigned long long err_key(uint64_t it, uint64_t ph, uint64_t bin, uint64_t row,
+                                                      uint64_t code) {
+  return (unsigned long long)((it << 44) | (ph << 40) | ((bin & 0xFFFFF) << 20) | ((row & 0xFFF) << 8) |
+                              (code & 0xFF));
+}
+constexpr unsigned long long kNoErr = ~0ull;
+
+struct SweepParams {
+  const void* x;            // Real2 [mix][FL][T][Mx]
+  void* W;                  // Real2 [mix][FL][D][R] (column-major R x D per bin)
+  void* Bf;                 // Real  [mix][FL][SK]
+  const void* V;            // Real  [mix][SK][T]
+  void* E;                  // Real  [mix][N][FL][T]
+  double* rowpow;           // [mix][FL][R]
+  double* objbin;           // [mix][FL]
+  const double* mu;         // [mix][R] pending rescale, or nullptr
+  const double* floor_abs;  // [mix]
+  unsigned long long* err;  // [mix]
+  int FL, bin_lo, T, TP, Mx, Ls, D, R, N, SK;
+  int iteration;  // 1-based number of the iteration whose sweep runs (sweep errors)
+  int do_sweep;   // 0: prologue only (finalize pass)
+  int has_prev;   // prologue evaluates objective/finite checks of iteration-1
+  int xoff, xp;   // x tile: Mx rows of xp = xoff + TP complex, x_m(t) at [m*xp + xoff + t]
+  int loff, lp;   // 1/lambda: N rows of lp = loff + TP, at [n*lp + loff + tau]
+  int off_y, off_x, off_e, off_l, off_w, off_lu, off_red, off_z, off_b, off_d;  // smem byte offsets
+  int woff[kMaxRows];  // per row p: n_p*lp + loff - l_p (weight index base)
+  int row0[kMaxSources], ntaps[kMaxSources], koff[kMaxSources + 1];
+};
+
+// ---------------------------------------------------------------------------
+// Small complex helpers.
+template <typename V> __device__ __forceinline__ V cmul(V a, V b) {
+  V r;
+  r.x = fma(a.x, b.x, -a.y * b.y);
+  r.y = fma(a.x, b.y, a.y * b.x);
+  return r;
+}
+template <typename V> __device__ __forceinline__ void cmac(V& acc, V a, V b) {  // acc += a*b
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+}
+template <typename V> __device__ __forceinline__ void cmsub(V& acc, V a, V b) {  // acc -= a*b
+  acc.x = fma(-a.x, b.x, acc.x);
+  acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(-a.x, b.y, acc.y);
+  acc.y = fma(-a.y, b.x, acc.y);
+}
+template <typename V> __device__ __forceinline__ auto cnorm(V a) -> decltype(a.x) { return fma(a.x, a.x, a.y * a.y); }
+template <typename V> __device__ __forceinline__ bool cfinite(V a) { return isfinite(a.x) && isfinite(a.y); }
+template <typename Real> __device__ __forceinline__ typename Cplx<Real>::T czero() {
+  typename Cplx<Real>::T z;
+  z.x = Real(0);
+  z.y = Real(0);
+  return z;
+}
+
+// Warp reduce-scatter of V values (V multiple of 32): afterwards lane L holds
+// in v[0..V/32) the warp sums of the original indices [L*V/32, (L+1)*V/32).
+// V-1 shuffles instead of 5*V for per-value butterflies.
+template <int CNT, int OFF, typename Real, int V>
+__device__ __forceinline__ void rs_level(Real (&v)[V], int lane) {
+  if constexpr (OFF >= 1) {
+    constexpr int H = CNT / 2;
+    const bool upper = (lane & OFF) != 0;
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      const Real send = upper ? v[i] : v[i + H];
+      const Real keep = upper ? v[i + H] : v[i];
+      v[i] = keep + __shfl_xor_sync(kFull, send, OFF);
+    }
+    rs_level<H, OFF / 2>(v, lane);
+  }
+}
+template <typename Real, int V>
+__device__ __forceinline__ void warp_reduce_scatter(Real (&v)[V], int lane) {
+  static_assert(V % 32 == 0, "pad the value count to a multiple of 32");
+  rs_level<V, 16>(v, lane);
+}
+
+template <typename T> __device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// Block sum of NQ doubles, fixed order; result valid in every thread.
+template <int NQ>
+__device__ __forceinline__ void block_sum_d(double (&v)[NQ], double* dred, int lane, int warp, int nw) {
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) v[q] = warp_sum(v[q]);
+  __syncthreads();  // dred may still be read from a previous call
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) dred[warp * NQ + q] = v[q];
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += dred[w * NQ + q];
+    v[q] = s;
+  }
+}
+
+// log|det A| of an n x n column-major complex matrix by one warp, partial
+// pivoting on |a| with the lowest row winning ties (estimator.cpp:41-53).
+// Returns 0 ok, CTF kind 4 (zero pivot) or 5 (tiny det).
+template <typename Real>
+__device__ int warp_logdet(typename Cplx<Real>::T* A, int n, int lane, double& out) {
+  using R2 = typename Cplx<Real>::T;
+  double acc = 0.0;
+  for (int c = 0; c < n; ++c) {
+    Real best = Real(-1);
+    int brow = n;
+    for (int r = c + lane; r < n; r += 32) {
+      const R2 a = A[c * n + r];
+      const Real m = sqrt(cnorm(a));
+      if (m > best) {
+        best = m;
+        brow = r;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const Real ob = __shfl_xor_sync(kFull, best, o);
+      const int orow = __shfl_xor_sync(kFull, brow, o);
+      if (ob > best || (ob == best && orow < brow)) {
+        best = ob;
+        brow = orow;
+      }
+    }
+    if (brow != c && brow < n)
+      for (int j = lane; j < n; j += 32) {
+        const R2 t = A[j * n + c];
+        A[j * n + c] = A[j * n + brow];
+        A[j * n + brow] = t;
+      }
+    __syncwarp();
+    const R2 pv = A[c * n + c];
+    const double mag = sqrt((double)pv.x * pv.x + (double)pv.y * pv.y);
+    if (!(mag > 0.0) || !isfinite(mag)) return 4;
+    acc += log(mag);
+    const Real inv = Real(1) / cnorm(pv);
+    R2 pinv;
+    pinv.x = pv.x * inv;
+    pinv.y = -pv.y * inv;
+    for (int r = c + 1 + lane; r < n; r += 32) {
+      const R2 f = cmul(A[c * n + r], pinv);
+      for (int j = c + 1; j < n; ++j) cmsub(A[j * n + r], f, A[j * n + c]);
+    }
+    __syncwarp();
+  }
+  if (acc < log(1e-300)) return 5;
+  out = acc;
+  return 0;
+}
+
+// Y(k, p) accessor: rows p < RREG live in registers, the rest in shared memory.
+template <typename R2, int FT, int RREG, int RS>
+struct YTile {
+  R2 reg[FT][RREG > 0 ? RREG : 1];
+  R2* sm;  // RS rows x TP
+  int tp;
+  template <int P> __device__ __forceinline__ R2 get(int k, int j) const {
+    if constexpr (P < RREG) return reg[k][P];
+    else return sm[(P - RREG) * tp + j];
+  }
+  template <int P> __device__ __forceinline__ void set(int k, int j, R2 v) {
+    if constexpr (P < RREG) reg[k][P] = v;
+    else sm[(P - RREG) * tp + j] = v;
+  }
+  // runtime row selection (pivot of the current step)
+  __device__ __forceinline__ R2 pick(int k, int j, int r) const {
+    if (r >= RREG) return sm[(r - RREG) * tp + j];
+    R2 out = reg[k][0];
+#pragma unroll
+    for (int q = 1; q < RREG; ++q)
+      if (q == r) out = reg[k][q];
+    return out;
+  }
+};
+
+// Compile-time loop helper.
+template <int I, int N, typename F> __device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (I < N) {
+    f(std::integral_constant<int, I>{});
+    static_for<I + 1, N>(f);
+  }
+}
+
+// Y = W x~ for the thread's frames (estimator.cpp:304-311 with the stacked
+// observation of BASELINE (a) built virtually from the x tile).
+template <typename Real, int RMAX, int FT, int RREG, typename Tile>
+__device__ __forceinline__ void demix_tile(Tile& Y, const typename Cplx<Real>::T* xs,
+                                           const typename Cplx<Real>::T* Ws, const SweepParams& p, int tid,
+                                           int NT) {
+  using R2 = typename Cplx<Real>::T;
+  constexpr int RC = 4;
+  static_for<0, (RMAX + RC - 1) / RC>([&](auto chunk) {
+    constexpr int r0 = decltype(chunk)::value * RC;
+    if (r0 < p.R) {
+      R2 acc[FT][RC];
+#pragma unroll
+      for (int k = 0; k < FT; ++k)
+#pragma unroll
+        for (int i = 0; i < RC; ++i) acc[k][i] = czero<Real>();
+      for (int c = 0; c < p.D; ++c) {
+        const int m = c / p.Ls, l = c - m * p.Ls;
+        const R2* xrow = xs + m * p.xp + p.xoff - l;
+        R2 w[RC];
+#pragma unroll
+        for (int i = 0; i < RC; ++i) w[i] = (r0 + i < p.R) ? Ws[c * p.R + r0 + i] : czero<Real>();
+#pragma unroll
+        for (int k = 0; k < FT; ++k) {
+          const R2 xv = xrow[tid + k * NT];
+#pragma unroll
+          for (int i = 0; i < RC; ++i) cmac(acc[k][i], w[i], xv);
+        }
+      }
+      static_for<0, RC>([&](auto ii) {
+        constexpr int P = r0 + decltype(ii)::value;
+        if constexpr (P < RMAX) {
+          if (P < p.R) {
+#pragma unroll
+            for (int k = 0; k < FT; ++k) {
+              const int j = tid + k * NT;
+              Y.template set<P>(k, j, (j < p.T) ? acc[k][decltype(ii)::value] : czero<Real>());
+            }
+          }
+        }
+      });
+    }
+  });
+}
+
+template <typename Real>
+__device__ __forceinline__ void record_err(unsigned long long* err, int mix, unsigned long long key) {
+  atomicMin(err + mix, key);
+}
+
+// ---------------------------------------------------------------------------
+// The fused per-bin iteration kernel.
+template <typename Real, int RMAX, int FT, int RREG, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepParams p) {
+  using R2 = typename Cplx<Real>::T;
+  constexpr int RS = RMAX - RREG;
+  constexpr int NV = 3 * RMAX;
+  constexpr int VP = ((NV + 31) / 32) * 32;
+  constexpr int VM = VP / 32;
+  static_assert(RMAX <= 32, "one lane per steering coefficient");
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NT = blockDim.x, NW = NT >> 5;
+  const int bin = blockIdx.x, mix = blockIdx.y;
+  const int gbin = p.bin_lo + bin;
+  const int T = p.T, TP = p.TP, R = p.R, D = p.D, N = p.N, SK = p.SK;
+
+  R2* Ysm = reinterpret_cast<R2*>(smem + p.off_y);
+  R2* xs = reinterpret_cast<R2*>(smem + p.off_x);
+  Real* Pq = reinterpret_cast<Real*>(smem + p.off_x);  // aliases xs after the last demix
+  Real* Es = reinterpret_cast<Real*>(smem + p.off_e);  // aliases xs after the last demix
+  Real* invl = reinterpret_cast<Real*>(smem + p.off_l);
+  R2* Ws = reinterpret_cast<R2*>(smem + p.off_w);
+  R2* Wlu = reinterpret_cast<R2*>(smem + p.off_lu);
+  Real* red = reinterpret_cast<Real*>(smem + p.off_red);
+  R2* zs = reinterpret_cast<R2*>(smem + p.off_z);
+  Real* Bs = reinterpret_cast<Real*>(smem + p.off_b);
+  double* dred = reinterpret_cast<double*>(smem + p.off_d);
+  __shared__ int s_bad;
+
+  const size_t tile = (size_t)mix * p.FL + bin;
+  const R2* xg = reinterpret_cast<const R2*>(p.x) + tile * (size_t)T * p.Mx;
+  R2* Wg = reinterpret_cast<R2*>(p.W) + tile * (size_t)R * D;
+  Real* Bg = reinterpret_cast<Real*>(p.Bf) + tile * SK;
+  const Real* Vg = reinterpret_cast<const Real*>(p.V) + (size_t)mix * SK * T;
+  const Real floor_abs = (Real)p.floor_abs[mix];
+  const int prev_it = p.iteration - 1;
+
+  if (tid == 0) s_bad = 0;
+  // ---- prologue: x tile (transposed to [m][t]), W, B with pending rescale
+  for (int i = tid; i < p.Mx * p.xp; i += NT) {
+    const int m = i / p.xp, t = i - m * p.xp - p.xoff;
+    if (t < 0 || t >= T) xs[i] = czero<Real>();
+  }
+  for (int e = tid; e < T * p.Mx; e += NT) {
+    const int t = e / p.Mx, m = e - t * p.Mx;
+    xs[m * p.xp + p.xoff + t] = xg[e];
+  }
+  for (int i = tid; i < R * D; i += NT) {
+    R2 w = Wg[i];
+    if (p.mu) {
+      const double mu = p.mu[(size_t)mix * R + (i % R)];
+      if (mu != 0.0) {
+        w.x = (Real)((double)w.x / mu);
+        w.y = (Real)((double)w.y / mu);
+      }
+    }
+    Ws[i] = w;
+    Wlu[i] = w;
+    if (p.has_prev && !cfinite(w)) s_bad = 1;
+  }
+  for (int i = tid; i < SK; i += NT) {
+    Real b = Bg[i];
+    if (p.mu) {
+      int n = 0;
+      while (i >= p.koff[n + 1]) ++n;
+      const double mu0 = p.mu[(size_t)mix * R + p.row0[n]];
+      if (mu0 != 0.0) b = (Real)fmax((double)b / (mu0 * mu0), (double)floor_abs);
+    }
+    Bs[i] = b;
+  }
+  __syncthreads();
+  if (p.has_prev && s_bad) {  // check_all_finite on W (estimator.cpp:494-496)
+    if (tid == 0) record_err<Real>(p.err, mix, err_key(prev_it, kPhFinite, gbin, 0, 1));
+    return;
+  }
+  // ---- lambda = max(B V, floor) -> 1/lambda and the log-lambda objective term
+  double logsum = 0.0;
+  for (int n = 0; n < N; ++n) {
+    Real* il = invl + n * p.lp;
+    for (int i = tid; i < p.loff; i += NT) il[i] = Real(0);
+    const int k0 = p.koff[n], k1 = p.koff[n + 1], Ln = p.ntaps[n];
+    for (int tau = tid; tau < TP; tau += NT) {
+      Real v = Real(0);
+      if (tau < T) {
+        Real lam = Real(0);
+        for (int k = k0; k < k1; ++k) lam = fma(Bs[k], Vg[(size_t)k * T + tau], lam);
+        lam = fmax(lam, floor_abs);
+        v = Real(1) / lam;
+        if (p.has_prev) logsum += (double)min(Ln, T - tau) * log((double)lam);
+      }
+      il[p.loff + tau] = v;
+    }
+  }
+  __syncthreads();
+
+  YTile<R2, FT, RREG, RS> Y;
+  Y.sm = Ysm;
+  Y.tp = TP;
+  demix_tile<Real, RMAX, FT, RREG>(Y, xs, Ws, p, tid, NT);
+
+  if (p.has_prev) {
+    // objective of the previous iteration (estimator.cpp:55-77): quadratic
+    // term from Y = W x~, log term above, -2T log|det W| by warp 0.
+    double quad = 0.0;
+    bool fin = true;
+    static_for<0, RMAX>([&](auto pp) {
+      constexpr int P = decltype(pp)::value;
+      if (P < R) {
+#pragma unroll
+        for (int k = 0; k < FT; ++k) {
+          const int j = tid + k * NT;
+          const R2 y = Y.template get<P>(k, j);
+          fin = fin && cfinite(y);
+          quad += (double)cnorm(y) * (double)invl[p.woff[P] + j];
+        }
+      }
+    });
+    if (!fin) s_bad = 1;
+    double ld = 0.0;
+    int lu_status = 0;
+    if (warp == 0) lu_status = warp_logdet<Real>(Wlu, R, lane, ld);
+    double v2[2] = {logsum, quad};
+    block_sum_d<2>(v2, dred, lane, warp, NW);  // contains __syncthreads: s_bad visible after
+    if (s_bad) {
+      if (tid == 0) record_err<Real>(p.err, mix, err_key(prev_it, kPhFinite, gbin, 0, 2));
+      return;
+    }
+    if (warp == 0 && lane == 0) {
+      if (lu_status != 0) {
+        record_err<Real>(p.err, mix, err_key(prev_it, kPhDet, gbin, 0, lu_status));
+        s_bad = 2;
+      } else {
+        p.objbin[tile] = v2[0] + v2[1] - 2.0 * (double)T * ld;
+      }
+    }
+    __syncthreads();
+    if (s_bad) return;
+  }
+
+  if (!p.do_sweep) {  // finalize pass: write the rescaled state and stop
+    for (int i = tid; i < R * D; i += NT) Wg[i] = Ws[i];
+    for (int i = tid; i < SK; i += NT) Bg[i] = Bs[i];
+    return;
+  }
+
+  // ---- ISS sweep (estimator.cpp:556-579): step r computes z from the
+  // current Y, then Y -= z y_r and W -= z w_r. The pass of step r applies
+  // step r-1's update and accumulates step r's sums in one sweep over Y.
+  R2 pv[FT];
+  for (int r = 0; r < R; ++r) {
+    const bool upd = r > 0;
+    Real acc[VP];
+#pragma unroll
+    for (int i = 0; i < VP; ++i) acc[i] = Real(0);
+    const R2* zw = zs + warp * RMAX;
+#pragma unroll
+    for (int k = 0; k < FT; ++k) {
+      const int j = tid + k * NT;
+      R2 yr = Y.pick(k, j, r);
+      if (upd) cmsub(yr, zw[r], pv[k]);
+      const Real ar2 = cnorm(yr);
+      static_for<0, RMAX>([&](auto pp) {
+        constexpr int P = decltype(pp)::value;
+        if (P < R) {
+          R2 y = Y.template get<P>(k, j);
+          if (upd) {
+            cmsub(y, zw[P], pv[k]);
+            Y.template set<P>(k, j, y);
+          }
+          const Real w = invl[p.woff[P] + j];
+          // numer_p += y_p conj(y_r) w ; denom_p += |y_r|^2 w
+          const Real tr = fma(y.x, yr.x, y.y * yr.y);
+          const Real ti = fma(y.y, yr.x, -y.x * yr.y);
+          acc[P] = fma(tr, w, acc[P]);
+          acc[RMAX + P] = fma(ti, w, acc[RMAX + P]);
+          acc[2 * RMAX + P] = fma(ar2, w, acc[2 * RMAX + P]);
+        }
+      });
+      pv[k] = yr;
+    }
+    warp_reduce_scatter(acc, lane);
+    Real* rb = red + (size_t)((r & 1) * NW + warp) * VP;
+#pragma unroll
+    for (int i = 0; i < VM; ++i) rb[lane * VM + i] = acc[i];
+    __syncthreads();
+    // every warp derives z redundantly (identical fixed-order sums)
+    const Real* rs = red + (size_t)((r & 1) * NW) * VP;
+    bool bad = false;
+    if (lane < R) {
+      Real nre = Real(0), nim = Real(0), den = Real(0);
+      for (int w = 0; w < NW; ++w) {
+        nre += rs[w * VP + lane];
+        nim += rs[w * VP + RMAX + lane];
+        den += rs[w * VP + 2 * RMAX + lane];
+      }
+      bad = !(den > Real(0)) || !isfinite(den);
+      R2 z;
+      if (lane == r) {
+        z.x = Real(1) - sqrt((Real)T / den);
+        z.y = Real(0);
+      } else {
+        z.x = nre / den;
+        z.y = nim / den;
+      }
+      zs[warp * RMAX + lane] = z;
+    }
+    const unsigned badm = __ballot_sync(kFull, bad);
+    __syncwarp();
+    if (badm) {  // estimator.cpp:451-454
+      if (tid == 0)
+        record_err<Real>(p.err, mix, err_key(p.iteration, kPhSweep, gbin, r, __ffs(badm) - 1));
+      return;
+    }
+    if (warp == 0) {  // iss_apply: W -= z w_r (estimator.cpp:298-302)
+      for (int c = lane; c < D; c += 32) {
+        const R2 wr = Ws[c * R + r];
+        for (int q = 0; q < R; ++q) cmsub(Ws[c * R + q], zs[q], wr);
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- epilogue: Y = W' x~ (estimator.cpp:607)
+  demix_tile<Real, RMAX, FT, RREG>(Y, xs, Ws, p, tid, NT);
+  __syncthreads();  // xs is dead: reuse the region for |y|^2 of register rows and E
+
+  // row powers (estimator.cpp:391-397) and |y|^2 export
+  {
+    Real rp[((RMAX + 31) / 32) * 32];
+#pragma unroll
+    for (int i = 0; i < ((RMAX + 31) / 32) * 32; ++i) rp[i] = Real(0);
+    static_for<0, RMAX>([&](auto pp) {
+      constexpr int P = decltype(pp)::value;
+      if (P < R) {
+#pragma unroll
+        for (int k = 0; k < FT; ++k) {
+          const int j = tid + k * NT;
+          const Real q = cnorm(Y.template get<P>(k, j));
+          rp[P] += q;
+          if constexpr (P < RREG) Pq[P * TP + j] = q;
+        }
+      }
+    });
+    constexpr int RP = ((RMAX + 31) / 32) * 32;
+    warp_reduce_scatter(rp, lane);
+    Real* rb = red + (size_t)warp * VP;
+#pragma unroll
+    for (int i = 0; i < RP / 32; ++i) rb[lane * (RP / 32) + i] = rp[i];
+  }
+  __syncthreads();
+  if (tid < R) {
+    double s = 0.0;
+    for (int w = 0; w < NW; ++w) s += (double)red[(size_t)w * VP + tid];
+    p.rowpow[tile * R + tid] = s;
+  }
+  // delayed energies E_n(tau) = sum_{l<L_n, tau+l<T} |y_{row0+l}(tau+l)|^2
+  Real* Eg = reinterpret_cast<Real*>(p.E);
+  for (int n = 0; n < N; ++n) {
+    const int r0 = p.row0[n], Ln = p.ntaps[n];
+    for (int tau = tid; tau < TP; tau += NT) {
+      Real e = Real(0);
+      for (int l = 0; l < Ln && tau + l < T; ++l) {
+        const int row = r0 + l;
+        e += (row < RREG) ? Pq[row * TP + tau + l] : cnorm(Ysm[(row - RREG) * TP + tau + l]);
+      }
+      Es[n * TP + tau] = e;
+      if (tau < T) Eg[(((size_t)mix * N + n) * p.FL + bin) * T + tau] = e;
+    }
+  }
+  for (int i = tid; i < R * D; i += NT) Wg[i] = Ws[i];
+  __syncthreads();
+
+  // ---- MU-B for this bin (estimator.cpp:313-346), 8 bases per pass
+  for (int n = 0; n < N; ++n) {
+    const int k0 = p.koff[n], k1 = p.koff[n + 1], Ln = p.ntaps[n];
+    const Real* il = invl + n * p.lp + p.loff;
+    for (int kb = k0; kb < k1; kb += 8) {
+      Real a[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) a[i] = Real(0);
+      for (int tau = tid; tau < T; tau += NT) {
+        const Real ilv = il[tau];
+        const Real an = Es[n * TP + tau] * (ilv * ilv);
+        const Real bn = ilv * (Real)min(Ln, T - tau);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (kb + q < k1) {
+            const Real v = Vg[(size_t)(kb + q) * T + tau];
+            a[q] = fma(an, v, a[q]);
+            a[8 + q] = fma(bn, v, a[8 + q]);
+          }
+      }
+      warp_reduce_scatter(a, lane);
+      Real* rb = red + (size_t)warp * VP;
+      __syncthreads();  // previous pass's reads of red are done
+      rb[lane] = a[0];
+      __syncthreads();
+      if (tid < 8 && kb + tid < k1) {
+        Real num = Real(0), den = Real(0);
+        for (int w = 0; w < NW; ++w) {
+          num += red[(size_t)w * VP + tid];
+          den += red[(size_t)w * VP + 8 + tid];
+        }
+        const Real b = Bs[kb + tid];
+        Bg[kb + tid] = fmax(b * sqrt(num / den), floor_abs);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// MU-V (estimator.cpp:348-382): partial numerator/denominator over a chunk
+// of this rank's bins, for one source and a tile of frames. lambda' is
+// recomputed with the updated bases; all taps contribute (:356-368).
+struct MuvParams {
+  const void* Bf;  // Real [mix][FL][SK]
+  const void* V;   // Real [mix][SK][T]
+  const void* E;   // Real [mix][N][FL][T]
+  void* part;      // Real [chunk][mix][2][SK][T]
+  const double* floor_abs;
+  int FL, T, N, SK, nmix, chunk_bins;
+  int koff[kMaxSources + 1], ntaps[kMaxSources];
+};
+
+template <typename Real, int KMAX>
+__global__ void __launch_bounds__(128) muv_partial_kernel(const MuvParams p) {
+  const int tau = blockIdx.x * blockDim.x + threadIdx.x;
+  const int mix = blockIdx.y / p.N, n = blockIdx.y - mix * p.N;
+  const int chunk = blockIdx.z;
+  const int i0 = chunk * p.chunk_bins, i1 = min(p.FL, i0 + p.chunk_bins);
+  const int k0 = p.koff[n], K = p.koff[n + 1] - k0;
+  extern __shared__ __align__(16) unsigned char smem[];
+  Real* Bsh = reinterpret_cast<Real*>(smem);  // chunk_bins x K
+  const Real* Bg = reinterpret_cast<const Real*>(p.Bf) + (size_t)mix * p.FL * p.SK;
+  for (int e = threadIdx.x; e < (i1 - i0) * K; e += blockDim.x) {
+    const int i = e / K, k = e - i * K;
+    Bsh[e] = Bg[(size_t)(i0 + i) * p.SK + k0 + k];
+  }
+  __syncthreads();
+  if (tau >= p.T) return;
+  const Real floor_abs = (Real)p.floor_abs[mix];
+  const Real cnt = (Real)min(p.ntaps[n], p.T - tau);
+  const Real* Vg = reinterpret_cast<const Real*>(p.V) + ((size_t)mix * p.SK + k0) * p.T + tau;
+  Real v[KMAX], num[KMAX], den[KMAX];
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    v[k] = (k < K) ? Vg[(size_t)k * p.T] : Real(0);
+    num[k] = Real(0);
+    den[k] = Real(0);
+  }
+  const Real* Eg = reinterpret_cast<const Real*>(p.E) + (((size_t)mix * p.N + n) * p.FL) * p.T + tau;
+  for (int i = i0; i < i1; ++i) {
+    const Real* b = Bsh + (i - i0) * K;
+    Real lam = Real(0);
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k)
+      if (k < K) lam = fma(b[k], v[k], lam);
+    lam = fmax(lam, floor_abs);
+    const Real il = Real(1) / lam;
+    const Real e = Eg[(size_t)i * p.T];
+    const Real an = e * (il * il), bn = il * cnt;
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k)
+      if (k < K) {
+        num[k] = fma(b[k], an, num[k]);
+        den[k] = fma(b[k], bn, den[k]);
+      }
+  }
+  Real* out = reinterpret_cast<Real*>(p.part) + (((size_t)chunk * p.nmix + mix) * 2 * p.SK + k0) * p.T + tau;
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k)
+    if (k < K) {
+      out[(size_t)k * p.T] = num[k];
+      out[(size_t)(p.SK + k) * p.T] = den[k];
+    }
+}
+
+// Sum of the chunk partials in fixed order, then either the packed buffer
+// for the all-reduce (world > 1) or directly the V update (world == 1).
+struct ApplyParams {
+  const void* part;     // Real [nchunk][mix][2][SK][T]
+  void* packed;         // Real [mix][2][SK][T] (all-reduce buffer)
+  void* V;              // Real [mix][SK][T]
+  const double* rowpow; // [mix][FL][R]
+  const double* objbin; // [mix][FL]
+  double* packed_d;     // [mix][R + 1]
+  double* mu;           // [mix][R]
+  double* objective;    // [mix][max_iters]
+  const double* floor_abs;
+  unsigned long long* err;
+  int nchunk, nmix, SK, T, FL, R, F_total, max_iters;
+  int obj_slot;         // iteration index (0-based) whose objective is summed, -1 if none
+  int mode;             // 0 = reduce to packed, 1 = apply from packed, 2 = reduce+apply (world 1)
+  int do_v;             // 0 for the objective-only finalize pass
+};
+
+template <typename Real>
+__global__ void __launch_bounds__(256) reduce_apply_kernel(const ApplyParams p) {
+  const int mix = blockIdx.y;
+  const size_t plane = (size_t)p.SK * p.T;
+  if (p.do_v) {
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < plane; e += (size_t)gridDim.x * blockDim.x) {
+      Real num, den;
+      if (p.mode == 1) {
+        const Real* pk = reinterpret_cast<const Real*>(p.packed) + (size_t)mix * 2 * plane;
+        num = pk[e];
+        den = pk[plane + e];
+      } else {
+        const Real* pt = reinterpret_cast<const Real*>(p.part);
+        num = Real(0);
+        den = Real(0);
+        for (int c = 0; c < p.nchunk; ++c) {
+          const Real* q = pt + ((size_t)c * p.nmix + mix) * 2 * plane;
+          num += q[e];
+          den += q[plane + e];
+        }
+        if (p.mode == 0) {
+          Real* pk = reinterpret_cast<Real*>(p.packed) + (size_t)mix * 2 * plane;
+          pk[e] = num;
+          pk[plane + e] = den;
+          continue;
+        }
+      }
+      Real* V = reinterpret_cast<Real*>(p.V) + (size_t)mix * plane;
+      V[e] = fmax(V[e] * sqrt(num / den), (Real)p.floor_abs[mix]);
+    }
+  }
+  if (blockIdx.x != 0) return;
+  // row powers -> mu (estimator.cpp:391-397) and the objective sum
+  double* pd = p.packed_d + (size_t)mix * (p.R + 1);
+  if (p.mode != 1) {
+    for (int r = threadIdx.x; r <= p.R; r += blockDim.x) {
+      double s = 0.0;
+      if (r < p.R) {
+        for (int i = 0; i < p.FL; ++i) s += p.rowpow[((size_t)mix * p.FL + i) * p.R + r];
+      } else if (p.obj_slot >= 0) {
+        for (int i = 0; i < p.FL; ++i) s += p.objbin[(size_t)mix * p.FL + i];
+      }
+      pd[r] = s;
+    }
+    if (p.mode == 0) return;
+    __syncthreads();
+  }
+  for (int r = threadIdx.x; r <= p.R; r += blockDim.x) {
+    if (r < p.R) {
+      if (p.do_v) p.mu[(size_t)mix * p.R + r] = sqrt(pd[r] / ((double)p.F_total * p.T));
+    } else if (p.obj_slot >= 0) {
+      const double obj = pd[r];
+      p.objective[(size_t)mix * p.max_iters + p.obj_slot] = obj;
+      if (!isfinite(obj)) atomicMin(p.err + mix, err_key(p.obj_slot + 1, kPhObj, 0, 0, 6));
+    }
+  }
+}
+
+// Mean power of the stacked observation (model.cpp:153-161, counted over
+// x~ incl. its zero pads): per (mixture, bin) partial sums.
+template <typename Real>
+__global__ void __launch_bounds__(256) mean_power_kernel(const void* x, double* part, int FL, int T, int Mx,
+                                                         int Ls) {
+  using R2 = typename Cplx<Real>::T;
+  const int bin = blockIdx.x, mix = blockIdx.y;
+  const R2* xg = reinterpret_cast<const R2*>(x) + ((size_t)mix * FL + bin) * (size_t)T * Mx;
+  double s = 0.0;
+  for (int e = threadIdx.x; e < T * Mx; e += blockDim.x) {
+    const int t = e / Mx;
+    s += (double)min(Ls, T - t) * ((double)xg[e].x * xg[e].x + (double)xg[e].y * xg[e].y);
+  }
+  __shared__ double sh[32];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+    part[(size_t)mix * FL + bin] = t;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Projection-back (proj/src/wiener.cpp:11-49, collapsed Wiener form):
+// H = W^-1 by Gauss-Jordan with partial pivoting (one warp, lowest row wins
+// ties), y = W x~, c_n(d, j) = sum_{l<L_n} H(d, r0_n + l) y_{r0_n + l}(j).
+struct ImageParams {
+  const void* x;     // Real2 [mix][FL][T][Mx]
+  const void* W;     // Real2 [mix][FL][D][R]
+  double* out;       // double2 [n][mix][FL][T][Dout]
+  unsigned long long* err;
+  int FL, bin_lo, T, Mx, Ls, D, R, N, nmix, current_only;
+  int row0[kMaxSources], ntaps[kMaxSources];
+};
+
+template <typename Real>
+__global__ void __launch_bounds__(256) image_kernel(const ImageParams p) {
+  using R2 = typename Cplx<Real>::T;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int bin = blockIdx.x, mix = blockIdx.y, tid = threadIdx.x, lane = tid & 31;
+  const int R = p.R, D = p.D, T = p.T;
+  const int xoff = p.Ls - 1, xp = xoff + T;
+  R2* A = reinterpret_cast<R2*>(smem);          // R x R
+  R2* H = A + R * R;                            // R x R
+  R2* Wsm = H + R * R;                          // R x D
+  R2* xs = Wsm + R * D;                         // Mx x xp
+  __shared__ int s_bad;
+  const size_t tile = (size_t)mix * p.FL + bin;
+  const R2* xg = reinterpret_cast<const R2*>(p.x) + tile * (size_t)T * p.Mx;
+  const R2* Wg = reinterpret_cast<const R2*>(p.W) + tile * (size_t)R * D;
+  if (tid == 0) s_bad = 0;
+  for (int i = tid; i < R * D; i += blockDim.x) {
+    Wsm[i] = Wg[i];
+    A[i] = Wg[i];
+    const int r = i % R, c = i / R;
+    H[i] = czero<Real>();
+    if (r == c) H[i].x = Real(1);
+  }
+  for (int i = tid; i < p.Mx * xp; i += blockDim.x) {
+    const int m = i / xp, t = i - m * xp - xoff;
+    if (t < 0) xs[i] = czero<Real>();
+  }
+  for (int e = tid; e < T * p.Mx; e += blockDim.x) {
+    const int t = e / p.Mx, m = e - t * p.Mx;
+    xs[m * xp + xoff + t] = xg[e];
+  }
+  __syncthreads();
+  if (tid < 32) {
+    for (int c = 0; c < R; ++c) {
+      Real best = Real(-1);
+      int brow = R;
+      for (int r = c + lane; r < R; r += 32) {
+        const Real m = sqrt(cnorm(A[c * R + r]));
+        if (m > best) { best = m; brow = r; }
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        const Real ob = __shfl_xor_sync(kFull, best, o);
+        const int orow = __shfl_xor_sync(kFull, brow, o);
+        if (ob > best || (ob == best && orow < brow)) { best = ob; brow = orow; }
+      }
+      if (brow != c && brow < R)
+        for (int j = lane; j < R; j += 32) {
+          R2 t = A[j * R + c]; A[j * R + c] = A[j * R + brow]; A[j * R + brow] = t;
+          t = H[j * R + c]; H[j * R + c] = H[j * R + brow]; H[j * R + brow] = t;
+        }
+      __syncwarp();
+      const R2 pv = A[c * R + c];
+      const Real nn = cnorm(pv);
+      R2 pinv; pinv.x = pv.x / nn; pinv.y = -pv.y / nn;
+      R2 f[2];
+      for (int q = 0; q < 2; ++q) {
+        const int r = lane + 32 * q;
+        f[q] = (r < R && r != c) ? cmul(A[c * R + r], pinv) : czero<Real>();
+      }
+      __syncwarp();
+      for (int q = 0; q < 2; ++q) {
+        const int r = lane + 32 * q;
+        if (r < R && r != c)
+          for (int j = 0; j < R; ++j) {
+            if (j != c) cmsub(A[j * R + r], f[q], A[j * R + c]);
+            cmsub(H[j * R + r], f[q], H[j * R + c]);
+          }
+      }
+      __syncwarp();
+    }
+    for (int r = lane; r < R; r += 32) {
+      const R2 pv = A[r * R + r];
+      const Real nn = cnorm(pv);
+      R2 pinv; pinv.x = pv.x / nn; pinv.y = -pv.y / nn;
+      for (int j = 0; j < R; ++j) {
+        const R2 h = cmul(H[j * R + r], pinv);
+        H[j * R + r] = h;
+        if (!cfinite(h)) s_bad = 1;
+      }
+    }
+  }
+  __syncthreads();
+  if (s_bad) {
+    if (tid == 0) atomicMin(p.err + mix, err_key(0, kPhImage, p.bin_lo + bin, 0, 9));
+    return;
+  }
+  const int Dout = p.current_only ? p.Mx : D;
+  for (int j = tid; j < T; j += blockDim.x) {
+    R2 y[kMaxRows];
+    for (int r = 0; r < R; ++r) {
+      R2 acc = czero<Real>();
+      for (int c = 0; c < D; ++c) {
+        const int m = c / p.Ls, l = c - m * p.Ls;
+        cmac(acc, Wsm[c * R + r], xs[m * xp + xoff + j - l]);
+      }
+      y[r] = acc;
+    }
+    for (int n = 0; n < p.N; ++n) {
+      double2* o = reinterpret_cast<double2*>(p.out) +
+                   ((((size_t)n * p.nmix + mix) * p.FL + bin) * T + j) * Dout;
+      for (int od = 0; od < Dout; ++od) {
+        const int d = p.current_only ? od * p.Ls : od;
+        R2 acc = czero<Real>();
+        for (int l = 0; l < p.ntaps[n]; ++l) cmac(acc, H[(p.row0[n] + l) * R + d], y[p.row0[n] + l]);
+        o[od] = make_double2((double)acc.x, (double)acc.y);
+      }
+    }
+  }
+}
+
+}  // namespace ctf

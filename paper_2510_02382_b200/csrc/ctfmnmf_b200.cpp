@@ -1,0 +1,194 @@
+// ctfmnmf_b200.cpp — the reference-shaped C++ API over the C ABI.
+#include "ctfmnmf_b200.hpp"
+
+#include "../../include/ctf_iss.h"
+
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <sstream>
+
+namespace ctfmnmf {
+namespace b200 {
+
+int CtfConfig::total_taps() const { return std::accumulate(taps_per_source.begin(), taps_per_source.end(), 0); }
+
+int CtfConfig::row_offset(int source) const {
+  int o = 0;
+  for (int n = 0; n < source; ++n) o += taps_per_source[static_cast<size_t>(n)];
+  return o;
+}
+
+void CtfConfig::validate() const {
+  if (num_sources < 1) throw ConfigError("n_sources must be >= 1");
+  if (num_channels < 1) throw ConfigError("n_channels must be >= 1");
+  if (static_cast<int>(taps_per_source.size()) != num_sources)
+    throw ConfigError("taps list must have one entry per source");
+  if (static_cast<int>(bases_per_source.size()) != num_sources)
+    throw ConfigError("bases list must have one entry per source");
+  for (int l : taps_per_source)
+    if (l < 1) throw ConfigError("every tap count must be >= 1");
+  for (int k : bases_per_source)
+    if (k < 1) throw ConfigError("every basis count must be >= 1");
+  if (total_taps() != num_channels)
+    throw ConfigError("sum of taps (" + std::to_string(total_taps()) + ") must equal n_channels (" +
+                      std::to_string(num_channels) + "): the demixing system must be square");
+  if (iterations < 0) throw ConfigError("iters must be >= 0");
+  if (!(psd_floor > 0.0)) throw ConfigError("floor must be > 0");
+  if (threads < 1) throw ConfigError("threads must be >= 1");
+}
+
+double MixtureSpectrogram::mean_power() const {
+  double total = 0.0;
+  std::int64_t count = 0;
+  for (const auto& b : bins) {
+    for (const auto& v : b.data) total += std::norm(v);
+    count += static_cast<std::int64_t>(b.data.size());
+  }
+  return count > 0 ? total / static_cast<double>(count) : 0.0;
+}
+
+std::string OptimizationTrace::to_csv() const {  // estimator.cpp:15-23
+  std::ostringstream out;
+  out << "iter,objective,t_demix_ms,t_mu_ms,t_rescale_ms\n";
+  out.precision(12);
+  for (size_t t = 0; t < objective.size(); ++t)
+    out << (t + 1) << ',' << objective[t] << ',' << demix_ms[t] << ',' << mu_ms[t] << ',' << rescale_ms[t] << '\n';
+  return out.str();
+}
+double OptimizationTrace::total_demix_ms() const { return std::accumulate(demix_ms.begin(), demix_ms.end(), 0.0); }
+double OptimizationTrace::total_mu_ms() const { return std::accumulate(mu_ms.begin(), mu_ms.end(), 0.0); }
+double OptimizationTrace::total_rescale_ms() const {
+  return std::accumulate(rescale_ms.begin(), rescale_ms.end(), 0.0);
+}
+
+namespace {
+
+[[noreturn]] void rethrow(const ctf_err& e) {
+  switch (e.code) {
+    case CTF_ERR_CONFIG: throw ConfigError(e.msg);
+    case CTF_ERR_IO: throw IoError(e.msg);
+    case CTF_ERR_DEGENERACY: throw DegeneracyError(e.msg, e.iteration, e.bin, e.row);
+    default: throw std::runtime_error(e.msg);
+  }
+}
+
+struct Ctx {
+  ctf_ctx* c = nullptr;
+  explicit Ctx(int device) {
+    ctf_err e{};
+    if (ctf_open(device, &c, &e) != CTF_OK) rethrow(e);
+  }
+  ~Ctx() { ctf_close(c); }
+};
+
+ctf_problem make_problem(const CtfConfig& config, const MixtureSpectrogram& x, const GpuOptions& gpu) {
+  config.validate();
+  if (config.num_sources > CTF_MAX_SOURCES) throw ConfigError("too many sources");
+  if (gpu.stack_taps < 1 || x.num_channels() * gpu.stack_taps != config.num_channels)
+    throw ConfigError("mixture has " + std::to_string(x.num_channels() * gpu.stack_taps) +
+                      " channels but config expects " + std::to_string(config.num_channels));
+  ctf_problem p{};
+  p.num_mixtures = 1;
+  p.num_bins = x.num_bins();
+  p.num_frames = x.num_frames();
+  p.num_mics = x.num_channels();
+  p.stack_taps = gpu.stack_taps;
+  p.num_sources = config.num_sources;
+  for (int n = 0; n < config.num_sources; ++n) {
+    p.taps_per_source[n] = config.taps_per_source[static_cast<size_t>(n)];
+    p.bases_per_source[n] = config.bases_per_source[static_cast<size_t>(n)];
+  }
+  p.iterations = config.iterations;
+  p.update_rule = config.update_rule == UpdateRule::Iss ? CTF_RULE_ISS : CTF_RULE_IP;
+  p.precision = gpu.precision == Precision::F32 ? CTF_F32 : CTF_F64;
+  p.x_precision = CTF_F64;
+  p.psd_floor = config.psd_floor;
+  p.seed = config.seed;
+  p.threads = config.threads;
+  return p;
+}
+
+// [bin][frame][channel] interleaved doubles (the reference Spectrogram layout)
+std::vector<double> flatten(const MixtureSpectrogram& x) {
+  const int F = x.num_bins(), T = x.num_frames(), M = x.num_channels();
+  std::vector<double> out(static_cast<size_t>(F) * T * M * 2);
+  for (int i = 0; i < F; ++i)
+    std::memcpy(out.data() + static_cast<size_t>(i) * T * M * 2, x.bins[static_cast<size_t>(i)].data.data(),
+                static_cast<size_t>(T) * M * sizeof(Complex));
+  return out;
+}
+
+}  // namespace
+
+SeparationResult run(const CtfConfig& config, const MixtureSpectrogram& x, const GpuOptions& gpu) {
+  const ctf_problem p = make_problem(config, x, gpu);
+  const int F = p.num_bins, T = p.num_frames, R = config.total_taps(), D = config.num_channels;
+  const std::vector<double> xf = flatten(x);
+  Ctx ctx(gpu.device);
+  ctf_err e{};
+  if (ctf_setup(ctx.c, &p, xf.data(), &e) != CTF_OK) rethrow(e);
+  if (ctf_iterate(ctx.c, config.iterations, &e) != CTF_OK) rethrow(e);
+  int sumK = 0;
+  for (int k : config.bases_per_source) sumK += k;
+  std::vector<double> W(static_cast<size_t>(F) * R * D * 2), B(static_cast<size_t>(F) * sumK),
+      V(static_cast<size_t>(sumK) * T), obj(static_cast<size_t>(config.iterations));
+  if (ctf_download(ctx.c, W.data(), B.data(), V.data(), obj.data(), &e) != CTF_OK) rethrow(e);
+  SeparationResult res;
+  res.demixing.assign(static_cast<size_t>(F), CMatrix(R, D));
+  for (int i = 0; i < F; ++i)
+    std::memcpy(res.demixing[static_cast<size_t>(i)].data.data(), W.data() + static_cast<size_t>(i) * R * D * 2,
+                static_cast<size_t>(R) * D * sizeof(Complex));
+  size_t ob = 0, ov = 0;
+  for (int n = 0; n < config.num_sources; ++n) {
+    const int K = config.bases_per_source[static_cast<size_t>(n)];
+    RMatrix b(F, K), v(K, T);
+    std::memcpy(b.data.data(), B.data() + ob, b.data.size() * 8);
+    std::memcpy(v.data.data(), V.data() + ov, v.data.size() * 8);
+    ob += b.data.size();
+    ov += v.data.size();
+    res.factors.bases.push_back(std::move(b));
+    res.factors.activations.push_back(std::move(v));
+  }
+  ctf_psd_floor(ctx.c, &res.factors.floor);
+  res.trace.objective = obj;
+  res.trace.demix_ms.resize(obj.size());
+  res.trace.mu_ms.resize(obj.size());
+  res.trace.rescale_ms.resize(obj.size());
+  ctf_trace_ms(ctx.c, res.trace.demix_ms.data(), res.trace.mu_ms.data(), res.trace.rescale_ms.data());
+  return res;
+}
+
+std::vector<MixtureSpectrogram> reconstruct_images(const std::vector<CMatrix>& demixing, const NmfFactors& factors,
+                                                   const MixtureSpectrogram& x, const CtfConfig& config,
+                                                   const GpuOptions& gpu) {
+  if (static_cast<int>(factors.bases.size()) != config.num_sources)
+    throw ConfigError("image reconstruction: factor count does not match config");
+  CtfConfig c0 = config;
+  c0.iterations = 0;
+  const ctf_problem p = make_problem(c0, x, gpu);
+  const int F = p.num_bins, T = p.num_frames, R = config.total_taps(), D = config.num_channels;
+  const std::vector<double> xf = flatten(x);
+  std::vector<double> W(static_cast<size_t>(F) * R * D * 2);
+  for (int i = 0; i < F; ++i)
+    std::memcpy(W.data() + static_cast<size_t>(i) * R * D * 2, demixing[static_cast<size_t>(i)].data.data(),
+                static_cast<size_t>(R) * D * sizeof(Complex));
+  Ctx ctx(gpu.device);
+  ctf_err e{};
+  if (ctf_setup(ctx.c, &p, xf.data(), &e) != CTF_OK) rethrow(e);
+  if (ctf_set_state(ctx.c, W.data(), nullptr, nullptr, &e) != CTF_OK) rethrow(e);
+  std::vector<double> img(static_cast<size_t>(config.num_sources) * F * T * D * 2);
+  if (ctf_project_back(ctx.c, CTF_IMAGES_FULL, img.data(), &e) != CTF_OK) rethrow(e);
+  std::vector<MixtureSpectrogram> out(static_cast<size_t>(config.num_sources));
+  for (int n = 0; n < config.num_sources; ++n) {
+    out[static_cast<size_t>(n)].bins.assign(static_cast<size_t>(F), CMatrix(D, T));
+    for (int i = 0; i < F; ++i)
+      std::memcpy(out[static_cast<size_t>(n)].bins[static_cast<size_t>(i)].data.data(),
+                  img.data() + (static_cast<size_t>(n) * F + i) * T * D * 2, static_cast<size_t>(D) * T * sizeof(Complex));
+  }
+  return out;
+}
+
+}  // namespace b200
+}  // namespace ctfmnmf

@@ -1,0 +1,118 @@
+// ctfmnmf_b200.hpp — C++ host API mirroring the reference library
+// (/root/reference/proj/include/ctfmnmf/{model,estimator,wiener,errors}.hpp)
+// over the C ABI in include/ctf_iss.h. Same names, argument meaning, output
+// layout and exceptions, with its own column-major matrix types because
+// Eigen is not part of this build. A reference caller swaps
+//   #include "ctfmnmf/estimator.hpp"   ->   #include "ctfmnmf_b200.hpp"
+// and `ctfmnmf::run` -> `ctfmnmf::b200::run`.
+#pragma once
+
+#include <complex>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace ctfmnmf {
+namespace b200 {
+
+using Complex = std::complex<double>;
+
+// Column-major dense matrices, element (r, c) at r + c * rows (Eigen layout).
+struct CMatrix {
+  int rows = 0, cols = 0;
+  std::vector<Complex> data;
+  CMatrix() = default;
+  CMatrix(int r, int c) : rows(r), cols(c), data(static_cast<size_t>(r) * c) {}
+  Complex& operator()(int r, int c) { return data[static_cast<size_t>(r) + static_cast<size_t>(c) * rows]; }
+  const Complex& operator()(int r, int c) const { return data[static_cast<size_t>(r) + static_cast<size_t>(c) * rows]; }
+};
+struct RMatrix {
+  int rows = 0, cols = 0;
+  std::vector<double> data;
+  RMatrix() = default;
+  RMatrix(int r, int c) : rows(r), cols(c), data(static_cast<size_t>(r) * c) {}
+  double& operator()(int r, int c) { return data[static_cast<size_t>(r) + static_cast<size_t>(c) * rows]; }
+  double operator()(int r, int c) const { return data[static_cast<size_t>(r) + static_cast<size_t>(c) * rows]; }
+};
+
+// errors.hpp:11-35
+struct ConfigError : std::runtime_error {
+  explicit ConfigError(const std::string& m) : std::runtime_error(m) {}
+};
+struct IoError : std::runtime_error {
+  explicit IoError(const std::string& m) : std::runtime_error(m) {}
+};
+struct DegeneracyError : std::runtime_error {
+  DegeneracyError(const std::string& m, int it = -1, int b = -1, int r = -1)
+      : std::runtime_error(m), iteration(it), bin(b), row(r) {}
+  int iteration, bin, row;
+};
+
+enum class UpdateRule { Ip, Iss };
+
+// model.hpp:21-35
+struct CtfConfig {
+  int num_sources = 2;
+  int num_channels = 4;
+  std::vector<int> taps_per_source;
+  std::vector<int> bases_per_source;
+  int iterations = 100;
+  UpdateRule update_rule = UpdateRule::Iss;
+  double psd_floor = 1e-10;
+  std::uint64_t seed = 0;
+  int threads = 1;
+  int total_taps() const;
+  int row_offset(int source) const;
+  void validate() const;  // throws ConfigError (model.cpp:32-50)
+};
+
+// model.hpp:55-66 — one channels x frames matrix per bin.
+struct MixtureSpectrogram {
+  std::vector<CMatrix> bins;
+  int num_bins() const { return static_cast<int>(bins.size()); }
+  int num_channels() const { return bins.empty() ? 0 : bins[0].rows; }
+  int num_frames() const { return bins.empty() ? 0 : bins[0].cols; }
+  double mean_power() const;
+};
+
+struct NmfFactors {  // model.hpp:70-80
+  std::vector<RMatrix> bases;        // B_n: F x K_n
+  std::vector<RMatrix> activations;  // V_n: K_n x T
+  double floor = 1e-12;
+};
+
+struct OptimizationTrace {  // estimator.hpp:25-40
+  std::vector<double> objective, demix_ms, mu_ms, rescale_ms;
+  std::string to_csv() const;
+  double total_demix_ms() const;
+  double total_mu_ms() const;
+  double total_rescale_ms() const;
+};
+
+struct SeparationResult {  // estimator.hpp:50-54
+  std::vector<CMatrix> demixing;
+  NmfFactors factors;
+  OptimizationTrace trace;
+};
+
+enum class Precision { F64, F32 };
+struct GpuOptions {
+  int device = 0;
+  Precision precision = Precision::F64;
+  // > 1: x holds num_channels / stack_taps microphones and the stacked
+  // observation x~(m*L + l, t) = x_m(t - l) is built on the GPU (BASELINE (a)).
+  int stack_taps = 1;
+};
+
+// estimator.hpp:122-123. CheckOptions instrumentation is not offered on the
+// GPU path.
+SeparationResult run(const CtfConfig& config, const MixtureSpectrogram& x, const GpuOptions& gpu = {});
+
+// wiener.hpp:18-20 (collapsed Wiener form, wiener.cpp:27-46).
+std::vector<MixtureSpectrogram> reconstruct_images(const std::vector<CMatrix>& demixing, const NmfFactors& factors,
+                                                   const MixtureSpectrogram& x, const CtfConfig& config,
+                                                   const GpuOptions& gpu = {});
+
+}  // namespace b200
+}  // namespace ctfmnmf
