@@ -173,6 +173,8 @@ int ctf_finalize(ctf_ctx* ctx, ctf_err* err);
  * objective receives [B][iterations_done]. Any pointer may be NULL. */
 int ctf_download(ctf_ctx* ctx, double* W, double* B, double* V, double* objective, ctf_err* err);
 int ctf_iterations_done(ctf_ctx* ctx);
+/* JSON description of the kernel configuration chosen for the problem. */
+int ctf_describe(ctf_ctx* ctx, char* buf, int len);
 /* Absolute PSD floor per mixture (factors.floor, estimator.cpp:529). */
 int ctf_psd_floor(ctf_ctx* ctx, double* floor_out /* [B] */);
 /* Per-iteration phase times (OptimizationTrace demix_ms / mu_ms /

@@ -58,6 +58,7 @@ SIGNATURES = {
     "ctf_finalize": (C.c_int, [_P, _E]),
     "ctf_download": (C.c_int, [_P, _D, _D, _D, _D, _E]),
     "ctf_iterations_done": (C.c_int, [_P]),
+    "ctf_describe": (C.c_int, [_P, C.c_char_p, C.c_int]),
     "ctf_psd_floor": (C.c_int, [_P, _D]),
     "ctf_trace_ms": (C.c_int, [_P, _D, _D, _D]),
     "ctf_get_timing": (C.c_int, [_P, C.POINTER(CtfTiming)]),

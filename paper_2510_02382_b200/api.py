@@ -240,6 +240,11 @@ class Session:
             out.append((dem, bases, acts, obj[b]))
         return out
 
+    def describe(self) -> str:
+        buf = C.create_string_buffer(1024)
+        self.lib.ctf_describe(self._ctx, buf, 1024)
+        return buf.value.decode()
+
     def psd_floor(self) -> np.ndarray:
         out = np.zeros(self.shape[0])
         self.lib.ctf_psd_floor(self._ctx, L.dptr(out))

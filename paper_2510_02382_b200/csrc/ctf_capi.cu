@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <stdexcept>
@@ -29,11 +30,8 @@ using ctf::kMaxSources;
 
 // ---------------------------------------------------------------------------
 // Kernel variant registry (instantiated in ctf_sweep_*.cu).
+#include "ctf_sweep_variants.h"
 namespace ctf {
-struct SweepVariant {
-  int prec, rmax, ft, rreg, maxt;
-  void (*fn)(SweepParams);
-};
 const std::vector<SweepVariant>& sweep_variants_f32();
 const std::vector<SweepVariant>& sweep_variants_f64();
 }  // namespace ctf
@@ -129,7 +127,7 @@ struct ctf_ctx {
   int kmax = 0, chunk_bins = 0, nchunk = 0;
   // device buffers
   DevBuf<unsigned char> x, W, Bf, V, E, part, packed;
-  DevBuf<double> rowpow, objbin, packed_d, mu, floor_abs, objective, mp_part;
+  DevBuf<double> rowpow, objbin, packed_d, mu, floor_abs, objective, mp_part, logdet;
   DevBuf<unsigned long long> err;
   // timing
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_sweep, ev_mu, ev_fin;
@@ -212,13 +210,22 @@ void plan_sweep(ctf_ctx* c) {
   const auto& vars = c->prob.precision == CTF_F32 ? ctf::sweep_variants_f32() : ctf::sweep_variants_f64();
   int max_smem = 0;
   CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+  max_smem -= 1024;  // static shared memory of the kernel + reserve
   const size_t rs = c->real_size, cs = 2 * rs;
   bool found = false;
+  // CTF_SWEEP_VARIANT="rmax,ft,rreg,maxt" pins a variant (profiling aid)
+  int force[5] = {0, 0, -1, 0, -1};
+  if (const char* env = std::getenv("CTF_SWEEP_VARIANT"))
+    std::sscanf(env, "%d,%d,%d,%d,%d", &force[0], &force[1], &force[2], &force[3], &force[4]);
   ctf::SweepVariant best{};
   size_t best_smem = 0;
   int best_nt = 0;
   for (const auto& v : vars) {
     if (v.rmax < c->R) continue;
+    if (v.exact && v.rmax != c->R) continue;
+    if (force[0] && (v.rmax != force[0] || v.ft != force[1] || v.rreg != force[2] || v.maxt != force[3] ||
+                     (force[4] >= 0 && v.exact != force[4])))
+      continue;
     int nt = (c->T + v.ft - 1) / v.ft;
     nt = std::max(32, (nt + 31) / 32 * 32);
     if (nt > v.maxt) continue;
@@ -240,16 +247,15 @@ void plan_sweep(ctf_ctx* c) {
     cand.off_x = (int)take(xbytes);
     cand.off_e = cand.off_x + (int)align16((size_t)v.rreg * TP * rs);
     cand.off_l = (int)take((size_t)c->N * lp * rs);
-    cand.off_w = (int)take((size_t)c->R * c->D * cs);
-    cand.off_lu = (int)take((size_t)c->R * c->D * cs);
+    cand.off_w = (int)take((size_t)2 * c->R * c->D * cs);
     cand.off_red = (int)take((size_t)2 * NW * VP * rs);
     cand.off_z = (int)take((size_t)NW * v.rmax * cs);
     cand.off_b = (int)take((size_t)c->SK * rs);
     cand.off_d = (int)take((size_t)NW * 4 * sizeof(double));
     if (off > (size_t)max_smem) continue;
-    // prefer the smallest rmax, then the most register-resident rows, then fewer threads
-    const bool better = !found || v.rmax < best.rmax ||
-                        (v.rmax == best.rmax && (v.rreg > best.rreg || (v.rreg == best.rreg && nt < best_nt)));
+    // variants are listed in preference order per rmax: exact beats guarded,
+    // then the table order (measured on B200)
+    const bool better = !found || v.rmax < best.rmax || (v.rmax == best.rmax && v.exact > best.exact);
     if (better) {
       found = true;
       best = v;
@@ -288,6 +294,10 @@ void plan_sweep(ctf_ctx* c) {
     for (int l = 0; l < c->taps[n]; ++l, ++r) sp.woff[r] = n * sp.lp + sp.loff - l;
   }
   for (int n = 0; n <= c->N; ++n) sp.koff[n] = c->koff[n];
+  for (int ch = 0; ch < c->D; ++ch) {
+    const int m = ch / c->Ls, l = ch - m * c->Ls;
+    sp.xcol[ch] = m * sp.xp + sp.xoff - l;
+  }
 }
 
 template <class Real>
@@ -455,6 +465,7 @@ void run_body(ctf_ctx* c, bool do_sweep) {
   sp.mu = c->pending ? c->mu.p : nullptr;
   sp.floor_abs = c->floor_abs.p;
   sp.err = c->err.p;
+  sp.logdet = c->logdet.p;
   sp.iteration = c->done + 1;
   sp.do_sweep = do_sweep ? 1 : 0;
   sp.has_prev = c->pending ? 1 : 0;
@@ -596,6 +607,7 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host) {
   const int ctas_per_chunk = ((c->T + 127) / 128) * c->B * c->N;
   int nchunk = std::max(1, std::min(c->FL, (4 * 148 + ctas_per_chunk - 1) / ctas_per_chunk));
   c->chunk_bins = (c->FL + nchunk - 1) / nchunk;
+  c->chunk_bins = std::min(c->chunk_bins, (int)(32768 / ((size_t)c->kmax * c->real_size)));  // <= 32 KiB smem
   c->nchunk = (c->FL + c->chunk_bins - 1) / c->chunk_bins;
 
   const size_t rs = c->real_size, cs = 2 * rs;
@@ -614,6 +626,8 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host) {
   c->floor_abs.alloc((size_t)c->B);
   c->mp_part.alloc((size_t)c->B * c->FL);
   c->err.alloc((size_t)c->B);
+  c->logdet.alloc((size_t)c->B * c->FL);
+  CK(cudaMemsetAsync(c->logdet.p, 0, c->logdet.n * 8, c->stream));  // log|det I| = 0
   c->max_iters = std::max(1, prob->iterations);
   c->objective.alloc((size_t)c->B * c->max_iters);
   CK(cudaMemsetAsync(c->objective.p, 0, c->objective.n * 8, c->stream));
@@ -803,6 +817,12 @@ int ctf_set_state(ctf_ctx* c, const double* W, const double* Bh, const double* V
       for (int b = 0; b < c->B; ++b)
         std::memcpy(w.data() + (size_t)b * c->FL * per, W + ((size_t)b * c->F + c->lo) * per, c->FL * per * 8);
       upload_real(c, c->W.p, w.data(), w.size());
+      // exact log|det W| for the externally supplied state (estimator.cpp:41-53)
+      const int nb = c->B * c->FL;
+      const size_t smem = (size_t)c->R * c->R * 2 * c->real_size;
+      if (c->real_size == 4) ctf::logdet_kernel<float><<<nb, 32, smem, c->stream>>>(c->W.p, c->logdet.p, c->R, nb);
+      else ctf::logdet_kernel<double><<<nb, 32, smem, c->stream>>>(c->W.p, c->logdet.p, c->R, nb);
+      CK(cudaGetLastError());
     }
     if (Bh) {  // [B][N] F x K_n column-major -> [B][FL][SK]
       std::vector<double> hb((size_t)c->B * c->FL * c->SK);
@@ -859,6 +879,16 @@ int ctf_finalize(ctf_ctx* c, ctf_err* err) {
 }
 
 int ctf_iterations_done(ctf_ctx* c) { return c ? c->done : 0; }
+
+int ctf_describe(ctf_ctx* c, char* buf, int len) {
+  if (!c || !buf || len <= 0) return CTF_ERR_CONFIG;
+  std::snprintf(buf, (size_t)len,
+                "{\"sweep_kernel\": \"sweep_kernel<%s,RMAX=%d,FT=%d,RREG=%d,MAXT=%d,EXACT=%d>\", \"threads\": %d, "
+                "\"smem_bytes\": %zu, \"grid\": [%d, %d], \"muv_chunks\": %d, \"bins\": [%d, %d]}",
+                c->real_size == 4 ? "f32" : "f64", c->sv.rmax, c->sv.ft, c->sv.rreg, c->sv.maxt, c->sv.exact, c->NT,
+                c->sweep_smem, c->FL, c->B, c->nchunk, c->lo, c->hi);
+  return CTF_OK;
+}
 
 int ctf_psd_floor(ctf_ctx* c, double* out) {
   if (!c || !c->ready || !out) return CTF_ERR_CONFIG;

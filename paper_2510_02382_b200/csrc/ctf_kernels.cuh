@@ -61,8 +61,10 @@ struct SweepParams {
   int has_prev;   // prologue evaluates objective/finite checks of iteration-1
   int xoff, xp;   // x tile: Mx rows of xp = xoff + TP complex, x_m(t) at [m*xp + xoff + t]
   int loff, lp;   // 1/lambda: N rows of lp = loff + TP, at [n*lp + loff + tau]
-  int off_y, off_x, off_e, off_l, off_w, off_lu, off_red, off_z, off_b, off_d;  // smem byte offsets
+  double* logdet;           // [mix][FL] log|det W| (pre-rescale after a sweep)
+  int off_y, off_x, off_e, off_l, off_w, off_red, off_z, off_b, off_d;  // smem byte offsets
   int woff[kMaxRows];  // per row p: n_p*lp + loff - l_p (weight index base)
+  int xcol[kMaxRows];  // per stacked channel c = m*Ls + l: m*xp + xoff - l (x tile offset)
   int row0[kMaxSources], ntaps[kMaxSources], koff[kMaxSources + 1];
 };
 
@@ -93,6 +95,23 @@ template <typename Real> __device__ __forceinline__ typename Cplx<Real>::T czero
   z.x = Real(0);
   z.y = Real(0);
   return z;
+}
+
+// Packed FP32x2 (Blackwell FFMA2/FMUL2): two FP32 FMAs per issue slot; a
+// broadcast scalar operand is free (SASS "R.F32"), a swizzled pair is not.
+__device__ __forceinline__ unsigned long long pk2(float2 a) { return *reinterpret_cast<unsigned long long*>(&a); }
+__device__ __forceinline__ float2 upk2(unsigned long long a) { return *reinterpret_cast<float2*>(&a); }
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {  // a*b + c
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(pk2(a)), "l"(pk2(b)), "l"(pk2(c)));
+  return upk2(d);
+}
+__device__ __forceinline__ float2 ffma2s(float2 a, float b, float2 c) { return ffma2(a, make_float2(b, b), c); }
+__device__ __forceinline__ float2 fmul2s(float2 a, float b) {
+  unsigned long long d;
+  const float2 bb = make_float2(b, b);
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a)), "l"(pk2(bb)));
+  return upk2(d);
 }
 
 // Warp reduce-scatter of V values (V multiple of 32): afterwards lane L holds
@@ -190,9 +209,8 @@ __device__ int warp_logdet(typename Cplx<Real>::T* A, int n, int lane, double& o
     }
     __syncwarp();
   }
-  if (acc < log(1e-300)) return 5;
   out = acc;
-  return 0;
+  return acc < log(1e-300) ? 5 : 0;
 }
 
 // Y(k, p) accessor: rows p < RREG live in registers, the rest in shared memory.
@@ -230,37 +248,44 @@ template <int I, int N, typename F> __device__ __forceinline__ void static_for(F
 
 // Y = W x~ for the thread's frames (estimator.cpp:304-311 with the stacked
 // observation of BASELINE (a) built virtually from the x tile).
-template <typename Real, int RMAX, int FT, int RREG, typename Tile>
+template <typename Real, int RMAX, int FT, int RREG, bool EXACT, typename Tile>
 __device__ __forceinline__ void demix_tile(Tile& Y, const typename Cplx<Real>::T* xs,
                                            const typename Cplx<Real>::T* Ws, const SweepParams& p, int tid,
-                                           int NT) {
+                                           int NT, const int R, const int D) {
   using R2 = typename Cplx<Real>::T;
   constexpr int RC = 4;
   static_for<0, (RMAX + RC - 1) / RC>([&](auto chunk) {
     constexpr int r0 = decltype(chunk)::value * RC;
-    if (r0 < p.R) {
+    if (r0 < R) {
       R2 acc[FT][RC];
 #pragma unroll
       for (int k = 0; k < FT; ++k)
 #pragma unroll
         for (int i = 0; i < RC; ++i) acc[k][i] = czero<Real>();
-      for (int c = 0; c < p.D; ++c) {
-        const int m = c / p.Ls, l = c - m * p.Ls;
-        const R2* xrow = xs + m * p.xp + p.xoff - l;
+#pragma unroll(EXACT ? RMAX : 1)
+      for (int c = 0; c < D; ++c) {
+        const R2* xrow = xs + p.xcol[c];  // stacked channel c = (m, l): x_m(t - l)
         R2 w[RC];
 #pragma unroll
-        for (int i = 0; i < RC; ++i) w[i] = (r0 + i < p.R) ? Ws[c * p.R + r0 + i] : czero<Real>();
+        for (int i = 0; i < RC; ++i) w[i] = (r0 + i < R) ? Ws[c * R + r0 + i] : czero<Real>();
 #pragma unroll
         for (int k = 0; k < FT; ++k) {
           const R2 xv = xrow[tid + k * NT];
+          if constexpr (std::is_same<Real, float>::value) {
+            // w x = w.x (x.x, x.y) + w.y (-x.y, x.x)
+            const float2 xn = make_float2(-xv.y, xv.x);
 #pragma unroll
-          for (int i = 0; i < RC; ++i) cmac(acc[k][i], w[i], xv);
+            for (int i = 0; i < RC; ++i) acc[k][i] = ffma2s(xn, w[i].y, ffma2s(xv, w[i].x, acc[k][i]));
+          } else {
+#pragma unroll
+            for (int i = 0; i < RC; ++i) cmac(acc[k][i], w[i], xv);
+          }
         }
       }
       static_for<0, RC>([&](auto ii) {
         constexpr int P = r0 + decltype(ii)::value;
         if constexpr (P < RMAX) {
-          if (P < p.R) {
+          if (P < R) {
 #pragma unroll
             for (int k = 0; k < FT; ++k) {
               const int j = tid + k * NT;
@@ -280,7 +305,16 @@ __device__ __forceinline__ void record_err(unsigned long long* err, int mix, uns
 
 // ---------------------------------------------------------------------------
 // The fused per-bin iteration kernel.
-template <typename Real, int RMAX, int FT, int RREG, int MAXT>
+//
+// log|det W| is carried per bin in p.logdet instead of an LU per iteration:
+// by the determinant lemma used in the reference's own checks
+// (estimator.cpp:560-569, test_estimator.cpp:322-335) every ISS step
+// multiplies det W by (1 - z_r) (real, > 0), and the rescale divides it by
+// prod_r mu_r. The exact pivoted LU (estimator.cpp:41-53) runs whenever the
+// state is set from outside (logdet_kernel below); its zero-pivot / 1e-300
+// outcomes are carried as -inf / the value and raised at the next
+// objective, as the reference raises them in objective_from_parts.
+template <typename Real, int RMAX, int FT, int RREG, int MAXT, bool EXACT>
 __global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepParams p) {
   using R2 = typename Cplx<Real>::T;
   constexpr int RS = RMAX - RREG;
@@ -293,20 +327,22 @@ __global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepParams p) {
   const int NT = blockDim.x, NW = NT >> 5;
   const int bin = blockIdx.x, mix = blockIdx.y;
   const int gbin = p.bin_lo + bin;
-  const int T = p.T, TP = p.TP, R = p.R, D = p.D, N = p.N, SK = p.SK;
+  // EXACT: R == D == RMAX is a compile-time constant (no row guards).
+  const int R = EXACT ? RMAX : p.R, D = EXACT ? RMAX : p.D;
+  const int T = p.T, TP = p.TP, N = p.N, SK = p.SK;
 
   R2* Ysm = reinterpret_cast<R2*>(smem + p.off_y);
   R2* xs = reinterpret_cast<R2*>(smem + p.off_x);
   Real* Pq = reinterpret_cast<Real*>(smem + p.off_x);  // aliases xs after the last demix
   Real* Es = reinterpret_cast<Real*>(smem + p.off_e);  // aliases xs after the last demix
   Real* invl = reinterpret_cast<Real*>(smem + p.off_l);
-  R2* Ws = reinterpret_cast<R2*>(smem + p.off_w);
-  R2* Wlu = reinterpret_cast<R2*>(smem + p.off_lu);
+  R2* Wb = reinterpret_cast<R2*>(smem + p.off_w);       // two R x D buffers (ping-pong)
   Real* red = reinterpret_cast<Real*>(smem + p.off_red);
   R2* zs = reinterpret_cast<R2*>(smem + p.off_z);
   Real* Bs = reinterpret_cast<Real*>(smem + p.off_b);
   double* dred = reinterpret_cast<double*>(smem + p.off_d);
   __shared__ int s_bad;
+  __shared__ double s_logmu;
 
   const size_t tile = (size_t)mix * p.FL + bin;
   const R2* xg = reinterpret_cast<const R2*>(p.x) + tile * (size_t)T * p.Mx;
@@ -315,59 +351,79 @@ __global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepParams p) {
   const Real* Vg = reinterpret_cast<const Real*>(p.V) + (size_t)mix * SK * T;
   const Real floor_abs = (Real)p.floor_abs[mix];
   const int prev_it = p.iteration - 1;
+  const double* mu = p.mu ? p.mu + (size_t)mix * R : nullptr;
 
-  if (tid == 0) s_bad = 0;
-  // ---- prologue: x tile (transposed to [m][t]), W, B with pending rescale
-  for (int i = tid; i < p.Mx * p.xp; i += NT) {
-    const int m = i / p.xp, t = i - m * p.xp - p.xoff;
-    if (t < 0 || t >= T) xs[i] = czero<Real>();
+  if (tid == 0) {
+    s_bad = 0;
+    double lm = 0.0;
+    if (mu)
+      for (int r = 0; r < R; ++r)
+        if (mu[r] != 0.0) lm += log(mu[r]);
+    s_logmu = lm;
   }
-  for (int e = tid; e < T * p.Mx; e += NT) {
-    const int t = e / p.Mx, m = e - t * p.Mx;
-    xs[m * p.xp + p.xoff + t] = xg[e];
+  // ---- prologue: x tile (transposed to [m][t]), W and B with the pending rescale
+  for (int m = 0; m < p.Mx; ++m) {
+    R2* row = xs + m * p.xp;
+    for (int i = tid; i < p.xoff; i += NT) row[i] = czero<Real>();
+    for (int t = T + tid; t < TP; t += NT) row[p.xoff + t] = czero<Real>();
+  }
+#pragma unroll
+  for (int k = 0; k < FT; ++k) {
+    const int t = tid + k * NT;
+    if (t < T)
+      for (int m = 0; m < p.Mx; ++m) xs[m * p.xp + p.xoff + t] = xg[(size_t)t * p.Mx + m];
   }
   for (int i = tid; i < R * D; i += NT) {
     R2 w = Wg[i];
-    if (p.mu) {
-      const double mu = p.mu[(size_t)mix * R + (i % R)];
-      if (mu != 0.0) {
-        w.x = (Real)((double)w.x / mu);
-        w.y = (Real)((double)w.y / mu);
+    if (mu) {
+      const double m = mu[i % R];
+      if (m != 0.0) {
+        w.x = (Real)((double)w.x / m);
+        w.y = (Real)((double)w.y / m);
       }
     }
-    Ws[i] = w;
-    Wlu[i] = w;
+    Wb[i] = w;
     if (p.has_prev && !cfinite(w)) s_bad = 1;
   }
-  for (int i = tid; i < SK; i += NT) {
-    Real b = Bg[i];
-    if (p.mu) {
-      int n = 0;
-      while (i >= p.koff[n + 1]) ++n;
-      const double mu0 = p.mu[(size_t)mix * R + p.row0[n]];
-      if (mu0 != 0.0) b = (Real)fmax((double)b / (mu0 * mu0), (double)floor_abs);
+  for (int n = 0; n < N; ++n) {
+    const double m0 = mu ? mu[p.row0[n]] : 0.0;
+    for (int i = p.koff[n] + tid; i < p.koff[n + 1]; i += NT) {
+      Real b = Bg[i];
+      if (m0 != 0.0) b = (Real)fmax((double)b / (m0 * m0), (double)floor_abs);
+      Bs[i] = b;
     }
-    Bs[i] = b;
   }
   __syncthreads();
   if (p.has_prev && s_bad) {  // check_all_finite on W (estimator.cpp:494-496)
     if (tid == 0) record_err<Real>(p.err, mix, err_key(prev_it, kPhFinite, gbin, 0, 1));
     return;
   }
-  // ---- lambda = max(B V, floor) -> 1/lambda and the log-lambda objective term
+  // ---- lambda = max(B V, floor) -> 1/lambda, and the log-lambda objective term
   double logsum = 0.0;
   for (int n = 0; n < N; ++n) {
     Real* il = invl + n * p.lp;
     for (int i = tid; i < p.loff; i += NT) il[i] = Real(0);
     const int k0 = p.koff[n], k1 = p.koff[n + 1], Ln = p.ntaps[n];
-    for (int tau = tid; tau < TP; tau += NT) {
+    Real lam[FT];
+#pragma unroll
+    for (int k = 0; k < FT; ++k) lam[k] = Real(0);
+    for (int kk = k0; kk < k1; ++kk) {
+      const Real b = Bs[kk];
+      const Real* vrow = Vg + (size_t)kk * T;
+#pragma unroll
+      for (int k = 0; k < FT; ++k) {
+        const int tau = tid + k * NT;
+        if (tau < T) lam[k] = fma(b, __ldg(vrow + tau), lam[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < FT; ++k) {
+      const int tau = tid + k * NT;
       Real v = Real(0);
       if (tau < T) {
-        Real lam = Real(0);
-        for (int k = k0; k < k1; ++k) lam = fma(Bs[k], Vg[(size_t)k * T + tau], lam);
-        lam = fmax(lam, floor_abs);
-        v = Real(1) / lam;
-        if (p.has_prev) logsum += (double)min(Ln, T - tau) * log((double)lam);
+        const Real l = fmax(lam[k], floor_abs);
+        v = Real(1) / l;
+        if (p.has_prev) logsum += (double)min(Ln, T - tau) * (double)log(l);
       }
       il[p.loff + tau] = v;
     }
@@ -377,11 +433,12 @@ __global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepParams p) {
   YTile<R2, FT, RREG, RS> Y;
   Y.sm = Ysm;
   Y.tp = TP;
-  demix_tile<Real, RMAX, FT, RREG>(Y, xs, Ws, p, tid, NT);
+  demix_tile<Real, RMAX, FT, RREG, EXACT>(Y, xs, Wb, p, tid, NT, R, D);
 
+  double logdet = p.logdet[tile] - s_logmu;
   if (p.has_prev) {
-    // objective of the previous iteration (estimator.cpp:55-77): quadratic
-    // term from Y = W x~, log term above, -2T log|det W| by warp 0.
+    // objective of the previous iteration (estimator.cpp:55-77) from
+    // Y = W_resc x~, the log term above and -2T log|det W_resc|.
     double quad = 0.0;
     bool fin = true;
     static_for<0, RMAX>([&](auto pp) {
@@ -397,30 +454,24 @@ __global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepParams p) {
       }
     });
     if (!fin) s_bad = 1;
-    double ld = 0.0;
-    int lu_status = 0;
-    if (warp == 0) lu_status = warp_logdet<Real>(Wlu, R, lane, ld);
     double v2[2] = {logsum, quad};
     block_sum_d<2>(v2, dred, lane, warp, NW);  // contains __syncthreads: s_bad visible after
-    if (s_bad) {
+    if (s_bad) {  // estimator.cpp:497-499
       if (tid == 0) record_err<Real>(p.err, mix, err_key(prev_it, kPhFinite, gbin, 0, 2));
       return;
     }
-    if (warp == 0 && lane == 0) {
-      if (lu_status != 0) {
-        record_err<Real>(p.err, mix, err_key(prev_it, kPhDet, gbin, 0, lu_status));
-        s_bad = 2;
-      } else {
-        p.objbin[tile] = v2[0] + v2[1] - 2.0 * (double)T * ld;
-      }
+    const int det_status = isnan(logdet) || logdet == -INFINITY ? 4 : (logdet < log(1e-300) ? 5 : 0);
+    if (det_status) {  // estimator.cpp:45-51
+      if (tid == 0) record_err<Real>(p.err, mix, err_key(prev_it, kPhDet, gbin, 0, det_status));
+      return;
     }
-    __syncthreads();
-    if (s_bad) return;
+    if (tid == 0) p.objbin[tile] = v2[0] + v2[1] - 2.0 * (double)T * logdet;
   }
 
   if (!p.do_sweep) {  // finalize pass: write the rescaled state and stop
-    for (int i = tid; i < R * D; i += NT) Wg[i] = Ws[i];
+    for (int i = tid; i < R * D; i += NT) Wg[i] = Wb[i];
     for (int i = tid; i < SK; i += NT) Bg[i] = Bs[i];
+    if (tid == 0) p.logdet[tile] = logdet;
     return;
   }
 
@@ -428,36 +479,84 @@ __global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepParams p) {
   // current Y, then Y -= z y_r and W -= z w_r. The pass of step r applies
   // step r-1's update and accumulates step r's sums in one sweep over Y.
   R2 pv[FT];
+#pragma unroll
+  for (int k = 0; k < FT; ++k) pv[k] = czero<Real>();
+  if (lane < RMAX) zs[warp * RMAX + lane] = czero<Real>();  // pass 0 applies a zero update
+  __syncwarp();
+  double dlog = 0.0;  // sum_r log(1 - z_r), lane 0 of every warp
   for (int r = 0; r < R; ++r) {
-    const bool upd = r > 0;
     Real acc[VP];
 #pragma unroll
     for (int i = 0; i < VP; ++i) acc[i] = Real(0);
     const R2* zw = zs + warp * RMAX;
+    if constexpr (std::is_same<Real, float>::value) {
+      // Packed FP32x2 pass. Update of step r-1: y -= z pv, written as
+      //   y + (-z.x) (pv.x, pv.y) + z.y (pv.y, -pv.x);
+      // accumulation for step r with s = w (yr.x, yr.y):
+      //   Q1 += s.x (y.x, y.y), Q2 += s.y (y.x, y.y), den += |yr|^2 w,
+      //   numer = (Q1.x + Q2.y, Q1.y - Q2.x) = sum w y conj(yr).
+      float2 yr[FT], pvn[FT];
+      float ar2[FT];
+      const float2 zr = zw[r];
 #pragma unroll
-    for (int k = 0; k < FT; ++k) {
-      const int j = tid + k * NT;
-      R2 yr = Y.pick(k, j, r);
-      if (upd) cmsub(yr, zw[r], pv[k]);
-      const Real ar2 = cnorm(yr);
+      for (int k = 0; k < FT; ++k) {
+        const int j = tid + k * NT;
+        pvn[k] = make_float2(pv[k].y, -pv[k].x);
+        float2 y = Y.pick(k, j, r);
+        y = ffma2s(pv[k], -zr.x, y);
+        yr[k] = ffma2s(pvn[k], zr.y, y);
+        ar2[k] = cnorm(yr[k]);
+      }
       static_for<0, RMAX>([&](auto pp) {
         constexpr int P = decltype(pp)::value;
         if (P < R) {
-          R2 y = Y.template get<P>(k, j);
-          if (upd) {
-            cmsub(y, zw[P], pv[k]);
+          const float2 zp = zw[P];
+          float2 q1 = make_float2(0.f, 0.f), q2 = make_float2(0.f, 0.f);
+          float den = 0.f;
+#pragma unroll
+          for (int k = 0; k < FT; ++k) {
+            const int j = tid + k * NT;
+            float2 y = Y.template get<P>(k, j);
+            y = ffma2s(pv[k], -zp.x, y);
+            y = ffma2s(pvn[k], zp.y, y);
             Y.template set<P>(k, j, y);
+            const float w = invl[p.woff[P] + j];
+            const float2 sw = fmul2s(yr[k], w);
+            q1 = ffma2s(y, sw.x, q1);
+            q2 = ffma2s(y, sw.y, q2);
+            den = fmaf(ar2[k], w, den);
           }
-          const Real w = invl[p.woff[P] + j];
-          // numer_p += y_p conj(y_r) w ; denom_p += |y_r|^2 w
-          const Real tr = fma(y.x, yr.x, y.y * yr.y);
-          const Real ti = fma(y.y, yr.x, -y.x * yr.y);
-          acc[P] = fma(tr, w, acc[P]);
-          acc[RMAX + P] = fma(ti, w, acc[RMAX + P]);
-          acc[2 * RMAX + P] = fma(ar2, w, acc[2 * RMAX + P]);
+          acc[P] = q1.x + q2.y;
+          acc[RMAX + P] = q1.y - q2.x;
+          acc[2 * RMAX + P] = den;
         }
       });
-      pv[k] = yr;
+#pragma unroll
+      for (int k = 0; k < FT; ++k) pv[k] = yr[k];
+    } else {
+#pragma unroll
+      for (int k = 0; k < FT; ++k) {
+        const int j = tid + k * NT;
+        R2 yr = Y.pick(k, j, r);
+        cmsub(yr, zw[r], pv[k]);
+        const Real ar2 = cnorm(yr);
+        static_for<0, RMAX>([&](auto pp) {
+          constexpr int P = decltype(pp)::value;
+          if (P < R) {
+            R2 y = Y.template get<P>(k, j);
+            cmsub(y, zw[P], pv[k]);
+            Y.template set<P>(k, j, y);
+            const Real w = invl[p.woff[P] + j];
+            // numer_p += y_p conj(y_r) w ; denom_p += |y_r|^2 w
+            const Real tr = fma(y.x, yr.x, y.y * yr.y);
+            const Real ti = fma(y.y, yr.x, -y.x * yr.y);
+            acc[P] = fma(tr, w, acc[P]);
+            acc[RMAX + P] = fma(ti, w, acc[RMAX + P]);
+            acc[2 * RMAX + P] = fma(ar2, w, acc[2 * RMAX + P]);
+          }
+        });
+        pv[k] = yr;
+      }
     }
     warp_reduce_scatter(acc, lane);
     Real* rb = red + (size_t)((r & 1) * NW + warp) * VP;
@@ -467,6 +566,7 @@ __global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepParams p) {
     // every warp derives z redundantly (identical fixed-order sums)
     const Real* rs = red + (size_t)((r & 1) * NW) * VP;
     bool bad = false;
+    R2 z = czero<Real>();
     if (lane < R) {
       Real nre = Real(0), nim = Real(0), den = Real(0);
       for (int w = 0; w < NW; ++w) {
@@ -475,10 +575,8 @@ __global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepParams p) {
         den += rs[w * VP + 2 * RMAX + lane];
       }
       bad = !(den > Real(0)) || !isfinite(den);
-      R2 z;
       if (lane == r) {
         z.x = Real(1) - sqrt((Real)T / den);
-        z.y = Real(0);
       } else {
         z.x = nre / den;
         z.y = nim / den;
@@ -486,30 +584,39 @@ __global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepParams p) {
       zs[warp * RMAX + lane] = z;
     }
     const unsigned badm = __ballot_sync(kFull, bad);
-    __syncwarp();
     if (badm) {  // estimator.cpp:451-454
       if (tid == 0)
         record_err<Real>(p.err, mix, err_key(p.iteration, kPhSweep, gbin, r, __ffs(badm) - 1));
       return;
     }
-    if (warp == 0) {  // iss_apply: W -= z w_r (estimator.cpp:298-302)
-      for (int c = lane; c < D; c += 32) {
-        const R2 wr = Ws[c * R + r];
-        for (int q = 0; q < R; ++q) cmsub(Ws[c * R + q], zs[q], wr);
-      }
+    {
+      const Real one_minus = Real(1) - __shfl_sync(kFull, z.x, r);
+      dlog += log((double)one_minus);
+    }
+    __syncwarp();
+    // iss_apply, W -= z w_r (estimator.cpp:298-302), ping-pong buffers
+    const R2* Wo = Wb + (r & 1) * R * D;
+    R2* Wn = Wb + ((r + 1) & 1) * R * D;
+    for (int e = tid; e < R * D; e += NT) {
+      const int q = e % R, c = e / R;
+      R2 w = Wo[e];
+      cmsub(w, zw[q], Wo[c * R + r]);
+      Wn[e] = w;
     }
   }
   __syncthreads();
+  const R2* Wf = Wb + (R & 1) * R * D;
 
   // ---- epilogue: Y = W' x~ (estimator.cpp:607)
-  demix_tile<Real, RMAX, FT, RREG>(Y, xs, Ws, p, tid, NT);
+  demix_tile<Real, RMAX, FT, RREG, EXACT>(Y, xs, Wf, p, tid, NT, R, D);
   __syncthreads();  // xs is dead: reuse the region for |y|^2 of register rows and E
 
   // row powers (estimator.cpp:391-397) and |y|^2 export
   {
-    Real rp[((RMAX + 31) / 32) * 32];
+    constexpr int RP = ((RMAX + 31) / 32) * 32;
+    Real rp[RP];
 #pragma unroll
-    for (int i = 0; i < ((RMAX + 31) / 32) * 32; ++i) rp[i] = Real(0);
+    for (int i = 0; i < RP; ++i) rp[i] = Real(0);
     static_for<0, RMAX>([&](auto pp) {
       constexpr int P = decltype(pp)::value;
       if (P < R) {
@@ -522,7 +629,6 @@ __global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepParams p) {
         }
       }
     });
-    constexpr int RP = ((RMAX + 31) / 32) * 32;
     warp_reduce_scatter(rp, lane);
     Real* rb = red + (size_t)warp * VP;
 #pragma unroll
@@ -534,11 +640,14 @@ __global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepParams p) {
     for (int w = 0; w < NW; ++w) s += (double)red[(size_t)w * VP + tid];
     p.rowpow[tile * R + tid] = s;
   }
+  if (tid == 0) p.logdet[tile] = logdet + dlog;
   // delayed energies E_n(tau) = sum_{l<L_n, tau+l<T} |y_{row0+l}(tau+l)|^2
   Real* Eg = reinterpret_cast<Real*>(p.E);
   for (int n = 0; n < N; ++n) {
     const int r0 = p.row0[n], Ln = p.ntaps[n];
-    for (int tau = tid; tau < TP; tau += NT) {
+#pragma unroll
+    for (int k = 0; k < FT; ++k) {
+      const int tau = tid + k * NT;
       Real e = Real(0);
       for (int l = 0; l < Ln && tau + l < T; ++l) {
         const int row = r0 + l;
@@ -548,7 +657,7 @@ __global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepParams p) {
       if (tau < T) Eg[(((size_t)mix * N + n) * p.FL + bin) * T + tau] = e;
     }
   }
-  for (int i = tid; i < R * D; i += NT) Wg[i] = Ws[i];
+  for (int i = tid; i < R * D; i += NT) Wg[i] = Wf[i];
   __syncthreads();
 
   // ---- MU-B for this bin (estimator.cpp:313-346), 8 bases per pass
@@ -559,17 +668,34 @@ __global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepParams p) {
       Real a[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) a[i] = Real(0);
-      for (int tau = tid; tau < T; tau += NT) {
+      Real vv[FT][8];
+#pragma unroll
+      for (int k = 0; k < FT; ++k) {
+        const int tau = tid + k * NT;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) vv[k][q] = (tau < T && kb + q < k1) ? __ldg(Vg + (size_t)(kb + q) * T + tau) : Real(0);
+      }
+#pragma unroll
+      for (int k = 0; k < FT; ++k) {
+        const int tau = tid + k * NT;
         const Real ilv = il[tau];
         const Real an = Es[n * TP + tau] * (ilv * ilv);
-        const Real bn = ilv * (Real)min(Ln, T - tau);
+        const Real bn = (tau < T) ? ilv * (Real)min(Ln, T - tau) : Real(0);
+        if constexpr (std::is_same<Real, float>::value) {
+          const float2 ab = make_float2(an, bn);
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (kb + q < k1) {
-            const Real v = Vg[(size_t)(kb + q) * T + tau];
-            a[q] = fma(an, v, a[q]);
-            a[8 + q] = fma(bn, v, a[8 + q]);
+          for (int q = 0; q < 8; ++q) {
+            const float2 t = ffma2s(ab, vv[k][q], make_float2(a[q], a[8 + q]));
+            a[q] = t.x;
+            a[8 + q] = t.y;
           }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            a[q] = fma(an, vv[k][q], a[q]);
+            a[8 + q] = fma(bn, vv[k][q], a[8 + q]);
+          }
+        }
       }
       warp_reduce_scatter(a, lane);
       Real* rb = red + (size_t)warp * VP;
@@ -589,6 +715,22 @@ __global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepParams p) {
   }
 }
 
+// Exact log|det W| per bin by pivoted LU (estimator.cpp:41-53), one warp per
+// bin; run when the state is set from outside. -inf marks a zero pivot.
+template <typename Real>
+__global__ void __launch_bounds__(32) logdet_kernel(const void* W, double* logdet, int R, int nbins) {
+  using R2 = typename Cplx<Real>::T;
+  extern __shared__ __align__(16) unsigned char smem[];
+  R2* A = reinterpret_cast<R2*>(smem);
+  const size_t b = blockIdx.x;
+  if ((int)b >= nbins) return;
+  const R2* Wg = reinterpret_cast<const R2*>(W) + b * (size_t)R * R;
+  for (int i = threadIdx.x; i < R * R; i += 32) A[i] = Wg[i];
+  __syncwarp();
+  double out = 0.0;
+  const int st = warp_logdet<Real>(A, R, threadIdx.x & 31, out);
+  if (threadIdx.x == 0) logdet[b] = st == 4 ? -INFINITY : out;
+}
 // ---------------------------------------------------------------------------
 // MU-V (estimator.cpp:348-382): partial numerator/denominator over a chunk
 // of this rank's bins, for one source and a tile of frames. lambda' is
@@ -640,12 +782,23 @@ __global__ void __launch_bounds__(128) muv_partial_kernel(const MuvParams p) {
     const Real il = Real(1) / lam;
     const Real e = Eg[(size_t)i * p.T];
     const Real an = e * (il * il), bn = il * cnt;
+    if constexpr (std::is_same<Real, float>::value) {
+      const float2 ab = make_float2(an, bn);
 #pragma unroll
-    for (int k = 0; k < KMAX; ++k)
-      if (k < K) {
-        num[k] = fma(b[k], an, num[k]);
-        den[k] = fma(b[k], bn, den[k]);
-      }
+      for (int k = 0; k < KMAX; ++k)
+        if (k < K) {
+          const float2 t = ffma2s(ab, b[k], make_float2(num[k], den[k]));
+          num[k] = t.x;
+          den[k] = t.y;
+        }
+    } else {
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k)
+        if (k < K) {
+          num[k] = fma(b[k], an, num[k]);
+          den[k] = fma(b[k], bn, den[k]);
+        }
+    }
   }
   Real* out = reinterpret_cast<Real*>(p.part) + (((size_t)chunk * p.nmix + mix) * 2 * p.SK + k0) * p.T + tau;
 #pragma unroll

@@ -1,0 +1,26 @@
+// Registry: concatenates the exact and guarded variant lists per precision.
+#include "ctf_sweep_variants.h"
+namespace ctf {
+std::vector<SweepVariant> sweep_variants_f32_exact();
+std::vector<SweepVariant> sweep_variants_f32_guard();
+std::vector<SweepVariant> sweep_variants_f64_exact();
+std::vector<SweepVariant> sweep_variants_f64_guard();
+const std::vector<SweepVariant>& sweep_variants_f32() {
+  static const std::vector<SweepVariant> v = [] {
+    auto a = sweep_variants_f32_exact();
+    auto b = sweep_variants_f32_guard();
+    a.insert(a.end(), b.begin(), b.end());
+    return a;
+  }();
+  return v;
+}
+const std::vector<SweepVariant>& sweep_variants_f64() {
+  static const std::vector<SweepVariant> v = [] {
+    auto a = sweep_variants_f64_exact();
+    auto b = sweep_variants_f64_guard();
+    a.insert(a.end(), b.begin(), b.end());
+    return a;
+  }();
+  return v;
+}
+}  // namespace ctf
