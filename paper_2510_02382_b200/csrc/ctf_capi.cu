@@ -226,9 +226,8 @@ void plan_sweep(ctf_ctx* c) {
     if (force[0] && (v.rmax != force[0] || v.ft != force[1] || v.rreg != force[2] || v.maxt != force[3] ||
                      (force[4] >= 0 && v.exact != force[4])))
       continue;
-    int nt = (c->T + v.ft - 1) / v.ft;
-    nt = std::max(32, (nt + 31) / 32 * 32);
-    if (nt > v.maxt) continue;
+    const int nt = v.maxt;  // exact CTA size of the variant
+    if (nt * v.ft < c->T) continue;
     const int TP = nt * v.ft;
     const int NW = nt / 32;
     const int VP = ((3 * v.rmax + 31) / 32) * 32;
@@ -253,9 +252,10 @@ void plan_sweep(ctf_ctx* c) {
     cand.off_b = (int)take((size_t)c->SK * rs);
     cand.off_d = (int)take((size_t)NW * 4 * sizeof(double));
     if (off > (size_t)max_smem) continue;
-    // variants are listed in preference order per rmax: exact beats guarded,
-    // then the table order (measured on B200)
-    const bool better = !found || v.rmax < best.rmax || (v.rmax == best.rmax && v.exact > best.exact);
+    // smallest RMAX, exact before guarded, then the smallest frame padding
+    // (fewest threads), then table order (measured on B200)
+    const bool better = !found || v.rmax < best.rmax ||
+                        (v.rmax == best.rmax && (v.exact > best.exact || (v.exact == best.exact && nt < best_nt)));
     if (better) {
       found = true;
       best = v;
@@ -603,11 +603,10 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host) {
   if (kmax > 32) throw CtfError(CTF_ERR_UNSUPPORTED, "more than 32 bases per source");
   c->kmax = kmax <= 8 ? 8 : kmax <= 16 ? 16 : kmax <= 24 ? 24 : 32;
   plan_sweep(c);
-  // MU-V bin chunks: enough CTAs to fill the GPU, deterministic fixed-order combine
-  const int ctas_per_chunk = ((c->T + 127) / 128) * c->B * c->N;
-  int nchunk = std::max(1, std::min(c->FL, (4 * 148 + ctas_per_chunk - 1) / ctas_per_chunk));
-  c->chunk_bins = (c->FL + nchunk - 1) / nchunk;
-  c->chunk_bins = std::min(c->chunk_bins, (int)(32768 / ((size_t)c->kmax * c->real_size)));  // <= 32 KiB smem
+  // MU-V bin chunks of a fixed size (64 bins): the summation order must not
+  // depend on the batch size, so a mixture gives bit-identical results alone
+  // or in any batch; chunk partials are combined in fixed order.
+  c->chunk_bins = 64;
   c->nchunk = (c->FL + c->chunk_bins - 1) / c->chunk_bins;
 
   const size_t rs = c->real_size, cs = 2 * rs;
@@ -615,7 +614,8 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host) {
   c->x.alloc(xcount * cs);
   c->W.alloc((size_t)c->B * plane_stride(c) * cs);
   c->Bf.alloc((size_t)c->B * c->FL * c->SK * rs);
-  c->V.alloc((size_t)c->B * c->SK * c->T * rs);
+  c->V.alloc(((size_t)c->B * c->SK * c->T + 4096) * rs);  // zero tail: the sweep reads V up to frame TP
+  CK(cudaMemsetAsync(c->V.p, 0, c->V.n, c->stream));
   c->E.alloc((size_t)c->B * c->N * c->FL * c->T * rs);
   c->part.alloc((size_t)c->nchunk * c->B * 2 * c->SK * c->T * rs);
   c->packed.alloc(c->world > 1 ? (size_t)c->B * 2 * c->SK * c->T * rs : 16);

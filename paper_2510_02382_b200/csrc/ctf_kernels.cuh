@@ -314,8 +314,15 @@ __device__ __forceinline__ void record_err(unsigned long long* err, int mix, uns
 // state is set from outside (logdet_kernel below); its zero-pivot / 1e-300
 // outcomes are carried as -inf / the value and raised at the next
 // objective, as the reference raises them in objective_from_parts.
-template <typename Real, int RMAX, int FT, int RREG, int MAXT, bool EXACT>
-__global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepParams p) {
+// NT: the exact CTA size (frame j = tid + k*NT folds into load immediates);
+// the launch bound targets 128 registers/thread (2 x 256 or 4 x 128 CTAs per SM).
+// fp64 tiles are shared-memory bound to one CTA per SM, so fp64 variants
+// get the full register file instead.
+template <typename Real> constexpr int sweep_min_blocks(int nt) {
+  return std::is_same<Real, float>::value ? (nt <= 512 ? 512 / nt : 1) : (nt <= 256 ? 256 / nt : 1);
+}
+template <typename Real, int RMAX, int FT, int RREG, int NT, bool EXACT>
+__global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(const SweepParams p) {
   using R2 = typename Cplx<Real>::T;
   constexpr int RS = RMAX - RREG;
   constexpr int NV = 3 * RMAX;
@@ -324,7 +331,7 @@ __global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepParams p) {
   static_assert(RMAX <= 32, "one lane per steering coefficient");
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int NT = blockDim.x, NW = NT >> 5;
+  constexpr int NW = NT >> 5;
   const int bin = blockIdx.x, mix = blockIdx.y;
   const int gbin = p.bin_lo + bin;
   // EXACT: R == D == RMAX is a compile-time constant (no row guards).
@@ -483,7 +490,7 @@ __global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepParams p) {
   for (int k = 0; k < FT; ++k) pv[k] = czero<Real>();
   if (lane < RMAX) zs[warp * RMAX + lane] = czero<Real>();  // pass 0 applies a zero update
   __syncwarp();
-  double dlog = 0.0;  // sum_r log(1 - z_r), lane 0 of every warp
+  double dprod = 1.0;  // prod_r (1 - z_r): det W' = det W prod_r (1 - z_r)
   for (int r = 0; r < R; ++r) {
     Real acc[VP];
 #pragma unroll
@@ -589,10 +596,7 @@ __global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepParams p) {
         record_err<Real>(p.err, mix, err_key(p.iteration, kPhSweep, gbin, r, __ffs(badm) - 1));
       return;
     }
-    {
-      const Real one_minus = Real(1) - __shfl_sync(kFull, z.x, r);
-      dlog += log((double)one_minus);
-    }
+    dprod *= (double)(Real(1) - __shfl_sync(kFull, z.x, r));
     __syncwarp();
     // iss_apply, W -= z w_r (estimator.cpp:298-302), ping-pong buffers
     const R2* Wo = Wb + (r & 1) * R * D;
@@ -604,12 +608,33 @@ __global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepParams p) {
       Wn[e] = w;
     }
   }
-  __syncthreads();
-  const R2* Wf = Wb + (R & 1) * R * D;
-
-  // ---- epilogue: Y = W' x~ (estimator.cpp:607)
-  demix_tile<Real, RMAX, FT, RREG, EXACT>(Y, xs, Wf, p, tid, NT, R, D);
+  // ---- epilogue. The reference recomputes Y = W' x~ after the sweep
+  // (estimator.cpp:607); here the last step's update is applied to the
+  // running Y instead (same values up to rounding, one R x T pass instead of
+  // an R x D x T product).
+  {
+    const R2* zw = zs + warp * RMAX;
+#pragma unroll
+    for (int k = 0; k < FT; ++k) {
+      const int j = tid + k * NT;
+      static_for<0, RMAX>([&](auto pp) {
+        constexpr int P = decltype(pp)::value;
+        if (P < R) {
+          R2 y = Y.template get<P>(k, j);
+          if constexpr (std::is_same<Real, float>::value) {
+            const float2 zp = zw[P];
+            y = ffma2s(pv[k], -zp.x, y);
+            y = ffma2s(make_float2(pv[k].y, -pv[k].x), zp.y, y);
+          } else {
+            cmsub(y, zw[P], pv[k]);
+          }
+          Y.template set<P>(k, j, y);
+        }
+      });
+    }
+  }
   __syncthreads();  // xs is dead: reuse the region for |y|^2 of register rows and E
+  const R2* Wf = Wb + (R & 1) * R * D;
 
   // row powers (estimator.cpp:391-397) and |y|^2 export
   {
@@ -640,7 +665,7 @@ __global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepParams p) {
     for (int w = 0; w < NW; ++w) s += (double)red[(size_t)w * VP + tid];
     p.rowpow[tile * R + tid] = s;
   }
-  if (tid == 0) p.logdet[tile] = logdet + dlog;
+  if (tid == 0) p.logdet[tile] = logdet + log(dprod);
   // delayed energies E_n(tau) = sum_{l<L_n, tau+l<T} |y_{row0+l}(tau+l)|^2
   Real* Eg = reinterpret_cast<Real*>(p.E);
   for (int n = 0; n < N; ++n) {
@@ -668,13 +693,16 @@ __global__ void __launch_bounds__(MAXT, 1) sweep_kernel(const SweepParams p) {
       Real a[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) a[i] = Real(0);
+      // V rows past k1 are clamped to a valid row (their sums are never
+      // written); frames past T read V's zero padding and meet an = bn = 0.
+      const Real* vrow[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) vrow[q] = Vg + (size_t)min(kb + q, k1 - 1) * T + tid;
       Real vv[FT][8];
 #pragma unroll
-      for (int k = 0; k < FT; ++k) {
-        const int tau = tid + k * NT;
+      for (int k = 0; k < FT; ++k)
 #pragma unroll
-        for (int q = 0; q < 8; ++q) vv[k][q] = (tau < T && kb + q < k1) ? __ldg(Vg + (size_t)(kb + q) * T + tau) : Real(0);
-      }
+        for (int q = 0; q < 8; ++q) vv[k][q] = __ldg(vrow[q] + k * NT);
 #pragma unroll
       for (int k = 0; k < FT; ++k) {
         const int tau = tid + k * NT;
@@ -772,33 +800,48 @@ __global__ void __launch_bounds__(128) muv_partial_kernel(const MuvParams p) {
     den[k] = Real(0);
   }
   const Real* Eg = reinterpret_cast<const Real*>(p.E) + (((size_t)mix * p.N + n) * p.FL) * p.T + tau;
-  for (int i = i0; i < i1; ++i) {
-    const Real* b = Bsh + (i - i0) * K;
-    Real lam = Real(0);
+  // E loads for the next UNR bins are issued before the current UNR bins
+  // are processed (latency hiding).
+  constexpr int UNR = 8;
+  Real ecur[UNR], enext[UNR];
 #pragma unroll
-    for (int k = 0; k < KMAX; ++k)
-      if (k < K) lam = fma(b[k], v[k], lam);
-    lam = fmax(lam, floor_abs);
-    const Real il = Real(1) / lam;
-    const Real e = Eg[(size_t)i * p.T];
-    const Real an = e * (il * il), bn = il * cnt;
-    if constexpr (std::is_same<Real, float>::value) {
-      const float2 ab = make_float2(an, bn);
+  for (int u = 0; u < UNR; ++u) ecur[u] = (i0 + u < i1) ? Eg[(size_t)(i0 + u) * p.T] : Real(0);
+  for (int ib = i0; ib < i1; ib += UNR) {
 #pragma unroll
-      for (int k = 0; k < KMAX; ++k)
-        if (k < K) {
-          const float2 t = ffma2s(ab, b[k], make_float2(num[k], den[k]));
-          num[k] = t.x;
-          den[k] = t.y;
+    for (int u = 0; u < UNR; ++u) enext[u] = (ib + UNR + u < i1) ? Eg[(size_t)(ib + UNR + u) * p.T] : Real(0);
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int i = ib + u;
+      if (i < i1) {
+        const Real* b = Bsh + (i - i0) * K;
+        Real lam = Real(0);
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k)
+          if (k < K) lam = fma(b[k], v[k], lam);
+        lam = fmax(lam, floor_abs);
+        const Real il = Real(1) / lam;
+        const Real an = ecur[u] * (il * il), bn = il * cnt;
+        if constexpr (std::is_same<Real, float>::value) {
+          const float2 ab = make_float2(an, bn);
+#pragma unroll
+          for (int k = 0; k < KMAX; ++k)
+            if (k < K) {
+              const float2 t = ffma2s(ab, b[k], make_float2(num[k], den[k]));
+              num[k] = t.x;
+              den[k] = t.y;
+            }
+        } else {
+#pragma unroll
+          for (int k = 0; k < KMAX; ++k)
+            if (k < K) {
+              num[k] = fma(b[k], an, num[k]);
+              den[k] = fma(b[k], bn, den[k]);
+            }
         }
-    } else {
-#pragma unroll
-      for (int k = 0; k < KMAX; ++k)
-        if (k < K) {
-          num[k] = fma(b[k], an, num[k]);
-          den[k] = fma(b[k], bn, den[k]);
-        }
+      }
     }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) ecur[u] = enext[u];
   }
   Real* out = reinterpret_cast<Real*>(p.part) + (((size_t)chunk * p.nmix + mix) * 2 * p.SK + k0) * p.T + tau;
 #pragma unroll
@@ -863,14 +906,18 @@ __global__ void __launch_bounds__(256) reduce_apply_kernel(const ApplyParams p) 
   // row powers -> mu (estimator.cpp:391-397) and the objective sum
   double* pd = p.packed_d + (size_t)mix * (p.R + 1);
   if (p.mode != 1) {
-    for (int r = threadIdx.x; r <= p.R; r += blockDim.x) {
+    // R+1 sums over this rank's bins: each warp takes quantities, lanes take
+    // strided bins, then a fixed butterfly (deterministic order).
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int r = warp; r <= p.R; r += nw) {
       double s = 0.0;
       if (r < p.R) {
-        for (int i = 0; i < p.FL; ++i) s += p.rowpow[((size_t)mix * p.FL + i) * p.R + r];
+        for (int i = lane; i < p.FL; i += 32) s += p.rowpow[((size_t)mix * p.FL + i) * p.R + r];
       } else if (p.obj_slot >= 0) {
-        for (int i = 0; i < p.FL; ++i) s += p.objbin[(size_t)mix * p.FL + i];
+        for (int i = lane; i < p.FL; i += 32) s += p.objbin[(size_t)mix * p.FL + i];
       }
-      pd[r] = s;
+      s = warp_sum(s);
+      if (lane == 0) pd[r] = s;
     }
     if (p.mode == 0) return;
     __syncthreads();
@@ -988,7 +1035,9 @@ __global__ void __launch_bounds__(256) image_kernel(const ImageParams p) {
         const int r = lane + 32 * q;
         if (r < R && r != c)
           for (int j = 0; j < R; ++j) {
-            if (j != c) cmsub(A[j * R + r], f[q], A[j * R + c]);
+            // columns < c are already eliminated in the pivot row (zero) and
+            // column c itself is never read again: update j > c only
+            if (j > c) cmsub(A[j * R + r], f[q], A[j * R + c]);
             cmsub(H[j * R + r], f[q], H[j * R + c]);
           }
       }
