@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""Benchmark of the ISS+NMF hot path of CTF-MNMF-ISS on B200.
+
+Metric (BASELINE.json): TF-bin*iter/s of the ISS+NMF loop (one TF-bin = one
+(mixture, frequency bin, frame)); roofline fractions reported alongside.
+
+Workload at N=1: BASELINE configs[1] — 64 mixtures, M=N=2, L=5 (stacked
+D=10), F=513, T=1000, K=10, 100 iterations (--dtype f32 by default; f64 via
+--dtype f64). Seeded synthetic mixtures from BASELINE's generator.
+
+  value : device-resident throughput — a "step" is one ISS+NMF iteration
+          (estimator.cpp:548-654) over the whole batch with x already in HBM;
+          K steps timed with CUDA events on the library's stream.
+  e2e   : the same metric through the public C-ABI call ctf_run() with HOST
+          buffers: per step the H2D of x (pinned), setup, 100 iterations and
+          the D2H of W/B/V/objective are all inside the timed region.
+
+Multi-GPU (torchrun): frequency sharding (contiguous bin ranges), one NCCL
+all-reduce per iteration inside the library; strong scaling of the same
+workload; times are the max over ranks.
+
+--impl reference times the CPU restatement of the reference (oracle/) on the
+host cores with all threads, one iteration of one mixture per step.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFGS = {  # BASELINE.json configs: B, F, T, M=N, L, K, rho, iterations
+    0: (1, 513, 500, 2, 2, 10, 0.6, 100),
+    1: (64, 513, 1000, 2, 5, 10, 0.6, 100),
+    2: (128, 1025, 2000, 3, 4, 20, 0.7, 100),
+    3: (256, 2049, 1000, 4, 8, 20, 0.8, 50),
+    4: (32, 1025, 4000, 6, 10, 16, 0.85, 50),
+}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def flops_per_tfbin(R, D, N, K):
+    """Algorithmic flops per TF-bin*iteration (SURVEY §8(d) convention:
+    complex MAC = 8, FMA = 2; logs/divisions not counted).
+    sweep kernel: ISS sweep 20R^2 + one demix 8RD + lambda and MU-B 6NK;
+    whole iteration adds MU-V 6NK (lambda' + numerator/denominator)."""
+    sweep = 20 * R * R + 8 * R * D + 6 * N * K
+    return sweep, sweep + 6 * N * K
+
+
+def bytes_per_tfbin(M, N, K, R, D, T, F, c):
+    """Algorithmic HBM bytes per TF-bin*iteration of the resident design
+    (SURVEY §8(d)): read x once, write+read energies E, read/write W, B, V
+    amortised."""
+    s = c // 2
+    return M * c + 2 * N * s + 2 * R * D * c / T + 2 * N * K * s / T + 2 * N * K * s / F
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            p = [v.strip() for v in l.split(",")]
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+            except (ValueError, IndexError):
+                continue
+            for name, v in zip(names, p[3:7]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+def peak_probe(device):
+    path = os.path.join(ROOT, "tools", "libctfpeak.so")
+    if not os.path.exists(path):
+        return None, None
+    lib = C.CDLL(path)
+    lib.ctf_peak_fp32_tflops.restype = C.c_double
+    lib.ctf_peak_fp64_tflops.restype = C.c_double
+    return lib.ctf_peak_fp32_tflops(device), lib.ctf_peak_fp64_tflops(device)
+
+
+def profile_traffic(prec):
+    """dram read+write bytes per TF-bin of the sweep kernel from the committed
+    ncu --set full capture (profiles/), scaled per launch by the caller."""
+    path = os.path.join(ROOT, "profiles", "sweep_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(prec)
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------
+def cpu_reference_arm(args, cfgn, steps, warmup, sample_note=True):
+    """The reference's algorithm on the host cores: the oracle restatement
+    (proj/src/estimator.cpp:548-654), one iteration of one mixture per step."""
+    from oracle import oracle as O
+    from paper_2510_02382_b200 import synth_mixtures
+    B, F, T, M, L, K, rho, iters = CFGS[cfgn]
+    N = M
+    threads = os.cpu_count() or 1
+    raw = synth_mixtures(1, F, T, M, N, L, K, rho, args.seed)[0]
+    x = O.stack_observation(raw, L)
+    cfg = O.config([L] * N, [K] * N, iterations=1, seed=args.seed, threads=threads)
+    floor = 1e-10 * O.mean_power(x)
+    Bf, V = O.random_factors(cfg, F, T)
+    R = M * L
+    W = np.zeros((F, R, R), complex)
+    W[:] = np.eye(R)
+    times = []
+    for s in range(warmup + steps):
+        t0 = time.perf_counter()
+        W, Bf, V, _ = O.step(cfg, x, floor, W, Bf, V)
+        dt = time.perf_counter() - t0
+        if s >= warmup:
+            times.append(dt)
+    sec = sum(times)
+    value = F * T * len(times) / sec
+    try:
+        model = [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")][0]
+    except (OSError, IndexError):
+        model = "unknown"
+    return {"value": value, "unit": "TF-bin*iter/s", "cores": threads, "kind": "port",
+            "sample": f"1 of {B} mixtures x {len(times)} iterations of cfg{cfgn} (F={F}, T={T}, D={R}), "
+                      f"oracle/ctf_oracle.cpp with parallel_for over bins on {threads} threads ({model}); "
+                      f"{sec:.2f} s", "seconds": sec}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cfg", type=int, default=1)
+    ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
+    ap.add_argument("--seed", type=int, default=20251002)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_env()
+    B, F, T, M, L, K, rho, iters = CFGS[args.cfg]
+    N, R = M, M * L
+    D = R
+    config = {"workload": f"BASELINE configs[{args.cfg}]: {B} mixtures, M=N={M}, L={L} (D={D}), F={F}, T={T}, "
+                          f"K={K}, {iters} iterations, tap variance {rho}^l",
+              "mixtures": B, "bins": F, "frames": T, "mics": M, "taps": L, "bases": K, "iterations": iters,
+              "parallelism": f"freq-shard x{world}" if world > 1 else "1 GPU",
+              "l2": "inputs larger than L2 (x alone is %.0f MB)" % (B * F * T * M * (8 if args.dtype == "f32" else 16) / 1e6)}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        ref = cpu_reference_arm(args, args.cfg, args.steps, args.warmup)
+        line = {"metric": "TF-bin*iter/s of the ISS+NMF loop", "value": ref["value"], "unit": "TF-bin*iter/s",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1e3 * ref["seconds"] / args.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE configs generator, seeded)",
+                "config": config, "impl": "reference",
+                "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": ref["value"], "unit": "TF-bin*iter/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2510_02382_b200 import Session, synth_mixtures
+    from paper_2510_02382_b200 import _lib as LB
+
+    device = local
+    torch.cuda.set_device(device)
+    if world > 1:
+        dist.init_process_group("gloo")
+    comm_id = None
+    if world > 1:
+        buf = (C.c_uint8 * 128)()
+        err = LB.CtfErr()
+        if rank == 0:
+            assert LB.load().ctf_comm_unique_id(buf, C.byref(err)) == 0, err.msg
+        t = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
+        dist.broadcast(t, 0)
+        comm_id = bytes(t.tolist())
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t[0])
+
+    prec = args.dtype
+    x = synth_mixtures(B, F, T, M, N, L, K, rho, args.seed, precision=prec)
+    s = Session(x, [L] * N, [K] * N, stack_taps=L, iterations=iters, precision=prec, seed=args.seed,
+                device=device, world_size=world, rank=rank, comm_id=comm_id)
+    desc = json.loads(s.describe())
+    stream = torch.cuda.ExternalStream(s.stream_ptr(), device=device)
+
+    # ---- device-resident loop: W warm-up iterations, then K timed iterations
+    s.iterate_async(max(args.warmup, 3))
+    torch.cuda.synchronize(device)
+    s.reset_timing()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(device) as clk:
+        torch.cuda.synchronize(device)
+        barrier()
+        ev0.record(stream)
+        s.iterate_async(args.steps)
+        ev1.record(stream)
+        ev1.synchronize()
+        torch.cuda.synchronize(device)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    timing = s.timing()  # per-kernel CUDA events on the library's stream
+    s.finalize()
+    ms = max_over_ranks(ms)
+    sweep_ms = max_over_ranks(timing.sweep_ms / max(1, timing.sweep_launches))
+    tfbins = B * F * T
+    value = tfbins * args.steps / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel (the fused sweep kernel)
+    fl_sweep, fl_iter = flops_per_tfbin(R, D, N, K)
+    p32, p64 = peak_probe(device) if rank == 0 else (None, None)
+    peak = p32 if prec == "f32" else p64
+    local_bins = s.bin_range[1] - s.bin_range[0]
+    units_per_launch = B * local_bins * T
+    achieved = fl_sweep * units_per_launch / (sweep_ms / 1e3) / 1e12
+    traffic_per_tfbin = profile_traffic(prec)
+    mp = measured_peaks()
+    hbm_peak = mp.get("hbm_gbs", 6650.0)
+    c = 8 if prec == "f32" else 16
+    bpt = bytes_per_tfbin(M, N, K, R, D, T, F, c)
+    roofline = {"bound": "fp32-cuda-core" if prec == "f32" else "fp64-cuda-core", "achieved": achieved,
+                "peak": peak, "unit": "TFLOP/s", "frac": (achieved / peak) if peak else None,
+                "traffic": traffic_per_tfbin * units_per_launch if traffic_per_tfbin else None,
+                "kernel": desc["sweep_kernel"], "kernel_ms": sweep_ms,
+                "flops_per_tfbin": fl_sweep, "units_per_launch": units_per_launch,
+                "peak_source": "in-run FFMA2/DFMA chain probe (tools/peak.cu); MEASURED_PEAKS.json has no CUDA-core peak",
+                "hbm": {"achieved": bpt * units_per_launch / (sweep_ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                        "frac": bpt * units_per_launch / (sweep_ms / 1e3) / 1e9 / hbm_peak,
+                        "bytes_per_tfbin": bpt, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"}}
+    gpu_launches = int(timing.launches)
+
+    # ---- end to end through the public C-ABI call with host buffers
+    s.close()
+    import ctypes
+    lib = LB.load()
+    xh = torch.from_numpy(x.view(np.float32 if prec == "f32" else np.float64)).pin_memory()
+    SK = N * K
+    outW = torch.empty(B * F * R * D * 2, dtype=torch.float64).pin_memory()
+    outB = torch.empty(B * F * SK, dtype=torch.float64).pin_memory()
+    outV = torch.empty(B * SK * T, dtype=torch.float64).pin_memory()
+    outO = torch.empty(B * iters, dtype=torch.float64).pin_memory()
+    from paper_2510_02382_b200.api import _problem
+    prob = _problem(B, F, T, M, L, [L] * N, [K] * N, iters, prec, prec, 1e-10, args.seed)
+    ctx = ctypes.c_void_p()
+    err = LB.CtfErr()
+    assert lib.ctf_open(device, ctypes.byref(ctx), ctypes.byref(err)) == 0, err.msg
+    if world > 1:
+        idb = (ctypes.c_uint8 * 128).from_buffer_copy(comm_id)
+        assert lib.ctf_comm_init(ctx, world, rank, idb, ctypes.byref(err)) == 0, err.msg
+    dp = lambda t: ctypes.cast(t.data_ptr(), ctypes.POINTER(ctypes.c_double))
+
+    def one_run():
+        rc = lib.ctf_run(ctx, ctypes.byref(prob), ctypes.c_void_p(xh.data_ptr()), dp(outW), dp(outB), dp(outV),
+                         dp(outO), ctypes.byref(err))
+        assert rc == 0, err.msg
+
+    one_run()  # warm-up
+    e2e_times = []
+    for _ in range(args.e2e_steps):
+        barrier()
+        t0 = time.perf_counter()
+        one_run()
+        e2e_times.append(max_over_ranks(time.perf_counter() - t0))
+    lib.ctf_close(ctx)
+    e2e_sec = statistics.median(e2e_times)
+    e2e_value = tfbins * iters / e2e_sec
+    lo, hi = s.bin_range
+    h2d = B * (hi - lo) * T * M * c + 2 * 8 * (B * (hi - lo) * SK + B * SK * T)  # x + initial B, V
+    d2h = 8 * (B * (hi - lo) * (R * D * 2 + SK) + B * SK * T + B * iters)
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_reference_arm(args, args.cfg, steps=8, warmup=1)
+            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        clocks = clk.summary()
+        line = {"metric": "TF-bin*iter/s of the ISS+NMF loop", "value": value, "unit": "TF-bin*iter/s",
+                "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": prec,
+                "data": "synthetic (BASELINE configs generator, seeded; no public dataset)", "config": config,
+                "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": {"value": e2e_value, "unit": "TF-bin*iter/s", "h2d_bytes_per_step": int(h2d),
+                        "d2h_bytes_per_step": int(d2h), "step": f"one ctf_run() of {iters} iterations",
+                        "seconds_per_step": e2e_sec},
+                "gpu_launches": gpu_launches, "clocks": clocks,
+                "kernels": {"sweep_ms_per_iteration": sweep_ms, "mu_ms_per_iteration": timing.mu_ms / args.steps,
+                            "variant": desc}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
