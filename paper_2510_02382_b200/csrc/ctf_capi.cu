@@ -206,6 +206,8 @@ void validate(const ctf_problem& p) {
 }
 
 // Chooses the sweep variant and lays out its shared memory.
+// CTF_SWEEP_KIND=0|1 restricts to frame-owner / row-per-warp kernels and
+// CTF_SWEEP_VARIANT="rmax,ft,rreg,nt[,exact]" pins one (profiling aids).
 void plan_sweep(ctf_ctx* c) {
   const auto& vars = c->prob.precision == CTF_F32 ? ctf::sweep_variants_f32() : ctf::sweep_variants_f64();
   int max_smem = 0;
@@ -213,60 +215,93 @@ void plan_sweep(ctf_ctx* c) {
   max_smem -= 1024;  // static shared memory of the kernel + reserve
   const size_t rs = c->real_size, cs = 2 * rs;
   bool found = false;
-  // CTF_SWEEP_VARIANT="rmax,ft,rreg,maxt" pins a variant (profiling aid)
   int force[5] = {0, 0, -1, 0, -1};
   if (const char* env = std::getenv("CTF_SWEEP_VARIANT"))
     std::sscanf(env, "%d,%d,%d,%d,%d", &force[0], &force[1], &force[2], &force[3], &force[4]);
+  int force_kind = -1;
+  if (const char* env = std::getenv("CTF_SWEEP_KIND")) force_kind = std::atoi(env);
   ctf::SweepVariant best{};
   size_t best_smem = 0;
-  int best_nt = 0;
+  int best_nt = 0, best_rank = 0;
+  const int lmax = std::max(1, *std::max_element(c->taps, c->taps + c->N));
+  const int loff = ((lmax + 3) / 4) * 4;
   for (const auto& v : vars) {
-    if (v.rmax < c->R) continue;
-    if (v.exact && v.rmax != c->R) continue;
+    if (force_kind >= 0 && v.kind != force_kind) continue;
     if (force[0] && (v.rmax != force[0] || v.ft != force[1] || v.rreg != force[2] || v.maxt != force[3] ||
                      (force[4] >= 0 && v.exact != force[4])))
       continue;
     const int nt = v.maxt;  // exact CTA size of the variant
-    if (nt * v.ft < c->T) continue;
-    const int TP = nt * v.ft;
     const int NW = nt / 32;
-    const int VP = ((3 * v.rmax + 31) / 32) * 32;
-    const int xoff = c->Ls - 1, xp = xoff + TP;
-    const int loff = ((std::max(1, *std::max_element(c->taps, c->taps + c->N)) + 3) / 4) * 4, lp = loff + TP;
+    int TP;
     size_t off = 0;
     auto take = [&](size_t bytes) {
       const size_t o = off;
       off = align16(off + bytes);
       return o;
     };
-    ctf::SweepParams& sp = c->sp;
-    ctf::SweepParams cand = sp;
-    cand.off_y = (int)take((size_t)(v.rmax - v.rreg) * TP * cs);
-    const size_t xbytes = std::max((size_t)c->Mx * xp * cs, align16((size_t)v.rreg * TP * rs) + (size_t)c->N * TP * rs);
-    cand.off_x = (int)take(xbytes);
-    cand.off_e = cand.off_x + (int)align16((size_t)v.rreg * TP * rs);
-    cand.off_l = (int)take((size_t)c->N * lp * rs);
-    cand.off_w = (int)take((size_t)2 * c->R * c->D * cs);
-    cand.off_red = (int)take((size_t)2 * NW * VP * rs);
-    cand.off_z = (int)take((size_t)NW * v.rmax * cs);
-    cand.off_b = (int)take((size_t)c->SK * rs);
-    cand.off_d = (int)take((size_t)NW * 4 * sizeof(double));
+    ctf::SweepParams cand = c->sp;
+    if (v.kind == 0) {
+      if (v.rmax < c->R || (v.exact && v.rmax != c->R)) continue;
+      if (v.lt > 0) {
+        bool equal = true;
+        for (int n = 0; n < c->N; ++n) equal = equal && c->taps[n] == v.lt;
+        if (!equal) continue;
+      }
+      if (nt * v.ft < c->T) continue;
+      TP = nt * v.ft;
+      const int VP = ((3 * v.rmax + 31) / 32) * 32;
+      const int xoff = c->Ls - 1, xp = xoff + TP;
+      cand.xoff = xoff;
+      cand.xp = xp;
+      cand.off_y = (int)take((size_t)(v.rmax - v.rreg) * TP * cs);
+      const size_t xbytes =
+          std::max((size_t)c->Mx * xp * cs, align16((size_t)v.rreg * TP * rs) + (size_t)c->N * TP * rs);
+      cand.off_x = (int)take(xbytes);
+      cand.off_e = cand.off_x + (int)align16((size_t)v.rreg * TP * rs);
+      cand.off_l = (int)take((size_t)c->N * (loff + TP) * rs);
+      cand.off_w = (int)take((size_t)2 * c->R * c->D * cs);
+      cand.off_red = (int)take((size_t)2 * NW * VP * rs);
+      cand.off_z = (int)take((size_t)NW * v.rmax * cs);
+      cand.off_b = (int)take((size_t)c->SK * rs);
+      cand.off_d = (int)take((size_t)NW * 4 * sizeof(double));
+    } else {
+      const int wpr = v.rreg;
+      if (v.rmax != c->R) continue;                 // one row per WPR warps
+      if (wpr > 1 && c->R > 15) continue;           // named barriers 1..15
+      if (c->Ls - 1 > v.ft) continue;               // stacked taps reach one chunk back
+      TP = 32 * wpr * v.ft;
+      if (TP < c->T) continue;
+      const int CH = v.ft + 2;
+      const size_t XP = (size_t)(TP / v.ft + 1) * CH;
+      cand.xoff = 0;
+      cand.xp = (int)XP;
+      cand.off_y = (int)take((size_t)2 * (TP / v.ft) * CH * cs);
+      cand.off_x = (int)take(std::max((size_t)c->Mx * XP * cs, (size_t)c->R * TP * rs));
+      cand.off_e = (int)take((size_t)c->N * TP * rs);
+      cand.off_l = (int)take((size_t)c->N * (loff + TP) * rs);
+      cand.off_w = (int)take((size_t)2 * c->R * c->D * cs);
+      cand.off_red = (int)take((size_t)2 * c->R * wpr * 4 * rs);
+      cand.off_z = (int)take(16);
+      cand.off_b = (int)take((size_t)c->SK * rs);
+      cand.off_d = (int)take((size_t)(NW * 4 + c->R) * sizeof(double));
+    }
     if (off > (size_t)max_smem) continue;
-    // smallest RMAX, exact before guarded, then the smallest frame padding
-    // (fewest threads), then table order (measured on B200)
-    const bool better = !found || v.rmax < best.rmax ||
-                        (v.rmax == best.rmax && (v.exact > best.exact || (v.exact == best.exact && nt < best_nt)));
+    // preference: frame-owner kernels (measured faster than row-per-warp on
+    // B200 for every shape so far), then
+    // the smallest RMAX, exact before guarded, then the least frame padding
+    // (fewest threads), then table order
+    const int rank = (v.kind == 1 ? 1000 : 0) + v.rmax * 4 + (v.exact ? 0 : 2) + (v.lt > 0 ? 0 : 1);
+    const bool better = !found || rank < best_rank || (rank == best_rank && nt < best_nt);
     if (better) {
       found = true;
       best = v;
+      best_rank = rank;
       best_smem = off;
       best_nt = nt;
-      cand.xoff = xoff;
-      cand.xp = xp;
       cand.loff = loff;
-      cand.lp = lp;
+      cand.lp = loff + TP;
       c->TP = TP;
-      sp = cand;
+      c->sp = cand;
     }
   }
   if (!found)
@@ -294,7 +329,7 @@ void plan_sweep(ctf_ctx* c) {
     for (int l = 0; l < c->taps[n]; ++l, ++r) sp.woff[r] = n * sp.lp + sp.loff - l;
   }
   for (int n = 0; n <= c->N; ++n) sp.koff[n] = c->koff[n];
-  for (int ch = 0; ch < c->D; ++ch) {
+  for (int ch = 0; ch < c->D && ch < ctf::kMaxRows; ++ch) {
     const int m = ch / c->Ls, l = ch - m * c->Ls;
     sp.xcol[ch] = m * sp.xp + sp.xoff - l;
   }
@@ -410,8 +445,12 @@ void launch_muv(ctf_ctx* c) {
   for (int n = 0; n <= c->N; ++n) mp.koff[n] = c->koff[n];
   for (int n = 0; n < c->N; ++n) mp.ntaps[n] = c->taps[n];
   dim3 grid((c->T + 127) / 128, c->B * c->N, c->nchunk);
-  const size_t smem = (size_t)c->chunk_bins * c->kmax * sizeof(Real);
+  const size_t smem = (size_t)((c->chunk_bins + 7) / 8 * 8) * c->kmax * sizeof(Real);
   switch (c->kmax) {
+    case 4: ctf::muv_partial_kernel<Real, 4><<<grid, 128, smem, c->stream>>>(mp); break;
+    case 10: ctf::muv_partial_kernel<Real, 10><<<grid, 128, smem, c->stream>>>(mp); break;
+    case 12: ctf::muv_partial_kernel<Real, 12><<<grid, 128, smem, c->stream>>>(mp); break;
+    case 20: ctf::muv_partial_kernel<Real, 20><<<grid, 128, smem, c->stream>>>(mp); break;
     case 8: ctf::muv_partial_kernel<Real, 8><<<grid, 128, smem, c->stream>>>(mp); break;
     case 16: ctf::muv_partial_kernel<Real, 16><<<grid, 128, smem, c->stream>>>(mp); break;
     case 24: ctf::muv_partial_kernel<Real, 24><<<grid, 128, smem, c->stream>>>(mp); break;
@@ -601,7 +640,7 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host) {
   c->koff[c->N] = k0;
   c->SK = k0;
   if (kmax > 32) throw CtfError(CTF_ERR_UNSUPPORTED, "more than 32 bases per source");
-  c->kmax = kmax <= 8 ? 8 : kmax <= 16 ? 16 : kmax <= 24 ? 24 : 32;
+  c->kmax = kmax <= 4 ? 4 : kmax <= 8 ? 8 : kmax <= 10 ? 10 : kmax <= 12 ? 12 : kmax <= 16 ? 16 : kmax <= 20 ? 20 : kmax <= 24 ? 24 : 32;
   plan_sweep(c);
   // MU-V bin chunks of a fixed size (64 bins): the summation order must not
   // depend on the batch size, so a mixture gives bit-identical results alone
@@ -883,9 +922,10 @@ int ctf_iterations_done(ctf_ctx* c) { return c ? c->done : 0; }
 int ctf_describe(ctf_ctx* c, char* buf, int len) {
   if (!c || !buf || len <= 0) return CTF_ERR_CONFIG;
   std::snprintf(buf, (size_t)len,
-                "{\"sweep_kernel\": \"sweep_kernel<%s,RMAX=%d,FT=%d,RREG=%d,MAXT=%d,EXACT=%d>\", \"threads\": %d, "
+                "{\"sweep_kernel\": \"%s<%s,RMAX=%d,FT=%d,%s=%d,NT=%d,EXACT=%d>\", \"threads\": %d, "
                 "\"smem_bytes\": %zu, \"grid\": [%d, %d], \"muv_chunks\": %d, \"bins\": [%d, %d]}",
-                c->real_size == 4 ? "f32" : "f64", c->sv.rmax, c->sv.ft, c->sv.rreg, c->sv.maxt, c->sv.exact, c->NT,
+                c->sv.kind ? "rowwarp_kernel" : "sweep_kernel", c->real_size == 4 ? "f32" : "f64", c->sv.rmax, c->sv.ft,
+                c->sv.kind ? "WPR" : "RREG", c->sv.rreg, c->sv.maxt, c->sv.exact, c->NT,
                 c->sweep_smem, c->FL, c->B, c->nchunk, c->lo, c->hi);
   return CTF_OK;
 }

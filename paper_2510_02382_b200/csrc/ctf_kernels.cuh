@@ -321,7 +321,10 @@ __device__ __forceinline__ void record_err(unsigned long long* err, int mix, uns
 template <typename Real> constexpr int sweep_min_blocks(int nt) {
   return std::is_same<Real, float>::value ? (nt <= 512 ? 512 / nt : 1) : (nt <= 256 ? 256 / nt : 1);
 }
-template <typename Real, int RMAX, int FT, int RREG, int NT, bool EXACT>
+// LT > 0 (EXACT only): every source has LT taps, so row P is (P / LT, P % LT)
+// at compile time and the ISS weights are addressed from one base pointer
+// per source with immediate offsets.
+template <typename Real, int RMAX, int FT, int RREG, int NT, bool EXACT, int LT = 0>
 __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(const SweepParams p) {
   using R2 = typename Cplx<Real>::T;
   constexpr int RS = RMAX - RREG;
@@ -446,8 +449,9 @@ __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(c
   if (p.has_prev) {
     // objective of the previous iteration (estimator.cpp:55-77) from
     // Y = W_resc x~, the log term above and -2T log|det W_resc|.
-    double quad = 0.0;
-    bool fin = true;
+    // per-thread sums in Real (<= 4*RMAX terms); a non-finite estimate makes
+    // sy (and quad) non-finite, which is the finite check of :497-499
+    Real qf = Real(0), sy = Real(0);
     static_for<0, RMAX>([&](auto pp) {
       constexpr int P = decltype(pp)::value;
       if (P < R) {
@@ -455,12 +459,13 @@ __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(c
         for (int k = 0; k < FT; ++k) {
           const int j = tid + k * NT;
           const R2 y = Y.template get<P>(k, j);
-          fin = fin && cfinite(y);
-          quad += (double)cnorm(y) * (double)invl[p.woff[P] + j];
+          sy += y.x + y.y;
+          qf = fma(cnorm(y), invl[p.woff[P] + j], qf);
         }
       }
     });
-    if (!fin) s_bad = 1;
+    if (!isfinite(sy) || !isfinite(qf)) s_bad = 1;
+    double quad = (double)qf;
     double v2[2] = {logsum, quad};
     block_sum_d<2>(v2, dred, lane, warp, NW);  // contains __syncthreads: s_bad visible after
     if (s_bad) {  // estimator.cpp:497-499
@@ -485,6 +490,16 @@ __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(c
   // ---- ISS sweep (estimator.cpp:556-579): step r computes z from the
   // current Y, then Y -= z y_r and W -= z w_r. The pass of step r applies
   // step r-1's update and accumulates step r's sums in one sweep over Y.
+  static_assert(LT == 0 || (EXACT && RMAX % LT == 0), "LT variants need an exact row count");
+  constexpr int NSRC = LT > 0 ? RMAX / LT : 1;
+  const Real* wsrc[NSRC];  // LT > 0: 1/lambda_n at this thread's frame 0
+#pragma unroll
+  for (int n = 0; n < NSRC; ++n) wsrc[n] = invl + n * p.lp + p.loff + tid;
+  auto weight = [&](auto pp, int k, int j) -> Real {
+    constexpr int P = decltype(pp)::value;
+    if constexpr (LT > 0) return wsrc[P / LT][k * NT - (P % LT)];
+    else return invl[p.woff[P] + j];
+  };
   R2 pv[FT];
 #pragma unroll
   for (int k = 0; k < FT; ++k) pv[k] = czero<Real>();
@@ -527,7 +542,7 @@ __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(c
             y = ffma2s(pv[k], -zp.x, y);
             y = ffma2s(pvn[k], zp.y, y);
             Y.template set<P>(k, j, y);
-            const float w = invl[p.woff[P] + j];
+            const float w = weight(pp, k, j);
             const float2 sw = fmul2s(yr[k], w);
             q1 = ffma2s(y, sw.x, q1);
             q2 = ffma2s(y, sw.y, q2);
@@ -553,7 +568,7 @@ __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(c
             R2 y = Y.template get<P>(k, j);
             cmsub(y, zw[P], pv[k]);
             Y.template set<P>(k, j, y);
-            const Real w = invl[p.woff[P] + j];
+            const Real w = weight(pp, k, j);
             // numer_p += y_p conj(y_r) w ; denom_p += |y_r|^2 w
             const Real tr = fma(y.x, yr.x, y.y * yr.y);
             const Real ti = fma(y.y, yr.x, -y.x * yr.y);
@@ -574,13 +589,27 @@ __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(c
     const Real* rs = red + (size_t)((r & 1) * NW) * VP;
     bool bad = false;
     R2 z = czero<Real>();
-    if (lane < R) {
-      Real nre = Real(0), nim = Real(0), den = Real(0);
+    Real nre = Real(0), nim = Real(0), den = Real(0);
+    if constexpr (EXACT && 3 * RMAX <= 32) {
+      // lane (q, p) = (lane / RMAX, lane % RMAX) sums quantity q of row p over
+      // the warps (fixed order), then row p's lane gathers its three sums
+      Real acc_q = Real(0);
+      if (lane < 3 * RMAX) {
+        const int q = lane / RMAX, pr = lane - q * RMAX;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) acc_q += rs[w * VP + q * RMAX + pr];
+      }
+      nre = __shfl_sync(kFull, acc_q, lane < RMAX ? lane : 0);
+      nim = __shfl_sync(kFull, acc_q, lane < RMAX ? RMAX + lane : 0);
+      den = __shfl_sync(kFull, acc_q, lane < RMAX ? 2 * RMAX + lane : 0);
+    } else if (lane < R) {
       for (int w = 0; w < NW; ++w) {
         nre += rs[w * VP + lane];
         nim += rs[w * VP + RMAX + lane];
         den += rs[w * VP + 2 * RMAX + lane];
       }
+    }
+    if (lane < R) {
       bad = !(den > Real(0)) || !isfinite(den);
       if (lane == r) {
         z.x = Real(1) - sqrt((Real)T / den);
@@ -685,43 +714,42 @@ __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(c
   for (int i = tid; i < R * D; i += NT) Wg[i] = Wf[i];
   __syncthreads();
 
-  // ---- MU-B for this bin (estimator.cpp:313-346), 8 bases per pass
+  // ---- MU-B for this bin (estimator.cpp:313-346), 16 bases per pass:
+  // a[q] numerator, a[16 + q] denominator of base kb + q
   for (int n = 0; n < N; ++n) {
     const int k0 = p.koff[n], k1 = p.koff[n + 1], Ln = p.ntaps[n];
     const Real* il = invl + n * p.lp + p.loff;
-    for (int kb = k0; kb < k1; kb += 8) {
+    for (int kb = k0; kb < k1; kb += 16) {
       Real a[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) a[i] = Real(0);
       // V rows past k1 are clamped to a valid row (their sums are never
       // written); frames past T read V's zero padding and meet an = bn = 0.
-      const Real* vrow[8];
+      const Real* vrow[16];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) vrow[q] = Vg + (size_t)min(kb + q, k1 - 1) * T + tid;
-      Real vv[FT][8];
-#pragma unroll
-      for (int k = 0; k < FT; ++k)
-#pragma unroll
-        for (int q = 0; q < 8; ++q) vv[k][q] = __ldg(vrow[q] + k * NT);
+      for (int q = 0; q < 16; ++q) vrow[q] = Vg + (size_t)min(kb + q, k1 - 1) * T + tid;
 #pragma unroll
       for (int k = 0; k < FT; ++k) {
         const int tau = tid + k * NT;
         const Real ilv = il[tau];
         const Real an = Es[n * TP + tau] * (ilv * ilv);
         const Real bn = (tau < T) ? ilv * (Real)min(Ln, T - tau) : Real(0);
+        Real vv[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) vv[q] = __ldg(vrow[q] + k * NT);
         if constexpr (std::is_same<Real, float>::value) {
           const float2 ab = make_float2(an, bn);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const float2 t = ffma2s(ab, vv[k][q], make_float2(a[q], a[8 + q]));
+          for (int q = 0; q < 16; ++q) {
+            const float2 t = ffma2s(ab, vv[q], make_float2(a[q], a[16 + q]));
             a[q] = t.x;
-            a[8 + q] = t.y;
+            a[16 + q] = t.y;
           }
         } else {
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            a[q] = fma(an, vv[k][q], a[q]);
-            a[8 + q] = fma(bn, vv[k][q], a[8 + q]);
+          for (int q = 0; q < 16; ++q) {
+            a[q] = fma(an, vv[q], a[q]);
+            a[16 + q] = fma(bn, vv[q], a[16 + q]);
           }
         }
       }
@@ -730,11 +758,11 @@ __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(c
       __syncthreads();  // previous pass's reads of red are done
       rb[lane] = a[0];
       __syncthreads();
-      if (tid < 8 && kb + tid < k1) {
+      if (tid < 16 && kb + tid < k1) {
         Real num = Real(0), den = Real(0);
         for (int w = 0; w < NW; ++w) {
           num += red[(size_t)w * VP + tid];
-          den += red[(size_t)w * VP + 8 + tid];
+          den += red[(size_t)w * VP + 16 + tid];
         }
         const Real b = Bs[kb + tid];
         Bg[kb + tid] = fmax(b * sqrt(num / den), floor_abs);
@@ -773,19 +801,25 @@ struct MuvParams {
   int koff[kMaxSources + 1], ntaps[kMaxSources];
 };
 
+// Bins are processed in groups of 8 with no per-bin guards (the B chunk is
+// zero-padded to whole groups; a padded bin has b = 0 and E = 0, so it adds
+// exactly 0), which lets the lambda' FMA chains of different bins overlap;
+// fp32 computes lambda' for two bins per FFMA2.
 template <typename Real, int KMAX>
 __global__ void __launch_bounds__(128) muv_partial_kernel(const MuvParams p) {
+  constexpr int G = 8;
   const int tau = blockIdx.x * blockDim.x + threadIdx.x;
   const int mix = blockIdx.y / p.N, n = blockIdx.y - mix * p.N;
   const int chunk = blockIdx.z;
   const int i0 = chunk * p.chunk_bins, i1 = min(p.FL, i0 + p.chunk_bins);
+  const int nb = i1 - i0, nbp = (nb + G - 1) / G * G;
   const int k0 = p.koff[n], K = p.koff[n + 1] - k0;
   extern __shared__ __align__(16) unsigned char smem[];
-  Real* Bsh = reinterpret_cast<Real*>(smem);  // chunk_bins x K
+  Real* Bsh = reinterpret_cast<Real*>(smem);  // [k][bin] (bins padded to nbp)
   const Real* Bg = reinterpret_cast<const Real*>(p.Bf) + (size_t)mix * p.FL * p.SK;
-  for (int e = threadIdx.x; e < (i1 - i0) * K; e += blockDim.x) {
-    const int i = e / K, k = e - i * K;
-    Bsh[e] = Bg[(size_t)(i0 + i) * p.SK + k0 + k];
+  for (int e = threadIdx.x; e < KMAX * nbp; e += blockDim.x) {
+    const int k = e / nbp, i = e - k * nbp;
+    Bsh[e] = (k < K && i < nb) ? Bg[(size_t)(i0 + i) * p.SK + k0 + k] : Real(0);
   }
   __syncthreads();
   if (tau >= p.T) return;
@@ -800,48 +834,51 @@ __global__ void __launch_bounds__(128) muv_partial_kernel(const MuvParams p) {
     den[k] = Real(0);
   }
   const Real* Eg = reinterpret_cast<const Real*>(p.E) + (((size_t)mix * p.N + n) * p.FL) * p.T + tau;
-  // E loads for the next UNR bins are issued before the current UNR bins
-  // are processed (latency hiding).
-  constexpr int UNR = 8;
-  Real ecur[UNR], enext[UNR];
+  Real ecur[G], enext[G];
 #pragma unroll
-  for (int u = 0; u < UNR; ++u) ecur[u] = (i0 + u < i1) ? Eg[(size_t)(i0 + u) * p.T] : Real(0);
-  for (int ib = i0; ib < i1; ib += UNR) {
+  for (int u = 0; u < G; ++u) ecur[u] = (u < nb) ? Eg[(size_t)(i0 + u) * p.T] : Real(0);
+  for (int g = 0; g < nbp; g += G) {
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) enext[u] = (ib + UNR + u < i1) ? Eg[(size_t)(ib + UNR + u) * p.T] : Real(0);
+    for (int u = 0; u < G; ++u) enext[u] = (g + G + u < nb) ? Eg[(size_t)(i0 + g + G + u) * p.T] : Real(0);
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int i = ib + u;
-      if (i < i1) {
-        const Real* b = Bsh + (i - i0) * K;
-        Real lam = Real(0);
+    for (int u = 0; u < G; u += 2) {
+      const int i = g + u;
+      Real la, lb;
+      if constexpr (std::is_same<Real, float>::value) {
+        float2 l2 = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int k = 0; k < KMAX; ++k)
-          if (k < K) lam = fma(b[k], v[k], lam);
-        lam = fmax(lam, floor_abs);
-        const Real il = Real(1) / lam;
-        const Real an = ecur[u] * (il * il), bn = il * cnt;
+        for (int k = 0; k < KMAX; ++k) l2 = ffma2s(*reinterpret_cast<const float2*>(Bsh + k * nbp + i), v[k], l2);
+        la = l2.x;
+        lb = l2.y;
+      } else {
+        la = lb = Real(0);
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) {
+          la = fma(Bsh[k * nbp + i], v[k], la);
+          lb = fma(Bsh[k * nbp + i + 1], v[k], lb);
+        }
+      }
+      const Real ila = Real(1) / fmax(la, floor_abs), ilb = Real(1) / fmax(lb, floor_abs);
+      const Real ana = ecur[u] * (ila * ila), bna = ila * cnt;
+      const Real anb = ecur[u + 1] * (ilb * ilb), bnb = ilb * cnt;
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k) {
+        const Real ba = Bsh[k * nbp + i], bb = Bsh[k * nbp + i + 1];
         if constexpr (std::is_same<Real, float>::value) {
-          const float2 ab = make_float2(an, bn);
-#pragma unroll
-          for (int k = 0; k < KMAX; ++k)
-            if (k < K) {
-              const float2 t = ffma2s(ab, b[k], make_float2(num[k], den[k]));
-              num[k] = t.x;
-              den[k] = t.y;
-            }
+          float2 t = ffma2s(make_float2(ana, bna), ba, make_float2(num[k], den[k]));
+          t = ffma2s(make_float2(anb, bnb), bb, t);
+          num[k] = t.x;
+          den[k] = t.y;
         } else {
-#pragma unroll
-          for (int k = 0; k < KMAX; ++k)
-            if (k < K) {
-              num[k] = fma(b[k], an, num[k]);
-              den[k] = fma(b[k], bn, den[k]);
-            }
+          num[k] = fma(ba, ana, num[k]);
+          den[k] = fma(ba, bna, den[k]);
+          num[k] = fma(bb, anb, num[k]);
+          den[k] = fma(bb, bnb, den[k]);
         }
       }
     }
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) ecur[u] = enext[u];
+    for (int u = 0; u < G; ++u) ecur[u] = enext[u];
   }
   Real* out = reinterpret_cast<Real*>(p.part) + (((size_t)chunk * p.nmix + mix) * 2 * p.SK + k0) * p.T + tau;
 #pragma unroll

@@ -1,0 +1,8 @@
+// fp32 sweep kernels for the stacked CTF configs (equal taps per source).
+#include "ctf_sweep_variants.h"
+namespace ctf {
+#define V(...) CTF_VL3(float, 1, __VA_ARGS__)
+std::vector<SweepVariant> sweep_variants_f32_taps() {
+  return {V(10, 4, 5, 5), V(4, 4, 4, 2), V(12, 4, 4, 4), V(6, 4, 4, 3), V(8, 4, 4, 4), V(16, 4, 2, 8)};
+}
+}  // namespace ctf

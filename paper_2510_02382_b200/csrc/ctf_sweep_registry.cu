@@ -5,10 +5,18 @@ std::vector<SweepVariant> sweep_variants_f32_exact();
 std::vector<SweepVariant> sweep_variants_f32_guard();
 std::vector<SweepVariant> sweep_variants_f64_exact();
 std::vector<SweepVariant> sweep_variants_f64_guard();
+std::vector<SweepVariant> sweep_variants_rowwarp_f32();
+std::vector<SweepVariant> sweep_variants_f32_taps();
+std::vector<SweepVariant> sweep_variants_f64_taps();
+std::vector<SweepVariant> sweep_variants_rowwarp_f64();
 const std::vector<SweepVariant>& sweep_variants_f32() {
   static const std::vector<SweepVariant> v = [] {
-    auto a = sweep_variants_f32_exact();
+    auto a = sweep_variants_rowwarp_f32();
+    auto t = sweep_variants_f32_taps();
+    a.insert(a.end(), t.begin(), t.end());
+    auto e = sweep_variants_f32_exact();
     auto b = sweep_variants_f32_guard();
+    a.insert(a.end(), e.begin(), e.end());
     a.insert(a.end(), b.begin(), b.end());
     return a;
   }();
@@ -16,8 +24,12 @@ const std::vector<SweepVariant>& sweep_variants_f32() {
 }
 const std::vector<SweepVariant>& sweep_variants_f64() {
   static const std::vector<SweepVariant> v = [] {
-    auto a = sweep_variants_f64_exact();
+    auto a = sweep_variants_rowwarp_f64();
+    auto t = sweep_variants_f64_taps();
+    a.insert(a.end(), t.begin(), t.end());
+    auto e = sweep_variants_f64_exact();
     auto b = sweep_variants_f64_guard();
+    a.insert(a.end(), e.begin(), e.end());
     a.insert(a.end(), b.begin(), b.end());
     return a;
   }();

@@ -6,6 +6,7 @@
 // (measured on B200).
 #pragma once
 #include "ctf_kernels.cuh"
+#include "ctf_rowwarp.cuh"
 
 #include <vector>
 
@@ -13,11 +14,22 @@ namespace ctf {
 struct SweepVariant {
   int prec, rmax, ft, rreg, maxt, exact;  // maxt == NT
   void (*fn)(SweepParams);
+  int kind = 0;  // 0: frame-owner sweep_kernel, 1: rowwarp_kernel (rmax = R, rreg = WPR)
+  int lt = 0;    // > 0: compiled for equal taps per source (taps == lt)
 };
 #define CTF_V(REAL, PREC, RMAX, FT, RREG, NT, EX) \
   SweepVariant { PREC, RMAX, FT, RREG, NT, EX, sweep_kernel<REAL, RMAX, FT, RREG, NT, EX> }
+// equal-taps variants: LT taps per source (row P = (P / LT, P % LT))
+#define CTF_VL(REAL, PREC, RMAX, FT, RREG, NT, LT) \
+  SweepVariant { PREC, RMAX, FT, RREG, NT, 1, sweep_kernel<REAL, RMAX, FT, RREG, NT, true, LT>, 0, LT }
+#define CTF_VL3(REAL, PREC, RMAX, FT, RREG, LT) \
+  CTF_VL(REAL, PREC, RMAX, FT, RREG, 128, LT), CTF_VL(REAL, PREC, RMAX, FT, RREG, 256, LT), \
+      CTF_VL(REAL, PREC, RMAX, FT, RREG, 512, LT)
 // one (RMAX, FT, RREG) at the three CTA sizes
 #define CTF_V3(REAL, PREC, RMAX, FT, RREG, EX) \
   CTF_V(REAL, PREC, RMAX, FT, RREG, 128, EX), CTF_V(REAL, PREC, RMAX, FT, RREG, 256, EX), \
       CTF_V(REAL, PREC, RMAX, FT, RREG, 512, EX)
+// rowwarp_kernel: R = NT / (32 * WPR) rows, FT frames per lane
+#define CTF_RW(REAL, PREC, FT, WPR, NT) \
+  SweepVariant { PREC, (NT) / (32 * (WPR)), FT, WPR, NT, 1, rowwarp_kernel<REAL, FT, WPR, NT>, 1, 0 }
 }  // namespace ctf
