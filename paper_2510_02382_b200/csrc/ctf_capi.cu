@@ -125,8 +125,9 @@ struct ctf_ctx {
   size_t sweep_smem = 0;
   ctf::SweepParams sp{};
   int kmax = 0, chunk_bins = 0, nchunk = 0;
+  int stream_grid = 0;
   // device buffers
-  DevBuf<unsigned char> x, W, Bf, V, E, part, packed;
+  DevBuf<unsigned char> x, W, Bf, V, E, part, packed, scratch;
   DevBuf<double> rowpow, objbin, packed_d, mu, floor_abs, objective, mp_part, logdet;
   DevBuf<unsigned long long> err;
   // timing
@@ -201,7 +202,7 @@ void validate(const ctf_problem& p) {
     throw CtfError(CTF_ERR_CONFIG, "empty problem (mixtures, bins and frames must be >= 1)");
   if (p.precision != CTF_F32 && p.precision != CTF_F64) throw CtfError(CTF_ERR_CONFIG, "unknown precision");
   if (p.x_precision != CTF_F32 && p.x_precision != CTF_F64) throw CtfError(CTF_ERR_CONFIG, "unknown x precision");
-  if (D > 32) throw CtfError(CTF_ERR_UNSUPPORTED, "D > 32 rows is not in the compiled kernel set yet");
+  if (D > ctf::kMaxRows) throw CtfError(CTF_ERR_UNSUPPORTED, "D > 64 rows is not in the compiled kernel set");
   if (p.num_bins >= (1 << 20)) throw CtfError(CTF_ERR_UNSUPPORTED, "too many bins");
 }
 
@@ -264,6 +265,22 @@ void plan_sweep(ctf_ctx* c) {
       cand.off_z = (int)take((size_t)NW * v.rmax * cs);
       cand.off_b = (int)take((size_t)c->SK * rs);
       cand.off_d = (int)take((size_t)NW * 4 * sizeof(double));
+    } else if (v.kind == 2) {  // streamed: any R <= 64, tile in global scratch
+      if (c->R > v.rmax) continue;
+      TP = nt * v.ft;
+      if (TP < c->T || (nt * (v.ft - 1) >= c->T && v.ft > 1)) continue;  // avoid mostly-empty frames
+      const int RG = v.rreg, NG = (c->R + RG - 1) / RG, VP = ((3 * RG + 31) / 32) * 32;
+      cand.xoff = c->Ls - 1;
+      cand.xp = cand.xoff + TP;
+      cand.off_y = 0;
+      cand.off_l = (int)take((size_t)c->N * (loff + TP) * rs);
+      cand.off_w = (int)take((size_t)2 * c->R * c->D * cs);
+      cand.off_red = (int)take((size_t)NW * NG * VP * rs);
+      cand.off_z = (int)take((size_t)c->R * cs);
+      cand.off_b = (int)take((size_t)c->SK * rs);
+      cand.off_d = (int)take((size_t)(NW * 4 + c->R) * sizeof(double));
+      cand.off_x = (int)take((size_t)(cand.xoff + TP) * cs);
+      cand.off_e = 0;
     } else {
       const int wpr = v.rreg;
       if (v.rmax != c->R) continue;                 // one row per WPR warps
@@ -290,7 +307,9 @@ void plan_sweep(ctf_ctx* c) {
     // B200 for every shape so far), then
     // the smallest RMAX, exact before guarded, then the least frame padding
     // (fewest threads), then table order
-    const int rank = (v.kind == 1 ? 1000 : 0) + v.rmax * 4 + (v.exact ? 0 : 2) + (v.lt > 0 ? 0 : 1);
+    // the streamed kernel only when nothing resident fits (rank 2000+)
+    const int rank = (v.kind == 2 ? 2000 : v.kind == 1 ? 1000 : 0) + v.rmax * 4 + (v.exact ? 0 : 2) +
+                     (v.lt > 0 ? 0 : 1);
     const bool better = !found || rank < best_rank || (rank == best_rank && nt < best_nt);
     if (better) {
       found = true;
@@ -310,7 +329,15 @@ void plan_sweep(ctf_ctx* c) {
   c->sv = best;
   c->NT = best_nt;
   c->sweep_smem = best_smem;
-  CK(cudaFuncSetAttribute((const void*)best.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)best_smem));
+  if (best.kind == 2) {
+    CK(cudaFuncSetAttribute((const void*)best.sfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)best_smem));
+    int per_sm = 0, nsm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, best.sfn, best_nt, best_smem));
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+    c->stream_grid = std::max(1, std::min(std::max(1, per_sm) * nsm, c->B * c->FL));
+  } else {
+    CK(cudaFuncSetAttribute((const void*)best.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)best_smem));
+  }
   ctf::SweepParams& sp = c->sp;
   sp.FL = c->FL;
   sp.bin_lo = c->lo;
@@ -512,7 +539,16 @@ void run_body(ctf_ctx* c, bool do_sweep) {
 
   cudaEvent_t e0 = take_event(c), e1 = take_event(c), e2 = take_event(c);
   CK(cudaEventRecord(e0, c->stream));
-  c->sv.fn<<<dim3(c->FL, c->B), c->NT, c->sweep_smem, c->stream>>>(sp);
+  if (c->sv.kind == 2) {
+    ctf::StreamParams st{};
+    st.s = sp;
+    st.scratch = c->scratch.p;
+    st.nwork = c->B * c->FL;
+    st.ngroups = (c->R + c->sv.rreg - 1) / c->sv.rreg;
+    c->sv.sfn<<<c->stream_grid, c->NT, c->sweep_smem, c->stream>>>(st);
+  } else {
+    c->sv.fn<<<dim3(c->FL, c->B), c->NT, c->sweep_smem, c->stream>>>(sp);
+  }
   CK(cudaGetLastError());
   CK(cudaEventRecord(e1, c->stream));
   c->timing.sweep_launches += 1;
@@ -665,6 +701,8 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host) {
   c->floor_abs.alloc((size_t)c->B);
   c->mp_part.alloc((size_t)c->B * c->FL);
   c->err.alloc((size_t)c->B);
+  if (c->sv.kind == 2) c->scratch.alloc((size_t)c->stream_grid * c->R * c->TP * cs);
+  else c->scratch.free();
   c->logdet.alloc((size_t)c->B * c->FL);
   CK(cudaMemsetAsync(c->logdet.p, 0, c->logdet.n * 8, c->stream));  // log|det I| = 0
   c->max_iters = std::max(1, prob->iterations);
@@ -924,8 +962,9 @@ int ctf_describe(ctf_ctx* c, char* buf, int len) {
   std::snprintf(buf, (size_t)len,
                 "{\"sweep_kernel\": \"%s<%s,RMAX=%d,FT=%d,%s=%d,NT=%d,EXACT=%d>\", \"threads\": %d, "
                 "\"smem_bytes\": %zu, \"grid\": [%d, %d], \"muv_chunks\": %d, \"bins\": [%d, %d]}",
-                c->sv.kind ? "rowwarp_kernel" : "sweep_kernel", c->real_size == 4 ? "f32" : "f64", c->sv.rmax, c->sv.ft,
-                c->sv.kind ? "WPR" : "RREG", c->sv.rreg, c->sv.maxt, c->sv.exact, c->NT,
+                c->sv.kind == 2 ? "stream_kernel" : c->sv.kind ? "rowwarp_kernel" : "sweep_kernel",
+                c->real_size == 4 ? "f32" : "f64", c->sv.rmax, c->sv.ft,
+                c->sv.kind == 2 ? "RG" : c->sv.kind ? "WPR" : "RREG", c->sv.rreg, c->sv.maxt, c->sv.exact, c->NT,
                 c->sweep_smem, c->FL, c->B, c->nchunk, c->lo, c->hi);
   return CTF_OK;
 }

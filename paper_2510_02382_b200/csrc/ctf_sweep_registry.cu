@@ -7,6 +7,8 @@ std::vector<SweepVariant> sweep_variants_f64_exact();
 std::vector<SweepVariant> sweep_variants_f64_guard();
 std::vector<SweepVariant> sweep_variants_rowwarp_f32();
 std::vector<SweepVariant> sweep_variants_f32_taps();
+std::vector<SweepVariant> sweep_variants_stream_f32();
+std::vector<SweepVariant> sweep_variants_stream_f64();
 std::vector<SweepVariant> sweep_variants_f64_taps();
 std::vector<SweepVariant> sweep_variants_rowwarp_f64();
 const std::vector<SweepVariant>& sweep_variants_f32() {
@@ -18,6 +20,8 @@ const std::vector<SweepVariant>& sweep_variants_f32() {
     auto b = sweep_variants_f32_guard();
     a.insert(a.end(), e.begin(), e.end());
     a.insert(a.end(), b.begin(), b.end());
+    auto st = sweep_variants_stream_f32();
+    a.insert(a.end(), st.begin(), st.end());
     return a;
   }();
   return v;
@@ -31,6 +35,8 @@ const std::vector<SweepVariant>& sweep_variants_f64() {
     auto b = sweep_variants_f64_guard();
     a.insert(a.end(), e.begin(), e.end());
     a.insert(a.end(), b.begin(), b.end());
+    auto st = sweep_variants_stream_f64();
+    a.insert(a.end(), st.begin(), st.end());
     return a;
   }();
   return v;

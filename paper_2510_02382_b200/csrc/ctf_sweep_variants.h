@@ -7,6 +7,7 @@
 #pragma once
 #include "ctf_kernels.cuh"
 #include "ctf_rowwarp.cuh"
+#include "ctf_stream.cuh"
 
 #include <vector>
 
@@ -14,8 +15,10 @@ namespace ctf {
 struct SweepVariant {
   int prec, rmax, ft, rreg, maxt, exact;  // maxt == NT
   void (*fn)(SweepParams);
-  int kind = 0;  // 0: frame-owner sweep_kernel, 1: rowwarp_kernel (rmax = R, rreg = WPR)
+  int kind = 0;  // 0: frame-owner sweep_kernel, 1: rowwarp_kernel (rmax = R, rreg = WPR),
+                 // 2: stream_kernel (rmax = 64, rreg = RG, launched through sfn)
   int lt = 0;    // > 0: compiled for equal taps per source (taps == lt)
+  void (*sfn)(StreamParams) = nullptr;
 };
 #define CTF_V(REAL, PREC, RMAX, FT, RREG, NT, EX) \
   SweepVariant { PREC, RMAX, FT, RREG, NT, EX, sweep_kernel<REAL, RMAX, FT, RREG, NT, EX> }
@@ -29,6 +32,9 @@ struct SweepVariant {
 #define CTF_V3(REAL, PREC, RMAX, FT, RREG, EX) \
   CTF_V(REAL, PREC, RMAX, FT, RREG, 128, EX), CTF_V(REAL, PREC, RMAX, FT, RREG, 256, EX), \
       CTF_V(REAL, PREC, RMAX, FT, RREG, 512, EX)
+// stream_kernel: any R <= 64 in groups of RG rows, FT frames per thread
+#define CTF_ST(REAL, PREC, FT, RG, NT, MINB) \
+  SweepVariant { PREC, 64, FT, RG, NT, 0, nullptr, 2, 0, stream_kernel<REAL, FT, RG, NT, MINB> }
 // rowwarp_kernel: R = NT / (32 * WPR) rows, FT frames per lane
 #define CTF_RW(REAL, PREC, FT, WPR, NT) \
   SweepVariant { PREC, (NT) / (32 * (WPR)), FT, WPR, NT, 1, rowwarp_kernel<REAL, FT, WPR, NT>, 1, 0 }

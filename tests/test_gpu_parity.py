@@ -250,3 +250,29 @@ def test_full_cfg1_batch_properties():
     t.iterate(iters)
     W1, B1, V1, o1 = t.download_raw()
     assert np.array_equal(W[0], W1[0]) and np.array_equal(o1[0], obj[0])
+
+
+@pytest.mark.parametrize("shape", [
+    # BASELINE configs[3] rows: M=N=4, L=8 (R=32), T=1000, K=20, tap variance 0.8^l
+    dict(M=4, L=8, T=1000, K=20, rho=0.8, F=9, iters=2, prec="f32", tol=1e-4),
+    # BASELINE configs[4] rows: M=N=6, L=10 (R=60), T=4000, K=16, tap variance 0.85^l
+    dict(M=6, L=10, T=4000, K=16, rho=0.85, F=3, iters=1, prec="f32", tol=1e-4),
+    # fp64 tile beyond one SM (R=12, T=2000): streamed path in double precision
+    dict(M=3, L=4, T=2000, K=20, rho=0.7, F=7, iters=2, prec="f64", tol=1e-9),
+    dict(M=4, L=8, T=1000, K=20, rho=0.8, F=5, iters=2, prec="f64", tol=1e-9),
+])
+def test_streamed_large_tiles(shape):
+    """Tiles that exceed one SM go through the streamed kernel; parity vs the oracle."""
+    M, L, T, K, F = shape["M"], shape["L"], shape["T"], shape["K"], shape["F"]
+    N, iters, seed = M, shape["iters"], 4
+    raw = synth_mixtures(1, F, T, M, N, L, K, shape["rho"], 12)
+    s = Session(raw if shape["prec"] == "f64" else raw.astype(np.complex64), [L] * N, [K] * N, stack_taps=L,
+                iterations=iters, precision=shape["prec"], seed=seed)
+    assert "stream_kernel" in s.describe()
+    s.iterate(iters)
+    W, B, V, obj = s.download_raw()
+    ref = O.run(O.config([L] * N, [K] * N, iterations=iters, seed=seed, threads=NPROC), O.stack_observation(raw[0], L))
+    tol = shape["tol"]
+    assert rel(W[0], ref["W"].reshape(F, -1)) <= tol
+    assert rel(B[0], ref["B"]) <= tol and rel(V[0], ref["V"]) <= tol
+    assert np.max(np.abs(obj[0] - ref["objective"]) / np.abs(ref["objective"])) <= tol
