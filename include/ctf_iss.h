@@ -145,6 +145,13 @@ void* ctf_stream(ctf_ctx* ctx);
  * contiguous ranges by rank. NCCL is loaded lazily (dlopen). */
 int ctf_comm_unique_id(uint8_t id[128], ctf_err* err);
 int ctf_comm_init(ctf_ctx* ctx, int world_size, int rank, const uint8_t id[128], ctf_err* err);
+/* In-process exchange group (testing the sharded path on one GPU): contexts
+ * of one process, each driven by its own host thread, all-reduce through host
+ * memory in fixed rank order instead of NCCL. */
+typedef struct ctf_group ctf_group;
+ctf_group* ctf_group_create(int world_size);
+void ctf_group_destroy(ctf_group* group);
+int ctf_comm_init_group(ctf_ctx* ctx, ctf_group* group, int rank, ctf_err* err);
 /* Local bin range [lo, hi) of this rank for a problem with num_bins bins. */
 void ctf_shard_range(int num_bins, int world_size, int rank, int* lo, int* hi);
 

@@ -50,6 +50,9 @@ SIGNATURES = {
     "ctf_stream": (_P, [_P]),
     "ctf_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8), _E]),
     "ctf_comm_init": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(C.c_uint8), _E]),
+    "ctf_group_create": (_P, [C.c_int]),
+    "ctf_group_destroy": (None, [_P]),
+    "ctf_comm_init_group": (C.c_int, [_P, _P, C.c_int, _E]),
     "ctf_shard_range": (None, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "ctf_setup": (C.c_int, [_P, C.POINTER(CtfProblem), _P, _E]),
     "ctf_set_state": (C.c_int, [_P, _D, _D, _D, _E]),

@@ -159,7 +159,8 @@ class Session:
     """
 
     def __init__(self, x: np.ndarray, taps, bases, *, stack_taps=1, iterations=100, precision="f64",
-                 psd_floor=1e-10, seed=0, device=0, world_size=1, rank=0, comm_id: Optional[bytes] = None):
+                 psd_floor=1e-10, seed=0, device=0, world_size=1, rank=0, comm_id: Optional[bytes] = None,
+                 group=None):
         self.lib = L.load()
         if x.ndim != 4:
             raise ConfigError("x must have shape [B, F, T, M]")
@@ -175,7 +176,9 @@ class Session:
         self._ctx = C.c_void_p()
         err = L.CtfErr()
         _check(self.lib.ctf_open(device, C.byref(self._ctx), C.byref(err)), err)
-        if world_size > 1:
+        if group is not None:  # in-process exchange group (testing the sharded path)
+            _check(self.lib.ctf_comm_init_group(self._ctx, group, rank, C.byref(err)), err)
+        elif world_size > 1:
             buf = (C.c_uint8 * 128).from_buffer_copy(comm_id)
             _check(self.lib.ctf_comm_init(self._ctx, world_size, rank, buf, C.byref(err)), err)
         self.world_size, self.rank = world_size, rank

@@ -17,6 +17,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
+#include <mutex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -103,12 +105,36 @@ size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
 
 }  // namespace
 
+// In-process exchange group: several contexts of one process (one per host
+// thread) reduce through host memory in fixed rank order. Used to exercise
+// the frequency-sharded path on a single GPU; production multi-GPU uses NCCL.
+struct ctf_group {
+  int world = 0;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  long generation = 0;
+  std::vector<std::vector<unsigned char>> slots;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    const long gen = generation;
+    if (++arrived == world) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return generation != gen; });
+    }
+  }
+};
+
 struct ctf_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   // multi-GPU
   int world = 1, rank = 0;
   NcclComm comm = nullptr;
+  ctf_group* group = nullptr;  // in-process exchange instead of NCCL
   // problem
   bool ready = false;
   ctf_problem prob{};
@@ -413,6 +439,36 @@ void download_real(ctf_ctx* c, double* dst, const void* src, size_t n) {
 
 void allreduce(ctf_ctx* c, void* buf, size_t count, int dtype, int op) {
   if (c->world <= 1 || count == 0) return;
+  if (c->group) {  // host exchange, fixed rank order (deterministic)
+    const size_t es = dtype == kNcclFloat ? 4 : 8;
+    ctf_group* g = c->group;
+    auto& mine = g->slots[(size_t)c->rank];
+    mine.resize(count * es);
+    CK(cudaMemcpyAsync(mine.data(), buf, count * es, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    g->barrier();
+    std::vector<unsigned char> out(count * es);
+    for (size_t i = 0; i < count; ++i) {
+      if (dtype == kNcclFloat) {
+        float a = 0.f;
+        for (int r = 0; r < g->world; ++r) a += reinterpret_cast<const float*>(g->slots[(size_t)r].data())[i];
+        reinterpret_cast<float*>(out.data())[i] = a;
+      } else if (dtype == kNcclDouble) {
+        double a = 0.0;
+        for (int r = 0; r < g->world; ++r) a += reinterpret_cast<const double*>(g->slots[(size_t)r].data())[i];
+        reinterpret_cast<double*>(out.data())[i] = a;
+      } else {  // uint64 min
+        unsigned long long a = ~0ull;
+        for (int r = 0; r < g->world; ++r)
+          a = std::min(a, reinterpret_cast<const unsigned long long*>(g->slots[(size_t)r].data())[i]);
+        reinterpret_cast<unsigned long long*>(out.data())[i] = a;
+      }
+    }
+    g->barrier();  // every rank has read every slot
+    CK(cudaMemcpyAsync(buf, out.data(), count * es, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return;
+  }
   const int rc = g_nccl.AllReduce(buf, buf, count, dtype, op, c->comm, c->stream);
   if (rc != 0)
     throw CtfError(CTF_ERR_CUDA, std::string("ncclAllReduce failed: ") +
@@ -874,6 +930,26 @@ int ctf_comm_init(ctf_ctx* c, int world, int rank, const uint8_t id[128], ctf_er
     std::memcpy(u.internal, id, 128);
     const int rc = g_nccl.CommInitRank(&c->comm, world, u, rank);
     if (rc != 0) throw CtfError(CTF_ERR_CUDA, "ncclCommInitRank failed");
+  });
+}
+
+ctf_group* ctf_group_create(int world_size) {
+  if (world_size < 1) return nullptr;
+  auto* g = new ctf_group();
+  g->world = world_size;
+  g->slots.resize((size_t)world_size);
+  return g;
+}
+
+void ctf_group_destroy(ctf_group* g) { delete g; }
+
+int ctf_comm_init_group(ctf_ctx* c, ctf_group* g, int rank, ctf_err* err) {
+  return guarded(err, [&] {
+    if (!c || !g) throw CtfError(CTF_ERR_CONFIG, "null context or group");
+    if (rank < 0 || rank >= g->world) throw CtfError(CTF_ERR_CONFIG, "bad rank");
+    c->world = g->world;
+    c->rank = rank;
+    c->group = g->world > 1 ? g : nullptr;
   });
 }
 

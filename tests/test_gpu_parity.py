@@ -276,3 +276,85 @@ def test_streamed_large_tiles(shape):
     assert rel(W[0], ref["W"].reshape(F, -1)) <= tol
     assert rel(B[0], ref["B"]) <= tol and rel(V[0], ref["V"]) <= tol
     assert np.max(np.abs(obj[0] - ref["objective"]) / np.abs(ref["objective"])) <= tol
+
+
+def _sharded_run(raw, L, K, iters, precision, seed, world):
+    """Runs `world` frequency shards as separate contexts on cuda:0, one host
+    thread each, exchanging through the in-process group (the NCCL path's
+    data flow with a host all-reduce)."""
+    import threading
+    from paper_2510_02382_b200 import _lib
+    lib = _lib.load()
+    grp = lib.ctf_group_create(world)
+    out, errs = [None] * world, [None] * world
+    N = raw.shape[3]
+
+    def worker(r):
+        try:
+            s = Session(raw, [L] * N, [K] * N, stack_taps=L, iterations=iters, precision=precision, seed=seed,
+                        world_size=world, rank=r, group=grp)
+            s.iterate(iters)
+            out[r] = (s.bin_range, s.download_raw())
+            s.close()
+        except Exception as e:  # noqa: BLE001
+            errs[r] = e
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    lib.ctf_group_destroy(grp)
+    return out, errs
+
+
+@pytest.mark.parametrize("precision,tol", [("f64", 1e-12), ("f32", 2e-5)])
+def test_frequency_sharded_contexts_match_single_context(precision, tol):
+    """The world > 1 path (shard ranges, packed all-reduce of MU-V sums, row
+    powers, objective, mean power, error words) reproduces the world = 1 run."""
+    B, F, T, M, L, K, iters, seed = 2, 37, 300, 2, 3, 4, 4, 6
+    raw = synth_mixtures(B, F, T, M, M, L, K, 0.6, 31)
+    if precision == "f32":
+        raw = raw.astype(np.complex64)
+    s = Session(raw, [L] * M, [K] * M, stack_taps=L, iterations=iters, precision=precision, seed=seed)
+    s.iterate(iters)
+    W1, B1, V1, o1 = s.download_raw()
+    s.close()
+    for world in (2, 3):
+        out, errs = _sharded_run(raw, L, K, iters, precision, seed, world)
+        assert not any(errs), errs
+        covered = []
+        for (lo, hi), (W, Bf, V, obj) in out:
+            covered.append((lo, hi))
+            assert rel(W[:, lo:hi], W1[:, lo:hi]) <= tol
+            Bl = Bf.reshape(B, M, K, F)[..., lo:hi]
+            assert rel(Bl, B1.reshape(B, M, K, F)[..., lo:hi]) <= tol
+            assert rel(V, V1) <= tol  # V is replicated on every rank
+            assert np.max(np.abs(obj - o1) / np.abs(o1)) <= tol
+        assert sorted(covered)[0][0] == 0 and sorted(covered)[-1][1] == F
+
+
+def test_frequency_sharded_degeneracy_reported_on_every_rank():
+    """A silent bin in rank 1's shard raises the same DegeneracyError on all ranks."""
+    g = np.random.default_rng(3)
+    F, T = 6, 40
+    x = g.standard_normal((1, F, T, 4)) + 1j * g.standard_normal((1, F, T, 4))
+    x[0, 4] = 0
+    import threading
+    from paper_2510_02382_b200 import _lib
+    lib = _lib.load()
+    grp = lib.ctf_group_create(2)
+    errs = [None, None]
+
+    def worker(r):
+        try:
+            s = Session(x, [2, 2], [3, 3], stack_taps=1, iterations=2, precision="f64", world_size=2, rank=r,
+                        group=grp)
+            s.iterate(2)
+        except DegeneracyError as e:
+            errs[r] = e
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(2)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    lib.ctf_group_destroy(grp)
+    for e in errs:
+        assert e is not None and e.iteration == 1 and e.bin == 4
