@@ -159,12 +159,15 @@ def cpu_reference_arm(args, cfgn, steps, warmup, sample_note=True):
     B, F, T, M, L, K, rho, iters = CFGS[cfgn]
     N = M
     threads = os.cpu_count() or 1
+    # bounded sample: all bins for cfg0/cfg1, a bin subset for the large
+    # tiles so one step (one iteration) stays around half a second
+    R = M * L
+    F = min(F, max(16, int(513 * (1000.0 / T) * (100.0 / (R * R)))))
     raw = synth_mixtures(1, F, T, M, N, L, K, rho, args.seed)[0]
     x = O.stack_observation(raw, L)
     cfg = O.config([L] * N, [K] * N, iterations=1, seed=args.seed, threads=threads)
     floor = 1e-10 * O.mean_power(x)
     Bf, V = O.random_factors(cfg, F, T)
-    R = M * L
     W = np.zeros((F, R, R), complex)
     W[:] = np.eye(R)
     times = []
@@ -181,7 +184,8 @@ def cpu_reference_arm(args, cfgn, steps, warmup, sample_note=True):
     except (OSError, IndexError):
         model = "unknown"
     return {"value": value, "unit": "TF-bin*iter/s", "cores": threads, "kind": "port",
-            "sample": f"1 of {B} mixtures x {len(times)} iterations of cfg{cfgn} (F={F}, T={T}, D={R}), "
+            "sample": f"1 of {B} mixtures, {F} of {CFGS[cfgn][1]} bins, {len(times)} iterations of cfg{cfgn} "
+                      f"(T={T}, D={R}), "
                       f"oracle/ctf_oracle.cpp with parallel_for over bins on {threads} threads ({model}); "
                       f"{sec:.2f} s", "seconds": sec}
 
@@ -197,6 +201,9 @@ def main():
     ap.add_argument("--seed", type=int, default=20251002)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--unique", type=int, default=16,
+                    help="distinct synthetic mixtures generated; the batch tiles them (seeds still differ per mixture)")
+    ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     world, rank, local = dist_env()
     B, F, T, M, L, K, rho, iters = CFGS[args.cfg]
@@ -254,7 +261,14 @@ def main():
         return float(t[0])
 
     prec = args.dtype
-    x = synth_mixtures(B, F, T, M, N, L, K, rho, args.seed, precision=prec)
+    # BASELINE's generator, one seed per mixture; for large batches a set of
+    # `--unique` mixtures is generated and tiled over the batch (throughput
+    # does not depend on the content; init seeds stay distinct per mixture)
+    nu = min(B, max(1, args.unique)) if B > 64 else B
+    xu = synth_mixtures(nu, F, T, M, N, L, K, rho, args.seed, precision=prec)
+    x = xu if nu == B else np.ascontiguousarray(np.concatenate([xu] * ((B + nu - 1) // nu))[:B])
+    del xu
+    config["inputs"] = f"{nu} distinct synthetic mixtures" + ("" if nu == B else f" tiled to {B}")
     s = Session(x, [L] * N, [K] * N, stack_taps=L, iterations=iters, precision=prec, seed=args.seed,
                 device=device, world_size=world, rank=rank, comm_id=comm_id)
     desc = json.loads(s.describe())
@@ -294,7 +308,10 @@ def main():
     mp = measured_peaks()
     hbm_peak = mp.get("hbm_gbs", 6650.0)
     c = 8 if prec == "f32" else 16
+    streamed = desc["sweep_kernel"].startswith("stream_kernel")
     bpt = bytes_per_tfbin(M, N, K, R, D, T, F, c)
+    if streamed:  # SURVEY §8(d) streamed sweep: every step reads and writes the R x T tile
+        bpt = 2 * M * c + R * c + 2 * R * R * c + bpt - M * c
     roofline = {"bound": "fp32-cuda-core" if prec == "f32" else "fp64-cuda-core", "achieved": achieved,
                 "peak": peak, "unit": "TFLOP/s", "frac": (achieved / peak) if peak else None,
                 "traffic": traffic_per_tfbin * units_per_launch if traffic_per_tfbin else None,
@@ -302,13 +319,49 @@ def main():
                 "flops_per_tfbin": fl_sweep, "units_per_launch": units_per_launch,
                 "peak_source": "in-run FFMA2/DFMA chain probe (tools/peak.cu); MEASURED_PEAKS.json has no CUDA-core peak",
                 "hbm": {"achieved": bpt * units_per_launch / (sweep_ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                        "note": ("streamed tile: bytes are the tile's read+write per step; when the per-CTA "
+                                 "scratch fits L2 (cfg3) the traffic is served by L2 and frac can exceed 1")
+                        if streamed else "resident tile: x read once, E written, W/B/V amortised",
                         "frac": bpt * units_per_launch / (sweep_ms / 1e3) / 1e9 / hbm_peak,
                         "bytes_per_tfbin": bpt, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"}}
     gpu_launches = int(timing.launches)
 
     # ---- end to end through the public C-ABI call with host buffers
     s.close()
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, LB, x, prec, device, world, rank, comm_id, barrier, max_over_ranks, s.bin_range,
+                      (B, F, T, M, N, L, K, R, D, iters, c))
+    del x
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_reference_arm(args, args.cfg, steps=8, warmup=1)
+            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        clocks = clk.summary()
+        line = {"metric": "TF-bin*iter/s of the ISS+NMF loop", "value": value, "unit": "TF-bin*iter/s",
+                "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": prec,
+                "data": "synthetic (BASELINE configs generator, seeded; no public dataset)", "config": config,
+                "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": e2e,
+                "gpu_launches": gpu_launches, "clocks": clocks,
+                "kernels": {"sweep_ms_per_iteration": sweep_ms, "mu_ms_per_iteration": timing.mu_ms / args.steps,
+                            "variant": desc}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, LB, x, prec, device, world, rank, comm_id, barrier, max_over_ranks, bin_range, dims):
+    """ctf_run() through the C ABI with pinned host buffers: per step the H2D of
+    x and the initial factors, all iterations, and the D2H of W, B, V and the
+    objective trace are inside the timed region."""
     import ctypes
+    import torch
+    from paper_2510_02382_b200.api import _problem
+    B, F, T, M, N, L, K, R, D, iters, c = dims
     lib = LB.load()
     xh = torch.from_numpy(x.view(np.float32 if prec == "f32" else np.float64)).pin_memory()
     SK = N * K
@@ -316,7 +369,6 @@ def main():
     outB = torch.empty(B * F * SK, dtype=torch.float64).pin_memory()
     outV = torch.empty(B * SK * T, dtype=torch.float64).pin_memory()
     outO = torch.empty(B * iters, dtype=torch.float64).pin_memory()
-    from paper_2510_02382_b200.api import _problem
     prob = _problem(B, F, T, M, L, [L] * N, [K] * N, iters, prec, prec, 1e-10, args.seed)
     ctx = ctypes.c_void_p()
     err = LB.CtfErr()
@@ -332,39 +384,19 @@ def main():
         assert rc == 0, err.msg
 
     one_run()  # warm-up
-    e2e_times = []
+    times = []
     for _ in range(args.e2e_steps):
         barrier()
         t0 = time.perf_counter()
         one_run()
-        e2e_times.append(max_over_ranks(time.perf_counter() - t0))
+        times.append(max_over_ranks(time.perf_counter() - t0))
     lib.ctf_close(ctx)
-    e2e_sec = statistics.median(e2e_times)
-    e2e_value = tfbins * iters / e2e_sec
-    lo, hi = s.bin_range
+    sec = statistics.median(times)
+    lo, hi = bin_range
     h2d = B * (hi - lo) * T * M * c + 2 * 8 * (B * (hi - lo) * SK + B * SK * T)  # x + initial B, V
     d2h = 8 * (B * (hi - lo) * (R * D * 2 + SK) + B * SK * T + B * iters)
-
-    if rank == 0:
-        cpu = None
-        if world == 1 and not args.no_cpu_baseline:
-            cpu = cpu_reference_arm(args, args.cfg, steps=8, warmup=1)
-            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
-        clocks = clk.summary()
-        line = {"metric": "TF-bin*iter/s of the ISS+NMF loop", "value": value, "unit": "TF-bin*iter/s",
-                "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps,
-                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": prec,
-                "data": "synthetic (BASELINE configs generator, seeded; no public dataset)", "config": config,
-                "roofline": roofline, "cpu_baseline": cpu,
-                "e2e": {"value": e2e_value, "unit": "TF-bin*iter/s", "h2d_bytes_per_step": int(h2d),
-                        "d2h_bytes_per_step": int(d2h), "step": f"one ctf_run() of {iters} iterations",
-                        "seconds_per_step": e2e_sec},
-                "gpu_launches": gpu_launches, "clocks": clocks,
-                "kernels": {"sweep_ms_per_iteration": sweep_ms, "mu_ms_per_iteration": timing.mu_ms / args.steps,
-                            "variant": desc}}
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    return {"value": B * F * T * iters / sec, "unit": "TF-bin*iter/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "step": f"one ctf_run() of {iters} iterations", "seconds_per_step": sec}
 
 
 if __name__ == "__main__":
