@@ -152,8 +152,11 @@ struct ctf_ctx {
   ctf::SweepParams sp{};
   int kmax = 0, chunk_bins = 0, nchunk = 0;
   int stream_grid = 0;
+  int cluster_size = 0;
   // device buffers
-  DevBuf<unsigned char> x, W, Bf, V, E, part, packed, scratch;
+  DevBuf<unsigned char> x, W, Bf, V, E, part, packed, scratch, cpivot, cwpivot;
+  DevBuf<double> cpart;
+  DevBuf<int> cbad;
   DevBuf<double> rowpow, objbin, packed_d, mu, floor_abs, objective, mp_part, logdet;
   DevBuf<unsigned long long> err;
   // timing
@@ -291,6 +294,37 @@ void plan_sweep(ctf_ctx* c) {
       cand.off_z = (int)take((size_t)NW * v.rmax * cs);
       cand.off_b = (int)take((size_t)c->SK * rs);
       cand.off_d = (int)take((size_t)NW * 4 * sizeof(double));
+    } else if (v.kind == 3) {  // cluster: CS = R / RB CTAs per bin
+      const int RB = v.rmax, CS = c->R / RB;
+      if (c->R % RB != 0 || CS < 2 || CS > 16) continue;
+      TP = nt * v.ft;
+      if (TP < c->T || (v.ft > 1 && nt * (v.ft - 1) >= c->T)) continue;
+      // sources touched by one CTA's rows (for the 1/lambda and energy buffers)
+      int nsrc = 1;
+      for (int q = 0; q < CS; ++q) {
+        int r0 = q * RB, n0 = 0, n1 = 0, acc = 0;
+        for (int n = 0; n < c->N; ++n) {
+          if (r0 >= acc && r0 < acc + c->taps[n]) n0 = n;
+          if (r0 + RB - 1 >= acc && r0 + RB - 1 < acc + c->taps[n]) n1 = n;
+          acc += c->taps[n];
+        }
+        nsrc = std::max(nsrc, n1 - n0 + 1);
+      }
+      const int VP = ((3 * RB + 31) / 32) * 32;
+      cand.xoff = c->Ls - 1;
+      cand.xp = cand.xoff + TP;
+      cand.off_y = (int)take(std::max((size_t)(RB - v.rreg) * TP * cs, (size_t)(nsrc + 1) * TP * rs));
+      // x stage + 1/lambda, reused for |y|^2 of the own rows in the epilogue
+      const size_t xb = (size_t)(cand.xoff + TP) * cs, lb = (size_t)nsrc * (loff + TP) * rs;
+      const size_t xl = std::max(align16(xb) + lb, (size_t)RB * TP * rs);
+      cand.off_x = (int)take(xl);
+      cand.off_l = cand.off_x + (int)align16(xb);
+      cand.off_w = (int)take((size_t)c->D * RB * cs);
+      cand.off_e = (int)take((size_t)c->D * cs);
+      cand.off_red = (int)take((size_t)2 * NW * VP * rs);
+      cand.off_z = (int)take((size_t)NW * RB * cs);
+      cand.off_b = (int)take((size_t)c->SK * rs);
+      cand.off_d = (int)take((size_t)(NW * 4 + c->R) * sizeof(double));
     } else if (v.kind == 2) {  // streamed: any R <= 64, tile in global scratch
       if (c->R > v.rmax) continue;
       TP = nt * v.ft;
@@ -333,9 +367,13 @@ void plan_sweep(ctf_ctx* c) {
     // B200 for every shape so far), then
     // the smallest RMAX, exact before guarded, then the least frame padding
     // (fewest threads), then table order
-    // the streamed kernel only when nothing resident fits (rank 2000+)
-    const int rank = (v.kind == 2 ? 2000 : v.kind == 1 ? 1000 : 0) + v.rmax * 4 + (v.exact ? 0 : 2) +
-                     (v.lt > 0 ? 0 : 1);
+    // resident single-CTA kernels first, then clusters (on-chip tile over
+    // several SMs), the streamed kernel only when nothing else fits
+    // (measured on B200: the cluster kernel is correct but slower than the
+    // streamed one for cfg3/cfg4 so far, so it ranks last; CTF_SWEEP_KIND=3
+    // selects it)
+    const int rank = (v.kind == 3 ? 3000 : v.kind == 2 ? 2000 : v.kind == 1 ? 1000 : 0) +
+                     (v.kind == 3 ? -v.rmax * 4 : v.rmax * 4) + (v.exact ? 0 : 2) + (v.lt > 0 ? 0 : 1);
     const bool better = !found || rank < best_rank || (rank == best_rank && nt < best_nt);
     if (better) {
       found = true;
@@ -355,7 +393,11 @@ void plan_sweep(ctf_ctx* c) {
   c->sv = best;
   c->NT = best_nt;
   c->sweep_smem = best_smem;
-  if (best.kind == 2) {
+  if (best.kind == 3) {
+    CK(cudaFuncSetAttribute((const void*)best.cfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)best_smem));
+    CK(cudaFuncSetAttribute((const void*)best.cfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    c->cluster_size = c->R / best.rmax;
+  } else if (best.kind == 2) {
     CK(cudaFuncSetAttribute((const void*)best.sfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)best_smem));
     int per_sm = 0, nsm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, best.sfn, best_nt, best_smem));
@@ -382,6 +424,11 @@ void plan_sweep(ctf_ctx* c) {
     for (int l = 0; l < c->taps[n]; ++l, ++r) sp.woff[r] = n * sp.lp + sp.loff - l;
   }
   for (int n = 0; n <= c->N; ++n) sp.koff[n] = c->koff[n];
+  {
+    int rr = 0;
+    for (int n = 0; n < c->N; ++n)
+      for (int l = 0; l < c->taps[n]; ++l) sp.srcr[rr++] = n;
+  }
   for (int ch = 0; ch < c->D && ch < ctf::kMaxRows; ++ch) {
     const int m = ch / c->Ls, l = ch - m * c->Ls;
     sp.xcol[ch] = m * sp.xp + sp.xoff - l;
@@ -595,7 +642,29 @@ void run_body(ctf_ctx* c, bool do_sweep) {
 
   cudaEvent_t e0 = take_event(c), e1 = take_event(c), e2 = take_event(c);
   CK(cudaEventRecord(e0, c->stream));
-  if (c->sv.kind == 2) {
+  if (c->sv.kind == 3) {
+    ctf::ClusterParams cl{};
+    cl.s = sp;
+    cl.pivot = c->cpivot.p;
+    cl.wpivot = c->cwpivot.p;
+    cl.part = c->cpart.p;
+    cl.bad = c->cbad.p;
+    cl.CS = c->cluster_size;
+    CK(cudaMemsetAsync(c->cbad.p, 0, c->cbad.n * sizeof(int), c->stream));
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(c->FL * c->cluster_size, c->B);
+    lc.blockDim = dim3(c->NT);
+    lc.dynamicSmemBytes = c->sweep_smem;
+    lc.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = c->cluster_size;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&lc, c->sv.cfn, cl));
+  } else if (c->sv.kind == 2) {
     ctf::StreamParams st{};
     st.s = sp;
     st.scratch = c->scratch.p;
@@ -759,6 +828,13 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host) {
   c->err.alloc((size_t)c->B);
   if (c->sv.kind == 2) c->scratch.alloc((size_t)c->stream_grid * c->R * c->TP * cs);
   else c->scratch.free();
+  if (c->sv.kind == 3) {
+    const size_t tiles = (size_t)c->B * c->FL;
+    c->cpivot.alloc(tiles * 2 * c->TP * cs);
+    c->cwpivot.alloc(tiles * 2 * c->D * cs);
+    c->cpart.alloc(tiles * c->cluster_size * 4);
+    c->cbad.alloc(tiles);
+  }
   c->logdet.alloc((size_t)c->B * c->FL);
   CK(cudaMemsetAsync(c->logdet.p, 0, c->logdet.n * 8, c->stream));  // log|det I| = 0
   c->max_iters = std::max(1, prob->iterations);
@@ -1038,9 +1114,9 @@ int ctf_describe(ctf_ctx* c, char* buf, int len) {
   std::snprintf(buf, (size_t)len,
                 "{\"sweep_kernel\": \"%s<%s,RMAX=%d,FT=%d,%s=%d,NT=%d,EXACT=%d>\", \"threads\": %d, "
                 "\"smem_bytes\": %zu, \"grid\": [%d, %d], \"muv_chunks\": %d, \"bins\": [%d, %d]}",
-                c->sv.kind == 2 ? "stream_kernel" : c->sv.kind ? "rowwarp_kernel" : "sweep_kernel",
+                c->sv.kind == 3 ? "cluster_kernel" : c->sv.kind == 2 ? "stream_kernel" : c->sv.kind ? "rowwarp_kernel" : "sweep_kernel",
                 c->real_size == 4 ? "f32" : "f64", c->sv.rmax, c->sv.ft,
-                c->sv.kind == 2 ? "RG" : c->sv.kind ? "WPR" : "RREG", c->sv.rreg, c->sv.maxt, c->sv.exact, c->NT,
+                c->sv.kind == 3 ? "RREG" : c->sv.kind == 2 ? "RG" : c->sv.kind ? "WPR" : "RREG", c->sv.rreg, c->sv.maxt, c->sv.exact, c->NT,
                 c->sweep_smem, c->FL, c->B, c->nchunk, c->lo, c->hi);
   return CTF_OK;
 }

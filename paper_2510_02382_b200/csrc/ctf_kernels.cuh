@@ -65,6 +65,7 @@ struct SweepParams {
   int off_y, off_x, off_e, off_l, off_w, off_red, off_z, off_b, off_d;  // smem byte offsets
   int woff[kMaxRows];  // per row p: n_p*lp + loff - l_p (weight index base)
   int xcol[kMaxRows];  // per stacked channel c = m*Ls + l: m*xp + xoff - l (x tile offset)
+  int srcr[kMaxRows];  // source of each row
   int row0[kMaxSources], ntaps[kMaxSources], koff[kMaxSources + 1];
 };
 

@@ -208,16 +208,39 @@ __global__ void __launch_bounds__(NT, MINB) stream_kernel(const StreamParams sp)
           if (row < R) {
             const R2 zp = zsh[row];
             const int wo = p.woff[row];
+            if constexpr (std::is_same<Real, float>::value) {
+              // packed FP32x2 (see sweep_kernel): y += (-z.x) pv + z.y (pv.y, -pv.x);
+              // Q1 += s.x y, Q2 += s.y y with s = w yr; numer = (Q1.x + Q2.y, Q1.y - Q2.x)
+              float2 q1 = make_float2(0.f, 0.f), q2 = q1;
+              float den = 0.f;
 #pragma unroll
-            for (int k = 0; k < FT; ++k) {
-              const int j = tid + k * NT;
-              R2 y = Yg[(size_t)row * TP + j];
-              cmsub(y, zp, pv[k]);
-              Yg[(size_t)row * TP + j] = y;
-              const Real w = invl[wo + j];
-              a[q] = fma(fma(y.x, yr[k].x, y.y * yr[k].y), w, a[q]);
-              a[RG + q] = fma(fma(y.y, yr[k].x, -y.x * yr[k].y), w, a[RG + q]);
-              a[2 * RG + q] = fma(ar2[k], w, a[2 * RG + q]);
+              for (int k = 0; k < FT; ++k) {
+                const int j = tid + k * NT;
+                float2 y = Yg[(size_t)row * TP + j];
+                y = ffma2s(pv[k], -zp.x, y);
+                y = ffma2s(make_float2(pv[k].y, -pv[k].x), zp.y, y);
+                Yg[(size_t)row * TP + j] = y;
+                const float w = invl[wo + j];
+                const float2 sw = fmul2s(yr[k], w);
+                q1 = ffma2s(y, sw.x, q1);
+                q2 = ffma2s(y, sw.y, q2);
+                den = fmaf(ar2[k], w, den);
+              }
+              a[q] = q1.x + q2.y;
+              a[RG + q] = q1.y - q2.x;
+              a[2 * RG + q] = den;
+            } else {
+#pragma unroll
+              for (int k = 0; k < FT; ++k) {
+                const int j = tid + k * NT;
+                R2 y = Yg[(size_t)row * TP + j];
+                cmsub(y, zp, pv[k]);
+                Yg[(size_t)row * TP + j] = y;
+                const Real w = invl[wo + j];
+                a[q] = fma(fma(y.x, yr[k].x, y.y * yr[k].y), w, a[q]);
+                a[RG + q] = fma(fma(y.y, yr[k].x, -y.x * yr[k].y), w, a[RG + q]);
+                a[2 * RG + q] = fma(ar2[k], w, a[2 * RG + q]);
+              }
             }
           }
         }

@@ -8,6 +8,8 @@ std::vector<SweepVariant> sweep_variants_f64_guard();
 std::vector<SweepVariant> sweep_variants_rowwarp_f32();
 std::vector<SweepVariant> sweep_variants_f32_taps();
 std::vector<SweepVariant> sweep_variants_stream_f32();
+std::vector<SweepVariant> sweep_variants_cluster_f32();
+std::vector<SweepVariant> sweep_variants_cluster_f64();
 std::vector<SweepVariant> sweep_variants_stream_f64();
 std::vector<SweepVariant> sweep_variants_f64_taps();
 std::vector<SweepVariant> sweep_variants_rowwarp_f64();
@@ -22,6 +24,8 @@ const std::vector<SweepVariant>& sweep_variants_f32() {
     a.insert(a.end(), b.begin(), b.end());
     auto st = sweep_variants_stream_f32();
     a.insert(a.end(), st.begin(), st.end());
+    auto cl = sweep_variants_cluster_f32();
+    a.insert(a.end(), cl.begin(), cl.end());
     return a;
   }();
   return v;
@@ -37,6 +41,8 @@ const std::vector<SweepVariant>& sweep_variants_f64() {
     a.insert(a.end(), b.begin(), b.end());
     auto st = sweep_variants_stream_f64();
     a.insert(a.end(), st.begin(), st.end());
+    auto cl = sweep_variants_cluster_f64();
+    a.insert(a.end(), cl.begin(), cl.end());
     return a;
   }();
   return v;

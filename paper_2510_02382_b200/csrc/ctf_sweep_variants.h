@@ -8,6 +8,7 @@
 #include "ctf_kernels.cuh"
 #include "ctf_rowwarp.cuh"
 #include "ctf_stream.cuh"
+#include "ctf_cluster.cuh"
 
 #include <vector>
 
@@ -19,6 +20,7 @@ struct SweepVariant {
                  // 2: stream_kernel (rmax = 64, rreg = RG, launched through sfn)
   int lt = 0;    // > 0: compiled for equal taps per source (taps == lt)
   void (*sfn)(StreamParams) = nullptr;
+  void (*cfn)(ClusterParams) = nullptr;  // kind 3: cluster_kernel (rmax = rows per CTA)
 };
 #define CTF_V(REAL, PREC, RMAX, FT, RREG, NT, EX) \
   SweepVariant { PREC, RMAX, FT, RREG, NT, EX, sweep_kernel<REAL, RMAX, FT, RREG, NT, EX> }
@@ -35,6 +37,9 @@ struct SweepVariant {
 // stream_kernel: any R <= 64 in groups of RG rows, FT frames per thread
 #define CTF_ST(REAL, PREC, FT, RG, NT, MINB) \
   SweepVariant { PREC, 64, FT, RG, NT, 0, nullptr, 2, 0, stream_kernel<REAL, FT, RG, NT, MINB> }
+// cluster_kernel: R = CS * RB rows over a cluster of CS CTAs
+#define CTF_CL(REAL, PREC, RB, FT, RREG, NT) \
+  SweepVariant { PREC, RB, FT, RREG, NT, 0, nullptr, 3, 0, nullptr, cluster_kernel<REAL, RB, FT, RREG, NT> }
 // rowwarp_kernel: R = NT / (32 * WPR) rows, FT frames per lane
 #define CTF_RW(REAL, PREC, FT, WPR, NT) \
   SweepVariant { PREC, (NT) / (32 * (WPR)), FT, WPR, NT, 1, rowwarp_kernel<REAL, FT, WPR, NT>, 1, 0 }
