@@ -328,7 +328,7 @@ void plan_sweep(ctf_ctx* c) {
     } else if (v.kind == 2) {  // streamed: any R <= 64, tile in global scratch
       if (c->R > v.rmax) continue;
       TP = nt * v.ft;
-      if (TP < c->T || (nt * (v.ft - 1) >= c->T && v.ft > 1)) continue;  // avoid mostly-empty frames
+      if (TP < c->T) continue;
       const int RG = v.rreg, NG = (c->R + RG - 1) / RG, VP = ((3 * RG + 31) / 32) * 32;
       cand.xoff = c->Ls - 1;
       cand.xp = cand.xoff + TP;
@@ -374,7 +374,8 @@ void plan_sweep(ctf_ctx* c) {
     // selects it)
     const int rank = (v.kind == 3 ? 3000 : v.kind == 2 ? 2000 : v.kind == 1 ? 1000 : 0) +
                      (v.kind == 3 ? -v.rmax * 4 : v.rmax * 4) + (v.exact ? 0 : 2) + (v.lt > 0 ? 0 : 1);
-    const bool better = !found || rank < best_rank || (rank == best_rank && nt < best_nt);
+    const bool better = !found || rank < best_rank ||
+                        (rank == best_rank && (TP < c->TP || (TP == c->TP && nt < best_nt)));
     if (better) {
       found = true;
       best = v;

@@ -367,3 +367,103 @@ def test_frequency_sharded_degeneracy_reported_on_every_rank():
     lib.ctf_group_destroy(grp)
     for e in errs:
         assert e is not None and e.iteration == 1 and e.bin == 4
+
+
+@pytest.mark.parametrize("case", [
+    dict(F=7, T=37, M=1, L=3, N=1, K=1, taps=None, prec="f64"),     # single source, T not a multiple of 32, K=1
+    dict(F=5, T=61, M=7, L=1, N=2, K=2, taps=[3, 4], prec="f64"),    # R=7: guarded runtime-R variant, unequal taps
+    dict(F=4, T=90, M=5, L=4, N=2, K=3, taps=[12, 8], prec="f64"),   # R=20: beyond the resident set -> streamed
+    dict(F=9, T=33, M=2, L=8, N=2, K=5, taps=None, prec="f32"),      # R=16 stacked, short frames
+])
+def test_odd_shapes(case):
+    """Shapes off the BASELINE grid, pre-stacked (stack_taps = 1) when taps are unequal."""
+    F, T, M, L, N, K = case["F"], case["T"], case["M"], case["L"], case["N"], case["K"]
+    g = np.random.default_rng(F * 1000 + T)
+    if case["taps"] is None:
+        raw = synth_mixtures(1, F, T, M, N, L, K, 0.6, 77)
+        taps, st, x = [L] * N, L, O.stack_observation(raw[0], L)
+        xin = raw
+    else:
+        taps, st = case["taps"], 1
+        D = sum(taps)
+        x = g.standard_normal((F, T, D)) + 1j * g.standard_normal((F, T, D))
+        xin = x[None]
+    iters, seed = 3, 5
+    tol = 1e-9 if case["prec"] == "f64" else 1e-4
+    s = Session(xin if case["prec"] == "f64" else xin.astype(np.complex64), taps, [K] * N, stack_taps=st,
+                iterations=iters, precision=case["prec"], seed=seed)
+    s.iterate(iters)
+    W, B, V, obj = s.download_raw()
+    ref = O.run(O.config(taps, [K] * N, iterations=iters, seed=seed), x)
+    assert rel(W[0], ref["W"].reshape(F, -1)) <= tol
+    assert rel(B[0], ref["B"]) <= tol and rel(V[0], ref["V"]) <= tol
+    assert np.max(np.abs(obj[0] - ref["objective"]) / np.abs(ref["objective"])) <= tol
+
+
+def test_ctf_run_end_to_end_matches_device_resident_path():
+    """ctf_run (host buffers in, host buffers out) == setup + iterate + download."""
+    import ctypes
+    from paper_2510_02382_b200 import _lib
+    from paper_2510_02382_b200.api import _problem
+    B, F, T, M, L, K, iters, seed = 3, 21, 120, 2, 3, 4, 5, 8
+    raw = synth_mixtures(B, F, T, M, M, L, K, 0.6, 5)
+    s = Session(raw, [L] * M, [K] * M, stack_taps=L, iterations=iters, precision="f64", seed=seed)
+    s.iterate(iters)
+    W1, B1, V1, o1 = s.download_raw()
+    s.close()
+    lib = _lib.load()
+    R, SK = M * L, M * K
+    W = np.zeros(B * F * R * R * 2)
+    Bf = np.zeros(B * F * SK)
+    V = np.zeros(B * SK * T)
+    o = np.zeros(B * iters)
+    prob = _problem(B, F, T, M, L, [L] * M, [K] * M, iters, "f64", "f64", 1e-10, seed)
+    ctx = ctypes.c_void_p()
+    err = _lib.CtfErr()
+    assert lib.ctf_open(0, ctypes.byref(ctx), ctypes.byref(err)) == 0
+    rc = lib.ctf_run(ctx, ctypes.byref(prob), _lib.vptr(raw), _lib.dptr(W), _lib.dptr(Bf), _lib.dptr(V), _lib.dptr(o),
+                     ctypes.byref(err))
+    lib.ctf_close(ctx)
+    assert rc == 0, err.msg
+    assert np.array_equal(W.view(np.complex128).reshape(B, F, -1), W1)
+    assert np.array_equal(Bf.reshape(B, -1), B1) and np.array_equal(V.reshape(B, -1), V1)
+    assert np.array_equal(o.reshape(B, iters), o1)
+
+
+def test_cpp_reference_mirror_runs_on_gpu(tmp_path):
+    """ctfmnmf::b200::run (csrc/ctfmnmf_b200.hpp, the reference-shaped C++ API)
+    on a pre-stacked observation equals the oracle's run()."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    csrc = os.path.join(root, "paper_2510_02382_b200", "csrc")
+    libdir = os.path.join(root, "paper_2510_02382_b200")
+    g = np.random.default_rng(2)
+    F, D, T = 6, 4, 40
+    x = g.standard_normal((F, T, D)) + 1j * g.standard_normal((F, T, D))
+    xf = tmp_path / "x.bin"
+    x.astype(np.complex128).tofile(xf)
+    src = tmp_path / "run.cpp"
+    src.write_text(f'''#include "ctfmnmf_b200.hpp"
+#include <cstdio>
+#include <fstream>
+using namespace ctfmnmf::b200;
+int main() {{
+  CtfConfig c; c.num_sources = 2; c.num_channels = 4; c.taps_per_source = {{2, 2}}; c.bases_per_source = {{3, 3}};
+  c.iterations = 6; c.seed = 21;
+  MixtureSpectrogram x; x.bins.assign({F}, CMatrix({D}, {T}));
+  std::ifstream in("{xf}", std::ios::binary);
+  for (auto& b : x.bins) in.read(reinterpret_cast<char*>(b.data.data()), b.data.size() * sizeof(Complex));
+  SeparationResult r = run(c, x);
+  for (double o : r.trace.objective) std::printf("%.17g\\n", o);
+  for (const auto& w : r.demixing) for (const auto& v : w.data) std::printf("%.17g %.17g\\n", v.real(), v.imag());
+  return 0;
+}}''')
+    exe = tmp_path / "run"
+    subprocess.run(["g++", "-std=c++17", "-O1", f"-I{csrc}", "-o", str(exe), str(src), f"-L{libdir}", "-lctfiss",
+                    f"-Wl,-rpath,{libdir}"], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    obj = np.array([float(v) for v in out[:6]])
+    W = np.array([complex(*map(float, l.split())) for l in out[6:] if l.strip()]).reshape(F, D, D)
+    ref = O.run(O.config([2, 2], [3, 3], iterations=6, seed=21), x)
+    assert np.max(np.abs(obj - ref["objective"]) / np.abs(ref["objective"])) <= 1e-9
+    assert rel(W, ref["W"]) <= 1e-9
