@@ -25,6 +25,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 using ctf::kMaxRows;
@@ -88,7 +89,8 @@ template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
-  void alloc(size_t count) {
+  void alloc(size_t count) {  // keeps the allocation when the size is unchanged
+    if (p && count == n) return;
     free();
     n = count;
     if (count) CK(cudaMalloc(&p, count * sizeof(T)));
@@ -157,6 +159,7 @@ struct ctf_ctx {
   DevBuf<unsigned char> x, W, Bf, V, E, part, packed, scratch, cpivot, cwpivot;
   DevBuf<double> cpart;
   DevBuf<int> cbad;
+  DevBuf<double> stage;  // double staging for host transfers (reused)
   DevBuf<double> rowpow, objbin, packed_d, mu, floor_abs, objective, mp_part, logdet;
   DevBuf<unsigned long long> err;
   // timing
@@ -463,12 +466,49 @@ void upload_real(ctf_ctx* c, void* dst, const double* src, size_t n) {
     CK(cudaMemcpyAsync(dst, src, n * 8, cudaMemcpyHostToDevice, c->stream));
     return;
   }
-  DevBuf<double> tmp;
-  tmp.alloc(n);
-  CK(cudaMemcpyAsync(tmp.p, src, n * 8, cudaMemcpyHostToDevice, c->stream));
-  convert_kernel<float><<<std::min<size_t>((n + 255) / 256, 4096), 256, 0, c->stream>>>(tmp.p, (float*)dst, n);
+  if (c->stage.n < n) c->stage.alloc(n);
+  CK(cudaMemcpyAsync(c->stage.p, src, n * 8, cudaMemcpyHostToDevice, c->stream));
+  convert_kernel<float><<<std::min<size_t>((n + 255) / 256, 4096), 256, 0, c->stream>>>(c->stage.p, (float*)dst, n);
   CK(cudaGetLastError());
-  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaStreamSynchronize(c->stream));  // the host source may be released by the caller
+}
+
+// Device-side gathers into the double staging buffer in the host layouts
+// (then one D2H per array straight into the caller's buffer).
+template <class Real>
+__global__ void gather_W_kernel(const Real* W, double* out, size_t n) {  // same layout, precision only
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    out[i] = (double)W[i];
+}
+// B: device [mix][FL][SK] -> [mix][n][k][FL] (each B_n column-major FL x K_n)
+template <class Real>
+__global__ void gather_B_kernel(const Real* B, double* out, int nmix, int FL, int SK) {
+  const size_t n = (size_t)nmix * FL * SK;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+    const size_t mix = e / ((size_t)FL * SK);
+    const size_t rem = e - mix * FL * SK;
+    const int kk = (int)(rem / FL), i = (int)(rem - (size_t)kk * FL);  // kk = global base index (koff[n] + k)
+    out[e] = (double)B[((size_t)mix * FL + i) * SK + kk];
+  }
+}
+// V: device [mix][SK][T] -> [mix][n] column-major K_n x T, i.e. [mix][n][t][k]
+struct VMap {
+  int koff[ctf::kMaxSources + 1];
+  int N;
+};
+template <class Real>
+__global__ void gather_V_kernel(const Real* V, double* out, int nmix, int SK, int T, VMap vm) {
+  const size_t n = (size_t)nmix * SK * T;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+    const size_t mix = e / ((size_t)SK * T);
+    const size_t rem = e - mix * SK * T;  // offset inside the mixture: sum over earlier sources + (k + t*K_n)
+    int src = 0;
+    while (rem >= (size_t)vm.koff[src + 1] * T) ++src;
+    const int K = vm.koff[src + 1] - vm.koff[src];
+    const size_t o = rem - (size_t)vm.koff[src] * T;
+    const int t = (int)(o / K), k = (int)(o - (size_t)t * K);
+    out[e] = (double)V[((size_t)mix * SK + vm.koff[src] + k) * T + t];
+  }
 }
 
 void download_real(ctf_ctx* c, double* dst, const void* src, size_t n) {
@@ -477,11 +517,10 @@ void download_real(ctf_ctx* c, double* dst, const void* src, size_t n) {
     CK(cudaStreamSynchronize(c->stream));
     return;
   }
-  DevBuf<double> tmp;
-  tmp.alloc(n);
-  convert_f32_kernel<double><<<std::min<size_t>((n + 255) / 256, 4096), 256, 0, c->stream>>>((const float*)src, tmp.p, n);
+  if (c->stage.n < n) c->stage.alloc(n);
+  convert_f32_kernel<double><<<std::min<size_t>((n + 255) / 256, 4096), 256, 0, c->stream>>>((const float*)src, c->stage.p, n);
   CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(dst, tmp.p, n * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(dst, c->stage.p, n * 8, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
 }
 
@@ -902,7 +941,11 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host) {
 
   // random_factors with mt19937_64(seed + b) (model.cpp:189-208, estimator.cpp:532-533)
   std::vector<double> hb((size_t)c->B * c->FL * c->SK), hv((size_t)c->B * c->SK * c->T);
-  for (int b = 0; b < c->B; ++b) {
+  // one independent mt19937_64 stream per mixture: threads over mixtures
+  const int nth = std::max(1, std::min<int>(c->B, (int)std::thread::hardware_concurrency()));
+  std::vector<std::thread> pool;
+  for (int w = 0; w < nth; ++w) pool.emplace_back([&, w] {
+  for (int b = w; b < c->B; b += nth) {
     std::mt19937_64 rng(prob->seed + (uint64_t)b);
     std::uniform_real_distribution<double> uni(0.1, 1.0);
     for (int n = 0; n < c->N; ++n) {
@@ -916,6 +959,8 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host) {
         for (int j = 0; j < c->T; ++j) hv[((size_t)b * c->SK + c->koff[n] + k) * c->T + j] = uni(rng);
     }
   }
+  });
+  for (auto& t : pool) t.join();
   upload_real(c, c->Bf.p, hb.data(), hb.size());
   upload_real(c, c->V.p, hv.data(), hv.size());
   // W = I (model.cpp:221-227)
@@ -1172,48 +1217,42 @@ int ctf_download(ctf_ctx* c, double* W, double* Bh, double* Vh, double* objectiv
     if (!c || !c->ready) throw CtfError(CTF_ERR_CONFIG, "ctf_setup has not been called");
     if (c->pending) throw CtfError(CTF_ERR_CONFIG, "call ctf_finalize before ctf_download");
     CK(cudaSetDevice(c->device));
-    if (W) {
-      std::vector<double> w((size_t)c->B * plane_stride(c) * 2);
-      download_real(c, w.data(), c->W.p, w.size());
+    const bool f32 = c->real_size == 4;
+    const size_t wn = (size_t)c->B * plane_stride(c) * 2, bn = (size_t)c->B * c->FL * c->SK,
+                 vn = (size_t)c->B * c->SK * c->T;
+    const size_t need = std::max(wn, std::max(bn, vn));
+    if (c->stage.n < need) c->stage.alloc(need);
+    auto grid = [](size_t n) { return (int)std::min<size_t>((n + 255) / 256, 8192); };
+    if (W) {  // this rank's bins of every mixture, one strided D2H
       const size_t per = (size_t)c->R * c->D * 2;
-      for (int b = 0; b < c->B; ++b)
-        std::memcpy(W + ((size_t)b * c->F + c->lo) * per, w.data() + (size_t)b * c->FL * per, c->FL * per * 8);
+      if (f32) gather_W_kernel<float><<<grid(wn), 256, 0, c->stream>>>((const float*)c->W.p, c->stage.p, wn);
+      else gather_W_kernel<double><<<grid(wn), 256, 0, c->stream>>>((const double*)c->W.p, c->stage.p, wn);
+      CK(cudaGetLastError());
+      CK(cudaMemcpy2DAsync(W + (size_t)c->lo * per, (size_t)c->F * per * 8, c->stage.p, (size_t)c->FL * per * 8,
+                           (size_t)c->FL * per * 8, c->B, cudaMemcpyDeviceToHost, c->stream));
     }
-    if (Bh) {
-      std::vector<double> hb((size_t)c->B * c->FL * c->SK);
-      download_real(c, hb.data(), c->Bf.p, hb.size());
-      for (int b = 0; b < c->B; ++b) {
-        size_t off = (size_t)b * c->F * c->SK;
-        for (int n = 0; n < c->N; ++n) {
-          const int K = c->bases[n];
-          for (int k = 0; k < K; ++k)
-            for (int i = c->lo; i < c->hi; ++i)
-              Bh[off + (size_t)i + (size_t)k * c->F] = hb[((size_t)b * c->FL + (i - c->lo)) * c->SK + c->koff[n] + k];
-          off += (size_t)c->F * K;
-        }
-      }
+    if (Bh) {  // [mix][n][k][FL] on the device -> columns [lo, hi) of each F x K_n host matrix
+      if (f32) gather_B_kernel<float><<<grid(bn), 256, 0, c->stream>>>((const float*)c->Bf.p, c->stage.p + need * 0, c->B, c->FL, c->SK);
+      else gather_B_kernel<double><<<grid(bn), 256, 0, c->stream>>>((const double*)c->Bf.p, c->stage.p, c->B, c->FL, c->SK);
+      CK(cudaGetLastError());
+      // every (mix, base) column is FL contiguous values at host offset mix*F*SK + kk*F + lo
+      CK(cudaMemcpy2DAsync(Bh + c->lo, (size_t)c->F * 8, c->stage.p, (size_t)c->FL * 8, (size_t)c->FL * 8,
+                           (size_t)c->B * c->SK, cudaMemcpyDeviceToHost, c->stream));
     }
+    CK(cudaStreamSynchronize(c->stream));  // the staging buffer is reused below
     if (Vh) {
-      std::vector<double> hv((size_t)c->B * c->SK * c->T);
-      download_real(c, hv.data(), c->V.p, hv.size());
-      for (int b = 0; b < c->B; ++b) {
-        size_t off = (size_t)b * c->SK * c->T;
-        for (int n = 0; n < c->N; ++n) {
-          const int K = c->bases[n];
-          for (int j = 0; j < c->T; ++j)
-            for (int k = 0; k < K; ++k)
-              Vh[off + (size_t)k + (size_t)j * K] = hv[((size_t)b * c->SK + c->koff[n] + k) * c->T + j];
-          off += (size_t)K * c->T;
-        }
-      }
+      VMap vm{};
+      vm.N = c->N;
+      for (int n = 0; n <= c->N; ++n) vm.koff[n] = c->koff[n];
+      if (f32) gather_V_kernel<float><<<grid(vn), 256, 0, c->stream>>>((const float*)c->V.p, c->stage.p, c->B, c->SK, c->T, vm);
+      else gather_V_kernel<double><<<grid(vn), 256, 0, c->stream>>>((const double*)c->V.p, c->stage.p, c->B, c->SK, c->T, vm);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(Vh, c->stage.p, vn * 8, cudaMemcpyDeviceToHost, c->stream));
     }
-    if (objective && c->done > 0) {
-      std::vector<double> o((size_t)c->B * c->max_iters);
-      CK(cudaMemcpyAsync(o.data(), c->objective.p, o.size() * 8, cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaStreamSynchronize(c->stream));
-      for (int b = 0; b < c->B; ++b)
-        for (int it = 0; it < c->done; ++it) objective[(size_t)b * c->done + it] = o[(size_t)b * c->max_iters + it];
-    }
+    if (objective && c->done > 0)
+      CK(cudaMemcpy2DAsync(objective, (size_t)c->done * 8, c->objective.p, (size_t)c->max_iters * 8,
+                           (size_t)c->done * 8, c->B, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
   });
 }
 
