@@ -55,12 +55,16 @@ def dist_env():
 
 
 def flops_per_tfbin(R, D, N, K):
-    """Algorithmic flops per TF-bin*iteration (SURVEY §8(d) convention:
-    complex MAC = 8, FMA = 2; logs/divisions not counted).
-    sweep kernel: ISS sweep 20R^2 + one demix 8RD + lambda and MU-B 6NK;
-    whole iteration adds MU-V 6NK (lambda' + numerator/denominator)."""
-    sweep = 20 * R * R + 8 * R * D + 6 * N * K
-    return sweep, sweep + 6 * N * K
+    """Algorithmic flops per TF-bin*iteration, SURVEY §8(d) convention
+    (complex MAC = 8, FMA = 2; logs/divisions not counted): the reference's
+    iteration is 20R^2 (sweep) + 16RD (two demixes) + 14NK (lambda three
+    times, MU-B, MU-V). The fused sweep kernel replaces the sweep, both
+    demixes, the MU-B lambda + GEMMs and the lambda refresh (8NK); the MU-V
+    kernel the rest (6NK). Returns (sweep kernel, iteration, executed), the
+    last being what the sweep kernel actually computes (one demix: the second
+    is replaced by carrying the swept Y)."""
+    sweep = 20 * R * R + 16 * R * D + 8 * N * K
+    return sweep, sweep + 6 * N * K, 20 * R * R + 8 * R * D + 6 * N * K
 
 
 def bytes_per_tfbin(M, N, K, R, D, T, F, c):
@@ -298,7 +302,7 @@ def main():
     value = tfbins * args.steps / (ms / 1e3)
 
     # ---- roofline of the dominant kernel (the fused sweep kernel)
-    fl_sweep, fl_iter = flops_per_tfbin(R, D, N, K)
+    fl_sweep, fl_iter, fl_exec = flops_per_tfbin(R, D, N, K)
     p32, p64 = peak_probe(device) if rank == 0 else (None, None)
     peak = p32 if prec == "f32" else p64
     local_bins = s.bin_range[1] - s.bin_range[0]
@@ -317,6 +321,9 @@ def main():
                 "traffic": traffic_per_tfbin * units_per_launch if traffic_per_tfbin else None,
                 "kernel": desc["sweep_kernel"], "kernel_ms": sweep_ms,
                 "flops_per_tfbin": fl_sweep, "units_per_launch": units_per_launch,
+                "flops_note": "algorithmic (SURVEY 8(d): 20R^2 + 16RD + 8NK for the sweep kernel's share)",
+                "executed_flops_per_tfbin": fl_exec,
+                "executed_tflops": fl_exec * units_per_launch / (sweep_ms / 1e3) / 1e12,
                 "peak_source": "in-run FFMA2/DFMA chain probe (tools/peak.cu); MEASURED_PEAKS.json has no CUDA-core peak",
                 "hbm": {"achieved": bpt * units_per_launch / (sweep_ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                         "note": ("streamed tile: bytes are the tile's read+write per step; when the per-CTA "

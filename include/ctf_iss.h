@@ -76,6 +76,11 @@ typedef enum ctf_status {
 
 typedef enum ctf_precision { CTF_F64 = 0, CTF_F32 = 1 } ctf_precision;
 typedef enum ctf_rule { CTF_RULE_IP = 0, CTF_RULE_ISS = 1 } ctf_rule;
+/* CheckOptions flags (estimator.hpp:45-48): exact per-update recomputations. */
+typedef enum ctf_check {
+  CTF_CHECK_DET_LEMMA = 1,     /* det(W - z w_r^H) == det(W) (1 - z_r) */
+  CTF_CHECK_NORMALIZATION = 2  /* weighted power of the updated row == 1 */
+} ctf_check;
 
 /* Degeneracy kinds carried in ctf_err.kind. */
 typedef enum ctf_err_kind {
@@ -118,7 +123,8 @@ typedef struct ctf_problem {
   double psd_floor;                            /* relative floor, model.hpp:29 */
   uint64_t seed;                               /* mixture b is seeded with seed + b */
   int32_t threads;                             /* accepted and ignored (GPU path) */
-  int32_t reserved[7];
+  int32_t checks;                              /* CheckOptions (estimator.hpp:45-48): CTF_CHECK_* bits */
+  int32_t reserved[6];
 } ctf_problem;
 
 /* Per-phase device times of the last ctf_iterate()/ctf_run(), CUDA events. */
@@ -188,6 +194,13 @@ int ctf_psd_floor(ctf_ctx* ctx, double* floor_out /* [B] */);
  * rescale_ms, estimator.hpp:25-40) from CUDA events; rescale is fused into
  * the next sweep and reported as 0. Arrays of ctf_iterations_done() entries. */
 int ctf_trace_ms(ctf_ctx* ctx, double* demix_ms, double* mu_ms, double* rescale_ms);
+
+/* OptimizationTrace check fields (estimator.hpp:31-34) per mixture, for a
+ * problem set up with checks != 0: max det-lemma error, max normalization
+ * error (maxima over all bins, steps and iterations so far, all ranks) and
+ * checked_updates = iterations * F * R. Any pointer may be NULL. */
+int ctf_check_stats(ctf_ctx* ctx, double* max_det_lemma_error /* [B] */,
+                    double* max_normalization_error /* [B] */, int64_t* checked_updates /* [B] */);
 int ctf_get_timing(ctf_ctx* ctx, ctf_timing* out);
 int ctf_reset_timing(ctf_ctx* ctx);
 

@@ -4,8 +4,8 @@ The product is libctfiss.so (CUDA kernels for sm_100a behind the C ABI in
 include/ctf_iss.h). This package is its Python binding; the C++ mirror of the
 reference API lives in csrc/ctfmnmf_b200.hpp.
 """
-from .api import (CtfConfig, ConfigError, DegeneracyError, DeviceError, IoError, OptimizationTrace,
+from .api import (CheckOptions, CtfConfig, ConfigError, DegeneracyError, DeviceError, IoError, OptimizationTrace,
                   SeparationResult, Session, reconstruct_images, run, synth_mixtures)
 
-__all__ = ["CtfConfig", "ConfigError", "DegeneracyError", "DeviceError", "IoError", "OptimizationTrace",
+__all__ = ["CheckOptions", "CtfConfig", "ConfigError", "DegeneracyError", "DeviceError", "IoError", "OptimizationTrace",
            "SeparationResult", "Session", "reconstruct_images", "run", "synth_mixtures"]

@@ -24,6 +24,9 @@ class CtfErr(C.Structure):
                 ("bin", C.c_int32), ("row", C.c_int32), ("msg", C.c_char * 256)]
 
 
+CTF_CHECK_DET_LEMMA, CTF_CHECK_NORMALIZATION = 1, 2
+
+
 class CtfProblem(C.Structure):
     _fields_ = [("num_mixtures", C.c_int32), ("num_bins", C.c_int32), ("num_frames", C.c_int32),
                 ("num_mics", C.c_int32), ("stack_taps", C.c_int32), ("num_sources", C.c_int32),
@@ -31,7 +34,7 @@ class CtfProblem(C.Structure):
                 ("bases_per_source", C.c_int32 * CTF_MAX_SOURCES), ("iterations", C.c_int32),
                 ("update_rule", C.c_int32), ("precision", C.c_int32), ("x_precision", C.c_int32),
                 ("psd_floor", C.c_double), ("seed", C.c_uint64), ("threads", C.c_int32),
-                ("reserved", C.c_int32 * 7)]
+                ("checks", C.c_int32), ("reserved", C.c_int32 * 6)]
 
 
 class CtfTiming(C.Structure):
@@ -65,6 +68,7 @@ SIGNATURES = {
     "ctf_psd_floor": (C.c_int, [_P, _D]),
     "ctf_trace_ms": (C.c_int, [_P, _D, _D, _D]),
     "ctf_get_timing": (C.c_int, [_P, C.POINTER(CtfTiming)]),
+    "ctf_check_stats": (C.c_int, [_P, _D, _D, C.POINTER(C.c_int64)]),
     "ctf_reset_timing": (C.c_int, [_P]),
     "ctf_run": (C.c_int, [_P, C.POINTER(CtfProblem), _P, _D, _D, _D, _D, _E]),
     "ctf_project_back": (C.c_int, [_P, C.c_int, _D, _E]),

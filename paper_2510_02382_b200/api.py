@@ -108,12 +108,26 @@ class CtfConfig:
 
 
 @dataclass
+class CheckOptions:
+    """estimator.hpp:45-48: exact per-update recomputations (slow; verification only)."""
+    det_lemma: bool = False
+    normalization: bool = False
+
+    def flags(self) -> int:
+        return (L.CTF_CHECK_DET_LEMMA if self.det_lemma else 0) | \
+            (L.CTF_CHECK_NORMALIZATION if self.normalization else 0)
+
+
+@dataclass
 class OptimizationTrace:
     """estimator.hpp:25-40."""
     objective: List[float]
     demix_ms: List[float]
     mu_ms: List[float]
     rescale_ms: List[float]
+    max_det_lemma_error: float = 0.0
+    max_normalization_error: float = 0.0
+    checked_updates: int = 0
 
     def to_csv(self) -> str:
         out = ["iter,objective,t_demix_ms,t_mu_ms,t_rescale_ms"]
@@ -133,7 +147,7 @@ class SeparationResult:
 
 
 def _problem(num_mixtures, F, T, num_mics, stack_taps, taps, bases, iterations, precision, x_precision,
-             psd_floor, seed, threads=1, rule=L.CTF_RULE_ISS) -> L.CtfProblem:
+             psd_floor, seed, threads=1, rule=L.CTF_RULE_ISS, checks=0) -> L.CtfProblem:
     p = L.CtfProblem()
     p.num_mixtures, p.num_bins, p.num_frames = num_mixtures, F, T
     p.num_mics, p.stack_taps, p.num_sources = num_mics, stack_taps, len(taps)
@@ -145,7 +159,7 @@ def _problem(num_mixtures, F, T, num_mics, stack_taps, taps, bases, iterations, 
     p.iterations, p.update_rule = iterations, rule
     p.precision = L.CTF_F32 if precision in ("f32", "float32") else L.CTF_F64
     p.x_precision = L.CTF_F32 if x_precision in ("f32", "float32", "complex64") else L.CTF_F64
-    p.psd_floor, p.seed, p.threads = psd_floor, seed, threads
+    p.psd_floor, p.seed, p.threads, p.checks = psd_floor, seed, threads, checks
     return p
 
 
@@ -160,7 +174,7 @@ class Session:
 
     def __init__(self, x: np.ndarray, taps, bases, *, stack_taps=1, iterations=100, precision="f64",
                  psd_floor=1e-10, seed=0, device=0, world_size=1, rank=0, comm_id: Optional[bytes] = None,
-                 group=None):
+                 group=None, checks: int = 0):
         self.lib = L.load()
         if x.ndim != 4:
             raise ConfigError("x must have shape [B, F, T, M]")
@@ -178,7 +192,7 @@ class Session:
         _check(self.lib.ctf_open(device, C.byref(self._ctx), C.byref(err)), err)
         if group is not None:  # in-process exchange group (testing the sharded path)
             _check(self.lib.ctf_comm_init_group(self._ctx, group, rank, C.byref(err)), err)
-        elif world_size > 1:
+        elif world_size > 1 or comm_id is not None:  # NCCL (a single-rank comm only under CTF_NCCL_SINGLE_RANK=1)
             buf = (C.c_uint8 * 128).from_buffer_copy(comm_id)
             _check(self.lib.ctf_comm_init(self._ctx, world_size, rank, buf, C.byref(err)), err)
         self.world_size, self.rank = world_size, rank
@@ -186,7 +200,7 @@ class Session:
         self.lib.ctf_shard_range(F, world_size, rank, C.byref(lo), C.byref(hi))
         self.bin_range = (lo.value, hi.value)
         self.problem = _problem(B, F, T, M, stack_taps, self.taps, self.bases, iterations, precision, xprec,
-                                psd_floor, seed)
+                                psd_floor, seed, checks=checks)
         _check(self.lib.ctf_setup(self._ctx, C.byref(self.problem), L.vptr(x), C.byref(err)), err)
 
     # -- state -----------------------------------------------------------
@@ -259,6 +273,16 @@ class Session:
         self.lib.ctf_trace_ms(self._ctx, L.dptr(a), L.dptr(b), L.dptr(c))
         return a[:n], b[:n], c[:n]
 
+    def check_stats(self):
+        """CheckOptions results per mixture (estimator.hpp:31-34):
+        (max_det_lemma_error [B], max_normalization_error [B], checked_updates [B])."""
+        B = self.shape[0]
+        d, n = np.zeros(B), np.zeros(B)
+        k = (C.c_int64 * B)()
+        if self.lib.ctf_check_stats(self._ctx, L.dptr(d), L.dptr(n), k) != 0:
+            raise DeviceError("ctf_check_stats failed")
+        return d, n, np.array(list(k), np.int64)
+
     def timing(self) -> L.CtfTiming:
         t = L.CtfTiming()
         self.lib.ctf_get_timing(self._ctx, C.byref(t))
@@ -299,8 +323,8 @@ def _spectrogram_to_abi(x: np.ndarray) -> np.ndarray:
     return np.ascontiguousarray(np.transpose(x, (0, 2, 1)))[None].astype(np.complex128)
 
 
-def run(config: CtfConfig, x: np.ndarray, precision: str = "f64", device: int = 0,
-        stack_taps: int = 1) -> SeparationResult:
+def run(config: CtfConfig, x: np.ndarray, checks: Optional[CheckOptions] = None, precision: str = "f64",
+        device: int = 0, stack_taps: int = 1) -> SeparationResult:
     """estimator.hpp:122-123 on the GPU. x: (F, channels, T) complex; with
     stack_taps = L > 1, x holds num_channels / L microphones and the
     stacked observation is built on the GPU."""
@@ -312,13 +336,17 @@ def run(config: CtfConfig, x: np.ndarray, precision: str = "f64", device: int = 
     xa = _spectrogram_to_abi(x)
     s = Session(xa, config.taps_per_source, config.bases_per_source, stack_taps=stack_taps,
                 iterations=config.iterations, precision=precision, psd_floor=config.psd_floor,
-                seed=config.seed, device=device)
+                seed=config.seed, device=device, checks=checks.flags() if checks else 0)
     try:
         s.iterate(config.iterations)
         dem, bases, acts, obj = s.download()[0]
         d, m, r = s.trace_ms()
-        return SeparationResult(dem, bases, acts, float(s.psd_floor()[0]),
-                                OptimizationTrace(list(obj), list(d), list(m), list(r)))
+        tr = OptimizationTrace(list(obj), list(d), list(m), list(r))
+        if checks and checks.flags():
+            cd, cn, ck = s.check_stats()
+            tr.max_det_lemma_error, tr.max_normalization_error, tr.checked_updates = \
+                float(cd[0]), float(cn[0]), int(ck[0])
+        return SeparationResult(dem, bases, acts, float(s.psd_floor()[0]), tr)
     finally:
         s.close()
 

@@ -72,7 +72,7 @@ struct NcclApi {
   }
 };
 NcclApi g_nccl;
-enum { kNcclFloat = 7, kNcclDouble = 8, kNcclUint64 = 5, kNcclSum = 0, kNcclMin = 3 };
+enum { kNcclFloat = 7, kNcclDouble = 8, kNcclUint64 = 5, kNcclSum = 0, kNcclMax = 2, kNcclMin = 3 };
 
 struct CtfError : std::runtime_error {
   int code, kind, iteration, mixture, bin, row;
@@ -135,6 +135,10 @@ struct ctf_ctx {
   cudaStream_t stream = nullptr;
   // multi-GPU
   int world = 1, rank = 0;
+  // the exchange path (reduce -> all-reduce -> apply) runs when there are
+  // peers, or for a single-rank NCCL communicator (CTF_NCCL_SINGLE_RANK=1:
+  // exercises the NCCL call itself on one GPU)
+  bool collective() const { return world > 1 || comm != nullptr; }
   NcclComm comm = nullptr;
   ctf_group* group = nullptr;  // in-process exchange instead of NCCL
   // problem
@@ -162,6 +166,7 @@ struct ctf_ctx {
   DevBuf<double> stage;  // double staging for host transfers (reused)
   DevBuf<double> rowpow, objbin, packed_d, mu, floor_abs, objective, mp_part, logdet;
   DevBuf<unsigned long long> err;
+  DevBuf<unsigned long long> chk;  // CheckOptions maxima [B][2] (double bit patterns)
   // timing
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_sweep, ev_mu, ev_fin;
   std::vector<cudaEvent_t> ev_pool;
@@ -212,6 +217,8 @@ cudaEvent_t take_event(ctf_ctx* c) {
 
 // CtfConfig::validate (model.cpp:32-50) plus the GPU path's own limits.
 void validate(const ctf_problem& p) {
+  if (p.checks < 0 || p.checks > (CTF_CHECK_DET_LEMMA | CTF_CHECK_NORMALIZATION))
+    throw CtfError(CTF_ERR_CONFIG, "unknown check flags");
   if (p.num_sources < 1) throw CtfError(CTF_ERR_CONFIG, "n_sources must be >= 1");
   if (p.num_sources > CTF_MAX_SOURCES) throw CtfError(CTF_ERR_CONFIG, "n_sources exceeds CTF_MAX_SOURCES");
   if (p.num_mics < 1 || p.stack_taps < 1) throw CtfError(CTF_ERR_CONFIG, "n_channels must be >= 1");
@@ -258,7 +265,9 @@ void plan_sweep(ctf_ctx* c) {
   int best_nt = 0, best_rank = 0;
   const int lmax = std::max(1, *std::max_element(c->taps, c->taps + c->N));
   const int loff = ((lmax + 3) / 4) * 4;
+  const int want_chk = c->prob.checks != 0;
   for (const auto& v : vars) {
+    if (v.chk != want_chk) continue;  // CheckOptions runs on the instrumented variants only
     if (force_kind >= 0 && v.kind != force_kind) continue;
     if (force[0] && (v.rmax != force[0] || v.ft != force[1] || v.rreg != force[2] || v.maxt != force[3] ||
                      (force[4] >= 0 && v.exact != force[4])))
@@ -525,7 +534,7 @@ void download_real(ctf_ctx* c, double* dst, const void* src, size_t n) {
 }
 
 void allreduce(ctf_ctx* c, void* buf, size_t count, int dtype, int op) {
-  if (c->world <= 1 || count == 0) return;
+  if (!c->collective() || count == 0) return;
   if (c->group) {  // host exchange, fixed rank order (deterministic)
     const size_t es = dtype == kNcclFloat ? 4 : 8;
     ctf_group* g = c->group;
@@ -544,10 +553,12 @@ void allreduce(ctf_ctx* c, void* buf, size_t count, int dtype, int op) {
         double a = 0.0;
         for (int r = 0; r < g->world; ++r) a += reinterpret_cast<const double*>(g->slots[(size_t)r].data())[i];
         reinterpret_cast<double*>(out.data())[i] = a;
-      } else {  // uint64 min
-        unsigned long long a = ~0ull;
-        for (int r = 0; r < g->world; ++r)
-          a = std::min(a, reinterpret_cast<const unsigned long long*>(g->slots[(size_t)r].data())[i]);
+      } else {  // uint64 min / max
+        unsigned long long a = op == kNcclMax ? 0ull : ~0ull;
+        for (int r = 0; r < g->world; ++r) {
+          const unsigned long long v = reinterpret_cast<const unsigned long long*>(g->slots[(size_t)r].data())[i];
+          a = op == kNcclMax ? std::max(a, v) : std::min(a, v);
+        }
         reinterpret_cast<unsigned long long*>(out.data())[i] = a;
       }
     }
@@ -565,7 +576,7 @@ void allreduce(ctf_ctx* c, void* buf, size_t count, int dtype, int op) {
 // Decodes the per-mixture error keys into the reference's exception text.
 void check_errors(ctf_ctx* c) {
   std::vector<unsigned long long> keys((size_t)c->B);
-  if (c->world > 1) allreduce(c, c->err.p, (size_t)c->B, kNcclUint64, kNcclMin);
+  if (c->collective()) allreduce(c, c->err.p, (size_t)c->B, kNcclUint64, kNcclMin);
   CK(cudaMemcpyAsync(keys.data(), c->err.p, keys.size() * 8, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   for (int b = 0; b < c->B; ++b) {
@@ -674,6 +685,8 @@ void run_body(ctf_ctx* c, bool do_sweep) {
   sp.mu = c->pending ? c->mu.p : nullptr;
   sp.floor_abs = c->floor_abs.p;
   sp.err = c->err.p;
+  sp.chk = c->chk.p;
+  sp.chk_flags = c->prob.checks;
   sp.logdet = c->logdet.p;
   sp.iteration = c->done + 1;
   sp.do_sweep = do_sweep ? 1 : 0;
@@ -722,7 +735,7 @@ void run_body(ctf_ctx* c, bool do_sweep) {
     launch_muv<Real>(c);
     c->timing.launches += 1;
   }
-  if (c->world > 1) {
+  if (c->collective()) {
     launch_apply<Real>(c, 0, obj_slot, do_sweep ? 1 : 0);
     if (do_sweep) allreduce(c, c->packed.p, (size_t)c->B * 2 * c->SK * c->T, sizeof(Real) == 4 ? kNcclFloat : kNcclDouble, kNcclSum);
     allreduce(c, c->packed_d.p, (size_t)c->B * (c->R + 1), kNcclDouble, kNcclSum);
@@ -858,7 +871,7 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host) {
   CK(cudaMemsetAsync(c->V.p, 0, c->V.n, c->stream));
   c->E.alloc((size_t)c->B * c->N * c->FL * c->T * rs);
   c->part.alloc((size_t)c->nchunk * c->B * 2 * c->SK * c->T * rs);
-  c->packed.alloc(c->world > 1 ? (size_t)c->B * 2 * c->SK * c->T * rs : 16);
+  c->packed.alloc(c->collective() ? (size_t)c->B * 2 * c->SK * c->T * rs : 16);
   c->rowpow.alloc((size_t)c->B * c->FL * c->R);
   c->objbin.alloc((size_t)c->B * c->FL);
   c->packed_d.alloc((size_t)c->B * (c->R + 1));
@@ -866,6 +879,7 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host) {
   c->floor_abs.alloc((size_t)c->B);
   c->mp_part.alloc((size_t)c->B * c->FL);
   c->err.alloc((size_t)c->B);
+  c->chk.alloc((size_t)c->B * 2);
   if (c->sv.kind == 2) c->scratch.alloc((size_t)c->stream_grid * c->R * c->TP * cs);
   else c->scratch.free();
   if (c->sv.kind == 3) {
@@ -881,6 +895,7 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host) {
   c->objective.alloc((size_t)c->B * c->max_iters);
   CK(cudaMemsetAsync(c->objective.p, 0, c->objective.n * 8, c->stream));
   CK(cudaMemsetAsync(c->err.p, 0xFF, c->err.n * 8, c->stream));
+  CK(cudaMemsetAsync(c->chk.p, 0, c->chk.n * 8, c->stream));
   CK(cudaMemsetAsync(c->E.p, 0, c->E.n, c->stream));
 
   // x: this rank's bins of every mixture, converted to the compute precision
@@ -918,7 +933,7 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host) {
   CK(cudaStreamSynchronize(c->stream));
   for (int b = 0; b < c->B; ++b)
     for (int i = 0; i < c->FL; ++i) sums[(size_t)b] += mp_part[(size_t)b * c->FL + i];
-  if (c->world > 1) {
+  if (c->collective()) {
     CK(cudaMemcpyAsync(c->mp_part.p, sums.data(), sums.size() * 8, cudaMemcpyHostToDevice, c->stream));
     allreduce(c, c->mp_part.p, sums.size(), kNcclDouble, kNcclSum);
     CK(cudaMemcpyAsync(sums.data(), c->mp_part.p, sums.size() * 8, cudaMemcpyDeviceToHost, c->stream));
@@ -1045,7 +1060,8 @@ int ctf_comm_init(ctf_ctx* c, int world, int rank, const uint8_t id[128], ctf_er
     if (world < 1 || rank < 0 || rank >= world) throw CtfError(CTF_ERR_CONFIG, "bad world/rank");
     c->world = world;
     c->rank = rank;
-    if (world == 1) return;
+    const char* single = std::getenv("CTF_NCCL_SINGLE_RANK");
+    if (world == 1 && !(single && std::atoi(single) == 1)) return;
     if (!g_nccl.load()) throw CtfError(CTF_ERR_CUDA, "libnccl.so.2 could not be loaded");
     CK(cudaSetDevice(c->device));
     NcclUid u;
@@ -1159,11 +1175,13 @@ int ctf_describe(ctf_ctx* c, char* buf, int len) {
   if (!c || !buf || len <= 0) return CTF_ERR_CONFIG;
   std::snprintf(buf, (size_t)len,
                 "{\"sweep_kernel\": \"%s<%s,RMAX=%d,FT=%d,%s=%d,NT=%d,EXACT=%d>\", \"threads\": %d, "
-                "\"smem_bytes\": %zu, \"grid\": [%d, %d], \"muv_chunks\": %d, \"bins\": [%d, %d]}",
+                "\"smem_bytes\": %zu, \"grid\": [%d, %d], \"muv_chunks\": %d, \"bins\": [%d, %d], "
+                "\"world\": %d, \"rank\": %d, \"collective\": \"%s\"}",
                 c->sv.kind == 3 ? "cluster_kernel" : c->sv.kind == 2 ? "stream_kernel" : c->sv.kind ? "rowwarp_kernel" : "sweep_kernel",
                 c->real_size == 4 ? "f32" : "f64", c->sv.rmax, c->sv.ft,
                 c->sv.kind == 3 ? "RREG" : c->sv.kind == 2 ? "RG" : c->sv.kind ? "WPR" : "RREG", c->sv.rreg, c->sv.maxt, c->sv.exact, c->NT,
-                c->sweep_smem, c->FL, c->B, c->nchunk, c->lo, c->hi);
+                c->sweep_smem, c->FL, c->B, c->nchunk, c->lo, c->hi, c->world, c->rank,
+                c->group ? "host-group" : c->comm ? "nccl" : "none");
   return CTF_OK;
 }
 
@@ -1186,6 +1204,29 @@ int ctf_trace_ms(ctf_ctx* c, double* demix_ms, double* mu_ms, double* rescale_ms
     if (demix_ms) demix_ms[i] = c->it_sweep_ms[off + i];
     if (mu_ms) mu_ms[i] = c->it_mu_ms[off + i];
     if (rescale_ms) rescale_ms[i] = 0.0;
+  }
+  return CTF_OK;
+}
+
+int ctf_check_stats(ctf_ctx* c, double* max_det, double* max_norm, int64_t* checked) {
+  if (!c || !c->ready) return CTF_ERR_CONFIG;
+  try {
+    std::vector<unsigned long long> v((size_t)c->B * 2);
+    CK(cudaSetDevice(c->device));
+    if (c->collective()) allreduce(c, c->chk.p, v.size(), kNcclUint64, kNcclMax);
+    CK(cudaMemcpyAsync(v.data(), c->chk.p, v.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int b = 0; b < c->B; ++b) {
+      double d, n;
+      std::memcpy(&d, &v[(size_t)b * 2], 8);
+      std::memcpy(&n, &v[(size_t)b * 2 + 1], 8);
+      const bool on = c->prob.checks != 0;
+      if (max_det) max_det[b] = d;
+      if (max_norm) max_norm[b] = n;
+      if (checked) checked[b] = on ? (int64_t)c->done * c->F * c->R : 0;
+    }
+  } catch (const CtfError&) {
+    return CTF_ERR_CUDA;
   }
   return CTF_OK;
 }

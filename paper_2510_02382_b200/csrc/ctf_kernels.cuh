@@ -67,6 +67,11 @@ struct SweepParams {
   int xcol[kMaxRows];  // per stacked channel c = m*Ls + l: m*xp + xoff - l (x tile offset)
   int srcr[kMaxRows];  // source of each row
   int row0[kMaxSources], ntaps[kMaxSources], koff[kMaxSources + 1];
+  // CheckOptions instrumentation (estimator.hpp:45-48), CHECK variants only:
+  // bit 0 det lemma, bit 1 row normalization; per mixture the running max of
+  // each error as a double bit pattern (non-negative doubles order as u64)
+  int chk_flags;
+  unsigned long long* chk;  // [mix][2]
 };
 
 // ---------------------------------------------------------------------------
@@ -166,9 +171,9 @@ __device__ __forceinline__ void block_sum_d(double (&v)[NQ], double* dred, int l
 // pivoting on |a| with the lowest row winning ties (estimator.cpp:41-53).
 // Returns 0 ok, CTF kind 4 (zero pivot) or 5 (tiny det).
 template <typename Real>
-__device__ int warp_logdet(typename Cplx<Real>::T* A, int n, int lane, double& out) {
+__device__ int warp_logdet(typename Cplx<Real>::T* A, int n, int lane, double& out, double* phase = nullptr) {
   using R2 = typename Cplx<Real>::T;
-  double acc = 0.0;
+  double acc = 0.0, ph = 0.0;
   for (int c = 0; c < n; ++c) {
     Real best = Real(-1);
     int brow = n;
@@ -189,6 +194,7 @@ __device__ int warp_logdet(typename Cplx<Real>::T* A, int n, int lane, double& o
         brow = orow;
       }
     }
+    if (brow != c && brow < n) ph += 3.14159265358979323846;  // a row swap flips the sign
     if (brow != c && brow < n)
       for (int j = lane; j < n; j += 32) {
         const R2 t = A[j * n + c];
@@ -200,6 +206,7 @@ __device__ int warp_logdet(typename Cplx<Real>::T* A, int n, int lane, double& o
     const double mag = sqrt((double)pv.x * pv.x + (double)pv.y * pv.y);
     if (!(mag > 0.0) || !isfinite(mag)) return 4;
     acc += log(mag);
+    ph += atan2((double)pv.y, (double)pv.x);
     const Real inv = Real(1) / cnorm(pv);
     R2 pinv;
     pinv.x = pv.x * inv;
@@ -211,7 +218,23 @@ __device__ int warp_logdet(typename Cplx<Real>::T* A, int n, int lane, double& o
     __syncwarp();
   }
   out = acc;
+  if (phase) *phase = ph;
   return acc < log(1e-300) ? 5 : 0;
+}
+
+// Det-lemma check of one ISS step (estimator.cpp:560-569): W' = W - z w_r^H
+// must satisfy det W' = det W (1 - z_r). Returns |det W' - pred| / |det W'|
+// from the log-magnitude/phase of both determinants (no overflow).
+__device__ __forceinline__ double det_lemma_error(double lm_before, double ph_before, double lm_after,
+                                                  double ph_after, double zr) {
+  const double mag = exp(lm_before - lm_after) * (1.0 - zr);
+  const double ang = ph_before - ph_after;
+  const double re = 1.0 - mag * cos(ang), im = -mag * sin(ang);
+  return sqrt(re * re + im * im);
+}
+
+__device__ __forceinline__ void chk_max(unsigned long long* slot, double e) {
+  if (e >= 0.0) atomicMax(slot, (unsigned long long)__double_as_longlong(e));  // NaN is ignored (std::max)
 }
 
 // Y(k, p) accessor: rows p < RREG live in registers, the rest in shared memory.
@@ -325,7 +348,9 @@ template <typename Real> constexpr int sweep_min_blocks(int nt) {
 // LT > 0 (EXACT only): every source has LT taps, so row P is (P / LT, P % LT)
 // at compile time and the ISS weights are addressed from one base pointer
 // per source with immediate offsets.
-template <typename Real, int RMAX, int FT, int RREG, int NT, bool EXACT, int LT = 0>
+// CHECK: CheckOptions instrumentation (exact recomputation of det W after
+// every step by a warp LU, and of each updated row's weighted power).
+template <typename Real, int RMAX, int FT, int RREG, int NT, bool EXACT, int LT = 0, bool CHECK = false>
 __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(const SweepParams p) {
   using R2 = typename Cplx<Real>::T;
   constexpr int RS = RMAX - RREG;
@@ -333,6 +358,7 @@ __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(c
   constexpr int VP = ((NV + 31) / 32) * 32;
   constexpr int VM = VP / 32;
   static_assert(RMAX <= 32, "one lane per steering coefficient");
+  static_assert(!CHECK || NV < VP, "the normalization sum needs a spare reduction slot");
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT >> 5;
@@ -507,6 +533,29 @@ __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(c
   if (lane < RMAX) zs[warp * RMAX + lane] = czero<Real>();  // pass 0 applies a zero update
   __syncwarp();
   double dprod = 1.0;  // prod_r (1 - z_r): det W' = det W prod_r (1 - z_r)
+  // CHECK: det of the current W (log-magnitude, phase; warp 0), and the
+  // running maxima of both errors (tid 0)
+  double c_lm = 0.0, c_ph = 0.0, c_det = 0.0, c_norm = 0.0;
+  int c_ok = 0;
+  R2* cscr = xs;  // the x tile is dead during the sweep
+  auto check_det = [&](const R2* Wcur, double zr, bool compare) {
+    if (warp == 0) {
+      for (int i = lane; i < R * D; i += 32) cscr[i] = Wcur[i];
+      __syncwarp();
+      double lm, ph;
+      const int st = warp_logdet<Real>(cscr, R, lane, lm, &ph);
+      if (compare && c_ok && st != 4) c_det = fmax(c_det, det_lemma_error(c_lm, c_ph, lm, ph, zr));
+      c_ok = st != 4;
+      c_lm = lm;
+      c_ph = ph;
+    }
+  };
+  if constexpr (CHECK) {
+    if (p.chk_flags & 1) {
+      __syncthreads();  // every warp is past the demix (xs reads)
+      check_det(Wb, 0.0, false);
+    }
+  }
   for (int r = 0; r < R; ++r) {
     Real acc[VP];
 #pragma unroll
@@ -544,6 +593,9 @@ __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(c
             y = ffma2s(pvn[k], zp.y, y);
             Y.template set<P>(k, j, y);
             const float w = weight(pp, k, j);
+            if constexpr (CHECK) {
+              if (P == r - 1) acc[NV] = fmaf(cnorm(y), w, acc[NV]);
+            }
             const float2 sw = fmul2s(yr[k], w);
             q1 = ffma2s(y, sw.x, q1);
             q2 = ffma2s(y, sw.y, q2);
@@ -570,6 +622,9 @@ __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(c
             cmsub(y, zw[P], pv[k]);
             Y.template set<P>(k, j, y);
             const Real w = weight(pp, k, j);
+            if constexpr (CHECK) {
+              if (P == r - 1) acc[NV] = fma(cnorm(y), w, acc[NV]);
+            }
             // numer_p += y_p conj(y_r) w ; denom_p += |y_r|^2 w
             const Real tr = fma(y.x, yr.x, y.y * yr.y);
             const Real ti = fma(y.y, yr.x, -y.x * yr.y);
@@ -626,7 +681,15 @@ __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(c
         record_err<Real>(p.err, mix, err_key(p.iteration, kPhSweep, gbin, r, __ffs(badm) - 1));
       return;
     }
-    dprod *= (double)(Real(1) - __shfl_sync(kFull, z.x, r));
+    const Real zr_real = __shfl_sync(kFull, z.x, r);
+    dprod *= (double)(Real(1) - zr_real);
+    if constexpr (CHECK) {
+      if ((p.chk_flags & 2) && r > 0 && tid == 0) {  // steering_row_power of row r-1 (estimator.cpp:571-576)
+        double q = 0.0;
+        for (int w = 0; w < NW; ++w) q += (double)rs[w * VP + NV];
+        c_norm = fmax(c_norm, fabs(q / T - 1.0));
+      }
+    }
     __syncwarp();
     // iss_apply, W -= z w_r (estimator.cpp:298-302), ping-pong buffers
     const R2* Wo = Wb + (r & 1) * R * D;
@@ -637,11 +700,18 @@ __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(c
       cmsub(w, zw[q], Wo[c * R + r]);
       Wn[e] = w;
     }
+    if constexpr (CHECK) {
+      if (p.chk_flags & 1) {
+        __syncthreads();  // W' complete
+        check_det(Wn, (double)zr_real, true);
+      }
+    }
   }
   // ---- epilogue. The reference recomputes Y = W' x~ after the sweep
   // (estimator.cpp:607); here the last step's update is applied to the
   // running Y instead (same values up to rounding, one R x T pass instead of
   // an R x D x T product).
+  Real lastn = Real(0);  // CHECK: weighted power of the last updated row
   {
     const R2* zw = zs + warp * RMAX;
 #pragma unroll
@@ -659,6 +729,9 @@ __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(c
             cmsub(y, zw[P], pv[k]);
           }
           Y.template set<P>(k, j, y);
+          if constexpr (CHECK) {
+            if (P == R - 1) lastn = fma(cnorm(y), weight(pp, k, j), lastn);
+          }
         }
       });
     }
@@ -684,6 +757,7 @@ __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(c
         }
       }
     });
+    if constexpr (CHECK) rp[RP - 1] = lastn;  // RMAX < 32: a spare slot
     warp_reduce_scatter(rp, lane);
     Real* rb = red + (size_t)warp * VP;
 #pragma unroll
@@ -694,6 +768,18 @@ __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(c
     double s = 0.0;
     for (int w = 0; w < NW; ++w) s += (double)red[(size_t)w * VP + tid];
     p.rowpow[tile * R + tid] = s;
+  }
+  if constexpr (CHECK) {
+    static_assert(!CHECK || RMAX < 32, "spare row-power slot");
+    if (tid == 0) {
+      if (p.chk_flags & 2) {
+        double q = 0.0;
+        for (int w = 0; w < NW; ++w) q += (double)red[(size_t)w * VP + 31];
+        c_norm = fmax(c_norm, fabs(q / T - 1.0));
+        chk_max(p.chk + (size_t)mix * 2 + 1, c_norm);
+      }
+      if (p.chk_flags & 1) chk_max(p.chk + (size_t)mix * 2, c_det);
+    }
   }
   if (tid == 0) p.logdet[tile] = logdet + log(dprod);
   // delayed energies E_n(tau) = sum_{l<L_n, tau+l<T} |y_{row0+l}(tau+l)|^2

@@ -13,6 +13,8 @@ std::vector<SweepVariant> sweep_variants_cluster_f64();
 std::vector<SweepVariant> sweep_variants_stream_f64();
 std::vector<SweepVariant> sweep_variants_f64_taps();
 std::vector<SweepVariant> sweep_variants_rowwarp_f64();
+std::vector<SweepVariant> sweep_variants_check_f32();
+std::vector<SweepVariant> sweep_variants_check_f64();
 const std::vector<SweepVariant>& sweep_variants_f32() {
   static const std::vector<SweepVariant> v = [] {
     auto a = sweep_variants_rowwarp_f32();
@@ -26,6 +28,8 @@ const std::vector<SweepVariant>& sweep_variants_f32() {
     a.insert(a.end(), st.begin(), st.end());
     auto cl = sweep_variants_cluster_f32();
     a.insert(a.end(), cl.begin(), cl.end());
+    auto ck = sweep_variants_check_f32();
+    a.insert(a.end(), ck.begin(), ck.end());
     return a;
   }();
   return v;
@@ -43,6 +47,8 @@ const std::vector<SweepVariant>& sweep_variants_f64() {
     a.insert(a.end(), st.begin(), st.end());
     auto cl = sweep_variants_cluster_f64();
     a.insert(a.end(), cl.begin(), cl.end());
+    auto ck = sweep_variants_check_f64();
+    a.insert(a.end(), ck.begin(), ck.end());
     return a;
   }();
   return v;

@@ -21,6 +21,7 @@ struct SweepVariant {
   int lt = 0;    // > 0: compiled for equal taps per source (taps == lt)
   void (*sfn)(StreamParams) = nullptr;
   void (*cfn)(ClusterParams) = nullptr;  // kind 3: cluster_kernel (rmax = rows per CTA)
+  int chk = 0;  // kind 0 compiled with the CheckOptions instrumentation
 };
 #define CTF_V(REAL, PREC, RMAX, FT, RREG, NT, EX) \
   SweepVariant { PREC, RMAX, FT, RREG, NT, EX, sweep_kernel<REAL, RMAX, FT, RREG, NT, EX> }
@@ -30,6 +31,15 @@ struct SweepVariant {
 #define CTF_VL3(REAL, PREC, RMAX, FT, RREG, LT) \
   CTF_VL(REAL, PREC, RMAX, FT, RREG, 128, LT), CTF_VL(REAL, PREC, RMAX, FT, RREG, 256, LT), \
       CTF_VL(REAL, PREC, RMAX, FT, RREG, 512, LT)
+// CheckOptions-instrumented guarded variants (runtime R <= RMAX)
+#define CTF_VCHK(REAL, PREC, RMAX, FT, RREG, NT)                                                                 \
+  SweepVariant {                                                                                                \
+    PREC, RMAX, FT, RREG, NT, 0, sweep_kernel<REAL, RMAX, FT, RREG, NT, false, 0, true>, 0, 0, nullptr, nullptr, \
+        1                                                                                                       \
+  }
+#define CTF_VCHK3(REAL, PREC, RMAX, FT, RREG)                                           \
+  CTF_VCHK(REAL, PREC, RMAX, FT, RREG, 128), CTF_VCHK(REAL, PREC, RMAX, FT, RREG, 256), \
+      CTF_VCHK(REAL, PREC, RMAX, FT, RREG, 512)
 // one (RMAX, FT, RREG) at the three CTA sizes
 #define CTF_V3(REAL, PREC, RMAX, FT, RREG, EX) \
   CTF_V(REAL, PREC, RMAX, FT, RREG, 128, EX), CTF_V(REAL, PREC, RMAX, FT, RREG, 256, EX), \

@@ -123,7 +123,13 @@ std::vector<double> flatten(const MixtureSpectrogram& x) {
 }  // namespace
 
 SeparationResult run(const CtfConfig& config, const MixtureSpectrogram& x, const GpuOptions& gpu) {
-  const ctf_problem p = make_problem(config, x, gpu);
+  return run(config, x, CheckOptions{}, gpu);
+}
+
+SeparationResult run(const CtfConfig& config, const MixtureSpectrogram& x, const CheckOptions& checks,
+                     const GpuOptions& gpu) {
+  ctf_problem p = make_problem(config, x, gpu);
+  p.checks = (checks.det_lemma ? CTF_CHECK_DET_LEMMA : 0) | (checks.normalization ? CTF_CHECK_NORMALIZATION : 0);
   const int F = p.num_bins, T = p.num_frames, R = config.total_taps(), D = config.num_channels;
   const std::vector<double> xf = flatten(x);
   Ctx ctx(gpu.device);
@@ -157,6 +163,9 @@ SeparationResult run(const CtfConfig& config, const MixtureSpectrogram& x, const
   res.trace.mu_ms.resize(obj.size());
   res.trace.rescale_ms.resize(obj.size());
   ctf_trace_ms(ctx.c, res.trace.demix_ms.data(), res.trace.mu_ms.data(), res.trace.rescale_ms.data());
+  if (p.checks)
+    ctf_check_stats(ctx.c, &res.trace.max_det_lemma_error, &res.trace.max_normalization_error,
+                    &res.trace.checked_updates);
   return res;
 }
 

@@ -84,6 +84,10 @@ struct NmfFactors {  // model.hpp:70-80
 
 struct OptimizationTrace {  // estimator.hpp:25-40
   std::vector<double> objective, demix_ms, mu_ms, rescale_ms;
+  // Populated when the corresponding CheckOptions flag is set.
+  double max_det_lemma_error = 0.0;
+  double max_normalization_error = 0.0;
+  std::int64_t checked_updates = 0;
   std::string to_csv() const;
   double total_demix_ms() const;
   double total_mu_ms() const;
@@ -107,7 +111,16 @@ struct GpuOptions {
 
 // estimator.hpp:122-123. CheckOptions instrumentation is not offered on the
 // GPU path.
-SeparationResult run(const CtfConfig& config, const MixtureSpectrogram& x, const GpuOptions& gpu = {});
+// estimator.hpp:45-48: exact per-update recomputations on the GPU (the
+// instrumented sweep variants; verification, not production).
+struct CheckOptions {
+  bool det_lemma = false;      // det(W - z w_r^H) == det(W) (1 - z_r)
+  bool normalization = false;  // w_r^H Q_r w_r == 1 after each row update
+};
+
+SeparationResult run(const CtfConfig& config, const MixtureSpectrogram& x, const CheckOptions& checks = {},
+                     const GpuOptions& gpu = {});
+SeparationResult run(const CtfConfig& config, const MixtureSpectrogram& x, const GpuOptions& gpu);
 
 // wiener.hpp:18-20 (collapsed Wiener form, wiener.cpp:27-46).
 std::vector<MixtureSpectrogram> reconstruct_images(const std::vector<CMatrix>& demixing, const NmfFactors& factors,

@@ -8,11 +8,12 @@ Tolerances are the ones BASELINE.json's north_star states:
 Inputs are seeded synthetic mixtures (BASELINE configs[0] generator)."""
 import os
 
+import json
 import numpy as np
 import pytest
 
 from oracle import oracle as O
-from paper_2510_02382_b200 import (ConfigError, CtfConfig, DegeneracyError, Session, reconstruct_images, run,
+from paper_2510_02382_b200 import (CheckOptions, ConfigError, CtfConfig, DegeneracyError, Session, reconstruct_images, run,
                                    synth_mixtures)
 
 pytestmark = pytest.mark.gpu
@@ -158,6 +159,63 @@ def test_run_api_prestacked_general_config():
     B0 = ref["B"][:F * 2].reshape(2, F).T
     assert rel(res.bases[0], B0) <= 1e-9
     assert len(res.trace.demix_ms) == 7 and all(t > 0 for t in res.trace.demix_ms)
+
+
+def test_check_options_hooks():
+    """CheckOptions on the GPU (test_run.cpp:116-134): 2 sources x 2 taps over a
+    4-channel stacked observation, 6 bins x 30 frames, 10 iterations ->
+    checked_updates = 240, det-lemma error < 1e-10, normalization < 1e-8, the
+    same order as the oracle's exact recomputation; and the instrumented run
+    returns the same state as the plain one."""
+    raw = synth_mixtures(1, 6, 30, 2, 2, 2, 3, 0.5, 19)
+    xm = np.transpose(O.stack_observation(raw[0], 2), (0, 2, 1))  # (F, D, T)
+    cfg = CtfConfig(2, 4, [2, 2], [3, 3], iterations=10, seed=5)
+    res = run(cfg, xm, CheckOptions(det_lemma=True, normalization=True))
+    assert res.trace.checked_updates == 10 * 6 * 4
+    assert 0.0 <= res.trace.max_det_lemma_error < 1e-10
+    assert 0.0 < res.trace.max_normalization_error < 1e-8
+    det, nrm, cnt = O.run_checked(O.config([2, 2], [3, 3], iterations=10, seed=5),
+                                  np.ascontiguousarray(np.transpose(xm, (0, 2, 1))))
+    assert cnt == 240 and det < 1e-10 and nrm < 1e-8
+    plain = run(cfg, xm)
+    assert rel(res.demixing, plain.demixing) <= 1e-12
+    assert plain.trace.checked_updates == 0 and plain.trace.max_det_lemma_error == 0.0
+    only = run(cfg, xm, CheckOptions(normalization=True))
+    assert only.trace.max_det_lemma_error == 0.0 and 0.0 < only.trace.max_normalization_error < 1e-8
+    # fp32 instrumented path: identities hold to single precision
+    r32 = run(cfg, xm, CheckOptions(det_lemma=True, normalization=True), precision="f32")
+    assert r32.trace.max_det_lemma_error < 1e-3 and r32.trace.max_normalization_error < 1e-3
+
+
+def test_check_options_sharded_max_over_ranks():
+    """With frequency shards the check maxima are reduced over ranks (host group)."""
+    import threading
+    from paper_2510_02382_b200 import _lib
+    raw = synth_mixtures(2, 9, 40, 2, 2, 2, 3, 0.6, 4)
+    s = Session(raw, [2, 2], [3, 3], stack_taps=2, iterations=3, precision="f64", checks=3)
+    s.iterate(3)
+    d1, n1, k1 = s.check_stats()
+    s.close()
+    lib = _lib.load()
+    grp = lib.ctf_group_create(2)
+    out = [None, None]
+
+    def worker(r):
+        t = Session(raw, [2, 2], [3, 3], stack_taps=2, iterations=3, precision="f64", checks=3, world_size=2,
+                    rank=r, group=grp)
+        t.iterate(3)
+        out[r] = t.check_stats()
+        t.close()
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(2)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    lib.ctf_group_destroy(grp)
+    assert k1[0] == 3 * 9 * 4 and np.all(d1 < 1e-10) and np.all(n1 < 1e-8)
+    for d, n, k in out:  # every rank reports the same (global) maxima and counts
+        assert np.array_equal(k, k1)
+        assert np.array_equal(d, out[0][0]) and np.array_equal(n, out[0][1])
+        assert np.all(d < 1e-10) and np.all(n < 1e-8) and np.all(n > 0)
 
 
 def test_batch_equals_individual_runs_bitwise():
@@ -339,6 +397,36 @@ def test_frequency_sharded_contexts_match_single_context(precision, tol):
             assert rel(V, V1) <= tol  # V is replicated on every rank
             assert np.max(np.abs(obj - o1) / np.abs(o1)) <= tol
         assert sorted(covered)[0][0] == 0 and sorted(covered)[-1][1] == F
+
+
+@pytest.mark.parametrize("precision,tol", [("f64", 1e-12), ("f32", 1e-5)])
+def test_nccl_single_rank_communicator(monkeypatch, precision, tol):
+    """The NCCL exchange itself on one GPU: a single-rank communicator
+    (CTF_NCCL_SINGLE_RANK=1) drives the reduce -> ncclAllReduce -> apply path
+    (packed MU-V sums, row powers, objective, mean power, error words) and must
+    reproduce the plain world = 1 run."""
+    from paper_2510_02382_b200 import _lib
+    import ctypes
+    B, F, T, M, L, K, iters, seed = 2, 37, 300, 2, 3, 4, 4, 6
+    raw = synth_mixtures(B, F, T, M, M, L, K, 0.6, 31)
+    if precision == "f32":
+        raw = raw.astype(np.complex64)
+    s = Session(raw, [L] * M, [K] * M, stack_taps=L, iterations=iters, precision=precision, seed=seed)
+    s.iterate(iters)
+    ref = s.download_raw()
+    s.close()
+    lib = _lib.load()
+    uid, err = (ctypes.c_uint8 * 128)(), _lib.CtfErr()
+    assert lib.ctf_comm_unique_id(uid, ctypes.byref(err)) == 0, err.msg
+    monkeypatch.setenv("CTF_NCCL_SINGLE_RANK", "1")
+    s = Session(raw, [L] * M, [K] * M, stack_taps=L, iterations=iters, precision=precision, seed=seed,
+                comm_id=bytes(uid))
+    assert json.loads(s.describe())["collective"] == "nccl"
+    s.iterate(iters)
+    got = s.download_raw()
+    s.close()
+    for a, b in zip(got, ref):
+        assert rel(a, b) <= tol
 
 
 def test_frequency_sharded_degeneracy_reported_on_every_rank():
