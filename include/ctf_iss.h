@@ -15,6 +15,13 @@
  *   std::vector<MixtureSpectrogram> reconstruct_images(W, factors, x, config)
  *       proj/include/ctfmnmf/wiener.hpp:18-20, body wiener.cpp:11-49
  *       -> ctf_project_back()
+ *   Spectrogram forward_stft(const TimeSignal&, int window_len, int hop)
+ *   TimeSignal inverse_stft(const Spectrogram&)
+ *       proj/include/ctfmnmf/stft.hpp:13-18, body stft.cpp:46-139
+ *       -> ctf_stft() / ctf_istft(); the front end feeding the estimator
+ *          directly: ctf_setup_signal(); the back end of cmd_separate
+ *          (reconstruct_images + image_to_signal, wiener.cpp:51-64):
+ *          ctf_images_to_signal()
  *   CtfConfig (model.hpp:21-35) + the stacked observation of BASELINE (a)
  *       -> ctf_problem
  *   ConfigError / IoError / DegeneracyError{iteration,bin,row}
@@ -215,6 +222,37 @@ int ctf_run(ctf_ctx* ctx, const ctf_problem* prob, const void* x_host, double* W
 #define CTF_IMAGES_FULL 0
 #define CTF_IMAGES_CURRENT_FRAME 1
 int ctf_project_back(ctf_ctx* ctx, int mode, double* images, ctf_err* err);
+
+/* ---- STFT front / back end (stft.cpp:46-139, fft.cpp:9-41), fp64.
+ * Bit-identical to the reference arithmetic (radix-2 DIT with the
+ * reference's twiddle recurrence, no FMA contraction). Layouts:
+ *   samples : [channel][length] doubles (TimeSignal.samples column-major)
+ *   spec    : [bin][frame][channel] complex (Spectrogram.data, types.hpp:32)
+ * window_len: power of two in [2, 8192]; hop divides window_len.
+ * Errors are the reference's ConfigError texts ("forward_stft: ...",
+ * "inverse_stft: ..."). */
+int64_t ctf_stft_frames(int64_t length, int hop); /* 1 + ceil(length / hop) */
+int ctf_stft(ctf_ctx* ctx, const double* samples, int64_t length, int channels, int window_len, int hop,
+             double* spec /* [window_len/2+1][frames][channels] complex */, ctf_err* err);
+/* original_length <= 0: padded length - window_len (stft.cpp:107-108).
+ * samples may be NULL to only validate and query *out_len. */
+int ctf_istft(ctf_ctx* ctx, const double* spec, int bins, int frames, int channels, int window_len, int hop,
+              int64_t original_length, double* samples /* [channels][out_len] */, int64_t* out_len,
+              ctf_err* err);
+/* ctf_setup() from time-domain signals: the STFT runs on the GPU and writes
+ * this rank's bins straight into the estimator's input (no host round trip).
+ * samples: [mixture][mic][length] doubles; prob->num_bins / num_frames may be
+ * 0 (filled in) or must match window_len/2+1 and ctf_stft_frames(). */
+int ctf_setup_signal(ctf_ctx* ctx, const ctf_problem* prob, const double* samples, int64_t length,
+                     int window_len, int hop, ctf_err* err);
+/* Back end of cmd_separate: projection-back of the microphone images
+ * (stack_taps > 1: current-frame channels; else the supplied channels) and
+ * their inverse STFT, on the GPU. out: [source][mixture][channel][out_len]
+ * (ref_channel < 0) or [source][mixture][out_len] (the reference channel,
+ * wiener.cpp:51-64). Needs every bin on this context (world 1). out may be
+ * NULL to query *out_len. */
+int ctf_images_to_signal(ctf_ctx* ctx, int ref_channel, int window_len, int hop, int64_t original_length,
+                         double* out, int64_t* out_len, ctf_err* err);
 
 /* Synthetic generator of BASELINE.json configs (host code, no GPU):
  * mixture b uses mt19937_64(base_seed + b); see DESIGN.md for draw order.

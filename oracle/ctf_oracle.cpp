@@ -1003,3 +1003,159 @@ int orc_reconstruct_images(const orc_config* c, int F, int T, const double* W, c
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// STFT front/back end: restatement of
+// proj/src/fft.cpp:9-41 (iterative radix-2 FFT, recursive twiddles) and
+// proj/src/stft.cpp:14-139 (periodic Hann, reflect padding, forward STFT,
+// weighted overlap-add inverse). Layouts: TimeSignal.samples is length x
+// channels column-major (sample t of channel c at c*length + t);
+// Spectrogram.data is [bin][frame][channel] complex (types.hpp:22-47).
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;  // std::numbers::pi
+
+bool pow2(long long n) { return n > 0 && (n & (n - 1)) == 0; }
+
+void fft_inplace(C* data, size_t n, bool inverse) {  // fft.cpp:9-41
+  if (n <= 1) return;
+  for (size_t i = 1, j = 0; i < n; ++i) {
+    size_t bit = n >> 1;
+    for (; j & bit; bit >>= 1) j ^= bit;
+    j ^= bit;
+    if (i < j) std::swap(data[i], data[j]);
+  }
+  const double sign = inverse ? 1.0 : -1.0;
+  for (size_t len = 2; len <= n; len <<= 1) {
+    const double angle = sign * 2.0 * kPi / static_cast<double>(len);
+    const C wlen(std::cos(angle), std::sin(angle));
+    for (size_t i = 0; i < n; i += len) {
+      C w(1.0, 0.0);
+      for (size_t k = 0; k < len / 2; ++k) {
+        const C u = data[i + k];
+        const C v = data[i + k + len / 2] * w;
+        data[i + k] = u + v;
+        data[i + k + len / 2] = u - v;
+        w *= wlen;
+      }
+    }
+  }
+  if (inverse) {
+    const double scale = 1.0 / static_cast<double>(n);
+    for (size_t i = 0; i < n; ++i) data[i] *= scale;
+  }
+}
+
+std::vector<double> hann(int len) {  // stft.cpp:14-19
+  std::vector<double> w(static_cast<size_t>(len));
+  for (int t = 0; t < len; ++t) w[static_cast<size_t>(t)] = 0.5 - 0.5 * std::cos(2.0 * kPi * t / len);
+  return w;
+}
+
+std::vector<double> pad_channel(const double* x, int64_t n, int window_len, int64_t padded_len) {  // :25-42
+  const int half = window_len / 2;
+  std::vector<double> out(static_cast<size_t>(padded_len), 0.0);
+  for (int t = 0; t < half; ++t) {
+    int64_t src = half - t;
+    if (src >= n) src = n - 1;
+    out[static_cast<size_t>(t)] = x[src];
+  }
+  for (int64_t t = 0; t < n; ++t) out[static_cast<size_t>(half + t)] = x[t];
+  for (int64_t t = half + n; t < padded_len; ++t) {
+    int64_t src = 2 * n - 2 - (t - half);
+    if (src < 0) src = 0;
+    if (src >= n) break;
+    out[static_cast<size_t>(t)] = x[src];
+  }
+  return out;
+}
+
+}  // namespace
+
+extern "C" {
+
+int orc_fft(double* data, int64_t n, int inverse, orc_err* err) {
+  return guarded(err, [&] {
+    if (!pow2(n)) throw ConfigError("fft: length must be a power of two");
+    fft_inplace(reinterpret_cast<C*>(data), static_cast<size_t>(n), inverse != 0);
+  });
+}
+
+void orc_hann(int len, double* out) {
+  const std::vector<double> w = hann(len);
+  std::memcpy(out, w.data(), w.size() * sizeof(double));
+}
+
+int64_t orc_stft_frames(int64_t length, int hop) { return 1 + (length + hop - 1) / hop; }
+
+int orc_forward_stft(const double* samples, int64_t n, int channels, int window_len, int hop, double* spec,
+                     orc_err* err) {  // stft.cpp:46-88
+  return guarded(err, [&] {
+    if (n == 0 || channels == 0) throw ConfigError("forward_stft: empty signal");
+    if (window_len <= 0 || !pow2(window_len))
+      throw ConfigError("forward_stft: window_len must be a power of two, got " + std::to_string(window_len));
+    if (hop <= 0 || window_len % hop != 0) throw ConfigError("forward_stft: hop must divide window_len");
+    if (n < window_len) throw ConfigError("forward_stft: signal shorter than one window");
+    const int bins = window_len / 2 + 1;
+    const int frames = static_cast<int>(1 + (n + hop - 1) / hop);
+    const int64_t padded_len = static_cast<int64_t>(frames - 1) * hop + window_len;
+    const std::vector<double> window = hann(window_len);
+    std::vector<C> frame(static_cast<size_t>(window_len));
+    C* out = reinterpret_cast<C*>(spec);
+    for (int c = 0; c < channels; ++c) {
+      const std::vector<double> padded = pad_channel(samples + static_cast<int64_t>(c) * n, n, window_len, padded_len);
+      for (int j = 0; j < frames; ++j) {
+        const int64_t start = static_cast<int64_t>(j) * hop;
+        for (int t = 0; t < window_len; ++t)
+          frame[static_cast<size_t>(t)] = C(padded[static_cast<size_t>(start + t)] * window[static_cast<size_t>(t)], 0.0);
+        fft_inplace(frame.data(), static_cast<size_t>(window_len), false);
+        for (int i = 0; i < bins; ++i)
+          out[(static_cast<size_t>(i) * frames + j) * channels + c] = frame[static_cast<size_t>(i)];
+      }
+    }
+  });
+}
+
+int orc_inverse_stft(const double* spec, int bins, int frames, int channels, int window_len, int hop,
+                     int64_t original_length, double* out, int64_t* out_len_ret, orc_err* err) {  // :90-139
+  return guarded(err, [&] {
+    if (bins != window_len / 2 + 1) throw ConfigError("inverse_stft: bin count does not match window length");
+    if (hop <= 0 || window_len % hop != 0) throw ConfigError("inverse_stft: hop must divide window_len");
+    const int64_t padded_len = static_cast<int64_t>(frames - 1) * hop + window_len;
+    const std::vector<double> window = hann(window_len);
+    std::vector<double> overlap(static_cast<size_t>(padded_len), 0.0);
+    for (int j = 0; j < frames; ++j)
+      for (int t = 0; t < window_len; ++t)
+        overlap[static_cast<size_t>(static_cast<int64_t>(j) * hop + t)] +=
+            window[static_cast<size_t>(t)] * window[static_cast<size_t>(t)];
+    const int half = window_len / 2;
+    const int64_t out_len = original_length > 0 ? original_length : padded_len - window_len;
+    if (out_len + half > padded_len) throw ConfigError("inverse_stft: original_length inconsistent with frames");
+    const double peak = *std::max_element(overlap.begin(), overlap.end());
+    for (int64_t t = half; t < half + out_len; ++t)
+      if (overlap[static_cast<size_t>(t)] < 1e-9 * peak)
+        throw ConfigError("inverse_stft: window/hop pair does not cover the signal");
+    if (out_len_ret) *out_len_ret = out_len;
+    if (!out) return;
+    const C* sp = reinterpret_cast<const C*>(spec);
+    auto at = [&](int i, int j, int c) { return sp[(static_cast<size_t>(i) * frames + j) * channels + c]; };
+    std::vector<C> frame(static_cast<size_t>(window_len));
+    std::vector<double> acc(static_cast<size_t>(padded_len));
+    for (int c = 0; c < channels; ++c) {
+      std::fill(acc.begin(), acc.end(), 0.0);
+      for (int j = 0; j < frames; ++j) {
+        for (int i = 0; i < bins; ++i) frame[static_cast<size_t>(i)] = at(i, j, c);
+        for (int i = bins; i < window_len; ++i) frame[static_cast<size_t>(i)] = std::conj(at(window_len - i, j, c));
+        fft_inplace(frame.data(), static_cast<size_t>(window_len), true);
+        const int64_t start = static_cast<int64_t>(j) * hop;
+        for (int t = 0; t < window_len; ++t)
+          acc[static_cast<size_t>(start + t)] += frame[static_cast<size_t>(t)].real() * window[static_cast<size_t>(t)];
+      }
+      for (int64_t t = 0; t < out_len; ++t)
+        out[static_cast<int64_t>(c) * out_len + t] =
+            acc[static_cast<size_t>(half + t)] / overlap[static_cast<size_t>(half + t)];
+    }
+  });
+}
+
+}  // extern "C"

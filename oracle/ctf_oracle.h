@@ -105,6 +105,17 @@ int orc_reconstruct_images(const orc_config* cfg, int F, int T, const double* W,
 int orc_run_checked(const orc_config* cfg, int F, int T, const double* x, double* max_det_err,
                     double* max_norm_err, int64_t* checked, orc_err* err);
 
+/* STFT front/back end (proj/src/fft.cpp, proj/src/stft.cpp). samples:
+ * [channels][length] (TimeSignal.samples column-major); spec: [bins][frames]
+ * [channels] complex (Spectrogram.data). */
+int orc_fft(double* data /* n complex, in place */, int64_t n, int inverse, orc_err* err);
+void orc_hann(int len, double* out);
+int64_t orc_stft_frames(int64_t length, int hop);
+int orc_forward_stft(const double* samples, int64_t length, int channels, int window_len, int hop, double* spec,
+                     orc_err* err);
+int orc_inverse_stft(const double* spec, int bins, int frames, int channels, int window_len, int hop,
+                     int64_t original_length, double* out /* may be NULL */, int64_t* out_len, orc_err* err);
+
 #ifdef __cplusplus
 }
 #endif

@@ -262,3 +262,50 @@ def reconstruct_images(cfg, W, x):
                                       C.byref(err))
     _check(rc, err)
     return img
+
+
+# ---- STFT front/back end (proj/src/fft.cpp, proj/src/stft.cpp) -------------
+def fft(data: np.ndarray, inverse=False) -> np.ndarray:
+    """fft.cpp:9-41 on a copy of a complex128 vector."""
+    a = np.array(data, dtype=np.complex128, copy=True)
+    err = OrcErr()
+    _check(lib().orc_fft(_d(a.view(np.float64)), C.c_int64(a.size), int(inverse), C.byref(err)), err)
+    return a
+
+
+def hann_window(n: int) -> np.ndarray:
+    out = np.zeros(n)
+    lib().orc_hann(n, _d(out))
+    return out
+
+
+def stft_frames(length: int, hop: int) -> int:
+    lib().orc_stft_frames.restype = C.c_int64
+    return int(lib().orc_stft_frames(C.c_int64(length), hop))
+
+
+def forward_stft(samples: np.ndarray, window_len: int, hop: int) -> np.ndarray:
+    """stft.cpp:46-88. samples: (channels, length) float64 -> spec (bins, frames, channels) complex128."""
+    s = np.ascontiguousarray(samples, dtype=np.float64)
+    chans, n = s.shape
+    bins = window_len // 2 + 1 if window_len > 0 else 0
+    frames = stft_frames(n, hop) if hop > 0 else 0
+    spec = np.zeros((max(bins, 0), max(frames, 0), chans), np.complex128)
+    err = OrcErr()
+    _check(lib().orc_forward_stft(_d(s), C.c_int64(n), chans, window_len, hop, _d(spec.view(np.float64)),
+                                  C.byref(err)), err)
+    return spec
+
+
+def inverse_stft(spec: np.ndarray, window_len: int, hop: int, original_length: int = 0) -> np.ndarray:
+    """stft.cpp:90-139. spec (bins, frames, channels) -> samples (channels, length)."""
+    sp = np.ascontiguousarray(spec, dtype=np.complex128)
+    bins, frames, chans = sp.shape
+    n = C.c_int64()
+    err = OrcErr()
+    _check(lib().orc_inverse_stft(_d(sp.view(np.float64)), bins, frames, chans, window_len, hop,
+                                  C.c_int64(original_length), None, C.byref(n), C.byref(err)), err)
+    out = np.zeros((chans, n.value))
+    _check(lib().orc_inverse_stft(_d(sp.view(np.float64)), bins, frames, chans, window_len, hop,
+                                  C.c_int64(original_length), _d(out), C.byref(n), C.byref(err)), err)
+    return out

@@ -69,6 +69,14 @@ SIGNATURES = {
     "ctf_trace_ms": (C.c_int, [_P, _D, _D, _D]),
     "ctf_get_timing": (C.c_int, [_P, C.POINTER(CtfTiming)]),
     "ctf_check_stats": (C.c_int, [_P, _D, _D, C.POINTER(C.c_int64)]),
+    "ctf_stft_frames": (C.c_int64, [C.c_int64, C.c_int]),
+    "ctf_stft": (C.c_int, [_P, _D, C.c_int64, C.c_int, C.c_int, C.c_int, _D, C.POINTER(CtfErr)]),
+    "ctf_istft": (C.c_int, [_P, _D, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, _D,
+                            C.POINTER(C.c_int64), C.POINTER(CtfErr)]),
+    "ctf_setup_signal": (C.c_int, [_P, C.POINTER(CtfProblem), _D, C.c_int64, C.c_int, C.c_int,
+                                   C.POINTER(CtfErr)]),
+    "ctf_images_to_signal": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int64, _D, C.POINTER(C.c_int64),
+                                       C.POINTER(CtfErr)]),
     "ctf_reset_timing": (C.c_int, [_P]),
     "ctf_run": (C.c_int, [_P, C.POINTER(CtfProblem), _P, _D, _D, _D, _D, _E]),
     "ctf_project_back": (C.c_int, [_P, C.c_int, _D, _E]),

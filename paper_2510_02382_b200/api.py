@@ -174,13 +174,26 @@ class Session:
 
     def __init__(self, x: np.ndarray, taps, bases, *, stack_taps=1, iterations=100, precision="f64",
                  psd_floor=1e-10, seed=0, device=0, world_size=1, rank=0, comm_id: Optional[bytes] = None,
-                 group=None, checks: int = 0):
+                 group=None, checks: int = 0, signal: Optional[np.ndarray] = None, window_len: int = 0,
+                 hop: int = 0):
+        """x: [B, F, T, M] spectrogram batch, or x=None with signal = [B, M, length]
+        float64 time-domain mixtures (the STFT runs on the GPU, ctf_setup_signal)."""
         self.lib = L.load()
-        if x.ndim != 4:
-            raise ConfigError("x must have shape [B, F, T, M]")
-        xprec = "f32" if x.dtype == np.complex64 else "f64"
-        x = np.ascontiguousarray(x, dtype=np.complex64 if xprec == "f32" else np.complex128)
-        B, F, T, M = x.shape
+        if signal is not None:
+            signal = np.ascontiguousarray(signal, dtype=np.float64)
+            if signal.ndim != 3:
+                raise ConfigError("signal must have shape [B, M, length]")
+            if hop <= 0:
+                raise ConfigError("forward_stft: hop must divide window_len")
+            B, M, n = signal.shape
+            F, T = window_len // 2 + 1, int(self.lib.ctf_stft_frames(n, hop))
+            xprec = precision
+        else:
+            if x.ndim != 4:
+                raise ConfigError("x must have shape [B, F, T, M]")
+            xprec = "f32" if x.dtype == np.complex64 else "f64"
+            x = np.ascontiguousarray(x, dtype=np.complex64 if xprec == "f32" else np.complex128)
+            B, F, T, M = x.shape
         self.shape = (B, F, T, M)
         self.taps, self.bases = list(taps), list(bases)
         self.stack_taps = stack_taps
@@ -201,7 +214,12 @@ class Session:
         self.bin_range = (lo.value, hi.value)
         self.problem = _problem(B, F, T, M, stack_taps, self.taps, self.bases, iterations, precision, xprec,
                                 psd_floor, seed, checks=checks)
-        _check(self.lib.ctf_setup(self._ctx, C.byref(self.problem), L.vptr(x), C.byref(err)), err)
+        if signal is not None:
+            self.signal_length, self.window_len, self.hop = signal.shape[2], window_len, hop
+            _check(self.lib.ctf_setup_signal(self._ctx, C.byref(self.problem), L.dptr(signal), signal.shape[2],
+                                             window_len, hop, C.byref(err)), err)
+        else:
+            _check(self.lib.ctf_setup(self._ctx, C.byref(self.problem), L.vptr(x), C.byref(err)), err)
 
     # -- state -----------------------------------------------------------
     def iterate(self, n: int):
@@ -304,6 +322,23 @@ class Session:
         _check(self.lib.ctf_project_back(self._ctx, mode, img.ctypes.data_as(L._D), C.byref(err)), err)
         return img
 
+    def images_to_signal(self, ref_channel: int = -1, window_len: int = 0, hop: int = 0,
+                         original_length: int = 0) -> np.ndarray:
+        """Projection-back + inverse STFT on the GPU (cmd_separate's back end,
+        wiener.cpp:51-64): [N, B, M, length] (ref_channel < 0) or [N, B, length]."""
+        window_len = window_len or getattr(self, "window_len", 0)
+        hop = hop or getattr(self, "hop", 0)
+        original_length = original_length or getattr(self, "signal_length", 0)
+        n, err = C.c_int64(), L.CtfErr()
+        _check(self.lib.ctf_images_to_signal(self._ctx, ref_channel, window_len, hop, original_length, None,
+                                             C.byref(n), C.byref(err)), err)
+        B, F, T, M = self.shape
+        shape = (len(self.taps), B, M, n.value) if ref_channel < 0 else (len(self.taps), B, n.value)
+        out = np.zeros(shape)
+        _check(self.lib.ctf_images_to_signal(self._ctx, ref_channel, window_len, hop, original_length, L.dptr(out),
+                                             C.byref(n), C.byref(err)), err)
+        return out
+
     def close(self):
         if self._ctx:
             self.lib.ctf_close(self._ctx)
@@ -314,6 +349,53 @@ class Session:
             self.close()
         except Exception:
             pass
+
+
+_stft_ctx = {}
+
+
+def _device_ctx(device: int):
+    """A context per device for the stateless STFT entry points."""
+    if device not in _stft_ctx:
+        lib, ctx, err = L.load(), C.c_void_p(), L.CtfErr()
+        _check(lib.ctf_open(device, C.byref(ctx), C.byref(err)), err)
+        _stft_ctx[device] = ctx
+    return _stft_ctx[device]
+
+
+def forward_stft(samples: np.ndarray, window_len: int, hop: int, device: int = 0) -> np.ndarray:
+    """stft.hpp:13-15 on the GPU. samples (channels, length) float64 ->
+    spectrogram (bins, frames, channels) complex128, bit-identical to the
+    reference arithmetic."""
+    lib = L.load()
+    s = np.ascontiguousarray(samples, dtype=np.float64)
+    if s.ndim != 2:
+        raise ConfigError("samples must have shape (channels, length)")
+    chans, n = s.shape
+    bins = window_len // 2 + 1 if window_len > 0 else 1
+    frames = int(lib.ctf_stft_frames(n, hop)) if hop > 0 else 1
+    spec = np.zeros((bins, max(frames, 1), chans), np.complex128)
+    err = L.CtfErr()
+    _check(lib.ctf_stft(_device_ctx(device), L.dptr(s), n, chans, window_len, hop, L.dptr(spec), C.byref(err)), err)
+    return spec
+
+
+def inverse_stft(spec: np.ndarray, window_len: int, hop: int, original_length: int = 0,
+                 device: int = 0) -> np.ndarray:
+    """stft.hpp:17-18 on the GPU: (bins, frames, channels) -> (channels, length)."""
+    lib = L.load()
+    sp = np.ascontiguousarray(spec, dtype=np.complex128)
+    if sp.ndim != 3:
+        raise ConfigError("spectrogram must have shape (bins, frames, channels)")
+    bins, frames, chans = sp.shape
+    n, err = C.c_int64(), L.CtfErr()
+    ctx = _device_ctx(device)
+    _check(lib.ctf_istft(ctx, L.dptr(sp), bins, frames, chans, window_len, hop, original_length, None,
+                         C.byref(n), C.byref(err)), err)
+    out = np.zeros((chans, n.value))
+    _check(lib.ctf_istft(ctx, L.dptr(sp), bins, frames, chans, window_len, hop, original_length, L.dptr(out),
+                         C.byref(n), C.byref(err)), err)
+    return out
 
 
 def _spectrogram_to_abi(x: np.ndarray) -> np.ndarray:

@@ -10,6 +10,7 @@
 //   reduce_apply_kernel   (V update, mu, objective trace)
 // with no host synchronisation inside the loop.
 #include "ctf_kernels.cuh"
+#include "ctf_stft.cuh"
 #include "../../include/ctf_iss.h"
 
 #include <cuda_runtime.h>
@@ -17,6 +18,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <complex>
+#include <functional>
 #include <condition_variable>
 #include <mutex>
 #include <cstdio>
@@ -167,6 +170,11 @@ struct ctf_ctx {
   DevBuf<double> rowpow, objbin, packed_d, mu, floor_abs, objective, mp_part, logdet;
   DevBuf<unsigned long long> err;
   DevBuf<unsigned long long> chk;  // CheckOptions maxima [B][2] (double bit patterns)
+  // STFT tables (window length stft_N) and scratch
+  int stft_N = 0;
+  DevBuf<double2> stft_twf, stft_twi;
+  DevBuf<double> stft_win, stft_in, stft_out, stft_frames;
+  DevBuf<double2> stft_spec;
   // timing
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_sweep, ev_mu, ev_fin;
   std::vector<cudaEvent_t> ev_pool;
@@ -822,10 +830,11 @@ void iterate_impl(ctf_ctx* c, int n, bool finalize) {
 
 size_t plane_stride(const ctf_ctx* c) { return (size_t)c->FL * c->R * c->D; }
 
-void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host) {
+void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host,
+                const std::function<void()>& fill_x = nullptr) {
   if (!prob) throw CtfError(CTF_ERR_CONFIG, "null problem");
   validate(*prob);
-  if (!x_host) throw CtfError(CTF_ERR_CONFIG, "null mixture");
+  if (!x_host && !fill_x) throw CtfError(CTF_ERR_CONFIG, "null mixture");
   CK(cudaSetDevice(c->device));
   c->ready = false;
   c->prob = *prob;
@@ -903,8 +912,9 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host) {
   const size_t per_mix = (size_t)c->FL * c->T * c->Mx;  // complex per mixture (local)
   const bool same = (xs_in == cs);
   DevBuf<unsigned char> stage;
-  if (!same) stage.alloc(per_mix * xs_in);
-  for (int b = 0; b < c->B; ++b) {
+  if (!same && !fill_x) stage.alloc(per_mix * xs_in);
+  if (fill_x) fill_x();  // device-side producer (the GPU STFT front end)
+  for (int b = 0; b < c->B && !fill_x; ++b) {
     const unsigned char* src =
         static_cast<const unsigned char*>(x_host) + ((size_t)b * c->F + c->lo) * c->T * c->Mx * xs_in;
     unsigned char* dst = c->x.p + (size_t)b * per_mix * cs;
@@ -1309,58 +1319,209 @@ int ctf_run(ctf_ctx* c, const ctf_problem* prob, const void* x_host, double* W_o
   });
 }
 
+}  // extern "C"
+
+namespace {
+
+// Projection-back images of this rank's bins into a device buffer
+// double2 [n][mix][FL][T][Dout] (wiener.cpp:11-49).
+void compute_images(ctf_ctx* c, int mode, DevBuf<double>& out) {
+  if (!c->ready) throw CtfError(CTF_ERR_CONFIG, "ctf_setup has not been called");
+  if (c->pending) throw CtfError(CTF_ERR_CONFIG, "call ctf_finalize before ctf_project_back");
+  CK(cudaSetDevice(c->device));
+  const int Dout = mode == CTF_IMAGES_CURRENT_FRAME ? c->Mx : c->D;
+  const size_t per_bin = (size_t)c->T * Dout;
+  out.alloc((size_t)c->N * c->B * c->FL * per_bin * 2);
+  ctf::ImageParams ip{};
+  ip.x = c->x.p;
+  ip.W = c->W.p;
+  ip.out = out.p;
+  ip.err = c->err.p;
+  ip.FL = c->FL;
+  ip.bin_lo = c->lo;
+  ip.T = c->T;
+  ip.Mx = c->Mx;
+  ip.Ls = c->Ls;
+  ip.D = c->D;
+  ip.R = c->R;
+  ip.N = c->N;
+  ip.nmix = c->B;
+  ip.current_only = mode == CTF_IMAGES_CURRENT_FRAME ? 1 : 0;
+  for (int n = 0; n < c->N; ++n) {
+    ip.row0[n] = c->row0[n];
+    ip.ntaps[n] = c->taps[n];
+  }
+  const size_t cs = 2 * (size_t)c->real_size;
+  const size_t smem = (size_t)(2 * c->R * c->R + c->R * c->D) * cs + (size_t)c->Mx * (c->Ls - 1 + c->T) * cs;
+  int max_smem = 0;
+  CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+  if (smem > (size_t)max_smem) throw CtfError(CTF_ERR_UNSUPPORTED, "projection-back tile exceeds shared memory");
+  CK(cudaMemsetAsync(c->err.p, 0xFF, c->err.n * 8, c->stream));
+  if (c->real_size == 4) {
+    CK(cudaFuncSetAttribute((const void*)ctf::image_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ctf::image_kernel<float><<<dim3(c->FL, c->B), 256, smem, c->stream>>>(ip);
+  } else {
+    CK(cudaFuncSetAttribute((const void*)ctf::image_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ctf::image_kernel<double><<<dim3(c->FL, c->B), 256, smem, c->stream>>>(ip);
+  }
+  CK(cudaGetLastError());
+  c->timing.launches += 1;
+  std::vector<unsigned long long> keys((size_t)c->B);
+  CK(cudaMemcpyAsync(keys.data(), c->err.p, keys.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (int b = 0; b < c->B; ++b)
+    if (keys[(size_t)b] != ctf::kNoErr)
+      throw CtfError(CTF_ERR_DEGENERACY, "image reconstruction: demixing matrix not invertible",
+                     CTF_KIND_SINGULAR_IMAGE, -1, b, (int)((keys[(size_t)b] >> 20) & 0xFFFFF), -1);
+}
+
+// ---------------------------------------------------------------------------
+// STFT front/back end (stft.cpp:46-139). Tables are built on the host with
+// the reference's own recurrences so the GPU transform is bit-identical.
+constexpr double kPi = 3.14159265358979323846;  // std::numbers::pi
+
+bool is_pow2(long long n) { return n > 0 && (n & (n - 1)) == 0; }
+
+void stft_tables(ctf_ctx* c, int N) {
+  if (c->stft_N == N) return;
+  std::vector<double2> twf((size_t)std::max(1, N - 1)), twi((size_t)std::max(1, N - 1));
+  for (int dir = 0; dir < 2; ++dir) {
+    const double sign = dir ? 1.0 : -1.0;  // fft.cpp:29
+    auto& tw = dir ? twi : twf;
+    for (int len = 2; len <= N; len <<= 1) {
+      const double angle = sign * 2.0 * kPi / static_cast<double>(len);
+      const std::complex<double> wlen(std::cos(angle), std::sin(angle));
+      std::complex<double> w(1.0, 0.0);
+      for (int k = 0; k < len / 2; ++k) {
+        tw[(size_t)(len / 2 - 1 + k)] = make_double2(w.real(), w.imag());
+        w *= wlen;
+      }
+    }
+  }
+  std::vector<double> win((size_t)N);
+  for (int t = 0; t < N; ++t) win[(size_t)t] = 0.5 - 0.5 * std::cos(2.0 * kPi * t / N);  // stft.cpp:14-19
+  c->stft_twf.alloc(twf.size());
+  c->stft_twi.alloc(twi.size());
+  c->stft_win.alloc(win.size());
+  CK(cudaMemcpy(c->stft_twf.p, twf.data(), twf.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->stft_twi.p, twi.data(), twi.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->stft_win.p, win.data(), win.size() * 8, cudaMemcpyHostToDevice));
+  c->stft_N = N;
+}
+
+void stft_validate(int64_t n, int channels, int N, int hop) {  // stft.cpp:47-55
+  if (n == 0 || channels == 0) throw CtfError(CTF_ERR_CONFIG, "forward_stft: empty signal");
+  if (N <= 0 || !is_pow2(N))
+    throw CtfError(CTF_ERR_CONFIG, "forward_stft: window_len must be a power of two, got " + std::to_string(N));
+  if (hop <= 0 || N % hop != 0) throw CtfError(CTF_ERR_CONFIG, "forward_stft: hop must divide window_len");
+  if (n < N) throw CtfError(CTF_ERR_CONFIG, "forward_stft: signal shorter than one window");
+  if (N < 2 || N > 8192) throw CtfError(CTF_ERR_UNSUPPORTED, "window_len outside [2, 8192]");
+}
+
+int log2i(int N) {
+  int l = 0;
+  while ((1 << l) < N) ++l;
+  return l;
+}
+
+// sequences per CTA: PF frames x CC channels within 64 KB of shared memory
+void stft_blocking(int N, int C, int& PF, int& CC) {
+  const int smax = std::max(1, 65536 / (N * 16));
+  CC = std::min(C, smax);
+  PF = std::max(1, smax / CC);
+}
+
+// samples (device) [S][C][n] -> spec (device) [S][hi-lo][frames][C]
+void launch_stft(ctf_ctx* c, const double* samples, int S, int64_t n, int C, int N, int hop, int lo, int hi,
+                 void* spec, bool f32) {
+  stft_tables(c, N);
+  ctf::StftParams p{};
+  p.samples = samples;
+  p.spec = spec;
+  p.tw = c->stft_twf.p;
+  p.window = c->stft_win.p;
+  p.n = n;
+  p.N = N;
+  p.logN = log2i(N);
+  p.hop = hop;
+  p.frames = (int)(1 + (n + hop - 1) / hop);
+  p.C = C;
+  p.bin_lo = lo;
+  p.bin_hi = hi;
+  stft_blocking(N, C, p.PF, p.CC);
+  p.out_f32 = f32 ? 1 : 0;
+  const size_t smem = (size_t)p.PF * p.CC * N * 16;
+  CK(cudaFuncSetAttribute((const void*)ctf::stft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ctf::stft_kernel<<<dim3((p.frames + p.PF - 1) / p.PF, S, (C + p.CC - 1) / p.CC), 256, smem, c->stream>>>(p);
+  CK(cudaGetLastError());
+  c->timing.launches += 1;
+}
+
+// Validates an inverse transform (stft.cpp:91-114) and returns out_len.
+int64_t istft_validate(int bins, int frames, int N, int hop, int64_t original_length) {
+  if (bins != N / 2 + 1) throw CtfError(CTF_ERR_CONFIG, "inverse_stft: bin count does not match window length");
+  if (hop <= 0 || N % hop != 0) throw CtfError(CTF_ERR_CONFIG, "inverse_stft: hop must divide window_len");
+  if (N < 2 || N > 8192 || !is_pow2(N)) throw CtfError(CTF_ERR_UNSUPPORTED, "window_len outside [2, 8192]");
+  if (frames < 1) throw CtfError(CTF_ERR_CONFIG, "inverse_stft: no frames");
+  const int64_t padded_len = (int64_t)(frames - 1) * hop + N;
+  std::vector<double> win((size_t)N), overlap((size_t)padded_len, 0.0);
+  for (int t = 0; t < N; ++t) win[(size_t)t] = 0.5 - 0.5 * std::cos(2.0 * kPi * t / N);
+  for (int j = 0; j < frames; ++j)
+    for (int t = 0; t < N; ++t) overlap[(size_t)((int64_t)j * hop + t)] += win[(size_t)t] * win[(size_t)t];
+  const int half = N / 2;
+  const int64_t out_len = original_length > 0 ? original_length : padded_len - N;
+  if (out_len + half > padded_len) throw CtfError(CTF_ERR_CONFIG, "inverse_stft: original_length inconsistent with frames");
+  const double peak = *std::max_element(overlap.begin(), overlap.end());
+  for (int64_t t = half; t < half + out_len; ++t)
+    if (overlap[(size_t)t] < 1e-9 * peak)
+      throw CtfError(CTF_ERR_CONFIG, "inverse_stft: window/hop pair does not cover the signal");
+  return out_len;
+}
+
+// spec (device, double2) [S][bins][frames][C] -> out (device) [S][C][out_len]
+void launch_istft(ctf_ctx* c, const double2* spec, int S, int bins, int frames, int C, int N, int hop,
+                  int64_t out_len, double* out) {
+  stft_tables(c, N);
+  ctf::IstftParams p{};
+  p.spec = spec;
+  c->stft_frames.alloc((size_t)S * C * frames * N);
+  p.frames_buf = c->stft_frames.p;
+  p.out = out;
+  p.tw = c->stft_twi.p;
+  p.window = c->stft_win.p;
+  p.scale = 1.0 / static_cast<double>(N);  // fft.cpp:38
+  p.out_len = out_len;
+  p.N = N;
+  p.logN = log2i(N);
+  p.hop = hop;
+  p.frames = frames;
+  p.bins = bins;
+  p.C = C;
+  p.S = S;
+  stft_blocking(N, C, p.PF, p.CC);
+  const size_t smem = (size_t)p.PF * p.CC * N * 16;
+  CK(cudaFuncSetAttribute((const void*)ctf::istft_frame_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ctf::istft_frame_kernel<<<dim3((frames + p.PF - 1) / p.PF, S, (C + p.CC - 1) / p.CC), 256, smem, c->stream>>>(p);
+  CK(cudaGetLastError());
+  const int64_t total = (int64_t)S * C * out_len;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 16));
+  ctf::ola_kernel<<<grid, 256, 0, c->stream>>>(p);
+  CK(cudaGetLastError());
+  c->timing.launches += 2;
+}
+
+}  // namespace
+
+extern "C" {
+
 int ctf_project_back(ctf_ctx* c, int mode, double* images, ctf_err* err) {
   return guarded(err, [&] {
-    if (!c || !c->ready) throw CtfError(CTF_ERR_CONFIG, "ctf_setup has not been called");
-    if (c->pending) throw CtfError(CTF_ERR_CONFIG, "call ctf_finalize before ctf_project_back");
+    if (!c) throw CtfError(CTF_ERR_CONFIG, "null context");
     if (!images) throw CtfError(CTF_ERR_CONFIG, "null output");
-    CK(cudaSetDevice(c->device));
-    const int Dout = mode == CTF_IMAGES_CURRENT_FRAME ? c->Mx : c->D;
-    // local bins of every mixture, per source: [n][mix][FL][T][Dout]
-    const size_t per_bin = (size_t)c->T * Dout;
     DevBuf<double> out;
-    out.alloc((size_t)c->N * c->B * c->FL * per_bin * 2);
-    ctf::ImageParams ip{};
-    ip.x = c->x.p;
-    ip.W = c->W.p;
-    ip.out = out.p;
-    ip.err = c->err.p;
-    ip.FL = c->FL;
-    ip.bin_lo = c->lo;
-    ip.T = c->T;
-    ip.Mx = c->Mx;
-    ip.Ls = c->Ls;
-    ip.D = c->D;
-    ip.R = c->R;
-    ip.N = c->N;
-    ip.nmix = c->B;
-    ip.current_only = mode == CTF_IMAGES_CURRENT_FRAME ? 1 : 0;
-    for (int n = 0; n < c->N; ++n) {
-      ip.row0[n] = c->row0[n];
-      ip.ntaps[n] = c->taps[n];
-    }
-    const size_t cs = 2 * (size_t)c->real_size;
-    const size_t smem = (size_t)(2 * c->R * c->R + c->R * c->D) * cs + (size_t)c->Mx * (c->Ls - 1 + c->T) * cs;
-    int max_smem = 0;
-    CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
-    if (smem > (size_t)max_smem) throw CtfError(CTF_ERR_UNSUPPORTED, "projection-back tile exceeds shared memory");
-    CK(cudaMemsetAsync(c->err.p, 0xFF, c->err.n * 8, c->stream));
-    if (c->real_size == 4) {
-      CK(cudaFuncSetAttribute((const void*)ctf::image_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      ctf::image_kernel<float><<<dim3(c->FL, c->B), 256, smem, c->stream>>>(ip);
-    } else {
-      CK(cudaFuncSetAttribute((const void*)ctf::image_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      ctf::image_kernel<double><<<dim3(c->FL, c->B), 256, smem, c->stream>>>(ip);
-    }
-    CK(cudaGetLastError());
-    c->timing.launches += 1;
-    std::vector<unsigned long long> keys((size_t)c->B);
-    CK(cudaMemcpyAsync(keys.data(), c->err.p, keys.size() * 8, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    for (int b = 0; b < c->B; ++b)
-      if (keys[(size_t)b] != ctf::kNoErr)
-        throw CtfError(CTF_ERR_DEGENERACY, "image reconstruction: demixing matrix not invertible",
-                       CTF_KIND_SINGULAR_IMAGE, -1, b, (int)((keys[(size_t)b] >> 20) & 0xFFFFF), -1);
+    compute_images(c, mode, out);
+    const int Dout = mode == CTF_IMAGES_CURRENT_FRAME ? c->Mx : c->D;
+    const size_t per_bin = (size_t)c->T * Dout;
     // scatter the local bins into the full-F host layout
     for (int n = 0; n < c->N; ++n)
       for (int b = 0; b < c->B; ++b) {
@@ -1368,6 +1529,99 @@ int ctf_project_back(ctf_ctx* c, int mode, double* images, ctf_err* err) {
         const double* src = out.p + ((((size_t)n * c->B + b) * c->FL) * per_bin) * 2;
         CK(cudaMemcpyAsync(dst, src, (size_t)c->FL * per_bin * 16, cudaMemcpyDeviceToHost, c->stream));
       }
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int64_t ctf_stft_frames(int64_t length, int hop) { return hop > 0 ? 1 + (length + hop - 1) / hop : -1; }
+
+int ctf_stft(ctf_ctx* c, const double* samples, int64_t length, int channels, int window_len, int hop,
+             double* spec, ctf_err* err) {
+  return guarded(err, [&] {
+    if (!c) throw CtfError(CTF_ERR_CONFIG, "null context");
+    stft_validate(length, channels, window_len, hop);
+    if (!samples || !spec) throw CtfError(CTF_ERR_CONFIG, "null buffer");
+    CK(cudaSetDevice(c->device));
+    const int bins = window_len / 2 + 1;
+    const int64_t frames = ctf_stft_frames(length, hop);
+    c->stft_in.alloc((size_t)channels * length);
+    c->stft_spec.alloc((size_t)bins * frames * channels);
+    CK(cudaMemcpyAsync(c->stft_in.p, samples, (size_t)channels * length * 8, cudaMemcpyHostToDevice, c->stream));
+    launch_stft(c, c->stft_in.p, 1, length, channels, window_len, hop, 0, bins, c->stft_spec.p, false);
+    CK(cudaMemcpyAsync(spec, c->stft_spec.p, (size_t)bins * frames * channels * 16, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int ctf_istft(ctf_ctx* c, const double* spec, int bins, int frames, int channels, int window_len, int hop,
+              int64_t original_length, double* samples, int64_t* out_len, ctf_err* err) {
+  return guarded(err, [&] {
+    if (!c) throw CtfError(CTF_ERR_CONFIG, "null context");
+    const int64_t len = istft_validate(bins, frames, window_len, hop, original_length);
+    if (out_len) *out_len = len;
+    if (!samples) return;
+    if (!spec) throw CtfError(CTF_ERR_CONFIG, "null spectrogram");
+    if (channels < 1) throw CtfError(CTF_ERR_CONFIG, "inverse_stft: no channels");
+    CK(cudaSetDevice(c->device));
+    c->stft_spec.alloc((size_t)bins * frames * channels);
+    c->stft_out.alloc((size_t)channels * len);
+    CK(cudaMemcpyAsync(c->stft_spec.p, spec, (size_t)bins * frames * channels * 16, cudaMemcpyHostToDevice, c->stream));
+    launch_istft(c, c->stft_spec.p, 1, bins, frames, channels, window_len, hop, len, c->stft_out.p);
+    CK(cudaMemcpyAsync(samples, c->stft_out.p, (size_t)channels * len * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int ctf_setup_signal(ctf_ctx* c, const ctf_problem* prob, const double* samples, int64_t length, int window_len,
+                     int hop, ctf_err* err) {
+  return guarded(err, [&] {
+    if (!c) throw CtfError(CTF_ERR_CONFIG, "null context");
+    if (!prob) throw CtfError(CTF_ERR_CONFIG, "null problem");
+    stft_validate(length, prob->num_mics, window_len, hop);
+    if (!samples) throw CtfError(CTF_ERR_CONFIG, "null signal");
+    ctf_problem p = *prob;
+    const int bins = window_len / 2 + 1;
+    const int frames = (int)ctf_stft_frames(length, hop);
+    if ((p.num_bins && p.num_bins != bins) || (p.num_frames && p.num_frames != frames))
+      throw CtfError(CTF_ERR_CONFIG, "num_bins / num_frames do not match the STFT of the signal");
+    p.num_bins = bins;
+    p.num_frames = frames;
+    p.x_precision = p.precision;
+    CK(cudaSetDevice(c->device));
+    setup_impl(c, &p, nullptr, [&] {
+      const size_t cnt = (size_t)p.num_mixtures * p.num_mics * length;
+      c->stft_in.alloc(cnt);
+      CK(cudaMemcpyAsync(c->stft_in.p, samples, cnt * 8, cudaMemcpyHostToDevice, c->stream));
+      launch_stft(c, c->stft_in.p, p.num_mixtures, length, p.num_mics, window_len, hop, c->lo, c->hi, c->x.p,
+                  c->real_size == 4);
+    });
+  });
+}
+
+int ctf_images_to_signal(ctf_ctx* c, int ref_channel, int window_len, int hop, int64_t original_length,
+                         double* out, int64_t* out_len, ctf_err* err) {
+  return guarded(err, [&] {
+    if (!c || !c->ready) throw CtfError(CTF_ERR_CONFIG, "ctf_setup has not been called");
+    if (c->FL != c->F) throw CtfError(CTF_ERR_CONFIG, "images_to_signal needs every bin on this rank (world 1)");
+    const int64_t len = istft_validate(c->F, c->T, window_len, hop, original_length);
+    if (ref_channel >= c->Mx)  // wiener.cpp:56-59
+      throw CtfError(CTF_ERR_CONFIG, "ref_channel " + std::to_string(ref_channel) + " out of range for " +
+                                         std::to_string(c->Mx) + " channels");
+    if (out_len) *out_len = len;
+    if (!out) return;
+    // the microphone images: current-frame channels of the stacked space
+    // (stack_taps > 1) or the supplied channels (stack_taps = 1); Dout = Mx
+    DevBuf<double> img;
+    compute_images(c, c->Ls > 1 ? CTF_IMAGES_CURRENT_FRAME : CTF_IMAGES_FULL, img);
+    const int S = c->N * c->B, C = c->Mx;
+    c->stft_out.alloc((size_t)S * C * len);
+    launch_istft(c, reinterpret_cast<const double2*>(img.p), S, c->F, c->T, C, window_len, hop, len, c->stft_out.p);
+    if (ref_channel < 0) {
+      CK(cudaMemcpyAsync(out, c->stft_out.p, (size_t)S * C * len * 8, cudaMemcpyDeviceToHost, c->stream));
+    } else {
+      CK(cudaMemcpy2DAsync(out, (size_t)len * 8, c->stft_out.p + (size_t)ref_channel * len, (size_t)C * len * 8,
+                           (size_t)len * 8, (size_t)S, cudaMemcpyDeviceToHost, c->stream));
+    }
     CK(cudaStreamSynchronize(c->stream));
   });
 }

@@ -1,0 +1,152 @@
+"""GPU STFT front end / WOLA back end vs the CPU oracle restatement of
+proj/src/stft.cpp + fft.cpp (itself pinned by test_stft_kats.py against the
+reference's test_stft.cpp cases). The GPU transform uses the reference's
+arithmetic (twiddle recurrence, no FMA contraction), so parity is bitwise."""
+import threading
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2510_02382_b200 import ConfigError, Session, forward_stft, inverse_stft
+from paper_2510_02382_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+
+def _signal(channels, length, seed):
+    return np.random.default_rng(seed).standard_normal((channels, length))
+
+
+@pytest.mark.parametrize("channels,length,window,hop", [
+    (1, 64, 8, 2),          # DC-test geometry
+    (2, 4096, 1024, 256),   # 16 kHz / 1024 / 25 %
+    (1, 2000, 512, 64),
+    (1, 2000, 512, 128),
+    (3, 1500, 512, 256),    # odd channel count
+    (2, 1024, 1024, 1024),  # length == window, hop == window
+    (1, 40, 2, 1),          # smallest window
+    (2, 20000, 8192, 2048),  # largest window
+    (5, 3001, 256, 32),
+])
+def test_forward_stft_bitwise(channels, length, window, hop):
+    s = _signal(channels, length, length + window)
+    ref = O.forward_stft(s, window, hop)
+    got = forward_stft(s, window, hop)
+    assert got.shape == ref.shape
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("channels,length,window,hop", [
+    (2, 4096, 1024, 256), (1, 2000, 512, 64), (3, 1500, 512, 256), (1, 40, 2, 1), (2, 20000, 8192, 2048)])
+def test_inverse_stft_bitwise_and_round_trip(channels, length, window, hop):
+    s = _signal(channels, length, 7 * length + hop)
+    spec = O.forward_stft(s, window, hop)
+    ref = O.inverse_stft(spec, window, hop, length)
+    got = inverse_stft(spec, window, hop, length)
+    assert np.array_equal(got, ref)
+    assert np.max(np.abs(got - s)) / np.max(np.abs(s)) < 1e-10
+    # default output length (original_length = 0)
+    assert np.array_equal(inverse_stft(spec, window, hop), O.inverse_stft(spec, window, hop))
+
+
+def test_inverse_of_arbitrary_spectrum_bitwise():
+    """Non-Hermitian-consistent bins 0 and N/2 (imaginary parts dropped as in the reference)."""
+    g = np.random.default_rng(4)
+    spec = g.standard_normal((9, 11, 2)) + 1j * g.standard_normal((9, 11, 2))
+    assert np.array_equal(inverse_stft(spec, 16, 4, 30), O.inverse_stft(spec, 16, 4, 30))
+    zero = inverse_stft(np.zeros((5, 12, 1), complex), 8, 2, 16)
+    assert zero.shape == (1, 16) and np.max(np.abs(zero)) == 0.0
+
+
+def test_stft_errors_match_reference_texts():
+    s = _signal(1, 256, 5)
+    with pytest.raises(ConfigError, match="window_len must be a power of two, got 100"):
+        forward_stft(s, 100, 25)
+    with pytest.raises(ConfigError, match="hop must divide window_len"):
+        forward_stft(s, 128, 24)
+    with pytest.raises(ConfigError, match="empty signal"):
+        forward_stft(np.zeros((1, 0)), 64, 16)
+    with pytest.raises(ConfigError, match="shorter than one window"):
+        forward_stft(_signal(1, 32, 5), 64, 16)
+    with pytest.raises(ConfigError, match="bin count does not match"):
+        inverse_stft(np.zeros((4, 3, 1), complex), 8, 2)
+    with pytest.raises(ConfigError, match="inconsistent with frames"):
+        inverse_stft(np.zeros((5, 3, 1), complex), 8, 2, 1000)
+
+
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_setup_from_signal_equals_host_spectrogram(precision):
+    """ctf_setup_signal (STFT on the GPU straight into the estimator input)
+    gives the same run as ctf_setup with the oracle's spectrogram."""
+    B, M, n, window, hop, L, K = 2, 2, 3000, 256, 64, 3, 4
+    sig = np.random.default_rng(12).standard_normal((B, M, n))
+    spec = np.stack([O.forward_stft(sig[b], window, hop) for b in range(B)])  # [B, F, T, M]
+    x = spec.astype(np.complex64) if precision == "f32" else spec
+    a = Session(x, [L] * M, [K] * M, stack_taps=L, iterations=3, precision=precision, seed=3)
+    a.iterate(3)
+    ra = a.download_raw()
+    a.close()
+    b = Session(None, [L] * M, [K] * M, stack_taps=L, iterations=3, precision=precision, seed=3,
+                signal=sig, window_len=window, hop=hop)
+    assert b.shape == a.shape
+    b.iterate(3)
+    rb = b.download_raw()
+    for u, v in zip(ra, rb):
+        assert np.array_equal(u, v)
+    b.close()
+
+
+def test_setup_from_signal_sharded():
+    """Each frequency shard transforms the signal and keeps its own bins."""
+    B, M, n, window, hop, L, K = 1, 2, 2000, 128, 32, 2, 3
+    sig = np.random.default_rng(2).standard_normal((B, M, n))
+    s = Session(None, [L] * M, [K] * M, stack_taps=L, iterations=2, precision="f64", seed=1, signal=sig,
+                window_len=window, hop=hop)
+    s.iterate(2)
+    W1, B1, V1, o1 = s.download_raw()
+    s.close()
+    lib = _lib.load()
+    grp = lib.ctf_group_create(2)
+    out = [None, None]
+
+    def worker(r):
+        t = Session(None, [L] * M, [K] * M, stack_taps=L, iterations=2, precision="f64", seed=1, signal=sig,
+                    window_len=window, hop=hop, world_size=2, rank=r, group=grp)
+        t.iterate(2)
+        out[r] = (t.bin_range, t.download_raw())
+        t.close()
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(2)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    lib.ctf_group_destroy(grp)
+    for (lo, hi), (W, Bf, V, obj) in out:
+        assert np.max(np.abs(W[:, lo:hi] - W1[:, lo:hi])) <= 1e-12 * np.max(np.abs(W1))
+        assert np.max(np.abs(V - V1)) <= 1e-12 * np.max(np.abs(V1))
+
+
+def test_images_to_signal_matches_oracle_istft():
+    """Back end of cmd_separate on the GPU: projection-back images -> iSTFT,
+    all channels and the reference channel, vs the oracle's inverse STFT of
+    the same images."""
+    B, M, n, window, hop, L, K = 2, 2, 2500, 256, 64, 2, 3
+    sig = np.random.default_rng(8).standard_normal((B, M, n))
+    s = Session(None, [L] * M, [K] * M, stack_taps=L, iterations=3, precision="f64", seed=9, signal=sig,
+                window_len=window, hop=hop)
+    s.iterate(3)
+    imgs = s.project_back(current_frame_only=True)  # [N, B, F, T, M]
+    allc = s.images_to_signal()                      # [N, B, M, n]
+    ref0 = s.images_to_signal(ref_channel=1)         # [N, B, n]
+    assert allc.shape == (M, B, M, n) and ref0.shape == (M, B, n)
+    for src in range(M):
+        for b in range(B):
+            expect = O.inverse_stft(imgs[src, b], window, hop, n)
+            assert np.array_equal(allc[src, b], expect)
+            assert np.array_equal(ref0[src, b], expect[1])
+    # the source images add up to the mixture: the separated signals sum back to the input
+    total = allc.sum(axis=0)
+    assert np.max(np.abs(total - sig)) <= 1e-8 * np.max(np.abs(sig))
+    with pytest.raises(ConfigError, match="out of range"):
+        s.images_to_signal(ref_channel=M)
+    s.close()
