@@ -3,6 +3,7 @@
 
 #include "../../include/ctf_iss.h"
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -197,6 +198,86 @@ std::vector<MixtureSpectrogram> reconstruct_images(const std::vector<CMatrix>& d
                   img.data() + (static_cast<size_t>(n) * F + i) * T * D * 2, static_cast<size_t>(D) * T * sizeof(Complex));
   }
   return out;
+}
+
+MixtureSpectrogram MixtureSpectrogram::from_spectrogram(const Spectrogram& spec) {  // model.cpp
+  MixtureSpectrogram m;
+  m.bins.assign(static_cast<size_t>(spec.bins), CMatrix(spec.channels, spec.frames));
+  for (int i = 0; i < spec.bins; ++i)
+    for (int j = 0; j < spec.frames; ++j)
+      for (int c = 0; c < spec.channels; ++c) m.bins[static_cast<size_t>(i)](c, j) = spec.at(i, j, c);
+  return m;
+}
+
+Spectrogram MixtureSpectrogram::to_spectrogram(const Spectrogram& meta) const {
+  Spectrogram s;
+  s.window_len = meta.window_len;
+  s.hop = meta.hop;
+  s.sample_rate = meta.sample_rate;
+  s.original_length = meta.original_length;
+  s.resize(num_bins(), num_frames(), num_channels());
+  for (int i = 0; i < s.bins; ++i)
+    for (int j = 0; j < s.frames; ++j)
+      for (int c = 0; c < s.channels; ++c) s.at(i, j, c) = bins[static_cast<size_t>(i)](c, j);
+  return s;
+}
+
+std::vector<double> hann_window(int window_len) {  // stft.cpp:14-19
+  std::vector<double> w(static_cast<size_t>(std::max(window_len, 0)));
+  for (int t = 0; t < window_len; ++t)
+    w[static_cast<size_t>(t)] = 0.5 - 0.5 * std::cos(2.0 * 3.14159265358979323846 * t / window_len);
+  return w;
+}
+
+Spectrogram forward_stft(const TimeSignal& signal, int window_len, int hop, const GpuOptions& gpu) {
+  Ctx ctx(gpu.device);
+  ctf_err e{};
+  const std::int64_t n = signal.length();
+  const int chans = signal.channels();
+  Spectrogram spec;
+  const std::int64_t frames = hop > 0 ? ctf_stft_frames(n, hop) : 0;
+  spec.resize(window_len > 0 ? window_len / 2 + 1 : 0, static_cast<int>(frames), chans);
+  spec.window_len = window_len;
+  spec.hop = hop;
+  spec.sample_rate = signal.sample_rate;
+  spec.original_length = n;
+  if (ctf_stft(ctx.c, signal.samples.data.data(), n, chans, window_len, hop,
+               reinterpret_cast<double*>(spec.data.data()), &e) != CTF_OK)
+    rethrow(e);
+  return spec;
+}
+
+TimeSignal inverse_stft(const Spectrogram& spec, const GpuOptions& gpu) {
+  Ctx ctx(gpu.device);
+  ctf_err e{};
+  std::int64_t len = 0;
+  const double* sp = reinterpret_cast<const double*>(spec.data.data());
+  if (ctf_istft(ctx.c, sp, spec.bins, spec.frames, spec.channels, spec.window_len, spec.hop, spec.original_length,
+                nullptr, &len, &e) != CTF_OK)
+    rethrow(e);
+  TimeSignal out;
+  out.sample_rate = spec.sample_rate;
+  out.samples = RMatrix(static_cast<int>(len), spec.channels);
+  if (ctf_istft(ctx.c, sp, spec.bins, spec.frames, spec.channels, spec.window_len, spec.hop, spec.original_length,
+                out.samples.data.data(), &len, &e) != CTF_OK)
+    rethrow(e);
+  return out;
+}
+
+TimeSignal image_to_signal(const MixtureSpectrogram& image, const Spectrogram& meta, int ref_channel,
+                           const GpuOptions& gpu) {  // wiener.cpp:51-64
+  TimeSignal all = inverse_stft(image.to_spectrogram(meta), gpu);
+  if (ref_channel < 0) return all;
+  if (ref_channel >= all.channels())
+    throw ConfigError("ref_channel " + std::to_string(ref_channel) + " out of range for " +
+                      std::to_string(all.channels()) + " channels");
+  TimeSignal mono;
+  mono.sample_rate = all.sample_rate;
+  mono.samples = RMatrix(all.samples.rows, 1);
+  std::copy(all.samples.data.begin() + static_cast<std::ptrdiff_t>(ref_channel) * all.samples.rows,
+            all.samples.data.begin() + static_cast<std::ptrdiff_t>(ref_channel + 1) * all.samples.rows,
+            mono.samples.data.begin());
+  return mono;
 }
 
 }  // namespace b200

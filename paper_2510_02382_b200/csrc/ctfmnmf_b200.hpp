@@ -67,6 +67,29 @@ struct CtfConfig {
   void validate() const;  // throws ConfigError (model.cpp:32-50)
 };
 
+// types.hpp:12-47 — time signal (length x channels, column-major) and the
+// one-sided STFT tensor indexed [bin][frame][channel].
+struct TimeSignal {
+  RMatrix samples;
+  double sample_rate = 0.0;
+  std::int64_t length() const { return samples.rows; }
+  int channels() const { return samples.cols; }
+};
+struct Spectrogram {
+  int bins = 0, frames = 0, channels = 0, window_len = 0, hop = 0;
+  double sample_rate = 0.0;
+  std::int64_t original_length = 0;
+  std::vector<Complex> data;  // (i * frames + j) * channels + c
+  Complex& at(int i, int j, int c) { return data[(static_cast<size_t>(i) * frames + j) * channels + c]; }
+  Complex at(int i, int j, int c) const { return data[(static_cast<size_t>(i) * frames + j) * channels + c]; }
+  void resize(int b, int f, int c) {
+    bins = b;
+    frames = f;
+    channels = c;
+    data.assign(static_cast<size_t>(b) * f * c, Complex(0, 0));
+  }
+};
+
 // model.hpp:55-66 — one channels x frames matrix per bin.
 struct MixtureSpectrogram {
   std::vector<CMatrix> bins;
@@ -74,6 +97,9 @@ struct MixtureSpectrogram {
   int num_channels() const { return bins.empty() ? 0 : bins[0].rows; }
   int num_frames() const { return bins.empty() ? 0 : bins[0].cols; }
   double mean_power() const;
+  static MixtureSpectrogram from_spectrogram(const Spectrogram& spec);
+  // meta supplies window/hop/rate fields for the round trip back to disk.
+  Spectrogram to_spectrogram(const Spectrogram& meta) const;
 };
 
 struct NmfFactors {  // model.hpp:70-80
@@ -109,8 +135,6 @@ struct GpuOptions {
   int stack_taps = 1;
 };
 
-// estimator.hpp:122-123. CheckOptions instrumentation is not offered on the
-// GPU path.
 // estimator.hpp:45-48: exact per-update recomputations on the GPU (the
 // instrumented sweep variants; verification, not production).
 struct CheckOptions {
@@ -126,6 +150,15 @@ SeparationResult run(const CtfConfig& config, const MixtureSpectrogram& x, const
 std::vector<MixtureSpectrogram> reconstruct_images(const std::vector<CMatrix>& demixing, const NmfFactors& factors,
                                                    const MixtureSpectrogram& x, const CtfConfig& config,
                                                    const GpuOptions& gpu = {});
+
+// stft.hpp:9-18 on the GPU (bit-identical to the reference arithmetic).
+std::vector<double> hann_window(int window_len);
+Spectrogram forward_stft(const TimeSignal& signal, int window_len, int hop, const GpuOptions& gpu = {});
+TimeSignal inverse_stft(const Spectrogram& spec, const GpuOptions& gpu = {});
+
+// wiener.hpp:22-24: inverse STFT of one source image; ref_channel < 0 keeps all.
+TimeSignal image_to_signal(const MixtureSpectrogram& image, const Spectrogram& meta, int ref_channel = -1,
+                           const GpuOptions& gpu = {});
 
 }  // namespace b200
 }  // namespace ctfmnmf

@@ -150,3 +150,50 @@ def test_images_to_signal_matches_oracle_istft():
     with pytest.raises(ConfigError, match="out of range"):
         s.images_to_signal(ref_channel=M)
     s.close()
+
+
+def test_cpp_mirror_stft_round_trip(tmp_path):
+    """ctfmnmf::b200::forward_stft / inverse_stft / image_to_signal (the
+    reference-shaped C++ API) on the GPU equal the oracle bit for bit."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    csrc = os.path.join(root, "paper_2510_02382_b200", "csrc")
+    libdir = os.path.join(root, "paper_2510_02382_b200")
+    s = _signal(2, 3000, 77)
+    sf = tmp_path / "s.bin"
+    s.tofile(sf)  # [channel][length] == TimeSignal.samples column-major
+    src = tmp_path / "stft.cpp"
+    src.write_text(f'''#include "ctfmnmf_b200.hpp"
+#include <cstdio>
+#include <fstream>
+using namespace ctfmnmf::b200;
+int main() {{
+  TimeSignal sig; sig.sample_rate = 16000; sig.samples = RMatrix(3000, 2);
+  std::ifstream in("{sf}", std::ios::binary);
+  in.read(reinterpret_cast<char*>(sig.samples.data.data()), sig.samples.data.size() * 8);
+  Spectrogram spec = forward_stft(sig, 512, 128);
+  std::printf("%d %d %d %lld\\n", spec.bins, spec.frames, spec.channels, (long long)spec.original_length);
+  for (const auto& v : spec.data) std::printf("%.17g %.17g\\n", v.real(), v.imag());
+  TimeSignal back = inverse_stft(spec);
+  for (double v : back.samples.data) std::printf("%.17g\\n", v);
+  TimeSignal one = image_to_signal(MixtureSpectrogram::from_spectrogram(spec), spec, 1);
+  for (double v : one.samples.data) std::printf("%.17g\\n", v);
+  try {{ forward_stft(sig, 100, 25); return 3; }} catch (const ConfigError&) {{}}
+  try {{ image_to_signal(MixtureSpectrogram::from_spectrogram(spec), spec, 2); return 4; }} catch (const ConfigError&) {{}}
+  return 0;
+}}''')
+    exe = tmp_path / "stft"
+    subprocess.run(["g++", "-std=c++17", "-O1", f"-I{csrc}", "-o", str(exe), str(src), f"-L{libdir}", "-lctfiss",
+                    f"-Wl,-rpath,{libdir}"], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    bins, frames, chans, olen = map(int, out[0].split())
+    ref = O.forward_stft(s, 512, 128)
+    assert (bins, frames, chans, olen) == (*ref.shape, 3000)
+    nspec = bins * frames * chans
+    spec = np.array([complex(*map(float, l.split())) for l in out[1:1 + nspec]]).reshape(ref.shape)
+    assert np.array_equal(spec, ref)
+    back = np.array([float(v) for v in out[1 + nspec:1 + nspec + 6000]]).reshape(2, 3000)
+    assert np.array_equal(back, O.inverse_stft(ref, 512, 128, 3000))
+    one = np.array([float(v) for v in out[1 + nspec + 6000:1 + nspec + 9000]])
+    assert np.array_equal(one, back[1])
