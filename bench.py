@@ -208,6 +208,7 @@ def main():
     ap.add_argument("--unique", type=int, default=16,
                     help="distinct synthetic mixtures generated; the batch tiles them (seeds still differ per mixture)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-frontend", action="store_true", help="skip the STFT/iSTFT front-end measurement")
     args = ap.parse_args()
     world, rank, local = dist_env()
     B, F, T, M, L, K, rho, iters = CFGS[args.cfg]
@@ -340,6 +341,9 @@ def main():
         e2e = run_e2e(args, LB, x, prec, device, world, rank, comm_id, barrier, max_over_ranks, s.bin_range,
                       (B, F, T, M, N, L, K, R, D, iters, c))
     del x
+    frontend = None
+    if rank == 0 and not args.no_frontend:
+        frontend = bench_frontend(args, LB, device, B, M, T, hbm_peak)
 
     if rank == 0:
         cpu = None
@@ -353,12 +357,78 @@ def main():
                 "data": "synthetic (BASELINE configs generator, seeded; no public dataset)", "config": config,
                 "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": e2e,
-                "gpu_launches": gpu_launches, "clocks": clocks,
+                "gpu_launches": gpu_launches, "clocks": clocks, "frontend": frontend,
                 "kernels": {"sweep_ms_per_iteration": sweep_ms, "mu_ms_per_iteration": timing.mu_ms / args.steps,
                             "variant": desc}}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def bench_frontend(args, LB, device, B, M, T, hbm_peak, window=1024, hop=256):
+    """STFT front end and WOLA inverse on the config's
+    mixtures as time signals: B x M channels of (T-1)*hop samples, window
+    1024 / hop 256 (16 kHz setup of test_stft.cpp:72-80), fp64. Device-timed
+    with CUDA events on the library stream; bytes are algorithmic (samples
+    read once, spectrogram written once, and the reverse for the inverse,
+    plus its windowed-frame scratch written and read once)."""
+    import ctypes
+    import torch
+    from oracle import oracle as O
+    lib = LB.load()
+    ctx, err = ctypes.c_void_p(), LB.CtfErr()
+    assert lib.ctf_open(device, ctypes.byref(ctx), ctypes.byref(err)) == 0, err.msg
+    stream = torch.cuda.ExternalStream(lib.ctf_stream(ctx), device=device)
+    n = (T - 1) * hop
+    frames = int(lib.ctf_stft_frames(n, hop))
+    bins = window // 2 + 1
+    g = torch.Generator(device=f"cuda:{device}").manual_seed(args.seed)
+    sig = torch.randn((B, M, n), dtype=torch.float64, device=f"cuda:{device}", generator=g)
+    spec = torch.empty((B, bins, frames, M), dtype=torch.complex128, device=f"cuda:{device}")
+    back = torch.empty((B, M, n), dtype=torch.float64, device=f"cuda:{device}")
+    torch.cuda.synchronize(device)
+
+    def fwd():
+        assert lib.ctf_stft_device(ctx, sig.data_ptr(), B, n, M, window, hop, spec.data_ptr(), 0,
+                                   ctypes.byref(err)) == 0, err.msg
+
+    def inv():
+        assert lib.ctf_istft_device(ctx, spec.data_ptr(), B, bins, frames, M, window, hop, n, back.data_ptr(),
+                                    ctypes.byref(err)) == 0, err.msg
+
+    def timed(fn, reps=5):
+        for _ in range(2):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1) / reps / 1e3
+
+    t_f = timed(fwd)
+    t_i = timed(inv)
+    rt_err = float((back - sig).abs().max() / sig.abs().max())
+    lib.ctf_close(ctx)
+    samples = B * M * n
+    b_f = samples * 8 + B * bins * frames * M * 16
+    b_i = B * bins * frames * M * 16 + samples * 8 + 2 * B * M * frames * window * 8
+    # CPU: the oracle restatement of stft.cpp on one mixture (bounded sample)
+    one = sig[0].cpu().numpy()
+    t0 = time.perf_counter()
+    O.forward_stft(one, window, hop)
+    t_cpu = time.perf_counter() - t0
+    del sig, spec, back
+    return {"workload": f"{B} mixtures x {M} mics x {n} samples, window {window}, hop {hop} -> {bins} bins x "
+                        f"{frames} frames (fp64, bit-identical to the reference arithmetic)",
+            "stft": {"ms": t_f * 1e3, "samples_per_s": samples / t_f, "gbs": b_f / t_f / 1e9,
+                     "hbm_frac": b_f / t_f / 1e9 / hbm_peak, "bytes": b_f},
+            "istft": {"ms": t_i * 1e3, "samples_per_s": samples / t_i, "gbs": b_i / t_i / 1e9,
+                      "hbm_frac": b_i / t_i / 1e9 / hbm_peak, "bytes": b_i},
+            "round_trip_max_rel_err": rt_err,
+            "cpu_stft": {"samples_per_s": M * n / t_cpu, "cores": 1, "kind": "port",
+                         "sample": f"1 mixture x {M} mics, oracle restatement of stft.cpp"}}
 
 
 def run_e2e(args, LB, x, prec, device, world, rank, comm_id, barrier, max_over_ranks, bin_range, dims):

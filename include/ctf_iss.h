@@ -239,6 +239,14 @@ int ctf_stft(ctf_ctx* ctx, const double* samples, int64_t length, int channels, 
 int ctf_istft(ctf_ctx* ctx, const double* spec, int bins, int frames, int channels, int window_len, int hop,
               int64_t original_length, double* samples /* [channels][out_len] */, int64_t* out_len,
               ctf_err* err);
+/* Device-pointer forms, stream-ordered on ctf_stream(ctx) (no synchronize):
+ * num_signals independent signals, samples [signal][channel][length],
+ * spec [signal][bin][frame][channel] (complex128, or complex64 output when
+ * out_precision == CTF_F32; the inverse takes complex128). */
+int ctf_stft_device(ctf_ctx* ctx, const double* samples, int num_signals, int64_t length, int channels,
+                    int window_len, int hop, void* spec, int out_precision, ctf_err* err);
+int ctf_istft_device(ctf_ctx* ctx, const double* spec, int num_signals, int bins, int frames, int channels,
+                     int window_len, int hop, int64_t original_length, double* samples, ctf_err* err);
 /* ctf_setup() from time-domain signals: the STFT runs on the GPU and writes
  * this rank's bins straight into the estimator's input (no host round trip).
  * samples: [mixture][mic][length] doubles; prob->num_bins / num_frames may be

@@ -73,6 +73,10 @@ SIGNATURES = {
     "ctf_stft": (C.c_int, [_P, _D, C.c_int64, C.c_int, C.c_int, C.c_int, _D, C.POINTER(CtfErr)]),
     "ctf_istft": (C.c_int, [_P, _D, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, _D,
                             C.POINTER(C.c_int64), C.POINTER(CtfErr)]),
+    "ctf_stft_device": (C.c_int, [_P, C.c_void_p, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                  C.c_int, C.POINTER(CtfErr)]),
+    "ctf_istft_device": (C.c_int, [_P, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                   C.c_int64, C.c_void_p, C.POINTER(CtfErr)]),
     "ctf_setup_signal": (C.c_int, [_P, C.POINTER(CtfProblem), _D, C.c_int64, C.c_int, C.c_int,
                                    C.POINTER(CtfErr)]),
     "ctf_images_to_signal": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int64, _D, C.POINTER(C.c_int64),

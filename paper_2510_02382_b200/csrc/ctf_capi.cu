@@ -170,6 +170,8 @@ struct ctf_ctx {
   DevBuf<double> rowpow, objbin, packed_d, mu, floor_abs, objective, mp_part, logdet;
   DevBuf<unsigned long long> err;
   DevBuf<unsigned long long> chk;  // CheckOptions maxima [B][2] (double bit patterns)
+  DevBuf<int4> gtab;                // gram_kernel task table
+  std::vector<int4> gtab_host;
   // STFT tables (window length stft_N) and scratch
   int stft_N = 0;
   DevBuf<double2> stft_twf, stft_twi;
@@ -253,6 +255,69 @@ void validate(const ctf_problem& p) {
   if (p.num_bins >= (1 << 20)) throw CtfError(CTF_ERR_UNSUPPORTED, "too many bins");
 }
 
+// Task table of gram_kernel: the (m, m', d) groups of the Hermitian half
+// (m < m' all lags, m == m' lags d >= 0), each with 2L-1-|d| weight lags;
+// threads are shared out in proportion to that count and every group's frame
+// range [U0, U1) is split into contiguous chunks of whole register blocks.
+void build_gram_table(ctf_ctx* c, int NT, int M, int L) {
+  struct Grp { int m, m2, d, alo, cnt; };
+  std::vector<Grp> gs;
+  for (int m = 0; m < M; ++m)
+    for (int m2 = m; m2 < M; ++m2)
+      for (int d = (m == m2 ? 0 : -(L - 1)); d <= L - 1; ++d) {
+        const int alo = std::max(-(L - 1), -(L - 1) - d), ahi = std::min(L - 1, L - 1 - d);
+        gs.push_back({m, m2, d, alo, ahi - alo + 1});
+      }
+  // sorted by lag count (descending): a warp spans at most two adjacent counts
+  std::stable_sort(gs.begin(), gs.end(), [](const Grp& a, const Grp& b) { return a.cnt > b.cnt; });
+  const int ng = (int)gs.size();
+  if (ng > NT) throw CtfError(CTF_ERR_UNSUPPORTED, "gram kernel: more lag groups than threads");
+  long total = 0;
+  for (const auto& g : gs) total += g.cnt;
+  std::vector<int> th((size_t)ng, 1);
+  int used = ng;
+  // largest-remainder share of the remaining threads, proportional to cnt
+  std::vector<double> want((size_t)ng);
+  for (int g = 0; g < ng; ++g) want[(size_t)g] = (double)NT * gs[(size_t)g].cnt / (double)total;
+  while (used < NT) {
+    int best = 0;
+    double bd = -1e30;
+    for (int g = 0; g < ng; ++g) {
+      const double deficit = want[(size_t)g] - th[(size_t)g];
+      if (deficit > bd) {
+        bd = deficit;
+        best = g;
+      }
+    }
+    th[(size_t)best] += 1;
+    ++used;
+  }
+  // frames u in [U0, U0 + len): chunks of one odd length (the last shorter)
+  const int U0 = -(L - 1), len = c->T + 2 * (L - 1);
+  std::vector<int4> tab((size_t)NT + 1 + 2 * ng);
+  int t = 0;
+  for (int g = 0; g < ng; ++g) {
+    const int want_n = th[(size_t)g];
+    const int clen = ((len + want_n - 1) / want_n) | 1;
+    const int n = (len + clen - 1) / clen;
+    const int t0 = t;
+    for (int i = 0; i < want_n; ++i) {
+      if (i < n) {
+        tab[(size_t)t] = make_int4(g, U0 + i * clen, U0 + std::min(len, (i + 1) * clen), 0);
+      } else {
+        tab[(size_t)t] = make_int4(-1, 0, 0, 0);
+      }
+      ++t;
+    }
+    tab[(size_t)NT + 1 + 2 * g] = make_int4(gs[(size_t)g].m, gs[(size_t)g].m2, gs[(size_t)g].d, gs[(size_t)g].alo);
+    tab[(size_t)NT + 2 + 2 * g] = make_int4(gs[(size_t)g].cnt, t0, t0 + n, 0);
+  }
+  tab[(size_t)NT] = make_int4(ng, 0, 0, 0);
+  c->gtab_host = tab;
+  c->gtab.alloc(tab.size());
+  CK(cudaMemcpy(c->gtab.p, tab.data(), tab.size() * sizeof(int4), cudaMemcpyHostToDevice));
+}
+
 // Chooses the sweep variant and lays out its shared memory.
 // CTF_SWEEP_KIND=0|1 restricts to frame-owner / row-per-warp kernels and
 // CTF_SWEEP_VARIANT="rmax,ft,rreg,nt[,exact]" pins one (profiling aids).
@@ -314,6 +379,32 @@ void plan_sweep(ctf_ctx* c) {
       cand.off_z = (int)take((size_t)NW * v.rmax * cs);
       cand.off_b = (int)take((size_t)c->SK * rs);
       cand.off_d = (int)take((size_t)NW * 4 * sizeof(double));
+    } else if (v.kind == 4) {  // covariance-domain (Gram) kernel: stacked equal taps, M = N
+      const int M = v.rreg, L = v.lt;
+      if (c->Mx != M || c->N != M || c->Ls != L || c->R != v.rmax || c->D != v.rmax) continue;
+      bool equal = true;
+      for (int n = 0; n < c->N; ++n) equal = equal && c->taps[n] == L;
+      if (!equal) continue;
+      if (nt * v.ft < c->T) continue;
+      TP = nt * v.ft;
+      const int UB = ctf::kGramUB, NA = 2 * L - 1;
+      const int U0 = -(L - 1), U1 = U0 + c->T + 2 * (L - 1) + UB;
+      cand.xoff = 2 * L;
+      cand.xp = cand.xoff + std::max(TP, U1) + 2 * L + UB;
+      const int gloff = 2 * L + 2;
+      const int glp = gloff + std::max(TP, U1) + 2 * L + UB;
+      cand.off_x = (int)take((size_t)M * cand.xp * cs);
+      cand.off_l = (int)take((size_t)c->N * glp * rs);
+      cand.off_y = (int)take((size_t)c->N * M * M * NA * NA * cs);
+      cand.off_e = (int)take(std::max((size_t)c->N * NA * (nt + 1) * cs, (size_t)c->R * TP * rs));
+      cand.off_w = (int)take((size_t)2 * c->R * c->D * cs);
+      cand.off_z = (int)take((size_t)(2 * c->R * std::max(1, L - 1) + c->R) * cs);
+      cand.off_red = (int)take((size_t)32 * NW * rs);
+      cand.off_b = (int)take((size_t)c->SK * rs);
+      cand.off_d = (int)take((size_t)NW * 4 * sizeof(double));
+      if ((size_t)M * cand.xp * cs < (size_t)c->N * TP * rs) continue;  // Es aliases the x tile
+      cand.loff = gloff;  // (re-set below with lp)
+      cand.lp = glp;
     } else if (v.kind == 3) {  // cluster: CS = R / RB CTAs per bin
       const int RB = v.rmax, CS = c->R / RB;
       if (c->R % RB != 0 || CS < 2 || CS > 16) continue;
@@ -392,7 +483,7 @@ void plan_sweep(ctf_ctx* c) {
     // (measured on B200: the cluster kernel is correct but slower than the
     // streamed one for cfg3/cfg4 so far, so it ranks last; CTF_SWEEP_KIND=3
     // selects it)
-    const int rank = (v.kind == 3 ? 3000 : v.kind == 2 ? 2000 : v.kind == 1 ? 1000 : 0) +
+    const int rank = (v.kind == 4 ? -1000 : v.kind == 3 ? 3000 : v.kind == 2 ? 2000 : v.kind == 1 ? 1000 : 0) +
                      (v.kind == 3 ? -v.rmax * 4 : v.rmax * 4) + (v.exact ? 0 : 2) + (v.lt > 0 ? 0 : 1);
     const bool better = !found || rank < best_rank ||
                         (rank == best_rank && (TP < c->TP || (TP == c->TP && nt < best_nt)));
@@ -402,8 +493,10 @@ void plan_sweep(ctf_ctx* c) {
       best_rank = rank;
       best_smem = off;
       best_nt = nt;
-      cand.loff = loff;
-      cand.lp = loff + TP;
+      if (v.kind != 4) {
+        cand.loff = loff;
+        cand.lp = loff + TP;
+      }
       c->TP = TP;
       c->sp = cand;
     }
@@ -424,8 +517,24 @@ void plan_sweep(ctf_ctx* c) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, best.sfn, best_nt, best_smem));
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
     c->stream_grid = std::max(1, std::min(std::max(1, per_sm) * nsm, c->B * c->FL));
+  } else if (best.kind == 4) {
+    CK(cudaFuncSetAttribute((const void*)best.gfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)best_smem));
+    build_gram_table(c, best_nt, best.rreg, best.lt);
   } else {
     CK(cudaFuncSetAttribute((const void*)best.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)best_smem));
+  }
+  // L2 prefetch distance of the one-CTA-per-bin kernels: the number of CTAs
+  // resident at once (the ones launched next start about that many items later)
+  c->sp.pf_stride = 0;
+  if (best.kind == 0 || best.kind == 4) {
+    int per_sm = 0, nsm = 0;
+    if (best.kind == 4)
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, best.gfn, best_nt, best_smem));
+    else
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, best.fn, best_nt, best_smem));
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+    const char* env = std::getenv("CTF_PREFETCH");
+    if (!(env && std::atoi(env) == 0)) c->sp.pf_stride = std::max(1, per_sm) * nsm;
   }
   ctf::SweepParams& sp = c->sp;
   sp.FL = c->FL;
@@ -732,6 +841,8 @@ void run_body(ctf_ctx* c, bool do_sweep) {
     st.nwork = c->B * c->FL;
     st.ngroups = (c->R + c->sv.rreg - 1) / c->sv.rreg;
     c->sv.sfn<<<c->stream_grid, c->NT, c->sweep_smem, c->stream>>>(st);
+  } else if (c->sv.kind == 4) {
+    c->sv.gfn<<<dim3(c->FL, c->B), c->NT, c->sweep_smem, c->stream>>>(sp, c->gtab.p);
   } else {
     c->sv.fn<<<dim3(c->FL, c->B), c->NT, c->sweep_smem, c->stream>>>(sp);
   }
@@ -1187,9 +1298,9 @@ int ctf_describe(ctf_ctx* c, char* buf, int len) {
                 "{\"sweep_kernel\": \"%s<%s,RMAX=%d,FT=%d,%s=%d,NT=%d,EXACT=%d>\", \"threads\": %d, "
                 "\"smem_bytes\": %zu, \"grid\": [%d, %d], \"muv_chunks\": %d, \"bins\": [%d, %d], "
                 "\"world\": %d, \"rank\": %d, \"collective\": \"%s\"}",
-                c->sv.kind == 3 ? "cluster_kernel" : c->sv.kind == 2 ? "stream_kernel" : c->sv.kind ? "rowwarp_kernel" : "sweep_kernel",
+                c->sv.kind == 4 ? "gram_kernel" : c->sv.kind == 3 ? "cluster_kernel" : c->sv.kind == 2 ? "stream_kernel" : c->sv.kind ? "rowwarp_kernel" : "sweep_kernel",
                 c->real_size == 4 ? "f32" : "f64", c->sv.rmax, c->sv.ft,
-                c->sv.kind == 3 ? "RREG" : c->sv.kind == 2 ? "RG" : c->sv.kind ? "WPR" : "RREG", c->sv.rreg, c->sv.maxt, c->sv.exact, c->NT,
+                c->sv.kind == 4 ? "M" : c->sv.kind == 3 ? "RREG" : c->sv.kind == 2 ? "RG" : c->sv.kind ? "WPR" : "RREG", c->sv.rreg, c->sv.maxt, c->sv.exact, c->NT,
                 c->sweep_smem, c->FL, c->B, c->nchunk, c->lo, c->hi, c->world, c->rank,
                 c->group ? "host-group" : c->comm ? "nccl" : "none");
   return CTF_OK;
@@ -1569,6 +1680,30 @@ int ctf_istft(ctf_ctx* c, const double* spec, int bins, int frames, int channels
     launch_istft(c, c->stft_spec.p, 1, bins, frames, channels, window_len, hop, len, c->stft_out.p);
     CK(cudaMemcpyAsync(samples, c->stft_out.p, (size_t)channels * len * 8, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int ctf_stft_device(ctf_ctx* c, const double* samples, int num_signals, int64_t length, int channels,
+                    int window_len, int hop, void* spec, int out_precision, ctf_err* err) {
+  return guarded(err, [&] {
+    if (!c) throw CtfError(CTF_ERR_CONFIG, "null context");
+    stft_validate(length, channels, window_len, hop);
+    if (!samples || !spec || num_signals < 1) throw CtfError(CTF_ERR_CONFIG, "null buffer");
+    CK(cudaSetDevice(c->device));
+    launch_stft(c, samples, num_signals, length, channels, window_len, hop, 0, window_len / 2 + 1, spec,
+                out_precision == CTF_F32);
+  });
+}
+
+int ctf_istft_device(ctf_ctx* c, const double* spec, int num_signals, int bins, int frames, int channels,
+                     int window_len, int hop, int64_t original_length, double* samples, ctf_err* err) {
+  return guarded(err, [&] {
+    if (!c) throw CtfError(CTF_ERR_CONFIG, "null context");
+    const int64_t len = istft_validate(bins, frames, window_len, hop, original_length);
+    if (!spec || !samples || num_signals < 1 || channels < 1) throw CtfError(CTF_ERR_CONFIG, "null buffer");
+    CK(cudaSetDevice(c->device));
+    launch_istft(c, reinterpret_cast<const double2*>(spec), num_signals, bins, frames, channels, window_len, hop,
+                 len, samples);
   });
 }
 

@@ -1,0 +1,541 @@
+// ctf_gram.cuh — covariance-domain ISS iteration kernel (fp32, stacked
+// equal-tap configs).
+//
+// The reference ships two equivalent forms of the ISS step: the
+// estimate-domain sums over frames (estimator.cpp:434-484, what run() uses)
+// and the covariance-domain form z from w_p^H Q_p w_r (estimator.cpp:89-101,
+// 275-302), which its own tests hold equal to 1e-10
+// (test_estimator.cpp:360-392). The frame-domain sweep costs ~20 R^2 flops per
+// TF-bin; here the weighted covariances are formed once per iteration and the
+// R steps run on R x D matrices:
+//
+//   C_p[(m,l'),(m',l'')] = sum_{j=l}^{T-1} x_m(j-l') conj(x_m'(j-l'')) / lambda_n(j-l)
+//
+// for row p = (n, l). With s = j - l, a = l - l', b = l - l'' every entry is
+// G_n(m,a; m',b) = sum_s x_m(s+a) conj(x_m'(s+b)) w_n(s), shared by all rows
+// of source n; with u = s + a and d = b - a it is the correlation
+// sum_u Q_{m,m',d}(u) w_n(u - a) of one product sequence Q = x_m conj(x_m'(.+d))
+// with the weights at 2L-1-|d| lags: about N*M^2*(2L-1)^2/2 packed FMAs per
+// TF-bin (Hermitian half) and no R x T tile. The upper limit j <= T-1 of row l
+// is restored exactly by subtracting the l "virtual" frames j in [T, T+l)
+// (whose x~ uses only real samples), carried through the steps as an
+// R x (L-1) tail of Y.
+//
+// Per (mixture, bin) CTA: prologue (x tile, rescale, lambda) as the sweep
+// kernel -> Gram (threads own (m, m', d, frame chunk) tasks; products and
+// weights blocked in registers) -> fixed-order reduction -> objective of the
+// previous iteration (w_r^H C_r w_r of the rescaled W) -> R covariance-domain
+// steps (W and the tail updated by the reference's rank-1 rule) -> one demix
+// Y = W' x~ for the delayed energies, row powers and MU-B.
+#pragma once
+#include "ctf_kernels.cuh"
+
+namespace ctf {
+
+// Gram task table (host-built, global memory), int4 entries:
+//   [0, NT)            per thread {group, u0, u1, 0}  (group -1: idle)
+//   [NT]               {ngroups, 0, 0, 0}
+//   [NT + 1 + 2g]      {m, m2, d, a_lo}
+//   [NT + 2 + 2g]      {cnt, t0, t1, 0}   (threads [t0, t1) hold the chunks, in order)
+constexpr int kGramUB = 4;  // frames per register block
+
+template <int CNT, int N, int UB, bool MASK>
+__device__ __forceinline__ void gram_step(const float2* __restrict__ x1, const float2* __restrict__ x2,
+                                          const float* __restrict__ w0, int lp, int u, int u1,
+                                          float2 (&acc)[N][CNT]) {
+  float2 q[UB];
+#pragma unroll
+  for (int i = 0; i < UB; ++i) {
+    const float2 a = x1[u + i], b = x2[u + i];
+    q[i] = make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+    if (MASK && u + i >= u1) q[i] = make_float2(0.f, 0.f);
+  }
+#pragma unroll
+  for (int n = 0; n < N; ++n) {
+    float w[UB + CNT - 1];  // w[k] = w_n(u - a_lo - (CNT-1) + k)
+    const float* wb = w0 + n * lp + u - (CNT - 1);
+#pragma unroll
+    for (int k = 0; k < UB + CNT - 1; ++k) w[k] = wb[k];
+#pragma unroll
+    for (int i = 0; i < UB; ++i)
+#pragma unroll
+      for (int j = 0; j < CNT; ++j) acc[n][j] = ffma2s(q[i], w[CNT - 1 + i - j], acc[n][j]);
+  }
+}
+
+// acc[n][j] += sum_{u in [u0, u1)} x1(u) conj(x2(u)) w_n(u - a_lo - j); w0
+// points at w_n(-a_lo). Chunks have odd lengths (host), so the threads of a
+// warp start on distinct banks and stay there: conflict-free x and w loads.
+template <int CNT, int N, int UB>
+__device__ __forceinline__ void gram_block(const float2* __restrict__ x1, const float2* __restrict__ x2,
+                                           const float* __restrict__ w0, int lp, int u0, int u1,
+                                           float2 (&acc)[N][CNT]) {
+  int u = u0;
+  for (; u + UB <= u1; u += UB) gram_step<CNT, N, UB, false>(x1, x2, w0, lp, u, u1, acc);
+  if (u < u1) gram_step<CNT, N, UB, true>(x1, x2, w0, lp, u, u1, acc);
+}
+
+template <int M, int L, int NT, int FT>
+__global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1))
+    gram_kernel(const SweepParams p, const int4* __restrict__ gtab) {
+  constexpr int N = M, R = M * L, D = M * L, NA = 2 * L - 1, NW = NT / 32;
+  constexpr int LT1 = L > 1 ? L - 1 : 1;
+  static_assert(D <= 32, "one lane per stacked channel in the covariance steps");
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int bin = blockIdx.x, mix = blockIdx.y;
+  const int gbin = p.bin_lo + bin;
+  const int T = p.T, TP = p.TP, SK = p.SK;
+
+  float2* xs = reinterpret_cast<float2*>(smem + p.off_x);    // M rows of xp: x_m(t) at [m*xp + xoff + t]
+  float* invl = reinterpret_cast<float*>(smem + p.off_l);    // N rows of lp: w_n(s) at [n*lp + loff + s]
+  float2* G = reinterpret_cast<float2*>(smem + p.off_y);     // [n][m][m'][a][b]
+  float2* part = reinterpret_cast<float2*>(smem + p.off_e);  // [n*NA + j][NT + 1] Gram partials
+  float* Pq = reinterpret_cast<float*>(smem + p.off_e);      // [r][TP] |y|^2 (after the steps)
+  float* Es = reinterpret_cast<float*>(smem + p.off_x);      // [n][TP] energies (x tile is dead then)
+  float2* Wb = reinterpret_cast<float2*>(smem + p.off_w);    // 2 x R x D (ping-pong)
+  float2* Yt = reinterpret_cast<float2*>(smem + p.off_z);    // 2 x R x LT1 tail frames (ping-pong)
+  float2* zs = Yt + 2 * R * LT1;                             // R
+  float* red = reinterpret_cast<float*>(smem + p.off_red);   // 32 * NW
+  float* Bs = reinterpret_cast<float*>(smem + p.off_b);
+  double* dred = reinterpret_cast<double*>(smem + p.off_d);
+  __shared__ int s_bad, s_badrow;
+  __shared__ double s_logmu, s_dprod;
+  constexpr int kNoRow = 1 << 30;
+
+  const size_t tile = (size_t)mix * p.FL + bin;
+  prefetch_next_tile(p, bin, mix, (size_t)T * M * sizeof(float2), (size_t)R * D * sizeof(float2));
+  const float2* xg = reinterpret_cast<const float2*>(p.x) + tile * (size_t)T * M;
+  float2* Wg = reinterpret_cast<float2*>(p.W) + tile * (size_t)R * D;
+  float* Bg = reinterpret_cast<float*>(p.Bf) + tile * SK;
+  const float* Vg = reinterpret_cast<const float*>(p.V) + (size_t)mix * SK * T;
+  const float floor_abs = (float)p.floor_abs[mix];
+  const int prev_it = p.iteration - 1;
+  const double* mu = p.mu ? p.mu + (size_t)mix * R : nullptr;
+  auto gidx = [](int n, int m, int m2, int a, int b) {  // a, b in [-(L-1), L-1]
+    return (((n * M + m) * M + m2) * NA + a + L - 1) * NA + b + L - 1;
+  };
+
+  if (tid == 0) {
+    s_bad = 0;
+    s_badrow = kNoRow;
+    double lm = 0.0;
+    if (mu)
+      for (int r = 0; r < R; ++r)
+        if (mu[r] != 0.0) lm += log(mu[r]);
+    s_logmu = lm;
+  }
+  // ---- prologue: zero-padded x tile, W and B with the pending rescale
+  if ((T * M) % 2 == 0) {
+    // the bin's T x M complex block is contiguous: 16-byte loads, all in
+    // flight before the first store (latency, not bandwidth, bounds this)
+    constexpr int XV = FT * M / 2;  // >= (T*M/2) / NT since T <= FT*NT
+    const int n16 = T * M / 2;
+    const float4* xv = reinterpret_cast<const float4*>(xg);
+    float4 v[XV];
+#pragma unroll
+    for (int i = 0; i < XV; ++i) {
+      const int e = tid + i * NT;
+      if (e < n16) v[i] = __ldg(xv + e);
+    }
+    for (int i = tid; i < M * p.xp; i += NT) {
+      const int t = i % p.xp - p.xoff;
+      if (t < 0 || t >= T) xs[i] = make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < XV; ++i) {
+      const int e = tid + i * NT;
+      if (e < n16) {
+        const int f0 = 2 * e, f1 = 2 * e + 1;
+        xs[(f0 % M) * p.xp + p.xoff + f0 / M] = make_float2(v[i].x, v[i].y);
+        xs[(f1 % M) * p.xp + p.xoff + f1 / M] = make_float2(v[i].z, v[i].w);
+      }
+    }
+  } else {
+    for (int i = tid; i < M * p.xp; i += NT) {
+      const int m = i / p.xp, t = i - m * p.xp - p.xoff;
+      xs[i] = (t >= 0 && t < T) ? xg[(size_t)t * M + m] : make_float2(0.f, 0.f);
+    }
+  }
+  for (int i = tid; i < R * D; i += NT) {
+    float2 w = Wg[i];
+    if (mu) {
+      const double m = mu[i % R];
+      if (m != 0.0) {
+        w.x = (float)((double)w.x / m);
+        w.y = (float)((double)w.y / m);
+      }
+    }
+    Wb[i] = w;
+    if (p.has_prev && !cfinite(w)) s_bad = 1;
+  }
+  for (int n = 0; n < N; ++n) {
+    const double m0 = mu ? mu[p.row0[n]] : 0.0;
+    for (int i = p.koff[n] + tid; i < p.koff[n + 1]; i += NT) {
+      float b = Bg[i];
+      if (m0 != 0.0) b = (float)fmax((double)b / (m0 * m0), (double)floor_abs);
+      Bs[i] = b;
+    }
+  }
+  __syncthreads();
+  if (p.has_prev && s_bad) {  // check_all_finite on W (estimator.cpp:494-496)
+    if (tid == 0) record_err<float>(p.err, mix, err_key(prev_it, kPhFinite, gbin, 0, 1));
+    return;
+  }
+  // ---- lambda = max(B V, floor) -> 1/lambda (zero outside [0, T)), log term
+  double logsum = 0.0;
+  for (int n = 0; n < N; ++n) {
+    float* il = invl + n * p.lp;
+    for (int i = tid; i < p.lp; i += NT) {
+      const int s = i - p.loff;
+      if (s < 0 || s >= T) il[i] = 0.f;
+    }
+    const int k0 = p.koff[n], k1 = p.koff[n + 1];
+    if (T % 4 == 0) {
+      // four consecutive frames per thread, 16-byte V loads (FT == 4 threads' worth)
+      static_assert(FT == 4, "vector lambda path assumes four frames per thread");
+      const int t4 = tid * 4;
+      if (t4 < T) {
+        float4 lam = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
+        for (int kk = k0; kk < k1; ++kk) {
+          const float b = Bs[kk];
+          const float4 v = __ldg(reinterpret_cast<const float4*>(Vg + (size_t)kk * T + t4));
+          lam.x = fmaf(b, v.x, lam.x);
+          lam.y = fmaf(b, v.y, lam.y);
+          lam.z = fmaf(b, v.z, lam.z);
+          lam.w = fmaf(b, v.w, lam.w);
+        }
+        const float lv[4] = {lam.x, lam.y, lam.z, lam.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float l = fmaxf(lv[i], floor_abs);
+          il[p.loff + t4 + i] = 1.f / l;
+          if (p.has_prev) logsum += (double)min(L, T - t4 - i) * (double)logf(l);
+        }
+      }
+    } else {
+      float lam[FT];
+#pragma unroll
+      for (int k = 0; k < FT; ++k) lam[k] = 0.f;
+#pragma unroll 4
+      for (int kk = k0; kk < k1; ++kk) {
+        const float b = Bs[kk];
+        const float* vrow = Vg + (size_t)kk * T;
+#pragma unroll
+        for (int k = 0; k < FT; ++k) {
+          const int tau = tid + k * NT;
+          if (tau < T) lam[k] = fmaf(b, __ldg(vrow + tau), lam[k]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < FT; ++k) {
+        const int tau = tid + k * NT;
+        if (tau < T) {
+          const float l = fmaxf(lam[k], floor_abs);
+          il[p.loff + tau] = 1.f / l;
+          if (p.has_prev) logsum += (double)min(L, T - tau) * (double)logf(l);
+        }
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- virtual tail frames j in [T, T+L-1): y_r(j) = sum_c W[r,c] x~_c(j)
+  for (int e = tid; e < R * (L - 1); e += NT) {
+    const int r = e % R, jj = e / R, j = T + jj;
+    float2 y = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int m = 0; m < M; ++m)
+#pragma unroll
+      for (int l = 0; l < L; ++l) cmac(y, Wb[(m * L + l) * R + r], xs[m * p.xp + p.xoff + j - l]);
+    Yt[r * LT1 + jj] = y;
+  }
+
+  // ---- Gram: this thread's (m, m', d) task over frames [u0, u1). The lag
+  // count is made warp-uniform (groups are sorted by it, so a warp spans at
+  // most two adjacent counts): no divergent code paths, extra lags discarded.
+  {
+    const int4 tk = gtab[tid];
+    const bool active = tk.x >= 0;
+    const int4 g0 = gtab[NT + 1 + 2 * max(tk.x, 0)], g1 = gtab[NT + 2 + 2 * max(tk.x, 0)];
+    const int cnt = active ? g1.x : 0;
+    const int cmax = __reduce_max_sync(kFull, cnt);
+    const float2* x1 = xs + g0.x * p.xp + p.xoff;
+    const float2* x2 = xs + g0.y * p.xp + p.xoff + g0.z;
+    const float* w0 = invl + p.loff - g0.w;
+    static_for<L, NA + 1>([&](auto cc) {
+      constexpr int C = decltype(cc)::value;
+      if (cmax == C) {
+        float2 acc[N][C];
+#pragma unroll
+        for (int n = 0; n < N; ++n)
+#pragma unroll
+          for (int j = 0; j < C; ++j) acc[n][j] = make_float2(0.f, 0.f);
+        if (active) gram_block<C, N, kGramUB>(x1, x2, w0, p.lp, tk.y, tk.z, acc);
+#pragma unroll
+        for (int n = 0; n < N; ++n)
+#pragma unroll
+          for (int j = 0; j < C; ++j)
+            if (j < cnt) part[(size_t)(n * NA + j) * (NT + 1) + tid] = acc[n][j];
+      }
+    });
+  }
+  __syncthreads();
+  // fixed-order reduction over each group's chunks, Hermitian mirror
+  {
+    const int ng = gtab[NT].x;
+    for (int e = tid; e < ng * N * NA; e += NT) {
+      const int g = e / (N * NA), rr = e - g * (N * NA), n = rr / NA, j = rr - n * NA;
+      const int4 g0 = gtab[NT + 1 + 2 * g], g1 = gtab[NT + 2 + 2 * g];
+      if (j >= g1.x) continue;
+      float2 s = make_float2(0.f, 0.f);
+      const float2* pr = part + (size_t)(n * NA + j) * (NT + 1);
+      for (int t = g1.y; t < g1.z; ++t) {
+        s.x += pr[t].x;
+        s.y += pr[t].y;
+      }
+      const int m = g0.x, m2 = g0.y, d = g0.z, a = g0.w + j, b = a + d;
+      G[gidx(n, m, m2, a, b)] = s;
+      G[gidx(n, m2, m, b, a)] = make_float2(s.x, (m == m2 && d == 0) ? s.y : -s.y);
+    }
+  }
+  __syncthreads();
+
+  // ---- covariance-domain quantities for row p and pivot r, one half-warp
+  // (lane c < D of the half holds stacked channel c):
+  // num = w_p^T C_p conj(w_r) - tail, den = Re(w_r^T C_p conj(w_r)) - tail
+  constexpr int HW = 16;
+  static_assert(D <= HW, "one half-warp per row");
+  const int hl = lane & (HW - 1), half = lane >> 4;
+  auto cov_row = [&](int pr, int r, const float2* Wc, const float2* Ytc, float& nre, float& nim, float& den) {
+    const int n = pr / L, l = pr - n * L;
+    float2 cn = make_float2(0.f, 0.f), cd = make_float2(0.f, 0.f);
+    if (hl < D && pr < R) {
+      const int m = hl / L, l1 = hl - m * L;
+      float2 q0 = make_float2(0.f, 0.f), q1 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int m2 = 0; m2 < M; ++m2)
+#pragma unroll
+        for (int l2 = 0; l2 < L; ++l2) {
+          const float2 c = G[gidx(n, m, m2, l - l1, l - l2)];
+          const float2 w = Wc[(m2 * L + l2) * R + r];
+          float2& q = ((m2 * L + l2) & 1) ? q1 : q0;
+          q.x = fmaf(c.x, w.x, fmaf(c.y, w.y, q.x));  // q += c conj(w)
+          q.y = fmaf(c.y, w.x, fmaf(-c.x, w.y, q.y));
+        }
+      const float2 q = make_float2(q0.x + q1.x, q0.y + q1.y);
+      cn = cmul(Wc[hl * R + pr], q);
+      cd = cmul(Wc[hl * R + r], q);
+    }
+#pragma unroll
+    for (int o = HW / 2; o >= 1; o >>= 1) {
+      cn.x += __shfl_xor_sync(kFull, cn.x, o);
+      cn.y += __shfl_xor_sync(kFull, cn.y, o);
+      cd.x += __shfl_xor_sync(kFull, cd.x, o);
+    }
+    nre = cn.x;
+    nim = cn.y;
+    den = cd.x;
+    if (pr < R)
+      for (int jj = 0; jj < l; ++jj) {  // virtual frames j = T + jj, weight w_n(j - l)
+        const float w = invl[n * p.lp + p.loff + T + jj - l];
+        const float2 yp = Ytc[pr * LT1 + jj], yr = Ytc[r * LT1 + jj];
+        nre -= w * fmaf(yp.x, yr.x, yp.y * yr.y);
+        nim -= w * fmaf(yp.y, yr.x, -yp.x * yr.y);
+        den -= w * fmaf(yr.x, yr.x, yr.y * yr.y);
+      }
+  };
+  constexpr int RPW = 2 * NW;  // rows in flight per pass
+
+  double logdet = p.logdet[tile] - s_logmu;
+  if (p.has_prev) {
+    // objective of the previous iteration (estimator.cpp:55-77): quadratic
+    // term sum_r w_r^T C_r conj(w_r) of the rescaled W under the new lambda
+    for (int r0 = 0; r0 < R; r0 += RPW) {
+      const int r = r0 + 2 * warp + half;
+      float nre, nim, den;
+      cov_row(r, r < R ? r : 0, Wb, Yt, nre, nim, den);
+      if (hl == 0 && r < R) red[r] = den;
+    }
+    double v1[1] = {logsum};
+    block_sum_d<1>(v1, dred, lane, warp, NW);  // contains __syncthreads: red visible after
+    double quad = 0.0;
+    for (int r = 0; r < R; ++r) quad += (double)red[r];
+    const int det_status = isnan(logdet) || logdet == -INFINITY ? 4 : (logdet < log(1e-300) ? 5 : 0);
+    if (det_status) {  // estimator.cpp:45-51
+      if (tid == 0) record_err<float>(p.err, mix, err_key(prev_it, kPhDet, gbin, 0, det_status));
+      return;
+    }
+    if (tid == 0) p.objbin[tile] = v1[0] + quad - 2.0 * (double)T * logdet;
+    __syncthreads();  // red is reused by the steps
+  }
+
+  if (!p.do_sweep) {  // finalize pass: write the rescaled state and stop
+    for (int i = tid; i < R * D; i += NT) Wg[i] = Wb[i];
+    for (int i = tid; i < SK; i += NT) Bg[i] = Bs[i];
+    if (tid == 0) p.logdet[tile] = logdet;
+    return;
+  }
+
+  // ---- R covariance-domain ISS steps (estimator.cpp:556-579, 275-302)
+  if (tid == 0) s_dprod = 1.0;
+  for (int r = 0; r < R; ++r) {
+    const float2* Wo = Wb + (r & 1) * R * D;
+    float2* Wn = Wb + ((r + 1) & 1) * R * D;
+    const float2* Yo = Yt + (r & 1) * R * LT1;
+    float2* Yn = Yt + ((r + 1) & 1) * R * LT1;
+    for (int p0 = 0; p0 < R; p0 += RPW) {
+      const int pr = p0 + 2 * warp + half;
+      float nre, nim, den;
+      cov_row(pr, r, Wo, Yo, nre, nim, den);
+      if (hl == 0 && pr < R) {
+        float2 z = make_float2(0.f, 0.f);
+        if (!(den > 0.f) || !isfinite(den)) {  // estimator.cpp:451-454
+          atomicMin(&s_badrow, pr);  // lowest failing row p
+        } else if (pr == r) {
+          z.x = 1.f - sqrtf((float)T / den);
+        } else {
+          z.x = nre / den;
+          z.y = nim / den;
+        }
+        zs[pr] = z;
+      }
+    }
+    __syncthreads();
+    if (s_badrow != kNoRow) {
+      if (tid == 0) record_err<float>(p.err, mix, err_key(p.iteration, kPhSweep, gbin, r, s_badrow));
+      return;
+    }
+    if (tid == 0) s_dprod *= (double)(1.f - zs[r].x);
+    // iss_apply, W -= z w_r (estimator.cpp:298-302), and the same on the tail
+    for (int e = tid; e < R * D; e += NT) {
+      const int q = e % R, c = e / R;
+      float2 w = Wo[e];
+      cmsub(w, zs[q], Wo[c * R + r]);
+      Wn[e] = w;
+    }
+    for (int e = tid; e < R * (L - 1); e += NT) {
+      const int q = e / LT1, jj = e - q * LT1;
+      float2 y = Yo[e];
+      cmsub(y, zs[q], Yo[r * LT1 + jj]);
+      Yn[e] = y;
+    }
+    __syncthreads();
+  }
+  const float2* Wf = Wb + (R & 1) * R * D;
+
+  // ---- Y = W' x~ (estimator.cpp:607) for this thread's frames: |y|^2 to
+  // shared memory, row powers and the finite check on the way
+  float rp[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) rp[i] = 0.f;
+  bool ybad = false;
+#pragma unroll 1
+  for (int k = 0; k < FT; ++k) {
+    const int j = tid + k * NT;
+    constexpr int RC = 4;
+    static_for<0, (R + RC - 1) / RC>([&](auto chunk) {
+      constexpr int r0 = decltype(chunk)::value * RC;
+      float2 acc[RC];
+#pragma unroll
+      for (int i = 0; i < RC; ++i) acc[i] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int m = 0; m < M; ++m)
+#pragma unroll
+        for (int l1 = 0; l1 < L; ++l1) {
+          const float2 xv = xs[m * p.xp + p.xoff + j - l1];
+          const float2 xn = make_float2(-xv.y, xv.x);
+#pragma unroll
+          for (int i = 0; i < RC; ++i)
+            if (r0 + i < R) {
+              const float2 w = Wf[(m * L + l1) * R + r0 + i];
+              acc[i] = ffma2s(xn, w.y, ffma2s(xv, w.x, acc[i]));
+            }
+        }
+#pragma unroll
+      for (int i = 0; i < RC; ++i)
+        if (r0 + i < R) {
+          const float q = (j < T) ? cnorm(acc[i]) : 0.f;
+          if (j < T && !cfinite(acc[i])) ybad = true;
+          Pq[(r0 + i) * TP + j] = q;
+          rp[r0 + i] += q;
+        }
+    });
+  }
+  if (ybad) s_bad = 1;  // check_all_finite on Y (estimator.cpp:497-499)
+  __syncthreads();      // Pq complete; the x tile is dead from here (Es aliases it)
+  if (s_bad) {
+    if (tid == 0) record_err<float>(p.err, mix, err_key(p.iteration, kPhFinite, gbin, 0, 2));
+    return;
+  }
+  // delayed energies E_n(tau) = sum_{l, tau+l<T} |y_(n,l)(tau+l)|^2 (l order)
+  float* Eg = reinterpret_cast<float*>(p.E);
+  for (int n = 0; n < N; ++n)
+#pragma unroll
+    for (int k = 0; k < FT; ++k) {
+      const int tau = tid + k * NT;
+      float e = 0.f;
+#pragma unroll
+      for (int l = 0; l < L; ++l)
+        if (tau + l < T) e += Pq[(n * L + l) * TP + tau + l];
+      Es[n * TP + tau] = e;
+      if (tau < T) Eg[(((size_t)mix * N + n) * p.FL + bin) * T + tau] = e;
+    }
+  // row powers (estimator.cpp:391-397)
+  warp_reduce_scatter(rp, lane);
+  red[warp * 32 + lane] = rp[0];
+  __syncthreads();
+  if (tid < R) {
+    double s = 0.0;
+    for (int w = 0; w < NW; ++w) s += (double)red[w * 32 + tid];
+    p.rowpow[tile * R + tid] = s;
+  }
+  if (tid == 0) p.logdet[tile] = logdet + log(s_dprod);
+  for (int i = tid; i < R * D; i += NT) Wg[i] = Wf[i];
+  __syncthreads();
+
+  // ---- MU-B for this bin (estimator.cpp:313-346), 16 bases per pass
+  for (int n = 0; n < N; ++n) {
+    const int k0 = p.koff[n], k1 = p.koff[n + 1];
+    const float* il = invl + n * p.lp + p.loff;
+    for (int kb = k0; kb < k1; kb += 16) {
+      float a[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) a[i] = 0.f;
+      const float* vrow[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) vrow[q] = Vg + (size_t)min(kb + q, k1 - 1) * T + tid;
+#pragma unroll
+      for (int k = 0; k < FT; ++k) {
+        const int tau = tid + k * NT;
+        const float ilv = il[tau];
+        const float an = Es[n * TP + tau] * (ilv * ilv);
+        const float bn = (tau < T) ? ilv * (float)min(L, T - tau) : 0.f;
+        const float2 ab = make_float2(an, bn);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const float vv = __ldg(vrow[q] + k * NT);
+          const float2 t = ffma2s(ab, vv, make_float2(a[q], a[16 + q]));
+          a[q] = t.x;
+          a[16 + q] = t.y;
+        }
+      }
+      warp_reduce_scatter(a, lane);
+      __syncthreads();  // previous pass's reads of red are done
+      red[warp * 32 + lane] = a[0];
+      __syncthreads();
+      if (tid < 16 && kb + tid < k1) {
+        float num = 0.f, den = 0.f;
+        for (int w = 0; w < NW; ++w) {
+          num += red[w * 32 + tid];
+          den += red[w * 32 + 16 + tid];
+        }
+        const float b = Bs[kb + tid];
+        Bg[kb + tid] = fmaxf(b * sqrtf(num / den), floor_abs);
+      }
+    }
+  }
+}
+
+}  // namespace ctf

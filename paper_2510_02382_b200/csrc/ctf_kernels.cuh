@@ -72,7 +72,24 @@ struct SweepParams {
   // each error as a double bit pattern (non-negative doubles order as u64)
   int chk_flags;
   unsigned long long* chk;  // [mix][2]
+  int pf_stride;  // > 0: prefetch into L2 the tiles of work item (mix*FL + bin) + pf_stride
 };
+
+// L2 prefetch of a contiguous block (bulk async, no registers or smem).
+__device__ __forceinline__ void prefetch_l2(const void* ptr, unsigned bytes) {
+  bytes &= ~15u;
+  if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
+}
+// The CTAs resident after this one start roughly pf_stride work items later:
+// warm L2 with the x tile and W of that item while this one runs.
+__device__ __forceinline__ void prefetch_next_tile(const SweepParams& p, int bin, int mix, size_t xbytes,
+                                                   size_t wbytes) {
+  if (p.pf_stride <= 0 || threadIdx.x != 0) return;
+  const size_t w = (size_t)mix * p.FL + bin + p.pf_stride;
+  if (w >= (size_t)gridDim.y * p.FL) return;
+  prefetch_l2(reinterpret_cast<const unsigned char*>(p.x) + w * xbytes, (unsigned)xbytes);
+  prefetch_l2(reinterpret_cast<const unsigned char*>(p.W) + w * wbytes, (unsigned)wbytes);
+}
 
 // ---------------------------------------------------------------------------
 // Small complex helpers.
@@ -382,6 +399,7 @@ __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(c
   __shared__ double s_logmu;
 
   const size_t tile = (size_t)mix * p.FL + bin;
+  prefetch_next_tile(p, bin, mix, (size_t)T * p.Mx * sizeof(R2), (size_t)R * D * sizeof(R2));
   const R2* xg = reinterpret_cast<const R2*>(p.x) + tile * (size_t)T * p.Mx;
   R2* Wg = reinterpret_cast<R2*>(p.W) + tile * (size_t)R * D;
   Real* Bg = reinterpret_cast<Real*>(p.Bf) + tile * SK;

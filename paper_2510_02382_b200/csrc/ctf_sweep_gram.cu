@@ -1,0 +1,9 @@
+// Covariance-domain (Gram) iteration kernels for the stacked equal-tap
+// configs, fp32: (M = N mics/sources, L taps, CTA size, frames per thread).
+#include "ctf_sweep_variants.h"
+namespace ctf {
+std::vector<SweepVariant> sweep_variants_gram_f32() {
+  return {CTF_GR(2, 2, 128, 4), CTF_GR(2, 2, 256, 4), CTF_GR(2, 3, 128, 4), CTF_GR(2, 3, 256, 4),
+          CTF_GR(2, 5, 256, 4), CTF_GR(2, 5, 512, 4), CTF_GR(3, 4, 256, 4), CTF_GR(3, 4, 512, 4)};
+}
+}  // namespace ctf

@@ -9,6 +9,7 @@
 #include "ctf_rowwarp.cuh"
 #include "ctf_stream.cuh"
 #include "ctf_cluster.cuh"
+#include "ctf_gram.cuh"
 
 #include <vector>
 
@@ -22,6 +23,7 @@ struct SweepVariant {
   void (*sfn)(StreamParams) = nullptr;
   void (*cfn)(ClusterParams) = nullptr;  // kind 3: cluster_kernel (rmax = rows per CTA)
   int chk = 0;  // kind 0 compiled with the CheckOptions instrumentation
+  void (*gfn)(SweepParams, const int4*) = nullptr;  // kind 4: gram_kernel (rreg = M, lt = L)
 };
 #define CTF_V(REAL, PREC, RMAX, FT, RREG, NT, EX) \
   SweepVariant { PREC, RMAX, FT, RREG, NT, EX, sweep_kernel<REAL, RMAX, FT, RREG, NT, EX> }
@@ -50,6 +52,11 @@ struct SweepVariant {
 // cluster_kernel: R = CS * RB rows over a cluster of CS CTAs
 #define CTF_CL(REAL, PREC, RB, FT, RREG, NT) \
   SweepVariant { PREC, RB, FT, RREG, NT, 0, nullptr, 3, 0, nullptr, cluster_kernel<REAL, RB, FT, RREG, NT> }
+// gram_kernel: covariance-domain steps, M mics = N sources, L taps (fp32)
+#define CTF_GR(M, L, NT, FT)                                                                           \
+  SweepVariant {                                                                                       \
+    1, (M) * (L), FT, M, NT, 1, nullptr, 4, L, nullptr, nullptr, 0, gram_kernel<M, L, NT, FT>          \
+  }
 // rowwarp_kernel: R = NT / (32 * WPR) rows, FT frames per lane
 #define CTF_RW(REAL, PREC, FT, WPR, NT) \
   SweepVariant { PREC, (NT) / (32 * (WPR)), FT, WPR, NT, 1, rowwarp_kernel<REAL, FT, WPR, NT>, 1, 0 }
