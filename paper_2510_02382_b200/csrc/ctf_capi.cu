@@ -170,6 +170,7 @@ struct ctf_ctx {
   DevBuf<double> rowpow, objbin, packed_d, mu, floor_abs, objective, mp_part, logdet;
   DevBuf<unsigned long long> err;
   DevBuf<unsigned long long> chk;  // CheckOptions maxima [B][2] (double bit patterns)
+  DevBuf<double> logmu;             // [B] sum_r log mu_r of the pending rescale
   DevBuf<int4> gtab;                // gram_kernel task table
   std::vector<int4> gtab_host;
   // STFT tables (window length stft_N) and scratch
@@ -767,6 +768,7 @@ void launch_apply(ctf_ctx* c, int mode, int obj_slot, int do_v) {
   ap.objbin = c->objbin.p;
   ap.packed_d = c->packed_d.p;
   ap.mu = c->mu.p;
+  ap.logmu = c->logmu.p;
   ap.objective = c->objective.p;
   ap.floor_abs = c->floor_abs.p;
   ap.err = c->err.p;
@@ -800,6 +802,7 @@ void run_body(ctf_ctx* c, bool do_sweep) {
   sp.rowpow = c->rowpow.p;
   sp.objbin = c->objbin.p;
   sp.mu = c->pending ? c->mu.p : nullptr;
+  sp.logmu = c->logmu.p;
   sp.floor_abs = c->floor_abs.p;
   sp.err = c->err.p;
   sp.chk = c->chk.p;
@@ -996,6 +999,7 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host,
   c->objbin.alloc((size_t)c->B * c->FL);
   c->packed_d.alloc((size_t)c->B * (c->R + 1));
   c->mu.alloc((size_t)c->B * c->R);
+  c->logmu.alloc((size_t)c->B);
   c->floor_abs.alloc((size_t)c->B);
   c->mp_part.alloc((size_t)c->B * c->FL);
   c->err.alloc((size_t)c->B);

@@ -39,40 +39,41 @@ namespace ctf {
 //   [NT + 2 + 2g]      {cnt, t0, t1, 0}   (threads [t0, t1) hold the chunks, in order)
 constexpr int kGramUB = 4;  // frames per register block
 
-template <int CNT, int N, int UB, bool MASK>
-__device__ __forceinline__ void gram_step(const float2* __restrict__ x1, const float2* __restrict__ x2,
-                                          const float* __restrict__ w0, int lp, int u, int u1,
-                                          float2 (&acc)[N][CNT]) {
-  float2 q[UB];
-#pragma unroll
-  for (int i = 0; i < UB; ++i) {
-    const float2 a = x1[u + i], b = x2[u + i];
-    q[i] = make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
-    if (MASK && u + i >= u1) q[i] = make_float2(0.f, 0.f);
-  }
-#pragma unroll
-  for (int n = 0; n < N; ++n) {
-    float w[UB + CNT - 1];  // w[k] = w_n(u - a_lo - (CNT-1) + k)
-    const float* wb = w0 + n * lp + u - (CNT - 1);
-#pragma unroll
-    for (int k = 0; k < UB + CNT - 1; ++k) w[k] = wb[k];
-#pragma unroll
-    for (int i = 0; i < UB; ++i)
-#pragma unroll
-      for (int j = 0; j < CNT; ++j) acc[n][j] = ffma2s(q[i], w[CNT - 1 + i - j], acc[n][j]);
-  }
-}
-
 // acc[n][j] += sum_{u in [u0, u1)} x1(u) conj(x2(u)) w_n(u - a_lo - j); w0
-// points at w_n(-a_lo). Chunks have odd lengths (host), so the threads of a
-// warp start on distinct banks and stay there: conflict-free x and w loads.
+// points at w_n(-a_lo). The weight window w_n(u - a_lo - (CNT-1) .. u + UB - 1
+// - a_lo) lives in registers and slides by UB per block (UB new loads per
+// source instead of UB + CNT - 1). Chunks have odd lengths (host), so the
+// threads of a warp start on distinct banks and stay there.
 template <int CNT, int N, int UB>
 __device__ __forceinline__ void gram_block(const float2* __restrict__ x1, const float2* __restrict__ x2,
                                            const float* __restrict__ w0, int lp, int u0, int u1,
                                            float2 (&acc)[N][CNT]) {
-  int u = u0;
-  for (; u + UB <= u1; u += UB) gram_step<CNT, N, UB, false>(x1, x2, w0, lp, u, u1, acc);
-  if (u < u1) gram_step<CNT, N, UB, true>(x1, x2, w0, lp, u, u1, acc);
+  constexpr int WN = UB + CNT - 1;
+  float wv[N][WN];
+#pragma unroll
+  for (int n = 0; n < N; ++n)
+#pragma unroll
+    for (int k = 0; k < CNT - 1; ++k) wv[n][k + UB] = w0[n * lp + u0 - (CNT - 1) + k];
+  for (int u = u0; u < u1; u += UB) {
+    float2 q[UB];
+#pragma unroll
+    for (int i = 0; i < UB; ++i) {
+      const float2 a = x1[u + i], b = x2[u + i];
+      q[i] = make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+      if (u + i >= u1) q[i] = make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+#pragma unroll
+      for (int k = 0; k < CNT - 1; ++k) wv[n][k] = wv[n][k + UB];
+#pragma unroll
+      for (int i = 0; i < UB; ++i) wv[n][CNT - 1 + i] = w0[n * lp + u + i];
+#pragma unroll
+      for (int i = 0; i < UB; ++i)
+#pragma unroll
+        for (int j = 0; j < CNT; ++j) acc[n][j] = ffma2s(q[i], wv[n][CNT - 1 + i - j], acc[n][j]);
+    }
+  }
 }
 
 template <int M, int L, int NT, int FT>
@@ -119,11 +120,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1))
   if (tid == 0) {
     s_bad = 0;
     s_badrow = kNoRow;
-    double lm = 0.0;
-    if (mu)
-      for (int r = 0; r < R; ++r)
-        if (mu[r] != 0.0) lm += log(mu[r]);
-    s_logmu = lm;
+    s_logmu = mu ? p.logmu[mix] : 0.0;
   }
   // ---- prologue: zero-padded x tile, W and B with the pending rescale
   if ((T * M) % 2 == 0) {

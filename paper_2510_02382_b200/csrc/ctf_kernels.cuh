@@ -53,6 +53,7 @@ struct SweepParams {
   double* rowpow;           // [mix][FL][R]
   double* objbin;           // [mix][FL]
   const double* mu;         // [mix][R] pending rescale, or nullptr
+  const double* logmu;      // [mix] sum_r log mu_r of the pending rescale
   const double* floor_abs;  // [mix]
   unsigned long long* err;  // [mix]
   int FL, bin_lo, T, TP, Mx, Ls, D, R, N, SK;
@@ -410,11 +411,7 @@ __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(c
 
   if (tid == 0) {
     s_bad = 0;
-    double lm = 0.0;
-    if (mu)
-      for (int r = 0; r < R; ++r)
-        if (mu[r] != 0.0) lm += log(mu[r]);
-    s_logmu = lm;
+    s_logmu = mu ? p.logmu[mix] : 0.0;
   }
   // ---- prologue: x tile (transposed to [m][t]), W and B with the pending rescale
   for (int m = 0; m < p.Mx; ++m) {
@@ -1004,6 +1001,7 @@ struct ApplyParams {
   const double* objbin; // [mix][FL]
   double* packed_d;     // [mix][R + 1]
   double* mu;           // [mix][R]
+  double* logmu;        // [mix] sum_r log mu_r over mu_r != 0 (the log|det| shift of the rescale)
   double* objective;    // [mix][max_iters]
   const double* floor_abs;
   unsigned long long* err;
@@ -1071,6 +1069,17 @@ __global__ void __launch_bounds__(256) reduce_apply_kernel(const ApplyParams p) 
       const double obj = pd[r];
       p.objective[(size_t)mix * p.max_iters + p.obj_slot] = obj;
       if (!isfinite(obj)) atomicMin(p.err + mix, err_key(p.obj_slot + 1, kPhObj, 0, 0, 6));
+    }
+  }
+  if (p.do_v && p.logmu) {  // once per mixture instead of in every bin's prologue
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double lm = 0.0;
+      for (int r = 0; r < p.R; ++r) {
+        const double m = p.mu[(size_t)mix * p.R + r];
+        if (m != 0.0) lm += log(m);
+      }
+      p.logmu[mix] = lm;
     }
   }
 }
