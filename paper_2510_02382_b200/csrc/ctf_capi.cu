@@ -399,7 +399,7 @@ void plan_sweep(ctf_ctx* c) {
       cand.off_y = (int)take((size_t)c->N * M * M * NA * NA * cs);
       cand.off_e = (int)take(std::max((size_t)c->N * NA * (nt + 1) * cs, (size_t)c->R * TP * rs));
       cand.off_w = (int)take((size_t)2 * c->R * c->D * cs);
-      cand.off_z = (int)take((size_t)(2 * c->R * std::max(1, L - 1) + c->R) * cs);
+      cand.off_z = (int)take((size_t)(2 * c->R * std::max(1, L - 1) + 2 * (c->D + std::max(1, L - 1))) * cs);
       cand.off_red = (int)take((size_t)32 * NW * rs);
       cand.off_b = (int)take((size_t)c->SK * rs);
       cand.off_d = (int)take((size_t)NW * 4 * sizeof(double));

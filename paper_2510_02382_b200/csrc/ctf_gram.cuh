@@ -95,8 +95,8 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1))
   float* Pq = reinterpret_cast<float*>(smem + p.off_e);      // [r][TP] |y|^2 (after the steps)
   float* Es = reinterpret_cast<float*>(smem + p.off_x);      // [n][TP] energies (x tile is dead then)
   float2* Wb = reinterpret_cast<float2*>(smem + p.off_w);    // 2 x R x D (ping-pong)
-  float2* Yt = reinterpret_cast<float2*>(smem + p.off_z);    // 2 x R x LT1 tail frames (ping-pong)
-  float2* zs = Yt + 2 * R * LT1;                             // R
+  float2* Yt = reinterpret_cast<float2*>(smem + p.off_z);    // R x LT1 tail frames (+ R x LT1 spare)
+  float2* zs = Yt + 2 * R * LT1;                             // 2 x (D + LT1) pivot buffers
   float* red = reinterpret_cast<float*>(smem + p.off_red);   // 32 * NW
   float* Bs = reinterpret_cast<float*>(smem + p.off_b);
   double* dred = reinterpret_cast<double*>(smem + p.off_d);
@@ -154,26 +154,27 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1))
       xs[i] = (t >= 0 && t < T) ? xg[(size_t)t * M + m] : make_float2(0.f, 0.f);
     }
   }
+  for (int i = tid; i < R * D; i += NT) Wb[i] = Wg[i];
+  for (int i = tid; i < SK; i += NT) Bs[i] = Bg[i];
+  __shared__ float s_imu[R];  // 1 / mu_r of the pending rescale (1 where none)
+  if (warp == 0 && lane < R) s_imu[lane] = (mu && mu[lane] != 0.0) ? (float)(1.0 / mu[lane]) : 1.f;
+  __syncthreads();
+  // pending rescale (estimator.cpp:399-411) in fp32: W rows * (1/mu_r),
+  // B_n * (1/mu_row0)^2 floored
   for (int i = tid; i < R * D; i += NT) {
-    float2 w = Wg[i];
-    if (mu) {
-      const double m = mu[i % R];
-      if (m != 0.0) {
-        w.x = (float)((double)w.x / m);
-        w.y = (float)((double)w.y / m);
-      }
-    }
+    float2 w = Wb[i];
+    const float im = s_imu[i % R];
+    w.x *= im;
+    w.y *= im;
     Wb[i] = w;
     if (p.has_prev && !cfinite(w)) s_bad = 1;
   }
-  for (int n = 0; n < N; ++n) {
-    const double m0 = mu ? mu[p.row0[n]] : 0.0;
-    for (int i = p.koff[n] + tid; i < p.koff[n + 1]; i += NT) {
-      float b = Bg[i];
-      if (m0 != 0.0) b = (float)fmax((double)b / (m0 * m0), (double)floor_abs);
-      Bs[i] = b;
+  if (mu)
+    for (int n = 0; n < N; ++n) {
+      if (mu[p.row0[n]] == 0.0) continue;  // estimator.cpp:405-406: silent row, no rescale
+      const float im = s_imu[p.row0[n]];
+      for (int i = p.koff[n] + tid; i < p.koff[n + 1]; i += NT) Bs[i] = fmaxf(Bs[i] * (im * im), floor_abs);
     }
-  }
   __syncthreads();
   if (p.has_prev && s_bad) {  // check_all_finite on W (estimator.cpp:494-496)
     if (tid == 0) record_err<float>(p.err, mix, err_key(prev_it, kPhFinite, gbin, 0, 1));
@@ -299,32 +300,51 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1))
   }
   __syncthreads();
 
-  // ---- covariance-domain quantities for row p and pivot r, one half-warp
-  // (lane c < D of the half holds stacked channel c):
-  // num = w_p^T C_p conj(w_r) - tail, den = Re(w_r^T C_p conj(w_r)) - tail
+  // ---- covariance-domain steps with register-resident rows: half-warp
+  // `row` = 2*warp + half owns W row p; its lane c < D holds W[p][c], the row
+  // c of C_p (D complex), and for c < l_p the tail frame T + c of y_p with
+  // its weight w_n(T + c - l_p). A step needs only the pivot row (W_r and its
+  // tail), published through shared memory: one barrier per step.
   constexpr int HW = 16;
-  static_assert(D <= HW, "one half-warp per row");
+  static_assert(D <= HW && L - 1 <= HW, "one half-warp per row");
+  static_assert(R <= 2 * NW, "a half-warp per row");
   const int hl = lane & (HW - 1), half = lane >> 4;
-  auto cov_row = [&](int pr, int r, const float2* Wc, const float2* Ytc, float& nre, float& nim, float& den) {
-    const int n = pr / L, l = pr - n * L;
-    float2 cn = make_float2(0.f, 0.f), cd = make_float2(0.f, 0.f);
-    if (hl < D && pr < R) {
-      const int m = hl / L, l1 = hl - m * L;
-      float2 q0 = make_float2(0.f, 0.f), q1 = make_float2(0.f, 0.f);
+  const int row = 2 * warp + half;
+  const bool rowv = row < R;
+  const int rn = rowv ? row / L : 0, rl = rowv ? row - rn * L : 0;
+  float2 creg[D];
+  float2 wreg = make_float2(0.f, 0.f), yreg = make_float2(0.f, 0.f);
+  float wt = 0.f;
+  {
+    const bool chan = rowv && hl < D;
+    const int m = hl / L, l1 = hl - m * L;
 #pragma unroll
-      for (int m2 = 0; m2 < M; ++m2)
+    for (int m2 = 0; m2 < M; ++m2)
 #pragma unroll
-        for (int l2 = 0; l2 < L; ++l2) {
-          const float2 c = G[gidx(n, m, m2, l - l1, l - l2)];
-          const float2 w = Wc[(m2 * L + l2) * R + r];
-          float2& q = ((m2 * L + l2) & 1) ? q1 : q0;
-          q.x = fmaf(c.x, w.x, fmaf(c.y, w.y, q.x));  // q += c conj(w)
-          q.y = fmaf(c.y, w.x, fmaf(-c.x, w.y, q.y));
-        }
-      const float2 q = make_float2(q0.x + q1.x, q0.y + q1.y);
-      cn = cmul(Wc[hl * R + pr], q);
-      cd = cmul(Wc[hl * R + r], q);
+      for (int l2 = 0; l2 < L; ++l2)
+        creg[m2 * L + l2] = chan ? G[gidx(rn, m, m2, rl - l1, rl - l2)] : make_float2(0.f, 0.f);
+    if (chan) wreg = Wb[hl * R + row];
+    if (rowv && hl < L - 1) yreg = Yt[row * LT1 + hl];                // carried for when this row pivots
+    if (rowv && hl < rl) wt = invl[rn * p.lp + p.loff + T + hl - rl];  // own truncation: frames T .. T+l-1
+  }
+  // (num, den) of this row against a pivot: pw[c * ps] = pivot W, py[c] = pivot tail
+  auto row_sums = [&](const float2* pw, int ps, const float2* py, float& nre, float& nim, float& den) {
+    float2 q0 = make_float2(0.f, 0.f), q1 = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const float2 w = pw[c * ps];
+      float2& q = (c & 1) ? q1 : q0;
+      q.x = fmaf(creg[c].x, w.x, fmaf(creg[c].y, w.y, q.x));  // q += C conj(w)
+      q.y = fmaf(creg[c].y, w.x, fmaf(-creg[c].x, w.y, q.y));
     }
+    const float2 q = make_float2(q0.x + q1.x, q0.y + q1.y);
+    const float2 wr = (hl < D) ? pw[hl * ps] : make_float2(0.f, 0.f);
+    float2 cn = cmul(wreg, q), cd = cmul(wr, q);
+    // virtual frames T + hl (hl < l_p): subtract w y_p conj(y_r), w |y_r|^2
+    const float2 yr = (hl < LT1) ? py[hl] : make_float2(0.f, 0.f);
+    cn.x -= wt * fmaf(yreg.x, yr.x, yreg.y * yr.y);
+    cn.y -= wt * fmaf(yreg.y, yr.x, -yreg.x * yr.y);
+    cd.x -= wt * fmaf(yr.x, yr.x, yr.y * yr.y);
 #pragma unroll
     for (int o = HW / 2; o >= 1; o >>= 1) {
       cn.x += __shfl_xor_sync(kFull, cn.x, o);
@@ -334,27 +354,15 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1))
     nre = cn.x;
     nim = cn.y;
     den = cd.x;
-    if (pr < R)
-      for (int jj = 0; jj < l; ++jj) {  // virtual frames j = T + jj, weight w_n(j - l)
-        const float w = invl[n * p.lp + p.loff + T + jj - l];
-        const float2 yp = Ytc[pr * LT1 + jj], yr = Ytc[r * LT1 + jj];
-        nre -= w * fmaf(yp.x, yr.x, yp.y * yr.y);
-        nim -= w * fmaf(yp.y, yr.x, -yp.x * yr.y);
-        den -= w * fmaf(yr.x, yr.x, yr.y * yr.y);
-      }
   };
-  constexpr int RPW = 2 * NW;  // rows in flight per pass
 
   double logdet = p.logdet[tile] - s_logmu;
   if (p.has_prev) {
     // objective of the previous iteration (estimator.cpp:55-77): quadratic
     // term sum_r w_r^T C_r conj(w_r) of the rescaled W under the new lambda
-    for (int r0 = 0; r0 < R; r0 += RPW) {
-      const int r = r0 + 2 * warp + half;
-      float nre, nim, den;
-      cov_row(r, r < R ? r : 0, Wb, Yt, nre, nim, den);
-      if (hl == 0 && r < R) red[r] = den;
-    }
+    float nre, nim, den;
+    row_sums(Wb + (rowv ? row : 0), R, Yt + (rowv ? row : 0) * LT1, nre, nim, den);
+    if (hl == 0 && rowv) red[row] = den;
     double v1[1] = {logsum};
     block_sum_d<1>(v1, dred, lane, warp, NW);  // contains __syncthreads: red visible after
     double quad = 0.0;
@@ -365,7 +373,6 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1))
       return;
     }
     if (tid == 0) p.objbin[tile] = v1[0] + quad - 2.0 * (double)T * logdet;
-    __syncthreads();  // red is reused by the steps
   }
 
   if (!p.do_sweep) {  // finalize pass: write the rescaled state and stop
@@ -376,51 +383,52 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1))
   }
 
   // ---- R covariance-domain ISS steps (estimator.cpp:556-579, 275-302)
-  if (tid == 0) s_dprod = 1.0;
+  float2* piv = zs;  // 2 x (D + LT1): pivot W row and tail, double-buffered by step parity
+  float* fac = red;  // (1 - z_r) per row, multiplied in row order at the end
+  constexpr int PV = D + LT1;
+  if (row == 0) {
+    if (hl < D) piv[hl] = wreg;
+    if (hl < LT1) piv[D + hl] = yreg;
+  }
+  __syncthreads();
   for (int r = 0; r < R; ++r) {
-    const float2* Wo = Wb + (r & 1) * R * D;
-    float2* Wn = Wb + ((r + 1) & 1) * R * D;
-    const float2* Yo = Yt + (r & 1) * R * LT1;
-    float2* Yn = Yt + ((r + 1) & 1) * R * LT1;
-    for (int p0 = 0; p0 < R; p0 += RPW) {
-      const int pr = p0 + 2 * warp + half;
-      float nre, nim, den;
-      cov_row(pr, r, Wo, Yo, nre, nim, den);
-      if (hl == 0 && pr < R) {
-        float2 z = make_float2(0.f, 0.f);
-        if (!(den > 0.f) || !isfinite(den)) {  // estimator.cpp:451-454
-          atomicMin(&s_badrow, pr);  // lowest failing row p
-        } else if (pr == r) {
-          z.x = 1.f - sqrtf((float)T / den);
-        } else {
-          z.x = nre / den;
-          z.y = nim / den;
-        }
-        zs[pr] = z;
+    const float2* pv = piv + (r & 1) * PV;
+    float nre, nim, den;
+    row_sums(pv, 1, pv + D, nre, nim, den);
+    float2 z = make_float2(0.f, 0.f);
+    if (rowv) {
+      if (!(den > 0.f) || !isfinite(den)) {  // estimator.cpp:451-454
+        if (hl == 0) atomicMin(&s_badrow, row);
+      } else if (row == r) {
+        z.x = 1.f - sqrtf((float)T / den);
+        if (hl == 0) fac[row] = 1.f - z.x;
+      } else {
+        z.x = nre / den;
+        z.y = nim / den;
       }
+    }
+    // iss_apply (estimator.cpp:298-302) on the own row and its tail
+    if (hl < D) cmsub(wreg, z, pv[hl]);
+    if (hl < LT1) cmsub(yreg, z, pv[D + hl]);
+    if (row == r + 1) {  // the next pivot publishes its updated row
+      float2* nx = piv + ((r + 1) & 1) * PV;
+      if (hl < D) nx[hl] = wreg;
+      if (hl < LT1) nx[D + hl] = yreg;
     }
     __syncthreads();
     if (s_badrow != kNoRow) {
       if (tid == 0) record_err<float>(p.err, mix, err_key(p.iteration, kPhSweep, gbin, r, s_badrow));
       return;
     }
-    if (tid == 0) s_dprod *= (double)(1.f - zs[r].x);
-    // iss_apply, W -= z w_r (estimator.cpp:298-302), and the same on the tail
-    for (int e = tid; e < R * D; e += NT) {
-      const int q = e % R, c = e / R;
-      float2 w = Wo[e];
-      cmsub(w, zs[q], Wo[c * R + r]);
-      Wn[e] = w;
-    }
-    for (int e = tid; e < R * (L - 1); e += NT) {
-      const int q = e / LT1, jj = e - q * LT1;
-      float2 y = Yo[e];
-      cmsub(y, zs[q], Yo[r * LT1 + jj]);
-      Yn[e] = y;
-    }
-    __syncthreads();
   }
-  const float2* Wf = Wb + (R & 1) * R * D;
+  float2* Wf = Wb;  // W' (column-major R x D) for the demix
+  if (rowv && hl < D) Wf[hl * R + row] = wreg;
+  if (tid == 0) {
+    double dp = 1.0;
+    for (int r = 0; r < R; ++r) dp *= (double)fac[r];
+    s_dprod = dp;
+  }
+  __syncthreads();
 
   // ---- Y = W' x~ (estimator.cpp:607) for this thread's frames: |y|^2 to
   // shared memory, row powers and the finite check on the way

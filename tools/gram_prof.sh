@@ -1,4 +1,2 @@
 for c in 0 1 2; do timeout 300 python tools/prof_cfg.py --cfg $c --prec f32 --iters 10 2>&1 | tail -1; done
-CTF_SWEEP_KIND=0 timeout 300 python tools/prof_cfg.py --cfg 1 --prec f32 --iters 10 2>&1 | tail -1
-timeout 300 python tools/prof_cfg.py --cfg 1 --prec f64 --iters 5 2>&1 | tail -1
 timeout 900 python -m pytest tests/test_gpu_parity.py -q -x 2>&1 | tail -2
