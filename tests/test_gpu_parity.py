@@ -89,6 +89,28 @@ def test_cfg0_fp32_tolerances():
     assert final <= 1e-3, final
 
 
+@pytest.mark.parametrize("M,L,T,K,rho", [(2, 5, 1000, 10, 0.6), (3, 4, 2000, 20, 0.7), (2, 3, 400, 4, 0.6)])
+def test_fp32_trajectory_cfg_geometries(M, L, T, K, rho):
+    """fp32 tolerance on the BASELINE cfg1 / cfg2 geometries (reduced F) and an
+    odd-lag shape: <= 1e-4 relative L2 per iteration against the fp64 oracle
+    over 30 iterations (the covariance-domain kernel serves these shapes)."""
+    F, iters, seed = 33, 30, 5
+    raw = synth_mixtures(1, F, T, M, M, L, K, rho, 1234 + M * L)
+    ref = O.run(O.config([L] * M, [K] * M, iterations=iters, seed=seed, threads=NPROC),
+                O.stack_observation(raw[0], L), history=True)
+    s = Session(raw.astype(np.complex64), [L] * M, [K] * M, stack_taps=L, iterations=iters, precision="f32",
+                seed=seed)
+    kern = json.loads(s.describe())["sweep_kernel"]
+    s.close()
+    hist = gpu_history(raw.astype(np.complex64), [L] * M, [K] * M, iters, "f32", seed, L)
+    for it, (W, B, V, obj) in enumerate(hist):
+        e = max(rel(W[0], ref["hist_W"][it].reshape(F, -1)), rel(B[0], ref["hist_B"][it]),
+                rel(V[0], ref["hist_V"][it]))
+        assert e <= 1e-4, f"{kern} it={it + 1}: {e:.2e}"
+    final = abs(hist[-1][3][0, -1] - ref["objective"][-1]) / abs(ref["objective"][-1])
+    assert final <= 1e-3, final
+
+
 def test_one_step_parity_from_oracle_state():
     """Restart the GPU from the oracle's state after 4 iterations (cfg1 shape,
     reduced F): one GPU iteration equals one oracle iteration (no trajectory
