@@ -44,36 +44,49 @@ constexpr int kGramUB = 4;  // frames per register block
 // - a_lo) lives in registers and slides by UB per block (UB new loads per
 // source instead of UB + CNT - 1). Chunks have odd lengths (host), so the
 // threads of a warp start on distinct banks and stay there.
+template <int CNT, int N, int UB, bool MASK>
+__device__ __forceinline__ void gram_step(const float2* __restrict__ x1, const float2* __restrict__ x2,
+                                          const float* __restrict__ w0, int lp, int u, int u1,
+                                          float (&wv)[N][UB + CNT - 1], float2 (&acc)[N][CNT]) {
+  float2 q[UB];
+#pragma unroll
+  for (int i = 0; i < UB; ++i) {
+    // q = a conj(b) = (a.x, a.y) b.x + (a.y, -a.x) b.y, packed
+    const float2 a = x1[u + i], b = x2[u + i];
+    q[i] = ffma2s(make_float2(a.y, -a.x), b.y, fmul2s(a, b.x));
+    if (MASK && u + i >= u1) q[i] = make_float2(0.f, 0.f);
+  }
+#pragma unroll
+  for (int n = 0; n < N; ++n) {
+#pragma unroll
+    for (int k = 0; k < CNT - 1; ++k) wv[n][k] = wv[n][k + UB];
+#pragma unroll
+    for (int i = 0; i < UB; ++i) wv[n][CNT - 1 + i] = w0[n * lp + u + i];
+#pragma unroll
+    for (int i = 0; i < UB; ++i)
+#pragma unroll
+      for (int j = 0; j < CNT; ++j) acc[n][j] = ffma2s(q[i], wv[n][CNT - 1 + i - j], acc[n][j]);
+  }
+}
+
+// acc[n][j] += sum_{u in [u0, u1)} x1(u) conj(x2(u)) w_n(u - a_lo - j); w0
+// points at w_n(-a_lo). The weight window w_n(u - a_lo - (CNT-1) .. u + UB - 1
+// - a_lo) lives in registers and slides by UB per block (UB new loads per
+// source instead of UB + CNT - 1). Chunks have odd lengths (host), so the
+// threads of a warp start on distinct banks and stay there; only the last
+// block of a chunk is masked.
 template <int CNT, int N, int UB>
 __device__ __forceinline__ void gram_block(const float2* __restrict__ x1, const float2* __restrict__ x2,
                                            const float* __restrict__ w0, int lp, int u0, int u1,
                                            float2 (&acc)[N][CNT]) {
-  constexpr int WN = UB + CNT - 1;
-  float wv[N][WN];
+  float wv[N][UB + CNT - 1];
 #pragma unroll
   for (int n = 0; n < N; ++n)
 #pragma unroll
     for (int k = 0; k < CNT - 1; ++k) wv[n][k + UB] = w0[n * lp + u0 - (CNT - 1) + k];
-  for (int u = u0; u < u1; u += UB) {
-    float2 q[UB];
-#pragma unroll
-    for (int i = 0; i < UB; ++i) {
-      const float2 a = x1[u + i], b = x2[u + i];
-      q[i] = make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
-      if (u + i >= u1) q[i] = make_float2(0.f, 0.f);
-    }
-#pragma unroll
-    for (int n = 0; n < N; ++n) {
-#pragma unroll
-      for (int k = 0; k < CNT - 1; ++k) wv[n][k] = wv[n][k + UB];
-#pragma unroll
-      for (int i = 0; i < UB; ++i) wv[n][CNT - 1 + i] = w0[n * lp + u + i];
-#pragma unroll
-      for (int i = 0; i < UB; ++i)
-#pragma unroll
-        for (int j = 0; j < CNT; ++j) acc[n][j] = ffma2s(q[i], wv[n][CNT - 1 + i - j], acc[n][j]);
-    }
-  }
+  int u = u0;
+  for (; u + UB <= u1; u += UB) gram_step<CNT, N, UB, false>(x1, x2, w0, lp, u, u1, wv, acc);
+  if (u < u1) gram_step<CNT, N, UB, true>(x1, x2, w0, lp, u, u1, wv, acc);
 }
 
 template <int M, int L, int NT, int FT>
@@ -331,11 +344,10 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1))
   auto row_sums = [&](const float2* pw, int ps, const float2* py, float& nre, float& nim, float& den) {
     float2 q0 = make_float2(0.f, 0.f), q1 = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int c = 0; c < D; ++c) {
+    for (int c = 0; c < D; ++c) {  // q += C conj(w) = (C.x, C.y) w.x + (C.y, -C.x) w.y
       const float2 w = pw[c * ps];
       float2& q = (c & 1) ? q1 : q0;
-      q.x = fmaf(creg[c].x, w.x, fmaf(creg[c].y, w.y, q.x));  // q += C conj(w)
-      q.y = fmaf(creg[c].y, w.x, fmaf(-creg[c].x, w.y, q.y));
+      q = ffma2s(make_float2(creg[c].y, -creg[c].x), w.y, ffma2s(creg[c], w.x, q));
     }
     const float2 q = make_float2(q0.x + q1.x, q0.y + q1.y);
     const float2 wr = (hl < D) ? pw[hl * ps] : make_float2(0.f, 0.f);
@@ -391,10 +403,11 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1))
     if (hl < LT1) piv[D + hl] = yreg;
   }
   __syncthreads();
+  const bool wrows = 2 * warp < R;  // warp-uniform: this warp owns at least one row
   for (int r = 0; r < R; ++r) {
     const float2* pv = piv + (r & 1) * PV;
-    float nre, nim, den;
-    row_sums(pv, 1, pv + D, nre, nim, den);
+    float nre = 0.f, nim = 0.f, den = 0.f;
+    if (wrows) row_sums(pv, 1, pv + D, nre, nim, den);
     float2 z = make_float2(0.f, 0.f);
     if (rowv) {
       if (!(den > 0.f) || !isfinite(den)) {  // estimator.cpp:451-454
@@ -439,34 +452,31 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1))
 #pragma unroll 1
   for (int k = 0; k < FT; ++k) {
     const int j = tid + k * NT;
-    constexpr int RC = 4;
-    static_for<0, (R + RC - 1) / RC>([&](auto chunk) {
-      constexpr int r0 = decltype(chunk)::value * RC;
-      float2 acc[RC];
+    static_assert(R % 2 == 0, "W columns are read in 16-byte pairs");
+    float2 acc[R];
 #pragma unroll
-      for (int i = 0; i < RC; ++i) acc[i] = make_float2(0.f, 0.f);
+    for (int i = 0; i < R; ++i) acc[i] = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int m = 0; m < M; ++m)
+    for (int m = 0; m < M; ++m)
 #pragma unroll
-        for (int l1 = 0; l1 < L; ++l1) {
-          const float2 xv = xs[m * p.xp + p.xoff + j - l1];
-          const float2 xn = make_float2(-xv.y, xv.x);
+      for (int l1 = 0; l1 < L; ++l1) {
+        const float2 xv = xs[m * p.xp + p.xoff + j - l1];
+        const float2 xn = make_float2(-xv.y, xv.x);
+        const float4* wc = reinterpret_cast<const float4*>(Wf + (m * L + l1) * R);
 #pragma unroll
-          for (int i = 0; i < RC; ++i)
-            if (r0 + i < R) {
-              const float2 w = Wf[(m * L + l1) * R + r0 + i];
-              acc[i] = ffma2s(xn, w.y, ffma2s(xv, w.x, acc[i]));
-            }
+        for (int i = 0; i < R; i += 2) {
+          const float4 w = wc[i / 2];
+          acc[i] = ffma2s(xn, w.y, ffma2s(xv, w.x, acc[i]));
+          acc[i + 1] = ffma2s(xn, w.w, ffma2s(xv, w.z, acc[i + 1]));
         }
+      }
 #pragma unroll
-      for (int i = 0; i < RC; ++i)
-        if (r0 + i < R) {
-          const float q = (j < T) ? cnorm(acc[i]) : 0.f;
-          if (j < T && !cfinite(acc[i])) ybad = true;
-          Pq[(r0 + i) * TP + j] = q;
-          rp[r0 + i] += q;
-        }
-    });
+    for (int i = 0; i < R; ++i) {
+      const float q = (j < T) ? cnorm(acc[i]) : 0.f;
+      if (j < T && !cfinite(acc[i])) ybad = true;
+      Pq[i * TP + j] = q;
+      rp[i] += q;
+    }
   }
   if (ybad) s_bad = 1;  // check_all_finite on Y (estimator.cpp:497-499)
   __syncthreads();      // Pq complete; the x tile is dead from here (Es aliases it)

@@ -1,1 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "trajectory" 2>&1 | tail -5
+for c in 0 1 2; do timeout 300 python tools/prof_cfg.py --cfg $c --prec f32 --iters 10 2>&1 | tail -1; done
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x 2>&1 | tail -2
