@@ -67,6 +67,22 @@ def flops_per_tfbin(R, D, N, K):
     return sweep, sweep + 6 * N * K, 20 * R * R + 8 * R * D + 6 * N * K
 
 
+def gram_executed_flops(M, N, L, K, R, D, T):
+    """Flops per TF-bin the covariance-domain kernel executes:
+    Gram = complex x real MAC (4) per (lag entry, frame) over the Hermitian
+    half of the (m, m', d) groups and all sources, one product per group and
+    frame (6), the R covariance-domain steps (~8 R^2 D per bin), one demix
+    (8RD), lambda + MU-B (6NK)."""
+    groups, entries = 0, 0
+    for m in range(M):
+        for m2 in range(m, M):
+            for d in range(0 if m == m2 else -(L - 1), L):
+                groups += 1
+                entries += 2 * L - 1 - abs(d)
+    frames = (T + 2 * (L - 1)) / T
+    return (4 * N * entries + 6 * groups) * frames + 8 * R * R * D / T + 8 * R * D + 6 * N * K
+
+
 def bytes_per_tfbin(M, N, K, R, D, T, F, c):
     """Algorithmic HBM bytes per TF-bin*iteration of the resident design
     (SURVEY §8(d)): read x once, write+read energies E, read/write W, B, V
@@ -142,14 +158,16 @@ def peak_probe(device):
     return lib.ctf_peak_fp32_tflops(device), lib.ctf_peak_fp64_tflops(device)
 
 
-def profile_traffic(prec):
-    """dram read+write bytes per TF-bin of the sweep kernel from the committed
-    ncu --set full capture (profiles/), scaled per launch by the caller."""
+def profile_traffic(kernel, prec):
+    """dram read+write bytes per TF-bin of the dominant kernel from the
+    committed ncu --set full capture (profiles/sweep_traffic.json, keyed
+    "<kernel>/<dtype>"), scaled per launch by the caller."""
     path = os.path.join(ROOT, "profiles", "sweep_traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        return d.get(prec)
+        v = d.get(f"{kernel}/{prec}")
+        return v.get("bytes_per_tfbin") if isinstance(v, dict) else v
     except (OSError, ValueError):
         return None
 
@@ -304,12 +322,14 @@ def main():
 
     # ---- roofline of the dominant kernel (the fused sweep kernel)
     fl_sweep, fl_iter, fl_exec = flops_per_tfbin(R, D, N, K)
+    if desc["sweep_kernel"].startswith("gram_kernel"):
+        fl_exec = gram_executed_flops(M, N, L, K, R, D, T)
     p32, p64 = peak_probe(device) if rank == 0 else (None, None)
     peak = p32 if prec == "f32" else p64
     local_bins = s.bin_range[1] - s.bin_range[0]
     units_per_launch = B * local_bins * T
     achieved = fl_sweep * units_per_launch / (sweep_ms / 1e3) / 1e12
-    traffic_per_tfbin = profile_traffic(prec)
+    traffic_per_tfbin = profile_traffic(desc["sweep_kernel"].split("<")[0], prec)
     mp = measured_peaks()
     hbm_peak = mp.get("hbm_gbs", 6650.0)
     c = 8 if prec == "f32" else 16
