@@ -38,6 +38,9 @@ namespace ctf {
 //   [NT + 1 + 2g]      {m, m2, d, a_lo}
 //   [NT + 2 + 2g]      {cnt, t0, t1, 0}   (threads [t0, t1) hold the chunks, in order)
 constexpr int kGramUB = 4;  // frames per register block
+#ifdef CTF_PHASE_TIMING
+__device__ unsigned long long g_phase[4096 * 12];  // dev instrumentation: clock64 per phase, tid 0
+#endif
 
 // acc[n][j] += sum_{u in [u0, u1)} x1(u) conj(x2(u)) w_n(u - a_lo - j); w0
 // points at w_n(-a_lo). The weight window w_n(u - a_lo - (CNT-1) .. u + UB - 1
@@ -118,6 +121,13 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1))
   constexpr int kNoRow = 1 << 30;
 
   const size_t tile = (size_t)mix * p.FL + bin;
+#ifdef CTF_PHASE_TIMING
+#define CTF_PHASE(k) \
+  if (tid == 0 && tile < 4096) g_phase[tile * 12 + (k)] = clock64();
+#else
+#define CTF_PHASE(k)
+#endif
+  CTF_PHASE(0);
   prefetch_next_tile(p, bin, mix, (size_t)T * M * sizeof(float2), (size_t)R * D * sizeof(float2));
   const float2* xg = reinterpret_cast<const float2*>(p.x) + tile * (size_t)T * M;
   float2* Wg = reinterpret_cast<float2*>(p.W) + tile * (size_t)R * D;
@@ -189,6 +199,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1))
       for (int i = p.koff[n] + tid; i < p.koff[n + 1]; i += NT) Bs[i] = fmaxf(Bs[i] * (im * im), floor_abs);
     }
   __syncthreads();
+  CTF_PHASE(1);
   if (p.has_prev && s_bad) {  // check_all_finite on W (estimator.cpp:494-496)
     if (tid == 0) record_err<float>(p.err, mix, err_key(prev_it, kPhFinite, gbin, 0, 1));
     return;
@@ -251,6 +262,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1))
     }
   }
   __syncthreads();
+  CTF_PHASE(2);
 
   // ---- virtual tail frames j in [T, T+L-1): y_r(j) = sum_c W[r,c] x~_c(j)
   for (int e = tid; e < R * (L - 1); e += NT) {
@@ -293,6 +305,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1))
     });
   }
   __syncthreads();
+  CTF_PHASE(3);
   // fixed-order reduction over each group's chunks, Hermitian mirror
   {
     const int ng = gtab[NT].x;
@@ -312,6 +325,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1))
     }
   }
   __syncthreads();
+  CTF_PHASE(4);
 
   // ---- covariance-domain steps with register-resident rows: half-warp
   // `row` = 2*warp + half owns W row p; its lane c < D holds W[p][c], the row
@@ -403,6 +417,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1))
     if (hl < LT1) piv[D + hl] = yreg;
   }
   __syncthreads();
+  CTF_PHASE(5);
   const bool wrows = 2 * warp < R;  // warp-uniform: this warp owns at least one row
   for (int r = 0; r < R; ++r) {
     const float2* pv = piv + (r & 1) * PV;
@@ -413,11 +428,12 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1))
       if (!(den > 0.f) || !isfinite(den)) {  // estimator.cpp:451-454
         if (hl == 0) atomicMin(&s_badrow, row);
       } else if (row == r) {
-        z.x = 1.f - sqrtf((float)T / den);
+        z.x = 1.f - sqrtf((float)T) * rsqrtf(den);
         if (hl == 0) fac[row] = 1.f - z.x;
       } else {
-        z.x = nre / den;
-        z.y = nim / den;
+        const float inv = __frcp_rn(den);
+        z.x = nre * inv;
+        z.y = nim * inv;
       }
     }
     // iss_apply (estimator.cpp:298-302) on the own row and its tail
@@ -442,6 +458,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1))
     s_dprod = dp;
   }
   __syncthreads();
+  CTF_PHASE(6);
 
   // ---- Y = W' x~ (estimator.cpp:607) for this thread's frames: |y|^2 to
   // shared memory, row powers and the finite check on the way
@@ -473,13 +490,17 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1))
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const float q = (j < T) ? cnorm(acc[i]) : 0.f;
-      if (j < T && !cfinite(acc[i])) ybad = true;
       Pq[i * TP + j] = q;
       rp[i] += q;
     }
   }
-  if (ybad) s_bad = 1;  // check_all_finite on Y (estimator.cpp:497-499)
+  // check_all_finite on Y (estimator.cpp:497-499): a non-finite estimate
+  // makes its row's power sum non-finite
+#pragma unroll
+  for (int i = 0; i < R; ++i) ybad |= !isfinite(rp[i]);
+  if (ybad) s_bad = 1;
   __syncthreads();      // Pq complete; the x tile is dead from here (Es aliases it)
+  CTF_PHASE(7);
   if (s_bad) {
     if (tid == 0) record_err<float>(p.err, mix, err_key(p.iteration, kPhFinite, gbin, 0, 2));
     return;
@@ -509,6 +530,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1))
   if (tid == 0) p.logdet[tile] = logdet + log(s_dprod);
   for (int i = tid; i < R * D; i += NT) Wg[i] = Wf[i];
   __syncthreads();
+  CTF_PHASE(8);
 
   // ---- MU-B for this bin (estimator.cpp:313-346), 16 bases per pass
   for (int n = 0; n < N; ++n) {
@@ -551,6 +573,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 3 : 1))
       }
     }
   }
+  CTF_PHASE(9);
 }
 
 }  // namespace ctf

@@ -7,3 +7,10 @@ std::vector<SweepVariant> sweep_variants_gram_f32() {
           CTF_GR(2, 5, 256, 4), CTF_GR(2, 5, 512, 4), CTF_GR(3, 4, 256, 4), CTF_GR(3, 4, 512, 4)};
 }
 }  // namespace ctf
+#ifdef CTF_PHASE_TIMING
+// dev instrumentation (builds with -DCTF_PHASE_TIMING only): per-CTA clock64
+// at the phase boundaries of gram_kernel, tiles < 4096
+extern "C" int ctf_debug_gram_phases(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, ctf::g_phase, sizeof(unsigned long long) * 4096 * 12);
+}
+#endif
