@@ -397,13 +397,13 @@ void plan_sweep(ctf_ctx* c) {
       cand.off_x = (int)take((size_t)M * cand.xp * cs);
       cand.off_l = (int)take((size_t)c->N * glp * rs);
       cand.off_y = (int)take((size_t)c->N * M * M * NA * NA * cs);
-      cand.off_e = (int)take(std::max((size_t)c->N * NA * (nt + 1) * cs, (size_t)c->R * TP * rs));
+      const int NS = c->real_size == 4 ? c->N : 1;  // sources per Gram pass (gram_ns)
+      cand.off_e = (int)take(std::max((size_t)NS * NA * (nt + 1) * cs, (size_t)L * TP * rs));
       cand.off_w = (int)take((size_t)2 * c->R * c->D * cs);
       cand.off_z = (int)take((size_t)(2 * c->R * std::max(1, L - 1) + 2 * (c->D + std::max(1, L - 1))) * cs);
       cand.off_red = (int)take((size_t)32 * NW * rs);
       cand.off_b = (int)take((size_t)c->SK * rs);
       cand.off_d = (int)take((size_t)NW * 4 * sizeof(double));
-      if ((size_t)M * cand.xp * cs < (size_t)c->N * TP * rs) continue;  // Es aliases the x tile
       cand.loff = gloff;  // (re-set below with lp)
       cand.lp = glp;
     } else if (v.kind == 3) {  // cluster: CS = R / RB CTAs per bin

@@ -1,10 +1,16 @@
 // Covariance-domain (Gram) iteration kernels for the stacked equal-tap
-// configs, fp32: (M = N mics/sources, L taps, CTA size, frames per thread).
+// configs: (M = N mics/sources, L taps, CTA size, frames per thread).
 #include "ctf_sweep_variants.h"
 namespace ctf {
+#define GF(...) CTF_GR(float, 1, __VA_ARGS__)
+#define GD(...) CTF_GR(double, 0, __VA_ARGS__)
 std::vector<SweepVariant> sweep_variants_gram_f32() {
-  return {CTF_GR(2, 2, 128, 4), CTF_GR(2, 2, 256, 4), CTF_GR(2, 3, 128, 4), CTF_GR(2, 3, 256, 4),
-          CTF_GR(2, 5, 256, 4), CTF_GR(2, 5, 512, 4), CTF_GR(3, 4, 256, 4), CTF_GR(3, 4, 512, 4)};
+  return {GF(2, 2, 128, 4), GF(2, 2, 256, 4), GF(2, 3, 128, 4), GF(2, 3, 256, 4),
+          GF(2, 5, 256, 4), GF(2, 5, 512, 4), GF(3, 4, 256, 4), GF(3, 4, 512, 4)};
+}
+std::vector<SweepVariant> sweep_variants_gram_f64() {
+  return {GD(2, 2, 128, 4), GD(2, 2, 256, 4), GD(2, 3, 128, 4), GD(2, 3, 256, 4),
+          GD(2, 5, 256, 4), GD(2, 5, 512, 4), GD(3, 4, 256, 4), GD(3, 4, 512, 4)};
 }
 }  // namespace ctf
 #ifdef CTF_PHASE_TIMING

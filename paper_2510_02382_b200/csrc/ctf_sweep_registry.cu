@@ -15,6 +15,7 @@ std::vector<SweepVariant> sweep_variants_f64_taps();
 std::vector<SweepVariant> sweep_variants_rowwarp_f64();
 std::vector<SweepVariant> sweep_variants_check_f32();
 std::vector<SweepVariant> sweep_variants_gram_f32();
+std::vector<SweepVariant> sweep_variants_gram_f64();
 std::vector<SweepVariant> sweep_variants_check_f64();
 const std::vector<SweepVariant>& sweep_variants_f32() {
   static const std::vector<SweepVariant> v = [] {
@@ -52,6 +53,8 @@ const std::vector<SweepVariant>& sweep_variants_f64() {
     a.insert(a.end(), cl.begin(), cl.end());
     auto ck = sweep_variants_check_f64();
     a.insert(a.end(), ck.begin(), ck.end());
+    auto gr = sweep_variants_gram_f64();
+    a.insert(a.end(), gr.begin(), gr.end());
     return a;
   }();
   return v;

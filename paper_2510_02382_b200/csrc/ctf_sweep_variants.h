@@ -52,10 +52,10 @@ struct SweepVariant {
 // cluster_kernel: R = CS * RB rows over a cluster of CS CTAs
 #define CTF_CL(REAL, PREC, RB, FT, RREG, NT) \
   SweepVariant { PREC, RB, FT, RREG, NT, 0, nullptr, 3, 0, nullptr, cluster_kernel<REAL, RB, FT, RREG, NT> }
-// gram_kernel: covariance-domain steps, M mics = N sources, L taps (fp32)
-#define CTF_GR(M, L, NT, FT)                                                                           \
-  SweepVariant {                                                                                       \
-    1, (M) * (L), FT, M, NT, 1, nullptr, 4, L, nullptr, nullptr, 0, gram_kernel<M, L, NT, FT>          \
+// gram_kernel: covariance-domain steps, M mics = N sources, L taps
+#define CTF_GR(REAL, PREC, M, L, NT, FT)                                                                 \
+  SweepVariant {                                                                                         \
+    PREC, (M) * (L), FT, M, NT, 1, nullptr, 4, L, nullptr, nullptr, 0, gram_kernel<REAL, M, L, NT, FT>   \
   }
 // rowwarp_kernel: R = NT / (32 * WPR) rows, FT frames per lane
 #define CTF_RW(REAL, PREC, FT, WPR, NT) \
