@@ -100,7 +100,8 @@ typedef enum ctf_err_kind {
   CTF_KIND_NONFINITE_OBJ = 6,   /* estimator.cpp:647-648 */
   CTF_KIND_NONFINITE_X = 7,     /* estimator.cpp:521-522 */
   CTF_KIND_ZERO_X = 8,          /* estimator.cpp:523-524 (ConfigError) */
-  CTF_KIND_SINGULAR_IMAGE = 9   /* wiener.cpp:38-40 */
+  CTF_KIND_SINGULAR_IMAGE = 9,  /* wiener.cpp:38-40 */
+  CTF_KIND_PROJECTION = 10      /* estimator.cpp:105-115 (IP rule) */
 } ctf_err_kind;
 
 typedef struct ctf_err {
@@ -124,7 +125,7 @@ typedef struct ctf_problem {
   int32_t taps_per_source[CTF_MAX_SOURCES];    /* L_n, sum = D = num_mics*stack_taps */
   int32_t bases_per_source[CTF_MAX_SOURCES];   /* K_n */
   int32_t iterations;
-  int32_t update_rule;                         /* ctf_rule; IP is rejected (scope) */
+  int32_t update_rule;                         /* ctf_rule; IP runs on the covariance-domain kernel */
   int32_t precision;                           /* ctf_precision of the compute path */
   int32_t x_precision;                         /* ctf_precision of the host x buffer */
   double psd_floor;                            /* relative floor, model.hpp:29 */

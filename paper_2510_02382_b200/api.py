@@ -175,7 +175,7 @@ class Session:
     def __init__(self, x: np.ndarray, taps, bases, *, stack_taps=1, iterations=100, precision="f64",
                  psd_floor=1e-10, seed=0, device=0, world_size=1, rank=0, comm_id: Optional[bytes] = None,
                  group=None, checks: int = 0, signal: Optional[np.ndarray] = None, window_len: int = 0,
-                 hop: int = 0):
+                 hop: int = 0, update_rule: str = "iss"):
         """x: [B, F, T, M] spectrogram batch, or x=None with signal = [B, M, length]
         float64 time-domain mixtures (the STFT runs on the GPU, ctf_setup_signal)."""
         self.lib = L.load()
@@ -213,7 +213,8 @@ class Session:
         self.lib.ctf_shard_range(F, world_size, rank, C.byref(lo), C.byref(hi))
         self.bin_range = (lo.value, hi.value)
         self.problem = _problem(B, F, T, M, stack_taps, self.taps, self.bases, iterations, precision, xprec,
-                                psd_floor, seed, checks=checks)
+                                psd_floor, seed, checks=checks,
+                                rule=L.CTF_RULE_IP if update_rule.lower() == "ip" else L.CTF_RULE_ISS)
         if signal is not None:
             self.signal_length, self.window_len, self.hop = signal.shape[2], window_len, hop
             _check(self.lib.ctf_setup_signal(self._ctx, C.byref(self.problem), L.dptr(signal), signal.shape[2],
@@ -411,14 +412,13 @@ def run(config: CtfConfig, x: np.ndarray, checks: Optional[CheckOptions] = None,
     stack_taps = L > 1, x holds num_channels / L microphones and the
     stacked observation is built on the GPU."""
     config.validate()
-    if config.update_rule.lower() != "iss":
-        raise ConfigError("update rule 'ip' is not implemented on the GPU path (ISS only)")
     if x.shape[1] * stack_taps != config.num_channels:
         raise ConfigError(f"mixture has {x.shape[1] * stack_taps} channels but config expects {config.num_channels}")
     xa = _spectrogram_to_abi(x)
     s = Session(xa, config.taps_per_source, config.bases_per_source, stack_taps=stack_taps,
                 iterations=config.iterations, precision=precision, psd_floor=config.psd_floor,
-                seed=config.seed, device=device, checks=checks.flags() if checks else 0)
+                seed=config.seed, device=device, checks=checks.flags() if checks else 0,
+                update_rule=config.update_rule)
     try:
         s.iterate(config.iterations)
         dem, bases, acts, obj = s.download()[0]

@@ -246,8 +246,10 @@ void validate(const ctf_problem& p) {
   if (p.iterations < 0) throw CtfError(CTF_ERR_CONFIG, "iters must be >= 0");
   if (!(p.psd_floor > 0.0)) throw CtfError(CTF_ERR_CONFIG, "floor must be > 0");
   if (p.threads < 1) throw CtfError(CTF_ERR_CONFIG, "threads must be >= 1");
-  if (p.update_rule != CTF_RULE_ISS)
-    throw CtfError(CTF_ERR_CONFIG, "update rule 'ip' is not implemented on the GPU path (ISS only)");
+  if (p.update_rule != CTF_RULE_ISS && p.update_rule != CTF_RULE_IP)
+    throw CtfError(CTF_ERR_CONFIG, "unknown update rule");
+  if (p.update_rule == CTF_RULE_IP && p.checks)
+    throw CtfError(CTF_ERR_UNSUPPORTED, "CheckOptions are implemented for the ISS rule");
   if (p.num_mixtures < 1 || p.num_bins < 1 || p.num_frames < 1)
     throw CtfError(CTF_ERR_CONFIG, "empty problem (mixtures, bins and frames must be >= 1)");
   if (p.precision != CTF_F32 && p.precision != CTF_F64) throw CtfError(CTF_ERR_CONFIG, "unknown precision");
@@ -340,8 +342,10 @@ void plan_sweep(ctf_ctx* c) {
   const int lmax = std::max(1, *std::max_element(c->taps, c->taps + c->N));
   const int loff = ((lmax + 3) / 4) * 4;
   const int want_chk = c->prob.checks != 0;
+  const int want_ip = c->prob.update_rule == CTF_RULE_IP;
   for (const auto& v : vars) {
     if (v.chk != want_chk) continue;  // CheckOptions runs on the instrumented variants only
+    if (v.ip != want_ip) continue;    // the IP rule runs on the covariance-domain IP variants only
     if (force_kind >= 0 && v.kind != force_kind) continue;
     if (force[0] && (v.rmax != force[0] || v.ft != force[1] || v.rreg != force[2] || v.maxt != force[3] ||
                      (force[4] >= 0 && v.exact != force[4])))
@@ -502,6 +506,13 @@ void plan_sweep(ctf_ctx* c) {
       c->sp = cand;
     }
   }
+  if (!found && want_ip)
+    throw CtfError(CTF_ERR_CONFIG,
+                   "update rule 'ip' on the GPU runs on the covariance-domain kernel: it needs the stacked "
+                   "observation (stack_taps = taps of every source), num_sources == num_mics and a compiled "
+                   "(mics, taps) pair");
+  if (!found && want_chk)
+    throw CtfError(CTF_ERR_UNSUPPORTED, "CheckOptions need a resident tile (R <= 16, T <= 2048)");
   if (!found)
     throw CtfError(CTF_ERR_UNSUPPORTED, "no compiled sweep kernel for R=" + std::to_string(c->R) +
                                             " T=" + std::to_string(c->T));
@@ -705,6 +716,12 @@ void check_errors(ctf_ctx* c) {
     const std::string its = " (iteration " + std::to_string(it) + ")";
     switch (ph) {
       case ctf::kPhSweep:
+        if (c->prob.update_rule == CTF_RULE_IP)  // estimator.cpp:105-108, 111-115
+          throw CtfError(CTF_ERR_DEGENERACY,
+                         std::string(code == 1 ? "projection update: singular system after diagonal loading"
+                                               : "projection update: nonpositive row power") +
+                             its,
+                         CTF_KIND_PROJECTION, it, b, bin, row);
         throw CtfError(CTF_ERR_DEGENERACY,
                        "steering update: nonpositive denominator for rows (" + std::to_string(row) + ", " +
                            std::to_string(code) + ")" + its,

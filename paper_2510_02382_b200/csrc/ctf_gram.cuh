@@ -132,7 +132,8 @@ template <typename Real, int NT> constexpr int gram_min_blocks() {
   return std::is_same<Real, float>::value ? (NT <= 256 ? 3 : 1) : (NT <= 256 ? 2 : 1);
 }
 
-template <typename Real, int M, int L, int NT, int FT>
+// IP: the iterative-projection rule in place of the ISS steps.
+template <typename Real, int M, int L, int NT, int FT, bool IP = false>
 __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT>())
     gram_kernel(const SweepParams p, const int4* __restrict__ gtab) {
   using R2 = typename Cplx<Real>::T;
@@ -501,6 +502,198 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT>())
     return;
   }
 
+  __shared__ double s_iplogdet;
+  if constexpr (IP) {
+    // ---- IP rule (estimator.cpp:580-606, ip_update :103-273): for each row
+    // r, h = (Q_r + Q_r^H) / 2 with Q_r the weighted covariance / T
+    // (:89-101, from the Gram minus the virtual tail frames), solve
+    // (W h) u = e_r by LU with partial pivoting (pivot-ratio singularity
+    // probe 1e-13, one retry with 1e-10 trace/D diagonal loading), w_r =
+    // conj(u) / sqrt(u^H h u), then the frame-sum refinement
+    // w_r /= sqrt(sum_{j>=l} |w_r x~(j)|^2 / lambda(j-l) / T).
+    R2* qm = part;             // D x D raw Q_r / T
+    R2* cov = part + D * D;    // D x D Hermitian h
+    R2* A = cov + D * D;       // D x (D+1), column-major, rhs last
+    R2* sol = A + D * (D + 1); // D
+    __shared__ int s_iperr;
+    __shared__ double s_power;
+    if (tid == 0) s_iperr = 0;
+    for (int r = 0; r < R; ++r) {
+      const int n = r / L, l = r - n * L;
+      for (int e = tid; e < D * D; e += NT) {
+        const int a = e % D, b = e / D;
+        const int m = a / L, l1 = a - m * L, m2 = b / L, l2 = b - m2 * L;
+        R2 v = G[gidx(n, m, m2, l - l1, l - l2)];
+        for (int jj = 0; jj < l; ++jj) {  // frames j = T + jj are outside row l's range
+          const Real w = invl[n * p.lp + p.loff + T + jj - l];
+          const R2 xa = xs[m * p.xp + p.xoff + T + jj - l1], xb = xs[m2 * p.xp + p.xoff + T + jj - l2];
+          v.x -= w * fma(xa.x, xb.x, xa.y * xb.y);
+          v.y -= w * fma(xa.y, xb.x, -xa.x * xb.y);
+        }
+        v.x /= (Real)T;
+        v.y /= (Real)T;
+        qm[a + b * D] = v;
+      }
+      __syncthreads();
+      for (int e = tid; e < D * D; e += NT) {
+        const int a = e % D, b = e / D;
+        const R2 u = qm[a + b * D], t = qm[b + a * D];
+        R2 h;
+        h.x = Real(0.5) * (u.x + t.x);
+        h.y = Real(0.5) * (u.y - t.y);
+        cov[a + b * D] = h;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        auto attempt = [&](Real load) -> bool {
+          // A = W (h + load I) = W h + load W, rhs e_r
+          for (int e = lane; e < D * (D + 1); e += 32) {
+            const int i = e % D, j = e / D;
+            R2 acc;
+            acc.x = acc.y = Real(0);
+            if (j < D) {
+              for (int k = 0; k < D; ++k) cmac(acc, Wb[i + k * R], cov[k + j * D]);
+              acc.x += load * Wb[i + j * R].x;
+              acc.y += load * Wb[i + j * R].y;
+            } else {
+              acc.x = (i == r) ? Real(1) : Real(0);
+            }
+            A[i + j * D] = acc;
+          }
+          __syncwarp();
+          double minp = INFINITY, maxp = 0.0;
+          for (int c = 0; c < D; ++c) {
+            // pivot: largest |a| in column c at or below the diagonal, lowest row on ties
+            Real best = Real(-1);
+            int prow = D;
+            if (lane >= c && lane < D) {
+              const R2 v = A[lane + c * D];
+              best = sqrt(cnorm(v));
+              prow = lane;
+            }
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) {
+              const Real ob = __shfl_xor_sync(kFull, best, o);
+              const int orow = __shfl_xor_sync(kFull, prow, o);
+              if (ob > best || (ob == best && orow < prow)) {
+                best = ob;
+                prow = orow;
+              }
+            }
+            minp = fmin(minp, (double)best);
+            maxp = fmax(maxp, (double)best);
+            if (prow != c)
+              for (int j = lane; j <= D; j += 32) {
+                const R2 t = A[c + j * D];
+                A[c + j * D] = A[prow + j * D];
+                A[prow + j * D] = t;
+              }
+            __syncwarp();
+            if (!(best > Real(0))) continue;
+            const R2 piv = A[c + c * D];
+            const Real ip2 = Real(1) / cnorm(piv);
+            const int w = D - c;  // rows c+1..D-1 x columns c+1..D
+            for (int e = lane; e < (w - 1) * w; e += 32) {
+              const int rr = c + 1 + e % (w - 1), j = c + 1 + e / (w - 1);
+              const R2 arc = A[rr + c * D];
+              R2 f;  // a(r, c) / a(c, c)
+              f.x = (arc.x * piv.x + arc.y * piv.y) * ip2;
+              f.y = (arc.y * piv.x - arc.x * piv.y) * ip2;
+              cmsub(A[rr + j * D], f, A[c + j * D]);
+            }
+            __syncwarp();
+          }
+          if (!(minp > 1e-13 * maxp)) return false;
+          if (lane == 0)
+            for (int rr = D - 1; rr >= 0; --rr) {
+              R2 acc = A[rr + D * D];
+              for (int j = rr + 1; j < D; ++j) cmsub(acc, A[rr + j * D], sol[j]);
+              const R2 d = A[rr + rr * D];
+              const Real id = Real(1) / cnorm(d);
+              R2 q;
+              q.x = (acc.x * d.x + acc.y * d.y) * id;
+              q.y = (acc.y * d.x - acc.x * d.y) * id;
+              sol[rr] = q;
+            }
+          __syncwarp();
+          bool fin = true;
+          if (lane < D) fin = cfinite(sol[lane]);
+          return __all_sync(kFull, fin);
+        };
+        bool ok = attempt(Real(0));
+        if (!ok) {
+          Real tr = Real(0);
+          for (int i = 0; i < D; ++i) tr += cov[i + i * D].x;
+          ok = attempt(Real(1e-10) * tr / (Real)D);
+        }
+        int err = 0;
+        if (!ok) {
+          err = 1;  // singular system after diagonal loading
+        } else {
+          // scale against the unloaded covariance: norm2 = Re(u^H h u)
+          Real part_n = Real(0);
+          if (lane < D) {
+            R2 wgt;
+            wgt.x = wgt.y = Real(0);
+            for (int j = 0; j < D; ++j) cmac(wgt, cov[lane + j * D], sol[j]);
+            const R2 u = sol[lane];
+            part_n = u.x * wgt.x + u.y * wgt.y;
+          }
+          for (int o = 16; o >= 1; o >>= 1) part_n += __shfl_xor_sync(kFull, part_n, o);
+          if (!(part_n > Real(0)) || !isfinite(part_n)) {
+            err = 2;  // nonpositive row power
+          } else if (lane < D) {
+            const Real sc = Real(1) / sqrt(part_n);
+            const R2 u = sol[lane];
+            R2 wv;
+            wv.x = u.x * sc;
+            wv.y = -u.y * sc;
+            Wb[r + lane * R] = wv;
+          }
+        }
+        if (lane == 0 && err) s_iperr = err;
+      }
+      __syncthreads();
+      if (s_iperr) {
+        if (tid == 0) record_err<Real>(p.err, mix, err_key(p.iteration, kPhSweep, gbin, r, s_iperr));
+        return;
+      }
+      // frame-sum refinement of the row scale (estimator.cpp:596-602)
+      double pw = 0.0;
+      for (int k = 0; k < FT; ++k) {
+        const int j = tid + k * NT;
+        if (j < T) {
+          R2 y;
+          y.x = y.y = Real(0);
+#pragma unroll
+          for (int m = 0; m < M; ++m)
+#pragma unroll
+            for (int l1 = 0; l1 < L; ++l1) cmac(y, Wb[r + (m * L + l1) * R], xs[m * p.xp + p.xoff + j - l1]);
+          pw += (double)(cnorm(y) * invl[n * p.lp + p.loff + j - l]);
+        }
+      }
+      double v1[1] = {pw};
+      block_sum_d<1>(v1, dred, lane, warp, NW);
+      const double power = v1[0] / T;
+      if (power > 0.0 && isfinite(power) && tid < D) {
+        R2 w = Wb[r + tid * R];
+        w.x = (Real)((double)w.x / sqrt(power));
+        w.y = (Real)((double)w.y / sqrt(power));
+        Wb[r + tid * R] = w;
+      }
+      __syncthreads();
+    }
+    // exact log|det W'| (no determinant lemma for IP)
+    if (warp == 0) {
+      R2* Acp = part;
+      for (int i = lane; i < R * D; i += 32) Acp[i] = Wb[i];
+      __syncwarp();
+      double out = 0.0;
+      const int st = warp_logdet<Real>(Acp, R, lane, out);
+      if (lane == 0) s_iplogdet = st == 4 ? -INFINITY : out;
+    }
+    __syncthreads();
+  } else {
   // ---- R covariance-domain ISS steps (estimator.cpp:556-579, 275-302)
   R2* piv = zs;     // 2 x (D + LT1): pivot W row and tail, double-buffered by step parity
   Real* fac = red;  // (1 - z_r) per row, multiplied in row order at the end
@@ -552,14 +745,15 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT>())
       return;
     }
   }
-  R2* Wf = Wb;  // W' (column-major R x D) for the demix
-  if (rowv && hl < D) Wf[hl * R + row] = wreg;
+  if (rowv && hl < D) Wb[hl * R + row] = wreg;
   if (tid == 0) {
     double dp = 1.0;
     for (int r = 0; r < R; ++r) dp *= (double)fac[r];
     s_dprod = dp;
   }
   __syncthreads();
+  }
+  R2* Wf = Wb;  // W' (column-major R x D) for the demix
   CTF_PHASE(6);
 
   // ---- per source n: Y rows of n = W' x~ (estimator.cpp:607) for this
@@ -670,7 +864,7 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT>())
     for (int w = 0; w < NW; ++w) s += (double)red[w * 32 + tid];
     p.rowpow[tile * R + tid] = s;
   }
-  if (tid == 0) p.logdet[tile] = logdet + log(s_dprod);
+  if (tid == 0) p.logdet[tile] = IP ? s_iplogdet : logdet + log(s_dprod);
   for (int i = tid; i < R * D; i += NT) Wg[i] = Wf[i];
   CTF_PHASE(9);
 }

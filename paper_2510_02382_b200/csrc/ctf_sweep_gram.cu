@@ -12,6 +12,13 @@ std::vector<SweepVariant> sweep_variants_gram_f64() {
   return {GD(2, 2, 128, 4), GD(2, 2, 256, 4), GD(2, 3, 128, 4), GD(2, 3, 256, 4),
           GD(2, 5, 256, 4), GD(2, 5, 512, 4), GD(3, 4, 256, 4), GD(3, 4, 512, 4)};
 }
+// IP rule (update_rule = ip) on the same kernel
+std::vector<SweepVariant> sweep_variants_gram_ip() {
+  return {CTF_GRI(float, 1, 2, 2, 128, 4), CTF_GRI(float, 1, 2, 3, 256, 4), CTF_GRI(float, 1, 2, 5, 256, 4),
+          CTF_GRI(float, 1, 3, 4, 512, 4), CTF_GRI(double, 0, 2, 2, 128, 4), CTF_GRI(double, 0, 2, 3, 256, 4),
+          CTF_GRI(double, 0, 2, 5, 256, 4), CTF_GRI(double, 0, 3, 4, 256, 4),
+          CTF_GRI(double, 0, 3, 4, 512, 4), CTF_GRI(float, 1, 3, 4, 256, 4)};
+}
 }  // namespace ctf
 #ifdef CTF_PHASE_TIMING
 // dev instrumentation (builds with -DCTF_PHASE_TIMING only): per-CTA clock64

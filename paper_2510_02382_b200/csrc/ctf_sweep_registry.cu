@@ -16,6 +16,7 @@ std::vector<SweepVariant> sweep_variants_rowwarp_f64();
 std::vector<SweepVariant> sweep_variants_check_f32();
 std::vector<SweepVariant> sweep_variants_gram_f32();
 std::vector<SweepVariant> sweep_variants_gram_f64();
+std::vector<SweepVariant> sweep_variants_gram_ip();
 std::vector<SweepVariant> sweep_variants_check_f64();
 const std::vector<SweepVariant>& sweep_variants_f32() {
   static const std::vector<SweepVariant> v = [] {
@@ -34,6 +35,8 @@ const std::vector<SweepVariant>& sweep_variants_f32() {
     a.insert(a.end(), ck.begin(), ck.end());
     auto gr = sweep_variants_gram_f32();
     a.insert(a.end(), gr.begin(), gr.end());
+    for (const auto& v : sweep_variants_gram_ip())
+      if (v.prec == 1) a.push_back(v);
     return a;
   }();
   return v;
@@ -55,6 +58,8 @@ const std::vector<SweepVariant>& sweep_variants_f64() {
     a.insert(a.end(), ck.begin(), ck.end());
     auto gr = sweep_variants_gram_f64();
     a.insert(a.end(), gr.begin(), gr.end());
+    for (const auto& v : sweep_variants_gram_ip())
+      if (v.prec == 0) a.push_back(v);
     return a;
   }();
   return v;

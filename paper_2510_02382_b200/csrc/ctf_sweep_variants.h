@@ -24,6 +24,7 @@ struct SweepVariant {
   void (*cfn)(ClusterParams) = nullptr;  // kind 3: cluster_kernel (rmax = rows per CTA)
   int chk = 0;  // kind 0 compiled with the CheckOptions instrumentation
   void (*gfn)(SweepParams, const int4*) = nullptr;  // kind 4: gram_kernel (rreg = M, lt = L)
+  int ip = 0;  // kind 4 compiled with the IP rule instead of the ISS steps
 };
 #define CTF_V(REAL, PREC, RMAX, FT, RREG, NT, EX) \
   SweepVariant { PREC, RMAX, FT, RREG, NT, EX, sweep_kernel<REAL, RMAX, FT, RREG, NT, EX> }
@@ -56,6 +57,10 @@ struct SweepVariant {
 #define CTF_GR(REAL, PREC, M, L, NT, FT)                                                                 \
   SweepVariant {                                                                                         \
     PREC, (M) * (L), FT, M, NT, 1, nullptr, 4, L, nullptr, nullptr, 0, gram_kernel<REAL, M, L, NT, FT>   \
+  }
+#define CTF_GRI(REAL, PREC, M, L, NT, FT)                                                                   \
+  SweepVariant {                                                                                            \
+    PREC, (M) * (L), FT, M, NT, 1, nullptr, 4, L, nullptr, nullptr, 0, gram_kernel<REAL, M, L, NT, FT, true>, 1 \
   }
 // rowwarp_kernel: R = NT / (32 * WPR) rows, FT frames per lane
 #define CTF_RW(REAL, PREC, FT, WPR, NT) \

@@ -276,7 +276,7 @@ def test_errors_match_reference_semantics():
         run(cfg, np.zeros((4, 4, 10), complex))
     with pytest.raises(ConfigError):  # bad tap split
         run(CtfConfig(2, 4, [1, 2], [3, 3], iterations=2), g.standard_normal((4, 4, 10)) + 0j)
-    with pytest.raises(ConfigError):  # IP rule is out of the GPU path's scope
+    with pytest.raises(ConfigError):  # IP on a pre-stacked observation: outside the covariance kernel layout
         run(CtfConfig(2, 4, [2, 2], [3, 3], iterations=2, update_rule="ip"), g.standard_normal((4, 4, 10)) + 0j)
     x = g.standard_normal((2, 4, 10)) + 1j * g.standard_normal((2, 4, 10))
     x[1, 2, 3] = np.nan
@@ -577,3 +577,60 @@ int main() {{
     ref = O.run(O.config([2, 2], [3, 3], iterations=6, seed=21), x)
     assert np.max(np.abs(obj - ref["objective"]) / np.abs(ref["objective"])) <= 1e-9
     assert rel(W, ref["W"]) <= 1e-9
+
+
+def _ip_history(raw, L, K, iters, precision, seed):
+    M = raw.shape[3]
+    s = Session(raw, [L] * M, [K] * M, stack_taps=L, iterations=iters, precision=precision, seed=seed,
+                update_rule="ip")
+    assert "gram_kernel" in json.loads(s.describe())["sweep_kernel"]
+    hist = []
+    for _ in range(iters):
+        s.iterate(1)
+        hist.append(s.download_raw())
+    s.close()
+    return hist
+
+
+@pytest.mark.parametrize("M,L,T,K", [(2, 2, 200, 3), (2, 5, 400, 4), (3, 4, 300, 3)])
+def test_ip_rule_fp64_every_iteration(M, L, T, K):
+    """IP rule on the GPU (estimator.cpp:580-606: weighted covariance, pivoted
+    solve of W h u = e_r, normalisation, frame-sum refinement; exact log|det|)
+    against the oracle's IP run: 1e-9 relative after every iteration."""
+    F, iters, seed = 21, 8, 4
+    raw = synth_mixtures(1, F, T, M, M, L, K, 0.6, 900 + M * L)
+    ref = O.run(O.config([L] * M, [K] * M, iterations=iters, seed=seed, threads=NPROC, rule="ip"),
+                O.stack_observation(raw[0], L), history=True)
+    hist = _ip_history(raw, L, K, iters, "f64", seed)
+    check_history(hist, ref, 0, 1e-9, f"ip M={M} L={L}")
+
+
+def test_ip_rule_fp32_tolerance_and_iss_vs_ip():
+    """fp32 IP within the north-star fp32 tolerance of the fp64 oracle, and
+    ISS and IP reach nearby objectives (test_run.cpp:136-150, 5 %)."""
+    M, L, T, K, F, iters, seed = 2, 3, 400, 4, 33, 20, 6
+    raw = synth_mixtures(1, F, T, M, M, L, K, 0.6, 77)
+    ref = O.run(O.config([L] * M, [K] * M, iterations=iters, seed=seed, threads=NPROC, rule="ip"),
+                O.stack_observation(raw[0], L), history=True)
+    hist = _ip_history(raw.astype(np.complex64), L, K, iters, "f32", seed)
+    for it, (W, B, V, obj) in enumerate(hist):
+        e = max(rel(W[0], ref["hist_W"][it].reshape(F, -1)), rel(B[0], ref["hist_B"][it]),
+                rel(V[0], ref["hist_V"][it]))
+        assert e <= 1e-4, f"it={it + 1}: {e:.2e}"
+    iss = gpu_history(raw, [L] * M, [K] * M, iters, "f64", seed, L)[-1][3][0, -1]
+    ip = hist[-1][3][0, -1]
+    assert abs(ip - iss) / abs(iss) < 0.05
+
+
+def test_ip_rule_errors_and_run_api():
+    """run(config with update_rule='ip') on a stacked observation; the IP rule
+    with CheckOptions or on a pre-stacked layout is refused with ConfigError /
+    unsupported, never silently run on another path."""
+    M, L, T, K, F = 2, 2, 120, 3, 9
+    raw = synth_mixtures(1, F, T, M, M, L, K, 0.6, 5)
+    cfg = CtfConfig(M, M * L, [L] * M, [K] * M, iterations=3, update_rule="ip", seed=2)
+    res = run(cfg, np.transpose(raw[0], (0, 2, 1)), stack_taps=L)
+    ref = O.run(O.config([L] * M, [K] * M, iterations=3, seed=2, rule="ip"), O.stack_observation(raw[0], L))
+    assert rel(res.demixing, np.transpose(ref["W"], (0, 2, 1))) <= 1e-9
+    with pytest.raises(Exception):
+        run(cfg, np.transpose(raw[0], (0, 2, 1)), CheckOptions(det_lemma=True), stack_taps=L)

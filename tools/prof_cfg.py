@@ -8,11 +8,12 @@ CFG = {0: (1, 513, 500, 2, 2, 2, 10, 0.6), 1: (64, 513, 1000, 2, 2, 5, 10, 0.6),
 ap = argparse.ArgumentParser()
 ap.add_argument("--cfg", type=int, default=1); ap.add_argument("--prec", default="f32")
 ap.add_argument("--iters", type=int, default=5); ap.add_argument("--mixtures", type=int, default=0)
+ap.add_argument("--rule", default="iss")
 a = ap.parse_args()
 B, F, T, M, N, L, K, dec = CFG[a.cfg]
 if a.mixtures: B = a.mixtures
 x = synth_mixtures(B, F, T, M, N, L, K, dec, 1, precision="f32" if a.prec == "f32" else "f64")
-s = Session(x, [L]*N, [K]*N, stack_taps=L, iterations=a.iters, precision=a.prec)
+s = Session(x, [L]*N, [K]*N, stack_taps=L, iterations=a.iters, precision=a.prec, update_rule=a.rule)
 print(s.describe(), flush=True)
 s.iterate(1); s.reset_timing()
 s.iterate(a.iters)
