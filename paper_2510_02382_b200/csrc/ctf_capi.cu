@@ -401,8 +401,8 @@ void plan_sweep(ctf_ctx* c) {
       cand.off_x = (int)take((size_t)M * cand.xp * cs);
       cand.off_l = (int)take((size_t)c->N * glp * rs);
       cand.off_y = (int)take((size_t)c->N * M * M * NA * NA * cs);
-      const int NS = c->real_size == 4 ? c->N : 1;  // sources per Gram pass (gram_ns)
-      cand.off_e = (int)take(std::max((size_t)NS * NA * (nt + 1) * cs, (size_t)L * TP * rs));
+      const int NS = c->real_size == 4 ? c->N : 1;  // sources per Gram pass (gram_ns) and per demix group
+      cand.off_e = (int)take(std::max((size_t)NS * NA * (nt + 1) * cs, (size_t)NS * L * TP * rs));
       cand.off_w = (int)take((size_t)2 * c->R * c->D * cs);
       cand.off_z = (int)take((size_t)(2 * c->R * std::max(1, L - 1) + 2 * (c->D + std::max(1, L - 1))) * cs);
       cand.off_red = (int)take((size_t)32 * NW * rs);

@@ -756,93 +756,115 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT>())
   R2* Wf = Wb;  // W' (column-major R x D) for the demix
   CTF_PHASE(6);
 
-  // ---- per source n: Y rows of n = W' x~ (estimator.cpp:607) for this
-  // thread's frames (|y|^2 to shared memory, row powers), delayed energies
-  // E_n(tau) = sum_{l, tau+l<T} |y_(n,l)(tau+l)|^2 in l order (estimator.cpp
-  // :318-330), then MU-B of source n (estimator.cpp:313-346, 16 bases per pass)
+  // ---- per source group (fp32: all sources, fp64: one): Y rows of the group
+  // = W' x~ (estimator.cpp:607) for this thread's frames (|y|^2 to shared
+  // memory, row powers), delayed energies E_n(tau) = sum_{l, tau+l<T}
+  // |y_(n,l)(tau+l)|^2 in l order (estimator.cpp:318-330, written in place of
+  // the source's first |y|^2 row), then MU-B per source (estimator.cpp
+  // :313-346, 16 bases per pass)
+  constexpr int NSD = F32 ? N : 1;
+  constexpr int GR = NSD * L;  // rows per group
   Real rp[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) rp[i] = Real(0);
   Real* Eg = reinterpret_cast<Real*>(p.E);
 #pragma unroll
-  for (int n = 0; n < N; ++n) {  // unrolled: the row-power register index n*L + i is static
+  for (int g0 = 0; g0 < N; g0 += NSD) {  // unrolled: the row-power register index is static
 #pragma unroll 1
     for (int k = 0; k < FT; ++k) {
       const int j = tid + k * NT;
-      R2 acc[L];
+      R2 acc[GR];
 #pragma unroll
-      for (int i = 0; i < L; ++i) acc[i].x = acc[i].y = Real(0);
+      for (int i = 0; i < GR; ++i) acc[i].x = acc[i].y = Real(0);
 #pragma unroll
       for (int m = 0; m < M; ++m)
 #pragma unroll
         for (int l1 = 0; l1 < L; ++l1) {
           const R2 xv = xs[m * p.xp + p.xoff + j - l1];
-          const R2* wc = Wf + (m * L + l1) * R + n * L;
+          const R2* wc = Wf + (m * L + l1) * R + g0 * L;
+          if constexpr (F32 && GR % 2 == 0) {  // W pairs with 16-byte loads
+            const float4* w4 = reinterpret_cast<const float4*>(wc);
 #pragma unroll
-          for (int i = 0; i < L; ++i) acc[i] = Ops::mac(wc[i], xv, acc[i]);
+            for (int i = 0; i < GR; i += 2) {
+              const float4 w = w4[i / 2];
+              acc[i] = Ops::mac(make_float2(w.x, w.y), xv, acc[i]);
+              acc[i + 1] = Ops::mac(make_float2(w.z, w.w), xv, acc[i + 1]);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < GR; ++i) acc[i] = Ops::mac(wc[i], xv, acc[i]);
+          }
         }
 #pragma unroll
-      for (int i = 0; i < L; ++i) {
+      for (int i = 0; i < GR; ++i) {
         const Real q = (j < T) ? cnorm(acc[i]) : Real(0);
         Pq[i * TP + j] = q;
-        rp[n * L + i] += q;
+        rp[g0 * L + i] += q;
       }
     }
-    __syncthreads();  // Pq of source n complete
+    __syncthreads();  // Pq of the group complete
 #pragma unroll
-    for (int k = 0; k < FT; ++k) {
-      const int tau = tid + k * NT;
-      Real e = Real(0);
-#pragma unroll
-      for (int l = 0; l < L; ++l)
-        if (tau + l < T) e += Pq[l * TP + tau + l];
-      Pq[tau] = e;  // row 0 entry tau is read only by this thread
-      if (tau < T) Eg[(((size_t)mix * N + n) * p.FL + bin) * T + tau] = e;
-    }
-    __syncthreads();  // E_n complete (MU-B reads it at this thread's frames only, but red is shared)
-    const int k0 = p.koff[n], k1 = p.koff[n + 1];
-    const Real* il = invl + n * p.lp + p.loff;
-    for (int kb = k0; kb < k1; kb += 16) {
-      Real a[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) a[i] = Real(0);
-      const Real* vrow[16];
-#pragma unroll
-      for (int q = 0; q < 16; ++q) vrow[q] = Vg + (size_t)min(kb + q, k1 - 1) * T + tid;
+    for (int n = g0; n < g0 + NSD; ++n) {
+      Real* pq = Pq + (size_t)(n - g0) * L * TP;
 #pragma unroll
       for (int k = 0; k < FT; ++k) {
         const int tau = tid + k * NT;
-        const Real ilv = il[tau];
-        const Real an = Pq[tau] * (ilv * ilv);
-        const Real bn = (tau < T) ? ilv * (Real)min(L, T - tau) : Real(0);
+        Real e = Real(0);
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const Real vv = __ldg(vrow[q] + k * NT);
-          if constexpr (F32) {
-            const float2 t = ffma2s(make_float2(an, bn), vv, make_float2(a[q], a[16 + q]));
-            a[q] = t.x;
-            a[16 + q] = t.y;
-          } else {
-            a[q] = fma(an, vv, a[q]);
-            a[16 + q] = fma(bn, vv, a[16 + q]);
-          }
-        }
-      }
-      warp_reduce_scatter(a, lane);
-      __syncthreads();  // previous pass's reads of red are done
-      red[warp * 32 + lane] = a[0];
-      __syncthreads();
-      if (tid < 16 && kb + tid < k1) {
-        Real num = Real(0), den = Real(0);
-        for (int w = 0; w < NW; ++w) {
-          num += red[w * 32 + tid];
-          den += red[w * 32 + 16 + tid];
-        }
-        const Real b = Bs[kb + tid];
-        Bg[kb + tid] = fmax(b * sqrt(num / den), floor_abs);
+        for (int l = 0; l < L; ++l)
+          if (tau + l < T) e += pq[l * TP + tau + l];
+        pq[tau] = e;  // entry tau of the source's first row is read only by this thread
+        if (tau < T) Eg[(((size_t)mix * N + n) * p.FL + bin) * T + tau] = e;
       }
     }
-    __syncthreads();  // Pq is rewritten by the next source
+    __syncthreads();  // red is shared by the MU-B passes below
+#pragma unroll
+    for (int n = g0; n < g0 + NSD; ++n) {
+      const Real* En = Pq + (size_t)(n - g0) * L * TP;
+      const int k0 = p.koff[n], k1 = p.koff[n + 1];
+      const Real* il = invl + n * p.lp + p.loff;
+      for (int kb = k0; kb < k1; kb += 16) {
+        Real a[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) a[i] = Real(0);
+        const Real* vrow[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) vrow[q] = Vg + (size_t)min(kb + q, k1 - 1) * T + tid;
+#pragma unroll
+        for (int k = 0; k < FT; ++k) {
+          const int tau = tid + k * NT;
+          const Real ilv = il[tau];
+          const Real an = En[tau] * (ilv * ilv);
+          const Real bn = (tau < T) ? ilv * (Real)min(L, T - tau) : Real(0);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const Real vv = __ldg(vrow[q] + k * NT);
+            if constexpr (F32) {
+              const float2 t = ffma2s(make_float2(an, bn), vv, make_float2(a[q], a[16 + q]));
+              a[q] = t.x;
+              a[16 + q] = t.y;
+            } else {
+              a[q] = fma(an, vv, a[q]);
+              a[16 + q] = fma(bn, vv, a[16 + q]);
+            }
+          }
+        }
+        warp_reduce_scatter(a, lane);
+        __syncthreads();  // previous pass's reads of red are done
+        red[warp * 32 + lane] = a[0];
+        __syncthreads();
+        if (tid < 16 && kb + tid < k1) {
+          Real num = Real(0), den = Real(0);
+          for (int w = 0; w < NW; ++w) {
+            num += red[w * 32 + tid];
+            den += red[w * 32 + 16 + tid];
+          }
+          const Real b = Bs[kb + tid];
+          Bg[kb + tid] = fmax(b * sqrt(num / den), floor_abs);
+        }
+      }
+    }
+    __syncthreads();  // Pq is rewritten by the next group
   }
   CTF_PHASE(7);
   // check_all_finite on Y (estimator.cpp:497-499): a non-finite estimate
