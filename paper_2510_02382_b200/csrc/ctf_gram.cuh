@@ -125,6 +125,14 @@ __device__ __forceinline__ void gram_block(const typename Cplx<Real>::T* __restr
   if (u < u1) gram_step<Real, CNT, NS, UB, true>(x1, x2, w0, lp, u, u1, wv, acc);
 }
 
+// 1/x correctly rounded (same value as the division, no slow path) and the
+// objective's log term: MUFU-based in fp32 (abs. error ~1e-6, far inside the
+// fp32 cost tolerance), exact in fp64.
+__device__ __forceinline__ float rcp_rn(float x) { return __frcp_rn(x); }
+__device__ __forceinline__ double rcp_rn(double x) { return 1.0 / x; }
+__device__ __forceinline__ float log_fast(float x) { return __logf(x); }
+__device__ __forceinline__ double log_fast(double x) { return log(x); }
+
 // Sources accumulated per Gram pass: all of them in fp32 (the conj products
 // are shared); one at a time in fp64 (register budget, half the partials).
 template <typename Real, int N> constexpr int gram_ns() { return std::is_same<Real, float>::value ? N : 1; }
@@ -307,8 +315,8 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT>())
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const Real l = fmax(lam[i], floor_abs);
-          il[p.loff + t4 + i] = Real(1) / l;
-          if (p.has_prev) logsum += (double)min(L, T - t4 - i) * (double)log(l);
+          il[p.loff + t4 + i] = rcp_rn(l);
+          if (p.has_prev) logsum += (double)min(L, T - t4 - i) * (double)log_fast(l);
         }
       }
     } else {
@@ -330,8 +338,8 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT>())
         const int tau = tid + k * NT;
         if (tau < T) {
           const Real l = fmax(lam[k], floor_abs);
-          il[p.loff + tau] = Real(1) / l;
-          if (p.has_prev) logsum += (double)min(L, T - tau) * (double)log(l);
+          il[p.loff + tau] = rcp_rn(l);
+          if (p.has_prev) logsum += (double)min(L, T - tau) * (double)log_fast(l);
         }
       }
     }

@@ -1,4 +1,2 @@
-CTF_SWEEP_KIND=0 timeout 300 python tools/prof_cfg.py --cfg 0 --prec f64 --iters 10 2>&1 | tail -1
-timeout 300 python tools/prof_cfg.py --cfg 0 --prec f64 --iters 10 2>&1 | tail -1
-CTF_SWEEP_KIND=0 timeout 300 python tools/prof_cfg.py --cfg 0 --prec f32 --iters 10 2>&1 | tail -1
-timeout 300 python tools/prof_cfg.py --cfg 0 --prec f32 --iters 10 2>&1 | tail -1
+for c in 1 2; do timeout 300 python tools/prof_cfg.py --cfg $c --prec f32 --iters 10 2>&1 | tail -1; done
+timeout 1500 python -m pytest tests/test_gpu_parity.py -q -x 2>&1 | tail -2
