@@ -22,6 +22,9 @@
  *          directly: ctf_setup_signal(); the back end of cmd_separate
  *          (reconstruct_images + image_to_signal, wiener.cpp:51-64):
  *          ctf_images_to_signal()
+ *   write_/read_spectrogram, write_/read_factors (container.hpp:22-29)
+ *       -> ctf_write_/ctf_read_spectrogram, ctf_write_/ctf_read_factors,
+ *          ctf_setup_spectrogram_files (a `.spec` straight into the estimator)
  *   CtfConfig (model.hpp:21-35) + the stacked observation of BASELINE (a)
  *       -> ctf_problem
  *   ConfigError / IoError / DegeneracyError{iteration,bin,row}
@@ -262,6 +265,33 @@ int ctf_setup_signal(ctf_ctx* ctx, const ctf_problem* prob, const double* sample
  * NULL to query *out_len. */
 int ctf_images_to_signal(ctf_ctx* ctx, int ref_channel, int window_len, int hop, int64_t original_length,
                          double* out, int64_t* out_len, ctf_err* err);
+
+/* ---- Binary containers (container.hpp:1-10, container.cpp; host only, no
+ * GPU). IoError texts of the reference ("cannot open file: ...", "...: bad or
+ * mismatched container magic", "...: truncated spectrogram container").
+ * Spectrogram body: complex64 [bin][frame][channel]; read/write it as complex64
+ * (precision CTF_F32, byte copy) or complex128 (CTF_F64, widened/narrowed
+ * exactly like get_complex/put_complex). */
+typedef struct ctf_spec_header {
+  uint32_t bins, frames, channels, window_len, hop, sample_rate;
+  uint64_t original_length;
+} ctf_spec_header;
+int ctf_read_spectrogram(const char* path, ctf_spec_header* hdr, void* data /* NULL: header only */,
+                         int out_precision, ctf_err* err);
+int ctf_write_spectrogram(const char* path, const ctf_spec_header* hdr, const void* data, int in_precision,
+                          ctf_err* err);
+/* ctf_setup() from one `.spec` file per mixture (the complex64 body is
+ * uploaded as stored, x_precision = f32); prob->num_bins/num_frames/num_mics
+ * may be 0 (taken from the files) or must match; hdr_out (optional) receives
+ * the first file's header (window/hop/rate for the inverse STFT). */
+int ctf_setup_spectrogram_files(ctf_ctx* ctx, const ctf_problem* prob, const char* const* paths, int num_paths,
+                                ctf_spec_header* hdr_out, ctf_err* err);
+/* NmfFactors container: B/V in the ctf_download layouts of ONE mixture
+ * (per source column-major F x K_n / K_n x T); the file stores them row-major. */
+int ctf_write_factors(const char* path, int num_sources, int bins, int frames, const int32_t* bases,
+                      double floor_abs, const double* B, const double* V, ctf_err* err);
+int ctf_read_factors(const char* path, int* num_sources, int* bins, int* frames, int32_t* bases /* [16] */,
+                     double* floor_abs, double* B /* NULL: header only */, double* V, ctf_err* err);
 
 /* Synthetic generator of BASELINE.json configs (host code, no GPU):
  * mixture b uses mt19937_64(base_seed + b); see DESIGN.md for draw order.

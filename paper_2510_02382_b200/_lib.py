@@ -37,6 +37,11 @@ class CtfProblem(C.Structure):
                 ("checks", C.c_int32), ("reserved", C.c_int32 * 6)]
 
 
+class CtfSpecHeader(C.Structure):
+    _fields_ = [("bins", C.c_uint32), ("frames", C.c_uint32), ("channels", C.c_uint32), ("window_len", C.c_uint32),
+                ("hop", C.c_uint32), ("sample_rate", C.c_uint32), ("original_length", C.c_uint64)]
+
+
 class CtfTiming(C.Structure):
     _fields_ = [("sweep_ms", C.c_double), ("mu_ms", C.c_double), ("finalize_ms", C.c_double),
                 ("sweep_launches", C.c_int64), ("launches", C.c_int64)]
@@ -77,6 +82,16 @@ SIGNATURES = {
                                   C.c_int, C.POINTER(CtfErr)]),
     "ctf_istft_device": (C.c_int, [_P, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                    C.c_int64, C.c_void_p, C.POINTER(CtfErr)]),
+    "ctf_read_spectrogram": (C.c_int, [C.c_char_p, C.POINTER(CtfSpecHeader), C.c_void_p, C.c_int,
+                                       C.POINTER(CtfErr)]),
+    "ctf_write_spectrogram": (C.c_int, [C.c_char_p, C.POINTER(CtfSpecHeader), C.c_void_p, C.c_int,
+                                        C.POINTER(CtfErr)]),
+    "ctf_setup_spectrogram_files": (C.c_int, [_P, C.POINTER(CtfProblem), C.POINTER(C.c_char_p), C.c_int,
+                                              C.POINTER(CtfSpecHeader), C.POINTER(CtfErr)]),
+    "ctf_write_factors": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int32), C.c_double,
+                                    _D, _D, C.POINTER(CtfErr)]),
+    "ctf_read_factors": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                   C.POINTER(C.c_int32), C.POINTER(C.c_double), _D, _D, C.POINTER(CtfErr)]),
     "ctf_setup_signal": (C.c_int, [_P, C.POINTER(CtfProblem), _D, C.c_int64, C.c_int, C.c_int,
                                    C.POINTER(CtfErr)]),
     "ctf_images_to_signal": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int64, _D, C.POINTER(C.c_int64),

@@ -175,11 +175,18 @@ class Session:
     def __init__(self, x: np.ndarray, taps, bases, *, stack_taps=1, iterations=100, precision="f64",
                  psd_floor=1e-10, seed=0, device=0, world_size=1, rank=0, comm_id: Optional[bytes] = None,
                  group=None, checks: int = 0, signal: Optional[np.ndarray] = None, window_len: int = 0,
-                 hop: int = 0, update_rule: str = "iss"):
+                 hop: int = 0, update_rule: str = "iss", spec_files: Optional[List[str]] = None):
         """x: [B, F, T, M] spectrogram batch, or x=None with signal = [B, M, length]
         float64 time-domain mixtures (the STFT runs on the GPU, ctf_setup_signal)."""
         self.lib = L.load()
-        if signal is not None:
+        if spec_files is not None:  # one .spec container per mixture (ctf_setup_spectrogram_files)
+            h, err = L.CtfSpecHeader(), L.CtfErr()
+            _check(self.lib.ctf_read_spectrogram(spec_files[0].encode(), C.byref(h), None, L.CTF_F64, C.byref(err)),
+                   err)
+            self.spec_header = {k: getattr(h, k) for k, _ in L.CtfSpecHeader._fields_}
+            B, F, T, M = len(spec_files), h.bins, h.frames, h.channels
+            xprec = "f32"
+        elif signal is not None:
             signal = np.ascontiguousarray(signal, dtype=np.float64)
             if signal.ndim != 3:
                 raise ConfigError("signal must have shape [B, M, length]")
@@ -215,7 +222,13 @@ class Session:
         self.problem = _problem(B, F, T, M, stack_taps, self.taps, self.bases, iterations, precision, xprec,
                                 psd_floor, seed, checks=checks,
                                 rule=L.CTF_RULE_IP if update_rule.lower() == "ip" else L.CTF_RULE_ISS)
-        if signal is not None:
+        if spec_files is not None:
+            arr = (C.c_char_p * len(spec_files))(*[f.encode() for f in spec_files])
+            self.window_len, self.hop = self.spec_header["window_len"], self.spec_header["hop"]
+            self.signal_length = self.spec_header["original_length"]
+            _check(self.lib.ctf_setup_spectrogram_files(self._ctx, C.byref(self.problem), arr, len(spec_files), None,
+                                                        C.byref(err)), err)
+        elif signal is not None:
             self.signal_length, self.window_len, self.hop = signal.shape[2], window_len, hop
             _check(self.lib.ctf_setup_signal(self._ctx, C.byref(self.problem), L.dptr(signal), signal.shape[2],
                                              window_len, hop, C.byref(err)), err)
@@ -397,6 +410,61 @@ def inverse_stft(spec: np.ndarray, window_len: int, hop: int, original_length: i
     _check(lib.ctf_istft(ctx, L.dptr(sp), bins, frames, chans, window_len, hop, original_length, L.dptr(out),
                          C.byref(n), C.byref(err)), err)
     return out
+
+
+# ---- containers (container.hpp:1-29): .spec spectrograms and .nmf factors
+def read_spectrogram(path: str, precision: str = "f64"):
+    """read_spectrogram (container.cpp:74-86): (header dict, spec (bins, frames, channels))."""
+    lib, h, err = L.load(), L.CtfSpecHeader(), L.CtfErr()
+    _check(lib.ctf_read_spectrogram(path.encode(), C.byref(h), None, L.CTF_F64, C.byref(err)), err)
+    f32 = precision in ("f32", "complex64")
+    spec = np.zeros((h.bins, h.frames, h.channels), np.complex64 if f32 else np.complex128)
+    _check(lib.ctf_read_spectrogram(path.encode(), C.byref(h), spec.ctypes.data_as(C.c_void_p),
+                                    L.CTF_F32 if f32 else L.CTF_F64, C.byref(err)), err)
+    hdr = {k: getattr(h, k) for k, _ in L.CtfSpecHeader._fields_}
+    return hdr, spec
+
+
+def write_spectrogram(path: str, spec: np.ndarray, window_len: int = 0, hop: int = 0, sample_rate: int = 0,
+                      original_length: int = 0):
+    """write_spectrogram (container.cpp:61-72): spec (bins, frames, channels) complex, stored as complex64."""
+    lib, err = L.load(), L.CtfErr()
+    f32 = spec.dtype == np.complex64
+    sp = np.ascontiguousarray(spec, dtype=np.complex64 if f32 else np.complex128)
+    h = L.CtfSpecHeader(sp.shape[0], sp.shape[1], sp.shape[2], window_len, hop, int(sample_rate), original_length)
+    _check(lib.ctf_write_spectrogram(path.encode(), C.byref(h), sp.ctypes.data_as(C.c_void_p),
+                                     L.CTF_F32 if f32 else L.CTF_F64, C.byref(err)), err)
+
+
+def write_factors(path: str, bases: List[np.ndarray], activations: List[np.ndarray], floor: float):
+    """write_factors (container.cpp:124-142): B_n (F, K_n), V_n (K_n, T) float64."""
+    lib, err = L.load(), L.CtfErr()
+    F, T = bases[0].shape[0], activations[0].shape[1]
+    ks = (C.c_int32 * len(bases))(*[b.shape[1] for b in bases])
+    Bf = np.concatenate([np.asarray(b, np.float64).ravel(order="F") for b in bases])
+    Vf = np.concatenate([np.asarray(v, np.float64).ravel(order="F") for v in activations])
+    _check(lib.ctf_write_factors(path.encode(), len(bases), F, T, ks, floor, L.dptr(Bf), L.dptr(Vf),
+                                 C.byref(err)), err)
+
+
+def read_factors(path: str):
+    """read_factors (container.cpp:144-165): (bases list, activations list, floor)."""
+    lib, err = L.load(), L.CtfErr()
+    ns, nb, nf, fl = C.c_int(), C.c_int(), C.c_int(), C.c_double()
+    ks = (C.c_int32 * L.CTF_MAX_SOURCES)()
+    _check(lib.ctf_read_factors(path.encode(), C.byref(ns), C.byref(nb), C.byref(nf), ks, C.byref(fl), None, None,
+                                C.byref(err)), err)
+    K = [ks[n] for n in range(ns.value)]
+    Bf, Vf = np.zeros(nb.value * sum(K)), np.zeros(sum(K) * nf.value)
+    _check(lib.ctf_read_factors(path.encode(), C.byref(ns), C.byref(nb), C.byref(nf), ks, C.byref(fl), L.dptr(Bf),
+                                L.dptr(Vf), C.byref(err)), err)
+    bases, acts, ob, ov = [], [], 0, 0
+    for k in K:
+        bases.append(Bf[ob:ob + nb.value * k].reshape(nb.value, k, order="F"))
+        acts.append(Vf[ov:ov + k * nf.value].reshape(k, nf.value, order="F"))
+        ob += nb.value * k
+        ov += k * nf.value
+    return bases, acts, fl.value
 
 
 def _spectrogram_to_abi(x: np.ndarray) -> np.ndarray:

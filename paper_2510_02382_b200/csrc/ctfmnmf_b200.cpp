@@ -280,5 +280,68 @@ TimeSignal image_to_signal(const MixtureSpectrogram& image, const Spectrogram& m
   return mono;
 }
 
+void write_spectrogram(const std::string& path, const Spectrogram& spec) {  // container.cpp:61-72
+  ctf_err e{};
+  const ctf_spec_header h{(uint32_t)spec.bins,       (uint32_t)spec.frames, (uint32_t)spec.channels,
+                          (uint32_t)spec.window_len, (uint32_t)spec.hop,    (uint32_t)spec.sample_rate,
+                          (uint64_t)spec.original_length};
+  if (ctf_write_spectrogram(path.c_str(), &h, spec.data.data(), CTF_F64, &e) != CTF_OK) rethrow(e);
+}
+
+Spectrogram read_spectrogram(const std::string& path) {  // container.cpp:74-86
+  ctf_err e{};
+  ctf_spec_header h{};
+  if (ctf_read_spectrogram(path.c_str(), &h, nullptr, CTF_F64, &e) != CTF_OK) rethrow(e);
+  Spectrogram s;
+  s.resize((int)h.bins, (int)h.frames, (int)h.channels);
+  s.window_len = (int)h.window_len;
+  s.hop = (int)h.hop;
+  s.sample_rate = (double)h.sample_rate;
+  s.original_length = (std::int64_t)h.original_length;
+  if (ctf_read_spectrogram(path.c_str(), &h, s.data.data(), CTF_F64, &e) != CTF_OK) rethrow(e);
+  return s;
+}
+
+void write_factors(const std::string& path, const NmfFactors& f) {  // container.cpp:124-142
+  ctf_err e{};
+  const int N = (int)f.bases.size();
+  if (N < 1) throw ConfigError("write_factors: no sources");
+  std::vector<int32_t> ks;
+  std::vector<double> B, V;
+  for (int n = 0; n < N; ++n) {
+    ks.push_back(f.bases[(size_t)n].cols);
+    B.insert(B.end(), f.bases[(size_t)n].data.begin(), f.bases[(size_t)n].data.end());
+    V.insert(V.end(), f.activations[(size_t)n].data.begin(), f.activations[(size_t)n].data.end());
+  }
+  if (ctf_write_factors(path.c_str(), N, f.bases[0].rows, f.activations[0].cols, ks.data(), f.floor, B.data(),
+                        V.data(), &e) != CTF_OK)
+    rethrow(e);
+}
+
+NmfFactors read_factors(const std::string& path) {  // container.cpp:144-165
+  ctf_err e{};
+  int N = 0, F = 0, T = 0;
+  int32_t ks[CTF_MAX_SOURCES] = {0};
+  double fl = 0.0;
+  if (ctf_read_factors(path.c_str(), &N, &F, &T, ks, &fl, nullptr, nullptr, &e) != CTF_OK) rethrow(e);
+  int sk = 0;
+  for (int n = 0; n < N; ++n) sk += ks[n];
+  std::vector<double> B((size_t)F * sk), V((size_t)sk * T);
+  if (ctf_read_factors(path.c_str(), &N, &F, &T, ks, &fl, B.data(), V.data(), &e) != CTF_OK) rethrow(e);
+  NmfFactors f;
+  f.floor = fl;
+  size_t ob = 0, ov = 0;
+  for (int n = 0; n < N; ++n) {
+    RMatrix b(F, ks[n]), v(ks[n], T);
+    std::copy(B.begin() + (std::ptrdiff_t)ob, B.begin() + (std::ptrdiff_t)(ob + b.data.size()), b.data.begin());
+    std::copy(V.begin() + (std::ptrdiff_t)ov, V.begin() + (std::ptrdiff_t)(ov + v.data.size()), v.data.begin());
+    ob += b.data.size();
+    ov += v.data.size();
+    f.bases.push_back(std::move(b));
+    f.activations.push_back(std::move(v));
+  }
+  return f;
+}
+
 }  // namespace b200
 }  // namespace ctfmnmf

@@ -156,6 +156,13 @@ std::vector<double> hann_window(int window_len);
 Spectrogram forward_stft(const TimeSignal& signal, int window_len, int hop, const GpuOptions& gpu = {});
 TimeSignal inverse_stft(const Spectrogram& spec, const GpuOptions& gpu = {});
 
+// container.hpp:22-29: .spec spectrogram and .nmf factor containers
+// (complex64 / float64 bodies, the reference's IoError texts).
+void write_spectrogram(const std::string& path, const Spectrogram& spec);
+Spectrogram read_spectrogram(const std::string& path);
+void write_factors(const std::string& path, const NmfFactors& factors);
+NmfFactors read_factors(const std::string& path);
+
 // wiener.hpp:22-24: inverse STFT of one source image; ref_channel < 0 keeps all.
 TimeSignal image_to_signal(const MixtureSpectrogram& image, const Spectrogram& meta, int ref_channel = -1,
                            const GpuOptions& gpu = {});

@@ -197,3 +197,33 @@ int main() {{
     assert np.array_equal(back, O.inverse_stft(ref, 512, 128, 3000))
     one = np.array([float(v) for v in out[1 + nspec + 6000:1 + nspec + 9000]])
     assert np.array_equal(one, back[1])
+
+
+def test_setup_from_spec_files_and_factor_file(tmp_path):
+    """`.spec` containers straight into the estimator (ctf_setup_spectrogram_files,
+    the reference's separate input), equal to a setup from the same complex64
+    array; the converged factors written as a `.nmf` container read back."""
+    from paper_2510_02382_b200 import read_factors, write_factors, write_spectrogram
+    B, M, n, window, hop, L, K = 2, 2, 2000, 128, 32, 2, 3
+    sig = np.random.default_rng(21).standard_normal((B, M, n))
+    specs = [O.forward_stft(sig[b], window, hop) for b in range(B)]
+    paths = []
+    for b, sp in enumerate(specs):
+        paths.append(str(tmp_path / f"m{b}.spec"))
+        write_spectrogram(paths[-1], sp, window, hop, 16000, n)
+    x = np.stack(specs).astype(np.complex64)
+    a = Session(x, [L] * M, [K] * M, stack_taps=L, iterations=3, precision="f32", seed=4)
+    a.iterate(3)
+    ra = a.download_raw()
+    a.close()
+    s = Session(None, [L] * M, [K] * M, stack_taps=L, iterations=3, precision="f32", seed=4, spec_files=paths)
+    assert s.spec_header["window_len"] == window and s.signal_length == n
+    s.iterate(3)
+    rb = s.download_raw()
+    for u, v in zip(ra, rb):
+        assert np.array_equal(u, v)
+    dem, bases, acts, obj = s.download()[0]
+    write_factors(str(tmp_path / "f.nmf"), bases, acts, float(s.psd_floor()[0]))
+    B2, V2, fl = read_factors(str(tmp_path / "f.nmf"))
+    assert all(np.array_equal(p, q) for p, q in zip(B2 + V2, bases + acts))
+    s.close()
