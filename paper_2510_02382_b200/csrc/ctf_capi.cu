@@ -400,10 +400,10 @@ void plan_sweep(ctf_ctx* c) {
       const int glp = gloff + std::max(TP, U1) + 2 * L + UB;
       cand.off_x = (int)take((size_t)M * cand.xp * cs);
       cand.off_l = (int)take((size_t)c->N * glp * rs);
-      cand.off_y = (int)take((size_t)c->N * M * M * NA * NA * cs);
-      const int NS = c->real_size == 4 ? c->N : 1;  // sources per Gram pass (gram_ns) and per demix group
+      cand.off_y = (int)take((size_t)c->N * (M * (M + 1) / 2) * NA * NA * cs);  // Hermitian half of the Gram
+      const int NS = (c->real_size == 4 && c->R <= 16) ? c->N : 1;  // sources per Gram pass (gram_ns) and demix group
       cand.off_e = (int)take(std::max((size_t)NS * NA * (nt + 1) * cs, (size_t)NS * L * TP * rs));
-      cand.off_w = (int)take((size_t)2 * c->R * c->D * cs);
+      cand.off_w = (int)take((size_t)c->R * c->D * cs);
       cand.off_z = (int)take((size_t)(2 * c->R * std::max(1, L - 1) + 2 * (c->D + std::max(1, L - 1))) * cs);
       cand.off_red = (int)take((size_t)32 * NW * rs);
       cand.off_b = (int)take((size_t)c->SK * rs);
@@ -491,7 +491,10 @@ void plan_sweep(ctf_ctx* c) {
     // covariance-domain first, except fp64 with R <= 4 where the frame-domain
     // sweep measured faster (cfg0 f64: 0.046 vs 0.051 ms per iteration)
     const int gram_rank = (c->real_size == 8 && c->R <= 4 && !want_ip) ? 500 : -1000;
-    const int rank = (v.kind == 4 ? gram_rank : v.kind == 3 ? 3000 : v.kind == 2 ? 2000 : v.kind == 1 ? 1000 : 0) +
+    // wide covariance tiles (R > 16, one CTA per SM) run best with the most threads
+    const int wide_bonus = (v.kind == 4 && c->R > 16) ? -nt / 128 : 0;
+    const int rank = wide_bonus +
+                     (v.kind == 4 ? gram_rank : v.kind == 3 ? 3000 : v.kind == 2 ? 2000 : v.kind == 1 ? 1000 : 0) +
                      (v.kind == 3 ? -v.rmax * 4 : v.rmax * 4) + (v.exact ? 0 : 2) + (v.lt > 0 ? 0 : 1);
     const bool better = !found || rank < best_rank ||
                         (rank == best_rank && (TP < c->TP || (TP == c->TP && nt < best_nt)));

@@ -135,20 +135,22 @@ __device__ __forceinline__ double log_fast(double x) { return log(x); }
 
 // Sources accumulated per Gram pass: all of them in fp32 (the conj products
 // are shared); one at a time in fp64 (register budget, half the partials).
-template <typename Real, int N> constexpr int gram_ns() { return std::is_same<Real, float>::value ? N : 1; }
-template <typename Real, int NT> constexpr int gram_min_blocks() {
-  return std::is_same<Real, float>::value ? (NT <= 256 ? 3 : 1) : (NT <= 256 ? 2 : 1);
+template <typename Real, int N, int R> constexpr int gram_ns() {
+  return (std::is_same<Real, float>::value && R <= 16) ? N : 1;
+}
+template <typename Real, int NT, int R> constexpr int gram_min_blocks() {
+  return R > 16 ? 1 : std::is_same<Real, float>::value ? (NT <= 256 ? 3 : 1) : (NT <= 256 ? 2 : 1);
 }
 
 // IP: the iterative-projection rule in place of the ISS steps.
 template <typename Real, int M, int L, int NT, int FT, bool IP = false>
-__global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT>())
+__global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
     gram_kernel(const SweepParams p, const int4* __restrict__ gtab) {
   using R2 = typename Cplx<Real>::T;
   using Ops = GOps<Real>;
   constexpr bool F32 = std::is_same<Real, float>::value;
   constexpr int N = M, R = M * L, D = M * L, NA = 2 * L - 1, NW = NT / 32;
-  constexpr int NS = gram_ns<Real, N>();
+  constexpr int NS = gram_ns<Real, N, R>();
   constexpr int LT1 = L > 1 ? L - 1 : 1;
   constexpr int CPB = 16 / (int)sizeof(R2);  // complex values per 16-byte load
   static_assert(D <= 32, "one lane per stacked channel in the covariance steps");
@@ -189,8 +191,18 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT>())
   const Real floor_abs = (Real)p.floor_abs[mix];
   const int prev_it = p.iteration - 1;
   const double* mu = p.mu ? p.mu + (size_t)mix * R : nullptr;
-  auto gidx = [](int n, int m, int m2, int a, int b) {  // a, b in [-(L-1), L-1]
-    return (((n * M + m) * M + m2) * NA + a + L - 1) * NA + b + L - 1;
+  // Gram table: Hermitian half, mic pairs m <= m2 packed (NP of them):
+  // G[n][pair(m, m2)][a][b], a, b in [-(L-1), L-1]; G(m > m2) = conj(G(m2, m, b, a))
+  constexpr int NP = M * (M + 1) / 2;
+  auto gidx = [](int n, int m, int m2, int a, int b) {  // requires m <= m2
+    const int pm = m * M - (m * (m - 1)) / 2 + (m2 - m);
+    return ((n * NP + pm) * NA + a + L - 1) * NA + b + L - 1;
+  };
+  auto gget = [&](int n, int m, int m2, int a, int b) -> R2 {
+    if (m <= m2) return G[gidx(n, m, m2, a, b)];
+    R2 v = G[gidx(n, m2, m, b, a)];
+    v.y = -v.y;
+    return v;
   };
 
   if (tid == 0) {
@@ -405,59 +417,97 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT>())
           sum.y += pr[t].y;
         }
         const int m = h0.x, m2 = h0.y, d = h0.z, a = h0.w + j, b = a + d;
-        G[gidx(n0 + n, m, m2, a, b)] = sum;
-        R2 mir = sum;
-        if (!(m == m2 && d == 0)) mir.y = -sum.y;
-        G[gidx(n0 + n, m2, m, b, a)] = mir;
+        G[gidx(n0 + n, m, m2, a, b)] = sum;  // groups have m <= m2
+        if (m == m2 && d != 0) {              // the mirrored lag of the same mic
+          R2 mir = sum;
+          mir.y = -sum.y;
+          G[gidx(n0 + n, m, m, b, a)] = mir;
+        }
       }
       __syncthreads();
     }
   }
   CTF_PHASE(4);
 
-  // ---- covariance-domain steps with register-resident rows: half-warp
-  // `row` = 2*warp + half owns W row p; its lane c < D holds W[p][c], the
-  // row c of C_p (D complex), the tail frame T + c of y_p (c < L-1) and, for
-  // c < l_p, its weight w_n(T + c - l_p). A step needs only the pivot row
-  // (W_r and its tail), published through shared memory: one barrier per step.
-  constexpr int HW = 16;
-  static_assert(D <= HW && L - 1 <= HW, "one half-warp per row");
-  static_assert(R <= 2 * NW, "a half-warp per row");
-  const int hl = lane & (HW - 1), half = lane >> 4;
-  const int row = 2 * warp + half;
-  const bool rowv = row < R;
-  const int rn = rowv ? row / L : 0, rl = rowv ? row - rn * L : 0;
-  R2 creg[D];
-  R2 wreg, yreg;
-  wreg.x = wreg.y = yreg.x = yreg.y = Real(0);
-  Real wt = Real(0);
-  {
-    const bool chan = rowv && hl < D;
-    const int m = hl / L, l1 = hl - m * L;
+  // ---- covariance-domain steps with register-resident rows. A group of LPR
+  // lanes (a half-warp when D <= 16, a warp for the wide tiles) owns KR rows
+  // p; its lane c < D holds W[p][c], the tail frame T + c of y_p (c < L-1)
+  // and, for c < l_p, its weight w_n(T + c - l_p); for D <= 16 also the row c
+  // of C_p (D complex, else read from the Gram table each step). A step needs
+  // only the pivot row (W_r and its tail), published through shared memory:
+  // one barrier per step.
+  constexpr bool WIDE = D > 16;
+  constexpr int LPR = WIDE ? 32 : 16;
+  constexpr int GROUPS = NT / LPR;
+  constexpr int KR = (R + GROUPS - 1) / GROUPS;  // rows per lane group
+  static_assert(L - 1 <= LPR, "tail frames per lane group");
+  static_assert(WIDE || KR == 1, "narrow tiles: one row per half-warp");
+  const int hl = lane & (LPR - 1);
+  const int slot = tid / LPR;
+  int rowk[KR], rnk[KR], rlk[KR];
+  bool rowvk[KR];
+  R2 wreg[KR], yreg[KR];
+  Real wt[KR];
+  R2 creg[WIDE ? 1 : D];
+#pragma unroll
+  for (int k = 0; k < KR; ++k) {
+    const int row = slot + k * GROUPS;
+    rowk[k] = row;
+    rowvk[k] = row < R;
+    rnk[k] = rowvk[k] ? row / L : 0;
+    rlk[k] = rowvk[k] ? row - rnk[k] * L : 0;
+    wreg[k].x = wreg[k].y = yreg[k].x = yreg[k].y = Real(0);
+    wt[k] = Real(0);
+    if (rowvk[k] && hl < D) wreg[k] = Wb[hl * R + row];
+    if (rowvk[k] && hl < L - 1) yreg[k] = Yt[row * LT1 + hl];                       // for when this row pivots
+    if (rowvk[k] && hl < rlk[k]) wt[k] = invl[rnk[k] * p.lp + p.loff + T + hl - rlk[k]];  // own truncation
+  }
+  const int mh = hl / L, l1h = hl - mh * L;  // stacked channel of this lane
+  if constexpr (!WIDE) {
+    const bool chan = rowvk[0] && hl < D;
 #pragma unroll
     for (int m2 = 0; m2 < M; ++m2)
 #pragma unroll
       for (int l2 = 0; l2 < L; ++l2) {
         R2 c;
         c.x = c.y = Real(0);
-        if (chan) c = G[gidx(rn, m, m2, rl - l1, rl - l2)];
+        if (chan) c = gget(rnk[0], mh, m2, rlk[0] - l1h, rlk[0] - l2);
         creg[m2 * L + l2] = c;
       }
-    if (chan) wreg = Wb[hl * R + row];
-    if (rowv && hl < L - 1) yreg = Yt[row * LT1 + hl];                // carried for when this row pivots
-    if (rowv && hl < rl) wt = invl[rn * p.lp + p.loff + T + hl - rl];  // own truncation: frames T .. T+l-1
   }
-  // (num, den) of this row against a pivot: pw[c * ps] = pivot W, py[c] = pivot tail
-  auto row_sums = [&](const R2* pw, int ps, const R2* py, Real& nre, Real& nim, Real& den) {
+  // (num, den) of row slot k against a pivot: pw[c * ps] = pivot W, py[c] = pivot tail
+  auto row_sums = [&](int k, const R2* pw, int ps, const R2* py, Real& nre, Real& nim, Real& den) {
     R2 q0, q1;
     q0.x = q0.y = q1.x = q1.y = Real(0);
+    if constexpr (WIDE) {
+      if (rowvk[k] && hl < D) {
+        // C_p[c][(m2, l2)] = G(n, m, m2, l - l1, l - l2): for m2 >= m the
+        // stored entry (stride -1 in l2), else the conjugate of (m2, m, l-l2, l-l1)
+        const int rn_ = rnk[k], a0 = rlk[k] - l1h;
 #pragma unroll
-    for (int c = 0; c < D; ++c) {  // q += C conj(w)
-      const R2 w = pw[c * ps];
-      if (c & 1)
-        q1 = Ops::macc(creg[c], w, q1);
-      else
-        q0 = Ops::macc(creg[c], w, q0);
+        for (int m2 = 0; m2 < M; ++m2)
+#pragma unroll
+          for (int l2 = 0; l2 < L; ++l2) {  // q += C conj(w), C from the Gram table
+            const int c = m2 * L + l2;
+            const R2 w = pw[c * ps];
+            const bool up = mh <= m2;
+            R2 cc = G[up ? gidx(rn_, mh, m2, a0, rlk[k] - l2) : gidx(rn_, m2, mh, rlk[k] - l2, a0)];
+            if (!up) cc.y = -cc.y;
+            if (c & 1)
+              q1 = Ops::macc(cc, w, q1);
+            else
+              q0 = Ops::macc(cc, w, q0);
+          }
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < D; ++c) {  // q += C conj(w)
+        const R2 w = pw[c * ps];
+        if (c & 1)
+          q1 = Ops::macc(creg[c], w, q1);
+        else
+          q0 = Ops::macc(creg[c], w, q0);
+      }
     }
     R2 q;
     q.x = q0.x + q1.x;
@@ -465,16 +515,16 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT>())
     R2 wr;
     wr.x = wr.y = Real(0);
     if (hl < D) wr = pw[hl * ps];
-    R2 cn = cmul(wreg, q), cd = cmul(wr, q);
+    R2 cn = cmul(wreg[k], q), cd = cmul(wr, q);
     // virtual frames T + hl (hl < l_p): subtract w y_p conj(y_r), w |y_r|^2
     R2 yr;
     yr.x = yr.y = Real(0);
     if (hl < LT1) yr = py[hl];
-    cn.x -= wt * fma(yreg.x, yr.x, yreg.y * yr.y);
-    cn.y -= wt * fma(yreg.y, yr.x, -yreg.x * yr.y);
-    cd.x -= wt * fma(yr.x, yr.x, yr.y * yr.y);
+    cn.x -= wt[k] * fma(yreg[k].x, yr.x, yreg[k].y * yr.y);
+    cn.y -= wt[k] * fma(yreg[k].y, yr.x, -yreg[k].x * yr.y);
+    cd.x -= wt[k] * fma(yr.x, yr.x, yr.y * yr.y);
 #pragma unroll
-    for (int o = HW / 2; o >= 1; o >>= 1) {
+    for (int o = LPR / 2; o >= 1; o >>= 1) {
       cn.x += __shfl_xor_sync(kFull, cn.x, o);
       cn.y += __shfl_xor_sync(kFull, cn.y, o);
       cd.x += __shfl_xor_sync(kFull, cd.x, o);
@@ -488,9 +538,13 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT>())
   if (p.has_prev) {
     // objective of the previous iteration (estimator.cpp:55-77): quadratic
     // term sum_r w_r^T C_r conj(w_r) of the rescaled W under the new lambda
-    Real nre, nim, den;
-    row_sums(Wb + (rowv ? row : 0), R, Yt + (rowv ? row : 0) * LT1, nre, nim, den);
-    if (hl == 0 && rowv) red[row] = den;
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      Real nre, nim, den;
+      const int rr = rowvk[k] ? rowk[k] : 0;
+      row_sums(k, Wb + rr, R, Yt + rr * LT1, nre, nim, den);
+      if (hl == 0 && rowvk[k]) red[rowk[k]] = den;
+    }
     double v1[1] = {logsum};
     block_sum_d<1>(v1, dred, lane, warp, NW);  // contains __syncthreads: red visible after
     double quad = 0.0;
@@ -531,7 +585,7 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT>())
       for (int e = tid; e < D * D; e += NT) {
         const int a = e % D, b = e / D;
         const int m = a / L, l1 = a - m * L, m2 = b / L, l2 = b - m2 * L;
-        R2 v = G[gidx(n, m, m2, l - l1, l - l2)];
+        R2 v = gget(n, m, m2, l - l1, l - l2);
         for (int jj = 0; jj < l; ++jj) {  // frames j = T + jj are outside row l's range
           const Real w = invl[n * p.lp + p.loff + T + jj - l];
           const R2 xa = xs[m * p.xp + p.xoff + T + jj - l1], xb = xs[m2 * p.xp + p.xoff + T + jj - l2];
@@ -706,46 +760,50 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT>())
   R2* piv = zs;     // 2 x (D + LT1): pivot W row and tail, double-buffered by step parity
   Real* fac = red;  // (1 - z_r) per row, multiplied in row order at the end
   constexpr int PV = D + LT1;
-  if (row == 0) {
-    if (hl < D) piv[hl] = wreg;
-    if (hl < LT1) piv[D + hl] = yreg;
+  if (rowk[0] == 0) {
+    if (hl < D) piv[hl] = wreg[0];
+    if (hl < LT1) piv[D + hl] = yreg[0];
   }
   __syncthreads();
   CTF_PHASE(5);
-  const bool wrows = 2 * warp < R;  // warp-uniform: this warp owns at least one row
+  const bool wrows = (tid / 32) * (32 / LPR) < R;  // warp-uniform: this warp owns at least one row
   for (int r = 0; r < R; ++r) {
     const R2* pv = piv + (r & 1) * PV;
-    Real nre = Real(0), nim = Real(0), den = Real(0);
-    if (wrows) row_sums(pv, 1, pv + D, nre, nim, den);
-    R2 z;
-    z.x = z.y = Real(0);
-    if (rowv) {
-      if (!(den > Real(0)) || !isfinite(den)) {  // estimator.cpp:451-454
-        if (hl == 0) atomicMin(&s_badrow, row);
-      } else if (row == r) {
-        if constexpr (F32)
-          z.x = 1.f - sqrtf((float)T) * rsqrtf(den);
-        else
-          z.x = 1.0 - sqrt((double)T / den);
-        if (hl == 0) fac[row] = Real(1) - z.x;
-      } else {
-        if constexpr (F32) {
-          const float inv = __frcp_rn(den);
-          z.x = nre * inv;
-          z.y = nim * inv;
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      Real nre = Real(0), nim = Real(0), den = Real(0);
+      if (wrows) row_sums(k, pv, 1, pv + D, nre, nim, den);
+      R2 z;
+      z.x = z.y = Real(0);
+      const int row = rowk[k];
+      if (rowvk[k]) {
+        if (!(den > Real(0)) || !isfinite(den)) {  // estimator.cpp:451-454
+          if (hl == 0) atomicMin(&s_badrow, row);
+        } else if (row == r) {
+          if constexpr (F32)
+            z.x = 1.f - sqrtf((float)T) * rsqrtf(den);
+          else
+            z.x = 1.0 - sqrt((double)T / den);
+          if (hl == 0) fac[row] = Real(1) - z.x;
         } else {
-          z.x = nre / den;
-          z.y = nim / den;
+          if constexpr (F32) {
+            const float inv = __frcp_rn(den);
+            z.x = nre * inv;
+            z.y = nim * inv;
+          } else {
+            z.x = nre / den;
+            z.y = nim / den;
+          }
         }
       }
-    }
-    // iss_apply (estimator.cpp:298-302) on the own row and its tail
-    if (hl < D) cmsub(wreg, z, pv[hl]);
-    if (hl < LT1) cmsub(yreg, z, pv[D + hl]);
-    if (row == r + 1) {  // the next pivot publishes its updated row
-      R2* nx = piv + ((r + 1) & 1) * PV;
-      if (hl < D) nx[hl] = wreg;
-      if (hl < LT1) nx[D + hl] = yreg;
+      // iss_apply (estimator.cpp:298-302) on the own row and its tail
+      if (hl < D) cmsub(wreg[k], z, pv[hl]);
+      if (hl < LT1) cmsub(yreg[k], z, pv[D + hl]);
+      if (row == r + 1) {  // the next pivot publishes its updated row
+        R2* nx = piv + ((r + 1) & 1) * PV;
+        if (hl < D) nx[hl] = wreg[k];
+        if (hl < LT1) nx[D + hl] = yreg[k];
+      }
     }
     __syncthreads();
     if (s_badrow != kNoRow) {
@@ -753,7 +811,9 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT>())
       return;
     }
   }
-  if (rowv && hl < D) Wb[hl * R + row] = wreg;
+#pragma unroll
+  for (int k = 0; k < KR; ++k)
+    if (rowvk[k] && hl < D) Wb[hl * R + rowk[k]] = wreg[k];
   if (tid == 0) {
     double dp = 1.0;
     for (int r = 0; r < R; ++r) dp *= (double)fac[r];
@@ -770,7 +830,7 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT>())
   // |y_(n,l)(tau+l)|^2 in l order (estimator.cpp:318-330, written in place of
   // the source's first |y|^2 row), then MU-B per source (estimator.cpp
   // :313-346, 16 bases per pass)
-  constexpr int NSD = F32 ? N : 1;
+  constexpr int NSD = NS;  // sources per demix group = per Gram pass
   constexpr int GR = NSD * L;  // rows per group
   Real rp[32];
 #pragma unroll

@@ -6,7 +6,8 @@ namespace ctf {
 #define GD(...) CTF_GR(double, 0, __VA_ARGS__)
 std::vector<SweepVariant> sweep_variants_gram_f32() {
   return {GF(2, 2, 128, 4), GF(2, 2, 256, 4), GF(2, 3, 128, 4), GF(2, 3, 256, 4),
-          GF(2, 5, 256, 4), GF(2, 5, 512, 4), GF(3, 4, 256, 4), GF(3, 4, 512, 4)};
+          GF(2, 5, 256, 4), GF(2, 5, 512, 4), GF(3, 4, 256, 4), GF(3, 4, 512, 4),
+          GF(4, 8, 256, 4), GF(4, 8, 512, 2)};  // wide tiles (BASELINE cfg3): warp per row, Gram table reads
 }
 std::vector<SweepVariant> sweep_variants_gram_f64() {
   return {GD(2, 2, 128, 4), GD(2, 2, 256, 4), GD(2, 3, 128, 4), GD(2, 3, 256, 4),

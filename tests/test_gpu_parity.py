@@ -89,10 +89,11 @@ def test_cfg0_fp32_tolerances():
     assert final <= 1e-3, final
 
 
-@pytest.mark.parametrize("M,L,T,K,rho", [(2, 5, 1000, 10, 0.6), (3, 4, 2000, 20, 0.7), (2, 3, 400, 4, 0.6)])
+@pytest.mark.parametrize("M,L,T,K,rho", [(2, 5, 1000, 10, 0.6), (3, 4, 2000, 20, 0.7), (2, 3, 400, 4, 0.6),
+                                         (4, 8, 1000, 20, 0.8)])
 def test_fp32_trajectory_cfg_geometries(M, L, T, K, rho):
-    """fp32 tolerance on the BASELINE cfg1 / cfg2 geometries (reduced F) and an
-    odd-lag shape: <= 1e-4 relative L2 per iteration against the fp64 oracle
+    """fp32 tolerance on the BASELINE cfg1 / cfg2 / cfg3 geometries (reduced F)
+    and an odd-lag shape (cfg3: the wide-tile path, a warp per row): <= 1e-4 relative L2 per iteration against the fp64 oracle
     over 30 iterations (the covariance-domain kernel serves these shapes)."""
     F, iters, seed = 33, 30, 5
     raw = synth_mixtures(1, F, T, M, M, L, K, rho, 1234 + M * L)

@@ -1,2 +1,1 @@
-for c in 1 2; do timeout 300 python tools/prof_cfg.py --cfg $c --prec f32 --iters 10 2>&1 | tail -1; done
-timeout 1500 python -m pytest tests/test_gpu_parity.py -q -x 2>&1 | tail -2
+CTF_SWEEP_VARIANT=32,2,4,512 timeout 600 python tools/prof_cfg.py --cfg 3 --prec f32 --iters 3 --mixtures 16 2>&1 | tail -2
