@@ -1,1 +1,2 @@
-CTF_SWEEP_VARIANT=32,2,4,512 timeout 600 python tools/prof_cfg.py --cfg 3 --prec f32 --iters 3 --mixtures 16 2>&1 | tail -2
+timeout 1500 python -m pytest tests -q -m gpu -x 2>&1 | tail -2
+python bench.py --cfg 3 --no-frontend > gpurun_out/b_c3_f32.json 2>gpurun_out/b_c3.err; tail -1 gpurun_out/b_c3.err
