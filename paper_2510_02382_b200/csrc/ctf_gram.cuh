@@ -463,6 +463,21 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
     if (rowvk[k] && hl < rlk[k]) wt[k] = invl[rnk[k] * p.lp + p.loff + T + hl - rlk[k]];  // own truncation
   }
   const int mh = hl / L, l1h = hl - mh * L;  // stacked channel of this lane
+  // wide tiles: Gram-table addressing of this lane's C_p row per mic m2
+  int gbase[WIDE ? KR : 1][M], gstr[WIDE ? KR : 1][M];
+  Real gsgn[WIDE ? KR : 1][M];
+  if constexpr (WIDE) {
+#pragma unroll
+    for (int k = 0; k < KR; ++k)
+#pragma unroll
+      for (int m2 = 0; m2 < M; ++m2) {
+        const bool up = mh <= m2;
+        const int a0 = rlk[k] - l1h, b0 = rlk[k];
+        gbase[k][m2] = (rowvk[k] && hl < D) ? (up ? gidx(rnk[k], mh, m2, a0, b0) : gidx(rnk[k], m2, mh, b0, a0)) : 0;
+        gstr[k][m2] = up ? -1 : -NA;
+        gsgn[k][m2] = up ? Real(1) : Real(-1);
+      }
+  }
   if constexpr (!WIDE) {
     const bool chan = rowvk[0] && hl < D;
 #pragma unroll
@@ -482,17 +497,16 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
     if constexpr (WIDE) {
       if (rowvk[k] && hl < D) {
         // C_p[c][(m2, l2)] = G(n, m, m2, l - l1, l - l2): for m2 >= m the
-        // stored entry (stride -1 in l2), else the conjugate of (m2, m, l-l2, l-l1)
-        const int rn_ = rnk[k], a0 = rlk[k] - l1h;
+        // stored entry (stride -1 in l2), else the conjugate of (m2, m, l-l2,
+        // l-l1) (stride -NA); bases, strides and signs precomputed per row
 #pragma unroll
         for (int m2 = 0; m2 < M; ++m2)
 #pragma unroll
           for (int l2 = 0; l2 < L; ++l2) {  // q += C conj(w), C from the Gram table
             const int c = m2 * L + l2;
             const R2 w = pw[c * ps];
-            const bool up = mh <= m2;
-            R2 cc = G[up ? gidx(rn_, mh, m2, a0, rlk[k] - l2) : gidx(rn_, m2, mh, rlk[k] - l2, a0)];
-            if (!up) cc.y = -cc.y;
+            R2 cc = G[gbase[k][m2] + l2 * gstr[k][m2]];
+            cc.y *= gsgn[k][m2];
             if (c & 1)
               q1 = Ops::macc(cc, w, q1);
             else

@@ -1,2 +1,2 @@
-timeout 1500 python -m pytest tests -q -m gpu -x 2>&1 | tail -2
-python bench.py --cfg 3 --no-frontend > gpurun_out/b_c3_f32.json 2>gpurun_out/b_c3.err; tail -1 gpurun_out/b_c3.err
+timeout 600 python tools/prof_cfg.py --cfg 3 --prec f32 --iters 3 --mixtures 16 2>&1 | tail -1
+timeout 1200 python -m pytest tests/test_gpu_parity.py -q -x -k "trajectory" 2>&1 | tail -2
