@@ -48,21 +48,50 @@ __device__ __forceinline__ double2 cmul_rn(double2 a, double2 b) {  // std::comp
 }
 
 // In-place radix-2 DIT over S sequences of N complex in shared memory, already
-// in bit-reversed order (fft.cpp:20-37 stage/butterfly order).
+// in bit-reversed order (fft.cpp:20-37 stage/butterfly order). Two stages
+// (s, s+1) run per shared-memory pass on the closed 4-element sets
+// {i, i+h, i+2h, i+3h} (h = 2^(s-1)): the same butterflies with the same
+// twiddles in the same order as two radix-2 passes, so the result is
+// bit-identical while the shared-memory traffic and barriers halve.
+__device__ __forceinline__ double2 cadd_rn(double2 a, double2 b) { return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y)); }
+__device__ __forceinline__ double2 csub_rn(double2 a, double2 b) { return make_double2(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y)); }
+
 __device__ __forceinline__ void block_fft(double2* a, int S, int N, int logN, const double2* __restrict__ tw) {
-  const int halfN = N >> 1, nb = S * halfN;
-  for (int s = 1; s <= logN; ++s) {
-    const int half = 1 << (s - 1);
-    const double2* w = tw + (half - 1);
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+  const int halfN = N >> 1, qN = N >> 2;
+  int s = 1;
+  if (logN & 1) {  // one radix-2 pass (len = 2) when the stage count is odd
+    for (int b = threadIdx.x; b < S * halfN; b += blockDim.x) {
       const int q = b / halfN, bb = b - q * halfN;
-      const int k = bb & (half - 1);
-      const int i = ((bb >> (s - 1)) << s) + k;
-      double2* base = a + (size_t)q * N;
-      const double2 u = base[i];
-      const double2 v = cmul_rn(base[i + half], __ldg(w + k));
-      base[i] = make_double2(__dadd_rn(u.x, v.x), __dadd_rn(u.y, v.y));
-      base[i + half] = make_double2(__dsub_rn(u.x, v.x), __dsub_rn(u.y, v.y));
+      double2* base = a + (size_t)q * N + 2 * bb;
+      const double2 u = base[0];
+      const double2 v = cmul_rn(base[1], __ldg(tw));
+      base[0] = cadd_rn(u, v);
+      base[1] = csub_rn(u, v);
+    }
+    __syncthreads();
+    s = 2;
+  }
+  for (; s < logN; s += 2) {
+    const int h = 1 << (s - 1), len = h << 1;
+    const double2* w1 = tw + (h - 1);    // stage s (length len), k < h
+    const double2* w2 = tw + (len - 1);  // stage s+1 (length 2len), k < len
+    for (int b = threadIdx.x; b < S * qN; b += blockDim.x) {
+      const int q = b / qN, qq = b - q * qN;
+      const int k = qq & (h - 1);
+      const int i = ((qq >> (s - 1)) << (s + 1)) + k;
+      double2* base = a + (size_t)q * N + i;
+      const double2 x0 = base[0], x1 = base[h], x2 = base[len], x3 = base[len + h];
+      const double2 t1 = __ldg(w1 + k);
+      double2 v = cmul_rn(x1, t1);
+      const double2 y0 = cadd_rn(x0, v), y1 = csub_rn(x0, v);
+      v = cmul_rn(x3, t1);
+      const double2 y2 = cadd_rn(x2, v), y3 = csub_rn(x2, v);
+      v = cmul_rn(y2, __ldg(w2 + k));
+      base[0] = cadd_rn(y0, v);
+      base[len] = csub_rn(y0, v);
+      v = cmul_rn(y3, __ldg(w2 + k + h));
+      base[h] = cadd_rn(y1, v);
+      base[len + h] = csub_rn(y1, v);
     }
     __syncthreads();
   }
