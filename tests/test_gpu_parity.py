@@ -635,3 +635,66 @@ def test_ip_rule_errors_and_run_api():
     assert rel(res.demixing, np.transpose(ref["W"], (0, 2, 1))) <= 1e-9
     with pytest.raises(Exception):
         run(cfg, np.transpose(raw[0], (0, 2, 1)), CheckOptions(det_lemma=True), stack_taps=L)
+
+
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_covariance_kernel_error_paths(precision):
+    """The error semantics of test_run.cpp:219-268 on the covariance-domain
+    kernel (stacked equal-tap input selects it): a NaN sample -> "non-finite"
+    (the finite checks), a silent bin -> the steering degeneracy at iteration 1
+    of the lowest silent bin, with the same messages as the oracle."""
+    M, L, K, F, T = 2, 3, 3, 7, 40
+    raw = synth_mixtures(1, F, T, M, M, L, K, 0.6, 11)
+    if precision == "f32":
+        raw = raw.astype(np.complex64)
+    s = Session(raw, [L] * M, [K] * M, stack_taps=L, iterations=2, precision=precision, seed=1)
+    assert "gram_kernel" in json.loads(s.describe())["sweep_kernel"]
+    s.close()
+    bad = raw.copy()
+    bad[0, 3, 5, 1] = np.nan
+    with pytest.raises(DegeneracyError) as e:
+        s = Session(bad, [L] * M, [K] * M, stack_taps=L, iterations=2, precision=precision, seed=1)
+        s.iterate(2)
+    assert "non-finite" in str(e.value)
+    silent = raw.copy()
+    silent[0, 2] = 0
+    silent[0, 5] = 0
+    ref_err = None
+    try:
+        O.run(O.config([L] * M, [K] * M, iterations=2, seed=1), O.stack_observation(silent[0].astype(complex), L))
+    except O.OracleError as oe:
+        ref_err = oe
+    assert ref_err is not None and ref_err.iteration == 1 and ref_err.bin == 2
+    with pytest.raises(DegeneracyError) as e:
+        s = Session(silent, [L] * M, [K] * M, stack_taps=L, iterations=2, precision=precision, seed=1)
+        s.iterate(2)
+    assert e.value.iteration == 1 and e.value.bin == 2 and "iteration 1" in str(e.value)
+    assert str(e.value).split(" (iteration")[0] == str(ref_err).split(" (iteration")[0]
+
+
+def test_covariance_kernel_sharded_degeneracy():
+    """A silent bin in rank 1's shard on the covariance-domain kernel raises the
+    same DegeneracyError on every rank."""
+    import threading
+    from paper_2510_02382_b200 import _lib
+    M, L, K, F, T = 2, 2, 3, 8, 40
+    raw = synth_mixtures(1, F, T, M, M, L, K, 0.6, 12).astype(np.complex64)
+    raw[0, 6] = 0
+    lib = _lib.load()
+    grp = lib.ctf_group_create(2)
+    errs = [None, None]
+
+    def worker(r):
+        try:
+            s = Session(raw, [L] * M, [K] * M, stack_taps=L, iterations=2, precision="f32", world_size=2, rank=r,
+                        group=grp)
+            s.iterate(2)
+        except DegeneracyError as e:
+            errs[r] = e
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(2)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    lib.ctf_group_destroy(grp)
+    for e in errs:
+        assert e is not None and e.iteration == 1 and e.bin == 6
