@@ -698,3 +698,25 @@ def test_covariance_kernel_sharded_degeneracy():
     lib.ctf_group_destroy(grp)
     for e in errs:
         assert e is not None and e.iteration == 1 and e.bin == 6
+
+
+@pytest.mark.parametrize("M,L,T,prec", [(2, 3, 37, "f64"), (2, 5, 1001, "f32"), (3, 4, 301, "f32"),
+                                        (3, 4, 301, "f64"), (2, 2, 511, "f32")])
+def test_covariance_kernel_odd_frame_counts(M, L, T, prec):
+    """Frame counts that are not multiples of 4 (scalar lambda path), odd T*M
+    (scalar x-tile path) and T just below a CTA tile: per-iteration parity
+    with the oracle (fp64 1e-9, fp32 1e-4)."""
+    F, K, iters, seed = 9, 3, 4, 8
+    raw = synth_mixtures(1, F, T, M, M, L, K, 0.6, 300 + T)
+    x = raw.astype(np.complex64) if prec == "f32" else raw
+    s = Session(x, [L] * M, [K] * M, stack_taps=L, iterations=iters, precision=prec, seed=seed)
+    assert "gram_kernel" in json.loads(s.describe())["sweep_kernel"]
+    s.close()
+    ref = O.run(O.config([L] * M, [K] * M, iterations=iters, seed=seed, threads=NPROC),
+                O.stack_observation(raw[0], L), history=True)
+    hist = gpu_history(x, [L] * M, [K] * M, iters, prec, seed, L)
+    tol = 1e-9 if prec == "f64" else 1e-4
+    for it, (W, B, V, obj) in enumerate(hist):
+        e = max(rel(W[0], ref["hist_W"][it].reshape(F, -1)), rel(B[0], ref["hist_B"][it]),
+                rel(V[0], ref["hist_V"][it]))
+        assert e <= tol, f"it={it + 1}: {e:.2e}"
