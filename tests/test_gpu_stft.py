@@ -227,3 +227,26 @@ def test_setup_from_spec_files_and_factor_file(tmp_path):
     B2, V2, fl = read_factors(str(tmp_path / "f.nmf"))
     assert all(np.array_equal(p, q) for p, q in zip(B2 + V2, bases + acts))
     s.close()
+
+
+def test_separate_pipeline_end_to_end_vs_oracle():
+    """cmd_separate's whole path on the GPU (ctfmnmf_main.cpp:179-240):
+    signal -> STFT -> ISS estimator (stacked CTF) -> projection-back images ->
+    inverse STFT of the reference channel, against the same chain on the CPU
+    oracle (forward_stft, run, reconstruct_images, inverse_stft): fp64 1e-9."""
+    M, L, K, n, window, hop, iters, seed = 2, 3, 3, 3000, 128, 32, 6, 5
+    sig = np.random.default_rng(99).standard_normal((1, M, n))
+    s = Session(None, [L] * M, [K] * M, stack_taps=L, iterations=iters, precision="f64", seed=seed, signal=sig,
+                window_len=window, hop=hop)
+    s.iterate(iters)
+    got = s.images_to_signal(ref_channel=0)  # [N, 1, n]
+    s.close()
+    spec = O.forward_stft(sig[0], window, hop)           # (F, T, M)
+    xst = O.stack_observation(spec, L)                    # (F, T, D)
+    cfg = O.config([L] * M, [K] * M, iterations=iters, seed=seed)
+    r = O.run(cfg, xst)
+    imgs = O.reconstruct_images(cfg, r["W"], xst)         # [N, F, T, D]
+    for src in range(M):
+        mic_img = imgs[src][:, :, [m * L for m in range(M)]]  # current-frame channels (l = 0)
+        want = O.inverse_stft(mic_img, window, hop, n)[0]
+        assert np.max(np.abs(got[src, 0] - want)) <= 1e-9 * np.max(np.abs(want))
