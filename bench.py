@@ -337,7 +337,12 @@ def main():
     bpt = bytes_per_tfbin(M, N, K, R, D, T, F, c)
     if streamed:  # SURVEY §8(d) streamed sweep: every step reads and writes the R x T tile
         bpt = 2 * M * c + R * c + 2 * R * R * c + bpt - M * c
-    roofline = {"bound": "fp32-cuda-core" if prec == "f32" else "fp64-cuda-core", "achieved": achieved,
+    roofline = {"bound": "fp32-cuda-core" if prec == "f32" else "fp64-cuda-core",
+                "bound_note": ("compute-bound on the CUDA-core FMA pipes: neither HBM-bound (the hbm sub-object "
+                               "shows a few % of HBM) nor a tensor-core contraction (each ISS step is R "
+                               "differently weighted inner products; the fp32/fp64 tolerances rule out "
+                               "bf16/tf32), so the peak is the FFMA2/DFMA chain rate measured in this run"),
+                "achieved": achieved,
                 "peak": peak, "unit": "TFLOP/s", "frac": (achieved / peak) if peak else None,
                 "traffic": traffic_per_tfbin * units_per_launch if traffic_per_tfbin else None,
                 "kernel": desc["sweep_kernel"], "kernel_ms": sweep_ms,
