@@ -846,42 +846,56 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
   // :313-346, 16 bases per pass)
   constexpr int NSD = NS;  // sources per demix group = per Gram pass
   constexpr int GR = NSD * L;  // rows per group
-  Real rp[32];
+  Real rp[R];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) rp[i] = Real(0);
+  for (int i = 0; i < R; ++i) rp[i] = Real(0);
   Real* Eg = reinterpret_cast<Real*>(p.E);
 #pragma unroll
   for (int g0 = 0; g0 < N; g0 += NSD) {  // unrolled: the row-power register index is static
+    // FB frames per pass would share the W loads
+    constexpr int FB = 1;  // 2 shares the W loads but spills at the 80-register budget (measured slower)
 #pragma unroll 1
-    for (int k = 0; k < FT; ++k) {
-      const int j = tid + k * NT;
-      R2 acc[GR];
+    for (int k = 0; k < FT; k += FB) {
+      R2 acc[FB][GR];
 #pragma unroll
-      for (int i = 0; i < GR; ++i) acc[i].x = acc[i].y = Real(0);
+      for (int f = 0; f < FB; ++f)
+#pragma unroll
+        for (int i = 0; i < GR; ++i) acc[f][i].x = acc[f][i].y = Real(0);
 #pragma unroll
       for (int m = 0; m < M; ++m)
 #pragma unroll
         for (int l1 = 0; l1 < L; ++l1) {
-          const R2 xv = xs[m * p.xp + p.xoff + j - l1];
+          R2 xv[FB];
+#pragma unroll
+          for (int f = 0; f < FB; ++f) xv[f] = xs[m * p.xp + p.xoff + tid + (k + f) * NT - l1];
           const R2* wc = Wf + (m * L + l1) * R + g0 * L;
           if constexpr (F32 && GR % 2 == 0) {  // W pairs with 16-byte loads
             const float4* w4 = reinterpret_cast<const float4*>(wc);
 #pragma unroll
             for (int i = 0; i < GR; i += 2) {
               const float4 w = w4[i / 2];
-              acc[i] = Ops::mac(make_float2(w.x, w.y), xv, acc[i]);
-              acc[i + 1] = Ops::mac(make_float2(w.z, w.w), xv, acc[i + 1]);
+#pragma unroll
+              for (int f = 0; f < FB; ++f) {
+                acc[f][i] = Ops::mac(make_float2(w.x, w.y), xv[f], acc[f][i]);
+                acc[f][i + 1] = Ops::mac(make_float2(w.z, w.w), xv[f], acc[f][i + 1]);
+              }
             }
           } else {
 #pragma unroll
-            for (int i = 0; i < GR; ++i) acc[i] = Ops::mac(wc[i], xv, acc[i]);
+            for (int i = 0; i < GR; ++i)
+#pragma unroll
+              for (int f = 0; f < FB; ++f) acc[f][i] = Ops::mac(wc[i], xv[f], acc[f][i]);
           }
         }
 #pragma unroll
-      for (int i = 0; i < GR; ++i) {
-        const Real q = (j < T) ? cnorm(acc[i]) : Real(0);
-        Pq[i * TP + j] = q;
-        rp[g0 * L + i] += q;
+      for (int f = 0; f < FB; ++f) {
+        const int j = tid + (k + f) * NT;
+#pragma unroll
+        for (int i = 0; i < GR; ++i) {
+          const Real q = (j < T) ? cnorm(acc[f][i]) : Real(0);
+          Pq[i * TP + j] = q;
+          rp[g0 * L + i] += q;
+        }
       }
     }
     __syncthreads();  // Pq of the group complete
@@ -956,8 +970,11 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
   for (int i = 0; i < R; ++i) ybad |= !isfinite(rp[i]);
   if (ybad) s_bad = 1;
   // row powers (estimator.cpp:391-397)
-  warp_reduce_scatter(rp, lane);
-  red[warp * 32 + lane] = rp[0];
+  Real rr[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) rr[i] = i < R ? rp[i < R ? i : 0] : Real(0);
+  warp_reduce_scatter(rr, lane);
+  red[warp * 32 + lane] = rr[0];
   __syncthreads();
   if (s_bad) {
     if (tid == 0) record_err<Real>(p.err, mix, err_key(p.iteration, kPhFinite, gbin, 0, 2));

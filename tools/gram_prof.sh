@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_stft.py -q -x 2>&1 | tail -2
-python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/fe.json 2>/dev/null; python -c "import json; d=json.load(open('gpurun_out/fe.json')); f=d['frontend']; print(f['stft'], f['istft'], f['round_trip_max_rel_err'])"
+for c in 0 1 2; do timeout 300 python tools/prof_cfg.py --cfg $c --prec f32 --iters 10 2>&1 | tail -1; done
+timeout 1500 python -m pytest tests/test_gpu_parity.py -q -x -k "fp32 or trajectory or odd or covariance" 2>&1 | tail -2
