@@ -944,6 +944,9 @@ __global__ void __launch_bounds__(128) muv_partial_kernel(const MuvParams p) {
     for (int u = 0; u < G; ++u) enext[u] = (g + G + u < nb) ? Eg[(size_t)(i0 + g + G + u) * p.T] : Real(0);
 #pragma unroll
     for (int u = 0; u < G; u += 2) {
+      // keep the B reads of one bin pair from being hoisted across the group
+      // (they would cost KMAX*G registers and the occupancy)
+      asm volatile("" ::: "memory");
       const int i = g + u;
       Real la, lb;
       if constexpr (std::is_same<Real, float>::value) {
