@@ -262,15 +262,20 @@ def main():
     torch.cuda.set_device(device)
     if world > 1:
         dist.init_process_group("gloo")
-    comm_id = None
-    if world > 1:
+    def new_comm_id():
+        """A fresh NCCL unique id from rank 0 for every communicator (an id is
+        not reused once its communicator has been created)."""
+        if world <= 1:
+            return None
         buf = (C.c_uint8 * 128)()
         err = LB.CtfErr()
         if rank == 0:
             assert LB.load().ctf_comm_unique_id(buf, C.byref(err)) == 0, err.msg
         t = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
         dist.broadcast(t, 0)
-        comm_id = bytes(t.tolist())
+        return bytes(t.tolist())
+
+    comm_id = new_comm_id()
 
     def barrier():
         if world > 1:
@@ -363,7 +368,7 @@ def main():
     s.close()
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, LB, x, prec, device, world, rank, comm_id, barrier, max_over_ranks, s.bin_range,
+        e2e = run_e2e(args, LB, x, prec, device, world, rank, new_comm_id(), barrier, max_over_ranks, s.bin_range,
                       (B, F, T, M, N, L, K, R, D, iters, c))
     del x
     frontend = None
