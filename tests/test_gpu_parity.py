@@ -720,3 +720,20 @@ def test_covariance_kernel_odd_frame_counts(M, L, T, prec):
         e = max(rel(W[0], ref["hist_W"][it].reshape(F, -1)), rel(B[0], ref["hist_B"][it]),
                 rel(V[0], ref["hist_V"][it]))
         assert e <= tol, f"it={it + 1}: {e:.2e}"
+
+
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_zero_iterations_returns_the_initial_state(precision):
+    """run() with iterations = 0 (the loop body never runs): identity W and the
+    host-drawn initial factors, as the oracle returns them."""
+    M, L, K, F, T = 2, 3, 3, 9, 64
+    raw = synth_mixtures(1, F, T, M, M, L, K, 0.6, 1)
+    x = raw.astype(np.complex64) if precision == "f32" else raw
+    s = Session(x, [L] * M, [K] * M, stack_taps=L, iterations=0, precision=precision, seed=7)
+    s.iterate(0)
+    W, B, V, obj = s.download_raw()
+    s.close()
+    ref = O.run(O.config([L] * M, [K] * M, iterations=0, seed=7), O.stack_observation(raw[0], L))
+    assert rel(W[0], ref["W"].reshape(F, -1)) == 0.0
+    tol = 0.0 if precision == "f64" else 1e-7
+    assert rel(B[0], ref["B"]) <= tol and rel(V[0], ref["V"]) <= tol
