@@ -1,2 +1,2 @@
-for c in 1 2; do timeout 300 python tools/prof_cfg.py --cfg $c --prec f32 --iters 6 2>&1 | tail -1; done
-timeout 300 python tools/prof_cfg.py --cfg 1 --prec f64 --iters 4 2>&1 | tail -1
+timeout 300 python tools/prof_cfg.py --cfg 0 --prec f64 --iters 20 2>&1 | tail -1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv python tools/prof_cfg.py --cfg 0 --prec f64 --iters 4 > gpurun_out/c0_launches.csv 2>&1; grep -E "sweep_kernel|muv|apply" gpurun_out/c0_launches.csv | awk -F'","' '{print $5, $(NF)}' | tail -8
