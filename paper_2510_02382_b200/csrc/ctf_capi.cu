@@ -441,6 +441,35 @@ void plan_sweep(ctf_ctx* c) {
       cand.off_z = (int)take((size_t)NW * RB * cs);
       cand.off_b = (int)take((size_t)c->SK * rs);
       cand.off_d = (int)take((size_t)(NW * 4 + c->R) * sizeof(double));
+    } else if (v.kind == 5) {  // frame-split cluster: stacked equal taps, M = N, CS CTAs per bin
+      const int L = v.lt, CS = v.cs;
+      if (c->R != v.rmax || c->D != v.rmax || c->Ls != L || c->Mx * L != c->R || c->N * L != c->R) continue;
+      bool equal = true;
+      for (int n = 0; n < c->N; ++n) equal = equal && c->taps[n] == L;
+      if (!equal) continue;
+      TP = nt * v.ft;  // frames per CTA
+      if ((long)CS * TP < c->T || (long)(CS - 1) * TP >= c->T) continue;  // no idle CTA
+      off = v.fbytes(c->SK);
+      if (off > (size_t)max_smem) continue;
+      // the cluster must be schedulable (same-GPC placement, shared memory)
+      CK(cudaFuncSetAttribute((const void*)v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)off));
+      if (CS > 8) CK(cudaFuncSetAttribute((const void*)v.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(CS * c->FL, c->B);
+      lc.blockDim = dim3(nt);
+      lc.dynamicSmemBytes = off;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = CS;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      int nclusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, (const void*)v.fn, &lc) != cudaSuccess || nclusters < 1) {
+        cudaGetLastError();
+        continue;
+      }
     } else if (v.kind == 2) {  // streamed: any R <= 64, tile in global scratch
       if (c->R > v.rmax) continue;
       TP = nt * v.ft;
@@ -488,13 +517,18 @@ void plan_sweep(ctf_ctx* c) {
     // (measured on B200: the cluster kernel is correct but slower than the
     // streamed one for cfg3/cfg4 so far, so it ranks last; CTF_SWEEP_KIND=3
     // selects it)
-    // covariance-domain first, except fp64 with R <= 4 where the frame-domain
+    // the frame-split cluster kernel (kind 5, only compiled for the wide
+    // stacked tiles R = 32 / 60) first, the fewest CTAs per cluster preferred
+    // (measured on B200: cfg3 45.6 ms per 16 mixtures at CS = 2 vs 51.9 at
+    // CS = 4 and 53.3 on the covariance kernel; cfg4 103 ms per 4 mixtures at
+    // CS = 8 vs 108 at CS = 16 and 212 streamed);
+    // covariance-domain next, except fp64 with R <= 4 where the frame-domain
     // sweep measured faster (cfg0 f64: 0.046 vs 0.051 ms per iteration)
     const int gram_rank = (c->real_size == 8 && c->R <= 4 && !want_ip) ? 500 : -1000;
     // wide covariance tiles (R > 16, one CTA per SM) run best with the most threads
     const int wide_bonus = (v.kind == 4 && c->R > 16) ? -nt / 128 : 0;
     const int rank = wide_bonus +
-                     (v.kind == 4 ? gram_rank : v.kind == 3 ? 3000 : v.kind == 2 ? 2000 : v.kind == 1 ? 1000 : 0) +
+                     (v.kind == 4 ? gram_rank : v.kind == 3 ? 3000 : v.kind == 2 ? 2000 : v.kind == 5 ? -2000 + v.cs : v.kind == 1 ? 1000 : 0) +
                      (v.kind == 3 ? -v.rmax * 4 : v.rmax * 4) + (v.exact ? 0 : 2) + (v.lt > 0 ? 0 : 1);
     const bool better = !found || rank < best_rank ||
                         (rank == best_rank && (TP < c->TP || (TP == c->TP && nt < best_nt)));
@@ -529,6 +563,10 @@ void plan_sweep(ctf_ctx* c) {
     CK(cudaFuncSetAttribute((const void*)best.cfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)best_smem));
     CK(cudaFuncSetAttribute((const void*)best.cfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     c->cluster_size = c->R / best.rmax;
+  } else if (best.kind == 5) {
+    CK(cudaFuncSetAttribute((const void*)best.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)best_smem));
+    if (best.cs > 8) CK(cudaFuncSetAttribute((const void*)best.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    c->cluster_size = best.cs;
   } else if (best.kind == 2) {
     CK(cudaFuncSetAttribute((const void*)best.sfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)best_smem));
     int per_sm = 0, nsm = 0;
@@ -860,6 +898,20 @@ void run_body(ctf_ctx* c, bool do_sweep) {
     lc.attrs = at;
     lc.numAttrs = 1;
     CK(cudaLaunchKernelEx(&lc, c->sv.cfn, cl));
+  } else if (c->sv.kind == 5) {
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(c->FL * c->cluster_size, c->B);
+    lc.blockDim = dim3(c->NT);
+    lc.dynamicSmemBytes = c->sweep_smem;
+    lc.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = c->cluster_size;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&lc, c->sv.fn, sp));
   } else if (c->sv.kind == 2) {
     ctf::StreamParams st{};
     st.s = sp;
@@ -1324,12 +1376,13 @@ int ctf_describe(ctf_ctx* c, char* buf, int len) {
   std::snprintf(buf, (size_t)len,
                 "{\"sweep_kernel\": \"%s<%s,RMAX=%d,FT=%d,%s=%d,NT=%d,EXACT=%d>\", \"threads\": %d, "
                 "\"smem_bytes\": %zu, \"grid\": [%d, %d], \"muv_chunks\": %d, \"bins\": [%d, %d], "
-                "\"world\": %d, \"rank\": %d, \"collective\": \"%s\"}",
-                c->sv.kind == 4 ? "gram_kernel" : c->sv.kind == 3 ? "cluster_kernel" : c->sv.kind == 2 ? "stream_kernel" : c->sv.kind ? "rowwarp_kernel" : "sweep_kernel",
+                "\"world\": %d, \"rank\": %d, \"collective\": \"%s\", \"cluster\": %d}",
+                c->sv.kind == 5 ? "fsplit_kernel" : c->sv.kind == 4 ? "gram_kernel" : c->sv.kind == 3 ? "cluster_kernel" : c->sv.kind == 2 ? "stream_kernel" : c->sv.kind ? "rowwarp_kernel" : "sweep_kernel",
                 c->real_size == 4 ? "f32" : "f64", c->sv.rmax, c->sv.ft,
-                c->sv.kind == 4 ? "M" : c->sv.kind == 3 ? "RREG" : c->sv.kind == 2 ? "RG" : c->sv.kind ? "WPR" : "RREG", c->sv.rreg, c->sv.maxt, c->sv.exact, c->NT,
+                c->sv.kind == 4 ? "M" : (c->sv.kind == 3 || c->sv.kind == 5) ? "RREG" : c->sv.kind == 2 ? "RG" : c->sv.kind ? "WPR" : "RREG", c->sv.rreg, c->sv.maxt, c->sv.exact, c->NT,
                 c->sweep_smem, c->FL, c->B, c->nchunk, c->lo, c->hi, c->world, c->rank,
-                c->group ? "host-group" : c->comm ? "nccl" : "none");
+                c->group ? "host-group" : c->comm ? "nccl" : "none",
+                (c->sv.kind == 3 || c->sv.kind == 5) ? c->cluster_size : 1);
   return CTF_OK;
 }
 

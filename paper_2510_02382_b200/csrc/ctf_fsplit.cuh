@@ -1,0 +1,705 @@
+// ctf_fsplit.cuh — frame-split thread-block-cluster ISS sweep for tiles that
+// exceed one SM (BASELINE cfg3: R = 32, T = 1000; cfg4: R = 60, T = 4000).
+//
+// Same contract and numerics as sweep_kernel (ctf_kernels.cuh): the bin-local
+// part of one iteration of proj/src/estimator.cpp:548-654 for the stacked
+// equal-taps layout (R = D = N*L, M = N). A cluster of CS CTAs handles one
+// (mixture, bin); CTA c owns frames [c*TC, (c+1)*TC) of ALL rows, so the
+// R x T estimate tile stays on chip (RREG rows per thread in registers, the
+// rest in shared memory) and every per-frame update is thread-private, as in
+// sweep_kernel. The only cross-CTA data per ISS step are the 3R weighted sums
+// (estimator.cpp:434-462) and the R steering coefficients z:
+//   1. each CTA reduces its frames' sums (warp reduce-scatter + fixed-order
+//      cross-warp sum) and pushes row p's partial to the CTA that owns row p
+//      (p % CS) with st.async into the owner's shared memory, completing
+//      bytes on the owner's mbarrier;
+//   2. the owner waits for all CS partials of its rows, sums them in CTA
+//      order, derives z_p (estimator.cpp:442-458) and pushes it to every
+//      CTA with st.async on their mbarriers;
+//   3. every CTA waits for all R coefficients and applies the step.
+// No cluster barrier per step: two one-way DSMEM hops, ordered by mbarrier
+// transaction counts (double-buffered by step parity). All CTAs derive
+// identical z (same inputs, same order), so the run is deterministic.
+// W: CTA c updates the columns [c*DC, (c+1)*DC) (W -= z w_r is column-local);
+// the demix stages the rescaled W four rows at a time in shared memory. Frame halos: the
+// stacked observation and the ISS weights reach L-1 frames back (x and
+// 1/lambda are loaded with that halo), the delayed energies reach L-1 frames
+// forward (|y|^2 of the next CTA's first L-1 frames, read over DSMEM).
+// Objective, row powers and MU-B partials are combined by CTA 0 in CTA order.
+#pragma once
+
+#include "ctf_cluster.cuh"
+#include "ctf_kernels.cuh"
+
+namespace ctf {
+
+template <typename Real, int R, int L, int FT, int NT, int CS, int RREG, int RG>
+struct FsplitLayout {
+  static constexpr int M = R / L;  // mics == sources
+  static constexpr int NW = NT / 32;
+  static constexpr int TC = FT * NT;  // frames per CTA
+  static constexpr int XOFF = L;      // x halo (>= L - 1 frames back)
+  static constexpr int XP = XOFF + TC;
+  static constexpr int LOFF = ((L + 3) / 4) * 4;  // 1/lambda halo
+  static constexpr int LP = LOFF + TC;
+  static constexpr int RC = (R + CS - 1) / CS;  // rows owned per CTA (max)
+  static constexpr int DC = RC;                 // W columns per CTA
+  static constexpr int NG = (R + RG - 1) / RG;  // row groups per pass
+  static constexpr int VP = ((3 * RG + 31) / 32) * 32;
+  static constexpr int NG2 = (R + 31) / 32;  // row-power groups
+  static constexpr int HL = L > 1 ? L - 1 : 1;
+  static constexpr int CH = 4 * (int)sizeof(Real);  // bytes per DSMEM message
+  static constexpr size_t RB_ = sizeof(Real), CB_ = 2 * sizeof(Real);
+  static constexpr size_t a16(size_t b) { return (b + 15) & ~size_t(15); }
+  static constexpr size_t mx(size_t a, size_t b) { return a > b ? a : b; }
+  static constexpr size_t off_y = 0;
+  static constexpr size_t off_x = off_y + a16((size_t)(R - RREG) * TC * CB_);
+  static constexpr size_t off_l = off_x + a16(mx((size_t)M * XP * CB_, (size_t)L * (TC + HL) * RB_));
+  static constexpr size_t off_w = off_l + a16((size_t)M * LP * RB_);
+  static constexpr size_t off_red = off_w + a16((size_t)2 * R * DC * CB_);
+  static constexpr size_t off_a =
+      off_red + a16(mx((size_t)NW * mx(mx((size_t)NG * VP, (size_t)NG2 * 32), 16) * RB_, (size_t)4 * R * CB_));
+  static constexpr size_t off_z = off_a + a16((size_t)2 * CS * RC * CH);
+  static constexpr size_t off_h = off_z + a16((size_t)2 * R * CH);
+  static constexpr size_t off_ex = off_h + a16((size_t)R * HL * RB_);
+  static constexpr size_t off_bar = off_ex + a16((size_t)(8 + R) * 8);
+  static constexpr size_t off_bs = off_bar + 64;
+  static size_t bytes(int SK) { return off_bs + a16((size_t)SK * RB_) + (size_t)2 * SK * 8; }
+};
+
+__device__ __forceinline__ uint32_t smem_u32addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t dsmem_map(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ double dsmem_ld_f64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ float dsmem_ld_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ double dsmem_ld(uint32_t a, double) { return dsmem_ld_f64(a); }
+__device__ __forceinline__ float dsmem_ld(uint32_t a, float) { return dsmem_ld_f32(a); }
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+// one local arrival that also expects `tx` bytes of st.async data this phase
+__device__ __forceinline__ void mbar_arm(uint32_t bar, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx) : "memory");
+}
+// The messages land in this CTA's shared memory, so the phase completion
+// (default .acquire.cta) orders them; a cluster-scope acquire would also
+// invalidate L1 on every wait (CCTL.IVALL, measured: 14 % of the stall samples).
+__device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+// 4-value message into another CTA's shared memory, completing its bytes on
+// that CTA's mbarrier (addresses already mapped with dsmem_map)
+__device__ __forceinline__ void msg_send(uint32_t raddr, uint32_t rbar, float a, float b, float c, float d) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                   raddr),
+               "f"(a), "f"(b), "f"(c), "f"(d), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void msg_send(uint32_t raddr, uint32_t rbar, double a, double b, double c, double d) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+               "d"(a), "d"(b), "r"(rbar)
+               : "memory");
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(raddr +
+                                                                                                           16),
+               "d"(c), "d"(d), "r"(rbar)
+               : "memory");
+}
+
+template <typename Real, int R, int L, int FT, int NT, int CS, int RREG, int RG, int MINB>
+__global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
+  using R2 = typename Cplx<Real>::T;
+  using LY = FsplitLayout<Real, R, L, FT, NT, CS, RREG, RG>;
+  constexpr int N = LY::M, M = LY::M, NW = LY::NW, TC = LY::TC, XP = LY::XP, XOFF = LY::XOFF;
+  constexpr int LP = LY::LP, LOFF = LY::LOFF, RC = LY::RC, DC = LY::DC, NG = LY::NG, VP = LY::VP;
+  constexpr int VM = VP / 32, HL = LY::HL, CH = LY::CH, RS = R - RREG;
+  static_assert(R % L == 0 && R <= 64 && R >= CS && RREG <= R, "stacked equal-taps tiles, one owner per row");
+  static_assert(TC % 32 == 0, "whole warps of frames");
+  static_assert(RC * CS <= NT, "one thread per (owned row, destination CTA)");
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c = (int)cluster_ctarank();
+  const int bin = blockIdx.x / CS, mix = blockIdx.y, gbin = p.bin_lo + bin;
+  const int T = p.T, SK = p.SK;
+  const int j0 = c * TC;  // first global frame of this CTA
+
+  R2* Ysm = reinterpret_cast<R2*>(smem + LY::off_y);      // RS x TC
+  R2* xs = reinterpret_cast<R2*>(smem + LY::off_x);       // M x XP (frames j0 - XOFF ..)
+  Real* Pn = reinterpret_cast<Real*>(smem + LY::off_x);   // epilogue: L x (TC + HL) |y|^2 of one source
+  Real* invl = reinterpret_cast<Real*>(smem + LY::off_l); // N x LP (frames j0 - LOFF ..)
+  R2* Wsl = reinterpret_cast<R2*>(smem + LY::off_w);      // 2 x DC x R (own columns, ping-pong)
+  Real* red = reinterpret_cast<Real*>(smem + LY::off_red);
+  double* dred = reinterpret_cast<double*>(smem + LY::off_red);
+  unsigned char* inA = smem + LY::off_a;  // [2][CS][RC] partial sums of the own rows
+  unsigned char* inZ = smem + LY::off_z;  // [2][R] steering coefficients (z.x, z.y, bad, 0)
+  Real* halo = reinterpret_cast<Real*>(smem + LY::off_h);  // R x HL |y|^2 of the first frames
+  double* ex = reinterpret_cast<double*>(smem + LY::off_ex);  // [0,4) objective, [4,4+R) row powers, [4+R,8+R) totals
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + LY::off_bar);  // A0 A1 Z0 Z1
+  Real* Bs = reinterpret_cast<Real*>(smem + LY::off_bs);
+  double* exmub = reinterpret_cast<double*>(smem + LY::off_bs + LY::a16((size_t)SK * sizeof(Real)));
+  __shared__ int s_wbad;
+
+  const size_t tile = (size_t)mix * p.FL + bin;
+  const R2* xg = reinterpret_cast<const R2*>(p.x) + tile * (size_t)T * M;
+  R2* Wg = reinterpret_cast<R2*>(p.W) + tile * (size_t)R * R;
+  Real* Bg = reinterpret_cast<Real*>(p.Bf) + tile * SK;
+  const Real* Vg = reinterpret_cast<const Real*>(p.V) + (size_t)mix * SK * T;
+  const Real floor_abs = (Real)p.floor_abs[mix];
+  const int prev_it = p.iteration - 1;
+  const double* mu = p.mu ? p.mu + (size_t)mix * R : nullptr;
+  const int nown = (R - c + CS - 1) / CS;  // rows p with p % CS == c
+  const uint32_t txA = (uint32_t)(CS * nown * CH), txZ = (uint32_t)(R * CH);
+  const uint32_t barA[2] = {smem_u32addr(bars + 0), smem_u32addr(bars + 1)};
+  const uint32_t barZ[2] = {smem_u32addr(bars + 2), smem_u32addr(bars + 3)};
+
+  if (tid == 0) {
+    s_wbad = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) mbar_init(smem_u32addr(bars + b), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_arm(barA[0], txA);  // steps 0 and 1
+    mbar_arm(barA[1], txA);
+    mbar_arm(barZ[0], txZ);
+    mbar_arm(barZ[1], txZ);
+  }
+  // z of "step -1" (zero update in the first pass)
+  for (int i = tid; i < R * CH / (int)sizeof(Real); i += NT)
+    reinterpret_cast<Real*>(inZ + (size_t)R * CH)[i] = Real(0);
+  // ---- prologue: x tile with its halo, own W columns and B with the pending rescale
+  {
+    // all of the thread's loads in flight before the transposing stores
+    constexpr int XPT = (XP * M + NT - 1) / NT;
+    R2 xv[XPT];
+#pragma unroll
+    for (int t = 0; t < XPT; ++t) {
+      const int e = tid + t * NT, i = e / M;
+      const int j = j0 - XOFF + i;
+      xv[t] = (e < XP * M && j >= 0 && j < T) ? xg[(size_t)j0 * M - XOFF * M + e] : czero<Real>();
+    }
+#pragma unroll
+    for (int t = 0; t < XPT; ++t) {
+      const int e = tid + t * NT, i = e / M, m = e - i * M;
+      if (e < XP * M) xs[m * XP + i] = xv[t];
+    }
+  }
+  for (int e = tid; e < R * DC; e += NT) {
+    const int q = e % R, i = e / R, col = c * DC + i;
+    R2 w = czero<Real>();
+    if (col < R) {
+      w = Wg[(size_t)col * R + q];
+      if (mu) {
+        const double m = mu[q];
+        if (m != 0.0) {
+          w.x = (Real)((double)w.x / m);
+          w.y = (Real)((double)w.y / m);
+        }
+      }
+      if (p.has_prev && !cfinite(w)) s_wbad = 1;
+    }
+    Wsl[e] = w;
+  }
+  for (int n = 0; n < N; ++n) {
+    const double m0 = mu ? mu[n * L] : 0.0;
+    for (int i = p.koff[n] + tid; i < p.koff[n + 1]; i += NT) {
+      Real b = Bg[i];
+      if (m0 != 0.0) b = (Real)fmax((double)b / (m0 * m0), (double)floor_abs);
+      Bs[i] = b;
+    }
+  }
+  cluster_sync_all();  // mbarriers initialised cluster-wide; Bs, inZ visible in the CTA
+  // ---- lambda = max(B V, floor) -> 1/lambda over the frames j0 - LOFF .. j0 + TC
+  double logsum = 0.0;
+  for (int n = 0; n < N; ++n) {
+    const int k0 = p.koff[n], k1 = p.koff[n + 1];
+    for (int i = tid; i < LP; i += NT) {
+      const int jl = i - LOFF, tau = j0 + jl;
+      Real v = Real(0);
+      if (tau >= 0 && tau < T) {
+        Real lam = Real(0);
+        int kk = k0;
+        for (; kk + 4 <= k1; kk += 4) {  // four loads in flight, same summation order
+          const Real v0 = __ldg(Vg + (size_t)kk * T + tau), v1 = __ldg(Vg + (size_t)(kk + 1) * T + tau);
+          const Real v2 = __ldg(Vg + (size_t)(kk + 2) * T + tau), v3 = __ldg(Vg + (size_t)(kk + 3) * T + tau);
+          lam = fma(Bs[kk], v0, lam);
+          lam = fma(Bs[kk + 1], v1, lam);
+          lam = fma(Bs[kk + 2], v2, lam);
+          lam = fma(Bs[kk + 3], v3, lam);
+        }
+        for (; kk < k1; ++kk) lam = fma(Bs[kk], __ldg(Vg + (size_t)kk * T + tau), lam);
+        lam = fmax(lam, floor_abs);
+        v = Real(1) / lam;
+        if (p.has_prev && jl >= 0) logsum += (double)min(L, T - tau) * (double)log(lam);
+      }
+      invl[n * LP + i] = v;
+    }
+  }
+  __syncthreads();
+
+  // ---- Y = (W / mu) x~ for the own frames (estimator.cpp:555), 4 rows per
+  // chunk: the chunk's rescaled W rows staged column-major in shared memory
+  // (the reduction buffer is free here), the next chunk prefetched into
+  // registers; the stacked channel (m, l) is x_m(t - l) from the x tile
+  YTile<R2, FT, RREG, RS> Y;
+  Y.sm = Ysm;
+  Y.tp = TC;
+  {
+    constexpr int NCH = (R + 3) / 4, WPT = (4 * R + NT - 1) / NT;
+    R2* wst = reinterpret_cast<R2*>(smem + LY::off_red);  // [R columns][4 rows]
+    R2 wpre[WPT];
+    auto fetch = [&](int r0) {
+#pragma unroll
+      for (int t = 0; t < WPT; ++t) {
+        const int e = tid + t * NT, cc = e >> 2, q = r0 + (e & 3);
+        R2 w = czero<Real>();
+        if (cc < R && q < R) {
+          w = Wg[(size_t)cc * R + q];
+          if (mu) {
+            const double m = mu[q];
+            if (m != 0.0) {
+              w.x = (Real)((double)w.x / m);
+              w.y = (Real)((double)w.y / m);
+            }
+          }
+        }
+        wpre[t] = w;
+      }
+    };
+    fetch(0);
+    static_for<0, NCH>([&](auto chunk) {
+      constexpr int r0 = decltype(chunk)::value * 4;
+      __syncthreads();  // the previous chunk's reads of wst are done
+#pragma unroll
+      for (int t = 0; t < WPT; ++t)
+        if (tid + t * NT < 4 * R) wst[tid + t * NT] = wpre[t];
+      __syncthreads();
+      if constexpr (r0 + 4 < R) fetch(r0 + 4);
+      R2 acc[FT][4];
+#pragma unroll
+      for (int k = 0; k < FT; ++k)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[k][i] = czero<Real>();
+#pragma unroll 4
+      for (int cc = 0; cc < R; ++cc) {
+        const int m = cc / L, l = cc - m * L;
+        const R2* xrow = xs + m * XP + XOFF - l + tid;
+        R2 w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) w[i] = wst[cc * 4 + i];
+#pragma unroll
+        for (int k = 0; k < FT; ++k) {
+          const R2 xv = xrow[k * NT];
+          if constexpr (std::is_same<Real, float>::value) {
+            const float2 xn = make_float2(-xv.y, xv.x);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[k][i] = ffma2s(xn, w[i].y, ffma2s(xv, w[i].x, acc[k][i]));
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) cmac(acc[k][i], w[i], xv);
+          }
+        }
+      }
+      static_for<0, 4>([&](auto ii) {
+        constexpr int P = r0 + decltype(ii)::value;
+        if constexpr (P < R) {
+#pragma unroll
+          for (int k = 0; k < FT; ++k) {
+            const int jl = tid + k * NT;
+            Y.template set<P>(k, jl, (j0 + jl < T) ? acc[k][decltype(ii)::value] : czero<Real>());
+          }
+        }
+      });
+    });
+    __syncthreads();  // wst (the reduction buffer) is reused by the objective sums
+  }
+
+  // ISS weights: w_p(j) = 1/lambda_{n_p}(j - l_p), row P = (P / L, P % L)
+  const Real* wsrc[N];
+#pragma unroll
+  for (int n = 0; n < N; ++n) wsrc[n] = invl + n * LP + LOFF + tid;
+  auto weight = [&](auto pp, int k) -> Real {
+    constexpr int P = decltype(pp)::value;
+    return wsrc[P / L][k * NT - (P % L)];
+  };
+
+  double logdet = p.logdet[tile] - (mu ? p.logmu[mix] : 0.0);
+  if (p.has_prev) {
+    // objective of the previous iteration (estimator.cpp:55-77): this CTA's
+    // frames, combined over the cluster in CTA order
+    Real qf = Real(0), sy = Real(0);
+    static_for<0, R>([&](auto pp) {
+      constexpr int P = decltype(pp)::value;
+#pragma unroll
+      for (int k = 0; k < FT; ++k) {
+        const R2 y = Y.template get<P>(k, tid + k * NT);
+        sy += y.x + y.y;
+        qf = fma(cnorm(y), weight(pp, k), qf);
+      }
+    });
+    double v4[4] = {logsum, (double)qf, s_wbad ? 1.0 : 0.0, (isfinite(sy) && isfinite(qf)) ? 0.0 : 1.0};
+    block_sum_d<4>(v4, dred, lane, warp, NW);
+    if (tid == 0)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ex[q] = v4[q];
+    cluster_sync_all();
+    if (tid < 4) {
+      double s = 0.0;
+      for (int q = 0; q < CS; ++q) s += dsmem_ld_f64(dsmem_map(smem_u32addr(ex + tid), (uint32_t)q));
+      ex[4 + R + tid] = s;
+    }
+    __syncthreads();
+    const double* tot = ex + 4 + R;
+    int status = 0;
+    unsigned long long key = 0;
+    if (tot[2] > 0.0) {  // check_all_finite on W (estimator.cpp:494-496)
+      status = 1;
+      key = err_key(prev_it, kPhFinite, gbin, 0, 1);
+    } else if (tot[3] > 0.0) {  // non-finite estimates (estimator.cpp:497-499)
+      status = 1;
+      key = err_key(prev_it, kPhFinite, gbin, 0, 2);
+    } else {
+      const int det_status = isnan(logdet) || logdet == -INFINITY ? 4 : (logdet < log(1e-300) ? 5 : 0);
+      if (det_status) {  // estimator.cpp:45-51
+        status = 1;
+        key = err_key(prev_it, kPhDet, gbin, 0, det_status);
+      }
+    }
+    if (status) {
+      if (c == 0 && tid == 0) record_err<Real>(p.err, mix, key);
+      cluster_sync_all();  // remote reads of ex done before any CTA exits
+      return;
+    }
+    if (c == 0 && tid == 0) p.objbin[tile] = tot[0] + tot[1] - 2.0 * (double)T * logdet;
+  }
+
+  if (!p.do_sweep) {  // finalize pass: write the rescaled state and stop
+    if (!p.has_prev) cluster_sync_all();  // every CTA is past its demix reads of W
+    for (int e = tid; e < R * DC; e += NT) {
+      const int q = e % R, i = e / R, col = c * DC + i;
+      if (col < R) Wg[(size_t)col * R + q] = Wsl[e];
+    }
+    if (c == 0) {
+      for (int i = tid; i < SK; i += NT) Bg[i] = Bs[i];
+      if (tid == 0) p.logdet[tile] = logdet;
+    }
+    cluster_sync_all();
+    return;
+  }
+
+  // ---- ISS sweep (estimator.cpp:556-579). The pass of step r applies step
+  // r-1's update (y_p -= z_p y_{r-1}) and accumulates step r's sums.
+  R2 pv[FT];
+#pragma unroll
+  for (int k = 0; k < FT; ++k) pv[k] = czero<Real>();
+  double dprod = 1.0;  // prod_r (1 - z_r): det W' = det W prod_r (1 - z_r)
+  int badrow = -1, badstep = 0;
+  for (int r = 0; r < R; ++r) {
+    const int buf = r & 1;
+    const unsigned char* zprev = inZ + (size_t)(buf ^ 1) * R * CH;
+    auto zof = [&](int P) -> R2 { return *reinterpret_cast<const R2*>(zprev + (size_t)P * CH); };
+    R2 yr[FT];
+    Real ar2[FT];
+    {
+      const R2 zr = zof(r);
+#pragma unroll
+      for (int k = 0; k < FT; ++k) {
+        R2 y = Y.pick(k, tid + k * NT, r);
+        if constexpr (std::is_same<Real, float>::value) {
+          y = ffma2s(pv[k], -zr.x, y);
+          y = ffma2s(make_float2(pv[k].y, -pv[k].x), zr.y, y);
+        } else {
+          cmsub(y, zr, pv[k]);
+        }
+        yr[k] = y;
+        ar2[k] = cnorm(y);
+      }
+    }
+    static_for<0, NG>([&](auto gg) {
+      constexpr int g = decltype(gg)::value;
+      Real a[VP];
+#pragma unroll
+      for (int i = 0; i < VP; ++i) a[i] = Real(0);
+      static_for<0, RG>([&](auto qq) {
+        constexpr int q = decltype(qq)::value, P = g * RG + q;
+        if constexpr (P < R) {
+          const R2 zp = zof(P);
+          if constexpr (std::is_same<Real, float>::value) {
+            // packed FP32x2 (see sweep_kernel): numer = (Q1.x + Q2.y, Q1.y - Q2.x)
+            float2 q1 = make_float2(0.f, 0.f), q2 = q1;
+            float den = 0.f;
+#pragma unroll
+            for (int k = 0; k < FT; ++k) {
+              const int jl = tid + k * NT;
+              float2 y = Y.template get<P>(k, jl);
+              y = ffma2s(pv[k], -zp.x, y);
+              y = ffma2s(make_float2(pv[k].y, -pv[k].x), zp.y, y);
+              Y.template set<P>(k, jl, y);
+              const float w = weight(std::integral_constant<int, P>{}, k);
+              const float2 sw = fmul2s(yr[k], w);
+              q1 = ffma2s(y, sw.x, q1);
+              q2 = ffma2s(y, sw.y, q2);
+              den = fmaf(ar2[k], w, den);
+            }
+            a[q] = q1.x + q2.y;
+            a[RG + q] = q1.y - q2.x;
+            a[2 * RG + q] = den;
+          } else {
+#pragma unroll
+            for (int k = 0; k < FT; ++k) {
+              const int jl = tid + k * NT;
+              R2 y = Y.template get<P>(k, jl);
+              cmsub(y, zp, pv[k]);
+              Y.template set<P>(k, jl, y);
+              const Real w = weight(std::integral_constant<int, P>{}, k);
+              a[q] = fma(fma(y.x, yr[k].x, y.y * yr[k].y), w, a[q]);
+              a[RG + q] = fma(fma(y.y, yr[k].x, -y.x * yr[k].y), w, a[RG + q]);
+              a[2 * RG + q] = fma(ar2[k], w, a[2 * RG + q]);
+            }
+          }
+        }
+      });
+      warp_reduce_scatter(a, lane);
+      Real* rb = red + ((size_t)warp * NG + g) * VP;
+#pragma unroll
+      for (int i = 0; i < VM; ++i) rb[lane * VM + i] = a[i];
+    });
+#pragma unroll
+    for (int k = 0; k < FT; ++k) pv[k] = yr[k];
+    __syncthreads();
+    // this CTA's partial of row `tid` -> the row's owner
+    if (tid < R) {
+      const int g = tid / RG, q = tid - g * RG;
+      Real nre = Real(0), nim = Real(0), den = Real(0);
+      for (int w = 0; w < NW; ++w) {
+        const Real* rb = red + ((size_t)w * NG + g) * VP;
+        nre += rb[q];
+        nim += rb[RG + q];
+        den += rb[2 * RG + q];
+      }
+      const int owner = tid % CS, lr = tid / CS;
+      const uint32_t la = smem_u32addr(inA + ((size_t)(buf * CS + c) * RC + lr) * CH);
+      msg_send(dsmem_map(la, (uint32_t)owner), dsmem_map(barA[buf], (uint32_t)owner), nre, nim, den, Real(0));
+    }
+    // owners: z of the own rows from the CS partials (CTA order), to every CTA
+    if (tid < nown * CS) {
+      const int lr = tid / CS, dest = tid - lr * CS, row = c + lr * CS;
+      mbar_wait_parity(barA[buf], (uint32_t)((r >> 1) & 1));
+      Real nre = Real(0), nim = Real(0), den = Real(0);
+      for (int q = 0; q < CS; ++q) {
+        const Real* e = reinterpret_cast<const Real*>(inA + ((size_t)(buf * CS + q) * RC + lr) * CH);
+        nre += e[0];
+        nim += e[1];
+        den += e[2];
+      }
+      const bool bad = !(den > Real(0)) || !isfinite(den);  // estimator.cpp:451-454
+      Real zx, zy = Real(0);
+      if (row == r) {
+        zx = Real(1) - sqrt((Real)T / den);
+      } else {
+        zx = nre / den;
+        zy = nim / den;
+      }
+      const uint32_t la = smem_u32addr(inZ + ((size_t)buf * R + row) * CH);
+      msg_send(dsmem_map(la, (uint32_t)dest), dsmem_map(barZ[buf], (uint32_t)dest), zx, zy, bad ? Real(1) : Real(0),
+               Real(0));
+      if (tid == 0) mbar_arm(barA[buf], txA);  // step r + 2
+    }
+    mbar_wait_parity(barZ[buf], (uint32_t)((r >> 1) & 1));
+    if (tid == 0) mbar_arm(barZ[buf], txZ);  // step r + 2
+    const unsigned char* zcur = inZ + (size_t)buf * R * CH;
+    {
+      const bool b1 = lane < R && reinterpret_cast<const Real*>(zcur + (size_t)lane * CH)[2] != Real(0);
+      const bool b2 = lane + 32 < R && reinterpret_cast<const Real*>(zcur + (size_t)(lane + 32) * CH)[2] != Real(0);
+      const unsigned m1 = __ballot_sync(kFull, b1), m2 = __ballot_sync(kFull, b2);
+      if (m1 | m2) {
+        badrow = m1 ? __ffs(m1) - 1 : 32 + __ffs(m2) - 1;
+        badstep = r;
+        break;
+      }
+    }
+    const Real zr_real = reinterpret_cast<const Real*>(zcur + (size_t)r * CH)[0];
+    dprod *= (double)(Real(1) - zr_real);
+    // iss_apply on the own W columns, W -= z w_r (estimator.cpp:298-302), ping-pong
+    const R2* Wo = Wsl + (size_t)(r & 1) * R * DC;
+    R2* Wn = Wsl + (size_t)((r + 1) & 1) * R * DC;
+    for (int e = tid; e < R * DC; e += NT) {
+      const int q = e % R, i = e / R;
+      R2 w = Wo[e];
+      cmsub(w, *reinterpret_cast<const R2*>(zcur + (size_t)q * CH), Wo[i * R + r]);
+      Wn[e] = w;
+    }
+  }
+  if (badrow >= 0) {
+    if (c == 0 && tid == 0) record_err<Real>(p.err, mix, err_key(p.iteration, kPhSweep, gbin, badstep, badrow));
+    cluster_sync_all();
+    return;
+  }
+
+  // ---- epilogue: last step's update, row-power partials, |y|^2 of the first
+  // HL frames for the previous CTA's delayed energies
+  {
+    const unsigned char* zl = inZ + (size_t)((R - 1) & 1) * R * CH;
+    static_for<0, LY::NG2>([&](auto gg) {
+      constexpr int g = decltype(gg)::value;
+      Real a[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) a[i] = Real(0);
+      static_for<0, 32>([&](auto qq) {
+        constexpr int q = decltype(qq)::value, P = g * 32 + q;
+        if constexpr (P < R) {
+          const R2 zp = *reinterpret_cast<const R2*>(zl + (size_t)P * CH);
+#pragma unroll
+          for (int k = 0; k < FT; ++k) {
+            const int jl = tid + k * NT;
+            R2 y = Y.template get<P>(k, jl);
+            if constexpr (std::is_same<Real, float>::value) {
+              y = ffma2s(pv[k], -zp.x, y);
+              y = ffma2s(make_float2(pv[k].y, -pv[k].x), zp.y, y);
+            } else {
+              cmsub(y, zp, pv[k]);
+            }
+            Y.template set<P>(k, jl, y);
+            const Real q2 = cnorm(y);
+            a[q] += q2;
+            if (jl < HL) halo[P * HL + jl] = q2;
+          }
+        }
+      });
+      warp_reduce_scatter(a, lane);
+      red[((size_t)warp * LY::NG2 + g) * 32 + lane] = a[0];
+    });
+  }
+  __syncthreads();
+  if (tid < R) {
+    const int g = tid / 32, q = tid - g * 32;
+    double s = 0.0;
+    for (int w = 0; w < NW; ++w) s += (double)red[((size_t)w * LY::NG2 + g) * 32 + q];
+    ex[4 + tid] = s;
+  }
+  cluster_sync_all();  // halos and row-power partials published
+
+  // delayed energies E_n(tau) = sum_{l<L, tau+l<T} |y_{nL+l}(tau+l)|^2 (estimator.cpp:321-332)
+  Real eown[N][FT];
+  Real* Eg = reinterpret_cast<Real*>(p.E);
+  static_for<0, N>([&](auto nn) {
+    constexpr int n = decltype(nn)::value;
+    __syncthreads();  // previous source's Pn reads done (Pn aliases the dead x tile)
+    static_for<0, L>([&](auto ll) {
+      constexpr int l = decltype(ll)::value, P = n * L + l;
+#pragma unroll
+      for (int k = 0; k < FT; ++k) {
+        const int jl = tid + k * NT;
+        Pn[l * (TC + HL) + jl] = cnorm(Y.template get<P>(k, jl));
+      }
+    });
+    for (int i = tid; i < L * HL; i += NT) {
+      const int l = i / HL, h = i - l * HL;
+      Real v = Real(0);
+      if (c + 1 < CS) v = dsmem_ld(dsmem_map(smem_u32addr(halo + (n * L + l) * HL + h), (uint32_t)(c + 1)), Real(0));
+      Pn[l * (TC + HL) + TC + h] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < FT; ++k) {
+      const int jl = tid + k * NT, tau = j0 + jl;
+      Real e = Real(0);
+      for (int l = 0; l < L && tau + l < T; ++l) e += Pn[l * (TC + HL) + jl + l];
+      eown[n][k] = e;
+      if (tau < T) Eg[(((size_t)mix * N + n) * p.FL + bin) * T + tau] = e;
+    }
+  });
+
+  // MU-B partials (estimator.cpp:313-346) over the own frames, 16 bases per pass
+  for (int n = 0; n < N; ++n) {
+    const int k0 = p.koff[n], k1 = p.koff[n + 1];
+    const Real* il = invl + n * LP + LOFF;
+    Real en[FT];
+#pragma unroll
+    for (int k = 0; k < FT; ++k) en[k] = eown[0][k];
+    static_for<1, N>([&](auto nn) {
+      constexpr int q = decltype(nn)::value;
+      if (n == q)
+#pragma unroll
+        for (int k = 0; k < FT; ++k) en[k] = eown[q][k];
+    });
+    for (int kb = k0; kb < k1; kb += 16) {
+      Real a[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) a[i] = Real(0);
+#pragma unroll
+      for (int k = 0; k < FT; ++k) {
+        const int jl = tid + k * NT, tau = j0 + jl;
+        const Real ilv = il[jl];
+        const Real an = en[k] * (ilv * ilv);
+        const Real bn = (tau < T) ? ilv * (Real)min(L, T - tau) : Real(0);
+        if (tau < T) {
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const Real v = __ldg(Vg + (size_t)min(kb + q, k1 - 1) * T + tau);
+            a[q] = fma(an, v, a[q]);
+            a[16 + q] = fma(bn, v, a[16 + q]);
+          }
+        }
+      }
+      warp_reduce_scatter(a, lane);
+      __syncthreads();  // previous pass's reads of red are done
+      red[(size_t)warp * 32 + lane] = a[0];
+      __syncthreads();
+      if (tid < 16 && kb + tid < k1) {
+        Real num = Real(0), den = Real(0);
+        for (int w = 0; w < NW; ++w) {
+          num += red[(size_t)w * 32 + tid];
+          den += red[(size_t)w * 32 + 16 + tid];
+        }
+        exmub[2 * (kb + tid)] = (double)num;
+        exmub[2 * (kb + tid) + 1] = (double)den;
+      }
+    }
+  }
+  cluster_sync_all();  // MU-B partials published
+
+  if (c == 0) {
+    for (int k = tid; k < SK; k += NT) {
+      double num = 0.0, den = 0.0;
+      for (int q = 0; q < CS; ++q) {
+        num += dsmem_ld_f64(dsmem_map(smem_u32addr(exmub + 2 * k), (uint32_t)q));
+        den += dsmem_ld_f64(dsmem_map(smem_u32addr(exmub + 2 * k + 1), (uint32_t)q));
+      }
+      Bg[k] = fmax(Bs[k] * (Real)sqrt(num / den), floor_abs);
+    }
+    for (int row = tid; row < R; row += NT) {
+      double s = 0.0;
+      for (int q = 0; q < CS; ++q) s += dsmem_ld_f64(dsmem_map(smem_u32addr(ex + 4 + row), (uint32_t)q));
+      p.rowpow[tile * R + row] = s;
+    }
+    if (tid == 0) p.logdet[tile] = logdet + log(dprod);
+  }
+  const R2* Wf = Wsl + (size_t)(R & 1) * R * DC;
+  for (int e = tid; e < R * DC; e += NT) {
+    const int q = e % R, i = e / R, col = c * DC + i;
+    if (col < R) Wg[(size_t)col * R + q] = Wf[e];
+  }
+  cluster_sync_all();  // CTA 0's remote reads done before any CTA exits
+}
+
+}  // namespace ctf

@@ -10,6 +10,7 @@
 #include "ctf_stream.cuh"
 #include "ctf_cluster.cuh"
 #include "ctf_gram.cuh"
+#include "ctf_fsplit.cuh"
 
 #include <vector>
 
@@ -25,6 +26,8 @@ struct SweepVariant {
   int chk = 0;  // kind 0 compiled with the CheckOptions instrumentation
   void (*gfn)(SweepParams, const int4*) = nullptr;  // kind 4: gram_kernel (rreg = M, lt = L)
   int ip = 0;  // kind 4 compiled with the IP rule instead of the ISS steps
+  int cs = 0;   // kind 5: CTAs per cluster (frame split)
+  size_t (*fbytes)(int) = nullptr;  // kind 5: dynamic shared memory for SK bases
 };
 #define CTF_V(REAL, PREC, RMAX, FT, RREG, NT, EX) \
   SweepVariant { PREC, RMAX, FT, RREG, NT, EX, sweep_kernel<REAL, RMAX, FT, RREG, NT, EX> }
@@ -61,6 +64,12 @@ struct SweepVariant {
 #define CTF_GRI(REAL, PREC, M, L, NT, FT)                                                                   \
   SweepVariant {                                                                                            \
     PREC, (M) * (L), FT, M, NT, 1, nullptr, 4, L, nullptr, nullptr, 0, gram_kernel<REAL, M, L, NT, FT, true>, 1 \
+  }
+// fsplit_kernel: R = M * L stacked rows, frames split over a cluster of CS CTAs
+#define CTF_FS(REAL, PREC, R, L, FT, NT, CS, RREG, RG, MINB)                                               \
+  SweepVariant {                                                                                         \
+    PREC, R, FT, RREG, NT, 1, fsplit_kernel<REAL, R, L, FT, NT, CS, RREG, RG, MINB>, 5, L, nullptr, nullptr, 0, \
+        nullptr, 0, CS, &FsplitLayout<REAL, R, L, FT, NT, CS, RREG, RG>::bytes                             \
   }
 // rowwarp_kernel: R = NT / (32 * WPR) rows, FT frames per lane
 #define CTF_RW(REAL, PREC, FT, WPR, NT) \
