@@ -158,15 +158,16 @@ def peak_probe(device):
     return lib.ctf_peak_fp32_tflops(device), lib.ctf_peak_fp64_tflops(device)
 
 
-def profile_traffic(kernel, prec):
+def profile_traffic(kernel, prec, cfgn):
     """dram read+write bytes per TF-bin of the dominant kernel from the
-    committed ncu --set full capture (profiles/sweep_traffic.json, keyed
-    "<kernel>/<dtype>"), scaled per launch by the caller."""
+    committed ncu --set full capture of that kernel on that BASELINE config
+    (profiles/sweep_traffic.json, keyed "<kernel>/<dtype>/cfg<n>"), scaled
+    per launch by the caller; None when no capture of this config exists."""
     path = os.path.join(ROOT, "profiles", "sweep_traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        v = d.get(f"{kernel}/{prec}")
+        v = d.get(f"{kernel}/{prec}/cfg{cfgn}")
         return v.get("bytes_per_tfbin") if isinstance(v, dict) else v
     except (OSError, ValueError):
         return None
@@ -334,7 +335,7 @@ def main():
     local_bins = s.bin_range[1] - s.bin_range[0]
     units_per_launch = B * local_bins * T
     achieved = fl_sweep * units_per_launch / (sweep_ms / 1e3) / 1e12
-    traffic_per_tfbin = profile_traffic(desc["sweep_kernel"].split("<")[0], prec)
+    traffic_per_tfbin = profile_traffic(desc["sweep_kernel"].split("<")[0], prec, args.cfg)
     mp = measured_peaks()
     hbm_peak = mp.get("hbm_gbs", 6650.0)
     c = 8 if prec == "f32" else 16
