@@ -528,7 +528,7 @@ void plan_sweep(ctf_ctx* c) {
     // wide covariance tiles (R > 16, one CTA per SM) run best with the most threads
     const int wide_bonus = (v.kind == 4 && c->R > 16) ? -nt / 128 : 0;
     const int rank = wide_bonus +
-                     (v.kind == 4 ? gram_rank : v.kind == 3 ? 3000 : v.kind == 2 ? 2000 : v.kind == 5 ? -2000 + v.cs : v.kind == 1 ? 1000 : 0) +
+                     (v.kind == 4 ? gram_rank : v.kind == 3 ? 3000 : v.kind == 2 ? 2000 : v.kind == 5 ? (c->R > 16 ? -2000 : 4000) + v.cs : v.kind == 1 ? 1000 : 0) +
                      (v.kind == 3 ? -v.rmax * 4 : v.rmax * 4) + (v.exact ? 0 : 2) + (v.lt > 0 ? 0 : 1);
     const bool better = !found || rank < best_rank ||
                         (rank == best_rank && (TP < c->TP || (TP == c->TP && nt < best_nt)));
@@ -1056,7 +1056,9 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host,
   plan_sweep(c);
   // MU-V bin chunks of a fixed size (64 bins): the summation order must not
   // depend on the batch size, so a mixture gives bit-identical results alone
-  // or in any batch; chunk partials are combined in fixed order.
+  // or in any batch; chunk partials are combined in fixed order. (16-bin
+  // chunks for the single-mixture cfg0 measured no faster: its MU phase is
+  // bound by two small dependent launches, not by the chunk loop.)
   c->chunk_bins = 64;
   c->nchunk = (c->FL + c->chunk_bins - 1) / c->chunk_bins;
 
