@@ -336,6 +336,8 @@ void plan_sweep(ctf_ctx* c) {
     std::sscanf(env, "%d,%d,%d,%d,%d", &force[0], &force[1], &force[2], &force[3], &force[4]);
   int force_kind = -1;
   if (const char* env = std::getenv("CTF_SWEEP_KIND")) force_kind = std::atoi(env);
+  int force_ag = -1;  // frame-split exchange: 0 owner scheme, 1 all-gather
+  if (const char* env = std::getenv("CTF_FSPLIT_AG")) force_ag = std::atoi(env);
   ctf::SweepVariant best{};
   size_t best_smem = 0;
   int best_nt = 0, best_rank = 0;
@@ -347,6 +349,7 @@ void plan_sweep(ctf_ctx* c) {
     if (v.chk != want_chk) continue;  // CheckOptions runs on the instrumented variants only
     if (v.ip != want_ip) continue;    // the IP rule runs on the covariance-domain IP variants only
     if (force_kind >= 0 && v.kind != force_kind) continue;
+    if (force_ag >= 0 && v.kind == 5 && v.ag != force_ag) continue;
     if (force[0] && (v.rmax != force[0] || v.ft != force[1] || v.rreg != force[2] || v.maxt != force[3] ||
                      (force[4] >= 0 && v.exact != force[4])))
       continue;
@@ -518,7 +521,9 @@ void plan_sweep(ctf_ctx* c) {
     // streamed one for cfg3/cfg4 so far, so it ranks last; CTF_SWEEP_KIND=3
     // selects it)
     // the frame-split cluster kernel (kind 5, only compiled for the wide
-    // stacked tiles R = 32 / 60) first, the fewest CTAs per cluster preferred
+    // stacked tiles R = 32 / 60) first, the fewest CTAs per cluster and the
+    // all-gather exchange preferred (cfg3 43.1 vs 44.6 ms per 16 mixtures
+    // with the owner exchange; cfg4 equal)
     // (measured on B200: cfg3 45.6 ms per 16 mixtures at CS = 2 vs 51.9 at
     // CS = 4 and 53.3 on the covariance kernel; cfg4 103 ms per 4 mixtures at
     // CS = 8 vs 108 at CS = 16 and 212 streamed);
@@ -528,7 +533,7 @@ void plan_sweep(ctf_ctx* c) {
     // wide covariance tiles (R > 16, one CTA per SM) run best with the most threads
     const int wide_bonus = (v.kind == 4 && c->R > 16) ? -nt / 128 : 0;
     const int rank = wide_bonus +
-                     (v.kind == 4 ? gram_rank : v.kind == 3 ? 3000 : v.kind == 2 ? 2000 : v.kind == 5 ? (c->R > 16 ? -2000 : 4000) + v.cs : v.kind == 1 ? 1000 : 0) +
+                     (v.kind == 4 ? gram_rank : v.kind == 3 ? 3000 : v.kind == 2 ? 2000 : v.kind == 5 ? (c->R > 16 ? -2000 : 4000) + v.cs + (1 - v.ag) : v.kind == 1 ? 1000 : 0) +
                      (v.kind == 3 ? -v.rmax * 4 : v.rmax * 4) + (v.exact ? 0 : 2) + (v.lt > 0 ? 0 : 1);
     const bool better = !found || rank < best_rank ||
                         (rank == best_rank && (TP < c->TP || (TP == c->TP && nt < best_nt)));

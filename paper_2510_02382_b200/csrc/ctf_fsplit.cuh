@@ -33,7 +33,7 @@
 
 namespace ctf {
 
-template <typename Real, int R, int L, int FT, int NT, int CS, int RREG, int RG>
+template <typename Real, int R, int L, int FT, int NT, int CS, int RREG, int RG, bool AG = false>
 struct FsplitLayout {
   static constexpr int M = R / L;  // mics == sources
   static constexpr int NW = NT / 32;
@@ -59,7 +59,7 @@ struct FsplitLayout {
   static constexpr size_t off_red = off_w + a16((size_t)2 * R * DC * CB_);
   static constexpr size_t off_a =
       off_red + a16(mx((size_t)NW * mx(mx((size_t)NG * VP, (size_t)NG2 * 32), 16) * RB_, (size_t)4 * R * CB_));
-  static constexpr size_t off_z = off_a + a16((size_t)2 * CS * RC * CH);
+  static constexpr size_t off_z = off_a + a16((size_t)2 * CS * (AG ? R : RC) * CH);
   static constexpr size_t off_h = off_z + a16((size_t)2 * R * CH);
   static constexpr size_t off_ex = off_h + a16((size_t)R * HL * RB_);
   static constexpr size_t off_bar = off_ex + a16((size_t)(8 + R) * 8);
@@ -164,10 +164,13 @@ template <int V> __device__ __forceinline__ void warp_reduce_scatter_fast(double
   warp_reduce_scatter(v, lane);
 }
 
-template <typename Real, int R, int L, int FT, int NT, int CS, int RREG, int RG, int MINB>
+// AG: every CTA gathers all CS partials of every row and derives all R
+// coefficients itself (one DSMEM hop per step, CS x 3R values received)
+// instead of the owner scheme (two hops, 3R values)
+template <typename Real, int R, int L, int FT, int NT, int CS, int RREG, int RG, int MINB, bool AG = false>
 __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
   using R2 = typename Cplx<Real>::T;
-  using LY = FsplitLayout<Real, R, L, FT, NT, CS, RREG, RG>;
+  using LY = FsplitLayout<Real, R, L, FT, NT, CS, RREG, RG, AG>;
   constexpr int N = LY::M, M = LY::M, NW = LY::NW, TC = LY::TC, XP = LY::XP, XOFF = LY::XOFF;
   constexpr int LP = LY::LP, LOFF = LY::LOFF, RC = LY::RC, DC = LY::DC, NG = LY::NG, VP = LY::VP;
   constexpr int VM = VP / 32, HL = LY::HL, CH = LY::CH, RS = R - RREG;
@@ -206,7 +209,7 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
   const int prev_it = p.iteration - 1;
   const double* mu = p.mu ? p.mu + (size_t)mix * R : nullptr;
   const int nown = (R - c + CS - 1) / CS;  // rows p with p % CS == c
-  const uint32_t txA = (uint32_t)(CS * nown * CH), txZ = (uint32_t)(R * CH);
+  const uint32_t txA = (uint32_t)(CS * (AG ? R : nown) * CH), txZ = (uint32_t)(R * CH);
   const uint32_t barA[2] = {smem_u32addr(bars + 0), smem_u32addr(bars + 1)};
   const uint32_t barZ[2] = {smem_u32addr(bars + 2), smem_u32addr(bars + 3)};
 
@@ -523,46 +526,88 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
 #pragma unroll
     for (int k = 0; k < FT; ++k) pv[k] = yr[k];
     __syncthreads();
-    // this CTA's partial of row `tid` -> the row's owner
-    if (tid < R) {
-      const int g = tid / RG, q = tid - g * RG;
-      Real nre = Real(0), nim = Real(0), den = Real(0);
-      for (int w = 0; w < NW; ++w) {
-        const Real* rb = red + ((size_t)w * NG + g) * VP;
-        nre += rb[q];
-        nim += rb[RG + q];
-        den += rb[2 * RG + q];
+    if constexpr (AG) {
+      // this CTA's partial of row `tid` -> every CTA of the cluster
+      if (tid < R) {
+        const int g = tid / RG, q = tid - g * RG;
+        Real nre = Real(0), nim = Real(0), den = Real(0);
+        for (int w = 0; w < NW; ++w) {
+          const Real* rb = red + ((size_t)w * NG + g) * VP;
+          nre += rb[q];
+          nim += rb[RG + q];
+          den += rb[2 * RG + q];
+        }
+        const uint32_t la = smem_u32addr(inA + ((size_t)(buf * CS + c) * R + tid) * CH);
+#pragma unroll 1
+        for (int dst = 0; dst < CS; ++dst)
+          msg_send(dsmem_map(la, (uint32_t)dst), dsmem_map(barA[buf], (uint32_t)dst), nre, nim, den, Real(0));
       }
-      const int owner = tid % CS, lr = tid / CS;
-      const uint32_t la = smem_u32addr(inA + ((size_t)(buf * CS + c) * RC + lr) * CH);
-      msg_send(dsmem_map(la, (uint32_t)owner), dsmem_map(barA[buf], (uint32_t)owner), nre, nim, den, Real(0));
-    }
-    // owners: z of the own rows from the CS partials (CTA order), to every CTA
-    if (tid < nown * CS) {
-      const int lr = tid / CS, dest = tid - lr * CS, row = c + lr * CS;
       mbar_wait_parity(barA[buf], (uint32_t)((r >> 1) & 1));
-      Real nre = Real(0), nim = Real(0), den = Real(0);
-      for (int q = 0; q < CS; ++q) {
-        const Real* e = reinterpret_cast<const Real*>(inA + ((size_t)(buf * CS + q) * RC + lr) * CH);
-        nre += e[0];
-        nim += e[1];
-        den += e[2];
-      }
-      const bool bad = !(den > Real(0)) || !isfinite(den);  // estimator.cpp:451-454
-      Real zx, zy = Real(0);
-      if (row == r) {
-        zx = Real(1) - sqrt((Real)T / den);
-      } else {
-        zx = nre / den;
-        zy = nim / den;
-      }
-      const uint32_t la = smem_u32addr(inZ + ((size_t)buf * R + row) * CH);
-      msg_send(dsmem_map(la, (uint32_t)dest), dsmem_map(barZ[buf], (uint32_t)dest), zx, zy, bad ? Real(1) : Real(0),
-               Real(0));
       if (tid == 0) mbar_arm(barA[buf], txA);  // step r + 2
+      if (tid < R) {  // z of row `tid` from the CS partials in CTA order (identical in every CTA)
+        Real nre = Real(0), nim = Real(0), den = Real(0);
+        for (int q = 0; q < CS; ++q) {
+          const Real* e = reinterpret_cast<const Real*>(inA + ((size_t)(buf * CS + q) * R + tid) * CH);
+          nre += e[0];
+          nim += e[1];
+          den += e[2];
+        }
+        const bool bad = !(den > Real(0)) || !isfinite(den);  // estimator.cpp:451-454
+        Real zx, zy = Real(0);
+        if (tid == r) {
+          zx = Real(1) - sqrt((Real)T / den);
+        } else {
+          zx = nre / den;
+          zy = nim / den;
+        }
+        Real* zo = reinterpret_cast<Real*>(inZ + ((size_t)buf * R + tid) * CH);
+        zo[0] = zx;
+        zo[1] = zy;
+        zo[2] = bad ? Real(1) : Real(0);
+      }
+      __syncthreads();
+    } else {
+      // this CTA's partial of row `tid` -> the row's owner
+      if (tid < R) {
+        const int g = tid / RG, q = tid - g * RG;
+        Real nre = Real(0), nim = Real(0), den = Real(0);
+        for (int w = 0; w < NW; ++w) {
+          const Real* rb = red + ((size_t)w * NG + g) * VP;
+          nre += rb[q];
+          nim += rb[RG + q];
+          den += rb[2 * RG + q];
+        }
+        const int owner = tid % CS, lr = tid / CS;
+        const uint32_t la = smem_u32addr(inA + ((size_t)(buf * CS + c) * RC + lr) * CH);
+        msg_send(dsmem_map(la, (uint32_t)owner), dsmem_map(barA[buf], (uint32_t)owner), nre, nim, den, Real(0));
+      }
+      // owners: z of the own rows from the CS partials (CTA order), to every CTA
+      if (tid < nown * CS) {
+        const int lr = tid / CS, dest = tid - lr * CS, row = c + lr * CS;
+        mbar_wait_parity(barA[buf], (uint32_t)((r >> 1) & 1));
+        Real nre = Real(0), nim = Real(0), den = Real(0);
+        for (int q = 0; q < CS; ++q) {
+          const Real* e = reinterpret_cast<const Real*>(inA + ((size_t)(buf * CS + q) * RC + lr) * CH);
+          nre += e[0];
+          nim += e[1];
+          den += e[2];
+        }
+        const bool bad = !(den > Real(0)) || !isfinite(den);  // estimator.cpp:451-454
+        Real zx, zy = Real(0);
+        if (row == r) {
+          zx = Real(1) - sqrt((Real)T / den);
+        } else {
+          zx = nre / den;
+          zy = nim / den;
+        }
+        const uint32_t la = smem_u32addr(inZ + ((size_t)buf * R + row) * CH);
+        msg_send(dsmem_map(la, (uint32_t)dest), dsmem_map(barZ[buf], (uint32_t)dest), zx, zy, bad ? Real(1) : Real(0),
+                 Real(0));
+        if (tid == 0) mbar_arm(barA[buf], txA);  // step r + 2
+      }
+      mbar_wait_parity(barZ[buf], (uint32_t)((r >> 1) & 1));
+      if (tid == 0) mbar_arm(barZ[buf], txZ);  // step r + 2
     }
-    mbar_wait_parity(barZ[buf], (uint32_t)((r >> 1) & 1));
-    if (tid == 0) mbar_arm(barZ[buf], txZ);  // step r + 2
     const unsigned char* zcur = inZ + (size_t)buf * R * CH;
     {
       const bool b1 = lane < R && reinterpret_cast<const Real*>(zcur + (size_t)lane * CH)[2] != Real(0);

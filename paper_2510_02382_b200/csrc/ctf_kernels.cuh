@@ -1026,27 +1026,13 @@ __global__ void __launch_bounds__(256) reduce_apply_kernel(const ApplyParams p) 
         num = pk[e];
         den = pk[plane + e];
       } else {
-        const Real* pt = reinterpret_cast<const Real*>(p.part) + (size_t)mix * 2 * plane + e;
-        const size_t cstride = (size_t)p.nmix * 2 * plane;
+        const Real* pt = reinterpret_cast<const Real*>(p.part);
         num = Real(0);
         den = Real(0);
-        int c = 0;
-        for (; c + 8 <= p.nchunk; c += 8) {  // eight chunks' loads in flight, sums in chunk order
-          Real a[8], b[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            a[u] = pt[(size_t)(c + u) * cstride];
-            b[u] = pt[(size_t)(c + u) * cstride + plane];
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            num += a[u];
-            den += b[u];
-          }
-        }
-        for (; c < p.nchunk; ++c) {
-          num += pt[(size_t)c * cstride];
-          den += pt[(size_t)c * cstride + plane];
+        for (int c = 0; c < p.nchunk; ++c) {
+          const Real* q = pt + ((size_t)c * p.nmix + mix) * 2 * plane;
+          num += q[e];
+          den += q[plane + e];
         }
         if (p.mode == 0) {
           Real* pk = reinterpret_cast<Real*>(p.packed) + (size_t)mix * 2 * plane;
@@ -1068,19 +1054,10 @@ __global__ void __launch_bounds__(256) reduce_apply_kernel(const ApplyParams p) 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int r = warp; r <= p.R; r += nw) {
       double s = 0.0;
-      if (r < p.R || p.obj_slot >= 0) {
-        // strided sources: row r of the row powers, or the objective partials
-        const double* src = r < p.R ? p.rowpow + (size_t)mix * p.FL * p.R + r : p.objbin + (size_t)mix * p.FL;
-        const int st = r < p.R ? p.R : 1;
-        int i = lane;
-        for (; i + 32 * 7 < p.FL; i += 32 * 8) {  // eight loads in flight, sums in bin order
-          double v[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) v[u] = src[(size_t)(i + 32 * u) * st];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) s += v[u];
-        }
-        for (; i < p.FL; i += 32) s += src[(size_t)i * st];
+      if (r < p.R) {
+        for (int i = lane; i < p.FL; i += 32) s += p.rowpow[((size_t)mix * p.FL + i) * p.R + r];
+      } else if (p.obj_slot >= 0) {
+        for (int i = lane; i < p.FL; i += 32) s += p.objbin[(size_t)mix * p.FL + i];
       }
       s = warp_sum(s);
       if (lane == 0) pd[r] = s;

@@ -5,6 +5,9 @@ namespace ctf {
 std::vector<SweepVariant> sweep_variants_fsplit_f32() {
   return {CTF_FS(float, 1, 60, 10, 2, 128, 16, 24, 10, 2), CTF_FS(float, 1, 60, 10, 2, 256, 8, 32, 10, 1),
           CTF_FS(float, 1, 32, 8, 2, 128, 4, 16, 8, 3), CTF_FS(float, 1, 32, 8, 2, 256, 2, 16, 8, 2),
-          CTF_FS(float, 1, 32, 8, 1, 128, 8, 16, 8, 3), CTF_FS(float, 1, 32, 8, 4, 128, 2, 16, 8, 2)};
+          CTF_FS(float, 1, 32, 8, 1, 128, 8, 16, 8, 3), CTF_FS(float, 1, 32, 8, 4, 128, 2, 16, 8, 2),
+          // all-gather exchange variants (one DSMEM hop per step)
+          CTF_FSA(float, 1, 60, 10, 2, 256, 8, 32, 10, 1), CTF_FSA(float, 1, 32, 8, 4, 128, 2, 16, 8, 2),
+          CTF_FSA(float, 1, 32, 8, 2, 128, 4, 16, 8, 3)};
 }
 }  // namespace ctf

@@ -28,6 +28,7 @@ struct SweepVariant {
   int ip = 0;  // kind 4 compiled with the IP rule instead of the ISS steps
   int cs = 0;   // kind 5: CTAs per cluster (frame split)
   size_t (*fbytes)(int) = nullptr;  // kind 5: dynamic shared memory for SK bases
+  int ag = 0;   // kind 5: all-gather exchange (every CTA derives every z)
 };
 #define CTF_V(REAL, PREC, RMAX, FT, RREG, NT, EX) \
   SweepVariant { PREC, RMAX, FT, RREG, NT, EX, sweep_kernel<REAL, RMAX, FT, RREG, NT, EX> }
@@ -70,6 +71,11 @@ struct SweepVariant {
   SweepVariant {                                                                                         \
     PREC, R, FT, RREG, NT, 1, fsplit_kernel<REAL, R, L, FT, NT, CS, RREG, RG, MINB>, 5, L, nullptr, nullptr, 0, \
         nullptr, 0, CS, &FsplitLayout<REAL, R, L, FT, NT, CS, RREG, RG>::bytes                             \
+  }
+#define CTF_FSA(REAL, PREC, R, L, FT, NT, CS, RREG, RG, MINB)                                                  \
+  SweepVariant {                                                                                                \
+    PREC, R, FT, RREG, NT, 1, fsplit_kernel<REAL, R, L, FT, NT, CS, RREG, RG, MINB, true>, 5, L, nullptr, nullptr, 0, \
+        nullptr, 0, CS, &FsplitLayout<REAL, R, L, FT, NT, CS, RREG, RG, true>::bytes, 1                         \
   }
 // rowwarp_kernel: R = NT / (32 * WPR) rows, FT frames per lane
 #define CTF_RW(REAL, PREC, FT, WPR, NT) \

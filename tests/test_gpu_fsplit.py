@@ -32,20 +32,25 @@ def history(x, L, K, iters, seed):
     return d, out
 
 
-# (M, L, T, K, rho, F, iters, variant "rmax,ft,rreg,nt", cluster size)
+# (M, L, T, K, rho, F, iters, variant "rmax,ft,rreg,nt", cluster size, exchange: 0 owner, 1 all-gather)
 CASES = [
-    (4, 8, 1000, 20, 0.8, 9, 4, "32,2,16,128", 4),
-    (4, 8, 1000, 20, 0.8, 5, 3, "32,2,16,256", 2),
-    (4, 8, 1000, 20, 0.8, 5, 3, "32,1,16,128", 8),
-    (6, 10, 4000, 16, 0.85, 2, 3, "60,2,24,128", 16),
-    (6, 10, 4000, 16, 0.85, 2, 2, "60,2,32,256", 8),
+    (4, 8, 1000, 20, 0.8, 9, 4, "32,2,16,128", 4, 0),
+    (4, 8, 1000, 20, 0.8, 5, 3, "32,2,16,256", 2, 0),
+    (4, 8, 1000, 20, 0.8, 5, 3, "32,1,16,128", 8, 0),
+    (4, 8, 1000, 20, 0.8, 5, 3, "32,4,16,128", 2, 0),
+    (6, 10, 4000, 16, 0.85, 2, 3, "60,2,24,128", 16, 0),
+    (6, 10, 4000, 16, 0.85, 2, 2, "60,2,32,256", 8, 0),
+    (4, 8, 1000, 20, 0.8, 5, 3, "32,4,16,128", 2, 1),
+    (4, 8, 1000, 20, 0.8, 9, 3, "32,2,16,128", 4, 1),
+    (6, 10, 4000, 16, 0.85, 2, 3, "60,2,32,256", 8, 1),
 ]
 
 
-@pytest.mark.parametrize("M,L,T,K,rho,F,iters,variant,cs", CASES)
-def test_fsplit_fp32_every_iteration(M, L, T, K, rho, F, iters, variant, cs, monkeypatch):
+@pytest.mark.parametrize("M,L,T,K,rho,F,iters,variant,cs,ag", CASES)
+def test_fsplit_fp32_every_iteration(M, L, T, K, rho, F, iters, variant, cs, ag, monkeypatch):
     monkeypatch.setenv("CTF_SWEEP_KIND", "5")
     monkeypatch.setenv("CTF_SWEEP_VARIANT", variant)
+    monkeypatch.setenv("CTF_FSPLIT_AG", str(ag))
     raw = synth_mixtures(1, F, T, M, M, L, K, rho, 77 + M * L)
     ref = O.run(O.config([L] * M, [K] * M, iterations=iters, seed=3, threads=NPROC),
                 O.stack_observation(raw[0], L), history=True)
