@@ -919,46 +919,56 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
       const Real* En = Pq + (size_t)(n - g0) * L * TP;
       const int k0 = p.koff[n], k1 = p.koff[n + 1];
       const Real* il = invl + n * p.lp + p.loff;
-      for (int kb = k0; kb < k1; kb += 16) {
-        Real a[32];
+      // KW bases per pass: 10 when the source's K is a multiple of 10 (the
+      // BASELINE K = 10 / 20: no idle lanes), else 16; numerators at [0, KW),
+      // denominators at [16, 16 + KW) of the 32 reduced values
+      auto mub = [&](auto kw) {
+        constexpr int KW = decltype(kw)::value;
+        for (int kb = k0; kb < k1; kb += KW) {
+          Real a[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) a[i] = Real(0);
-        const Real* vrow[16];
+          for (int i = 0; i < 32; ++i) a[i] = Real(0);
+          const Real* vrow[KW];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) vrow[q] = Vg + (size_t)min(kb + q, k1 - 1) * T + tid;
+          for (int q = 0; q < KW; ++q) vrow[q] = Vg + (size_t)min(kb + q, k1 - 1) * T + tid;
 #pragma unroll
-        for (int k = 0; k < FT; ++k) {
-          const int tau = tid + k * NT;
-          const Real ilv = il[tau];
-          const Real an = En[tau] * (ilv * ilv);
-          const Real bn = (tau < T) ? ilv * (Real)min(L, T - tau) : Real(0);
+          for (int k = 0; k < FT; ++k) {
+            const int tau = tid + k * NT;
+            const Real ilv = il[tau];
+            const Real an = En[tau] * (ilv * ilv);
+            const Real bn = (tau < T) ? ilv * (Real)min(L, T - tau) : Real(0);
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const Real vv = __ldg(vrow[q] + k * NT);
-            if constexpr (F32) {
-              const float2 t = ffma2s(make_float2(an, bn), vv, make_float2(a[q], a[16 + q]));
-              a[q] = t.x;
-              a[16 + q] = t.y;
-            } else {
-              a[q] = fma(an, vv, a[q]);
-              a[16 + q] = fma(bn, vv, a[16 + q]);
+            for (int q = 0; q < KW; ++q) {
+              const Real vv = __ldg(vrow[q] + k * NT);
+              if constexpr (F32) {
+                const float2 t = ffma2s(make_float2(an, bn), vv, make_float2(a[q], a[16 + q]));
+                a[q] = t.x;
+                a[16 + q] = t.y;
+              } else {
+                a[q] = fma(an, vv, a[q]);
+                a[16 + q] = fma(bn, vv, a[16 + q]);
+              }
             }
           }
-        }
-        warp_reduce_scatter(a, lane);
-        __syncthreads();  // previous pass's reads of red are done
-        red[warp * 32 + lane] = a[0];
-        __syncthreads();
-        if (tid < 16 && kb + tid < k1) {
-          Real num = Real(0), den = Real(0);
-          for (int w = 0; w < NW; ++w) {
-            num += red[w * 32 + tid];
-            den += red[w * 32 + 16 + tid];
+          warp_reduce_scatter(a, lane);
+          __syncthreads();  // previous pass's reads of red are done
+          red[warp * 32 + lane] = a[0];
+          __syncthreads();
+          if (tid < KW && kb + tid < k1) {
+            Real num = Real(0), den = Real(0);
+            for (int w = 0; w < NW; ++w) {
+              num += red[w * 32 + tid];
+              den += red[w * 32 + 16 + tid];
+            }
+            const Real b = Bs[kb + tid];
+            Bg[kb + tid] = fmax(b * sqrt(num / den), floor_abs);
           }
-          const Real b = Bs[kb + tid];
-          Bg[kb + tid] = fmax(b * sqrt(num / den), floor_abs);
         }
-      }
+      };
+      if ((k1 - k0) % 10 == 0)
+        mub(std::integral_constant<int, 10>{});
+      else
+        mub(std::integral_constant<int, 16>{});
     }
     __syncthreads();  // Pq is rewritten by the next group
   }
