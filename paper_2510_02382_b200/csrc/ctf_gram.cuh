@@ -899,6 +899,7 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
       }
     }
     __syncthreads();  // Pq of the group complete
+    CTF_PHASE(7);
 #pragma unroll
     for (int n = g0; n < g0 + NSD; ++n) {
       Real* pq = Pq + (size_t)(n - g0) * L * TP;
@@ -972,7 +973,7 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
     }
     __syncthreads();  // Pq is rewritten by the next group
   }
-  CTF_PHASE(7);
+  CTF_PHASE(8);
   // check_all_finite on Y (estimator.cpp:497-499): a non-finite estimate
   // makes its row's power sum non-finite
   bool ybad = false;

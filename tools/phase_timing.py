@@ -19,7 +19,7 @@ lib = _lib.load()
 buf = (C.c_ulonglong * (4096 * 12))()
 assert lib.ctf_debug_gram_phases(buf) == 0
 a = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 12).astype(np.int64)
-names = ["prologue", "lambda", "gram", "reduce", "objective", "steps", "demix", "energies", "mu_b"]
+names = ["prologue", "lambda", "gram", "reduce", "objective", "steps", "demix", "energies+mu_b", "tail"]
 d = np.diff(a[:, :10], axis=1)
 tot = a[:, 9] - a[:, 0]
 print("CTA cycles: mean %.0f median %.0f" % (tot.mean(), np.median(tot)))
