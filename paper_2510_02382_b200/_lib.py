@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libctfiss.so")
+LIB_PATH = os.environ.get("CTF_DEV_LIB") or os.path.join(_HERE, "libctfiss.so")  # CTF_DEV_LIB: tools/dev_build.sh builds
 
 CTF_MAX_SOURCES = 16
 CTF_OK, CTF_ERR_CONFIG, CTF_ERR_IO, CTF_ERR_DEGENERACY, CTF_ERR_CUDA, CTF_ERR_UNSUPPORTED = 0, 2, 3, 4, 5, 6

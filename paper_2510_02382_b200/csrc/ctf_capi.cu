@@ -262,8 +262,47 @@ void validate(const ctf_problem& p) {
 // (m < m' all lags, m == m' lags d >= 0), each with 2L-1-|d| weight lags;
 // threads are shared out in proportion to that count and every group's frame
 // range [U0, U1) is split into contiguous chunks of whole register blocks.
+// Dev knob for the Gram task layout (measurement only): CTF_GRAM_TUNE =
+// "xpk|rot_0,rot_1,...|cadd_0,...|order_0,..." (x-row padding, per-group chunk
+// rotation, chunk-length increments, group permutation after the sort).
+struct GramTune {
+  int xpk = 0;
+  std::vector<int> rot, cadd, order;
+};
+static GramTune gram_tune() {
+  GramTune t;
+  const char* e = std::getenv("CTF_GRAM_TUNE");
+  if (!e) return t;
+  std::string s(e);
+  std::vector<std::string> parts;
+  size_t a = 0;
+  for (;;) {
+    const size_t b = s.find('|', a);
+    parts.push_back(s.substr(a, b == std::string::npos ? std::string::npos : b - a));
+    if (b == std::string::npos) break;
+    a = b + 1;
+  }
+  auto ints = [](const std::string& q) {
+    std::vector<int> v;
+    size_t i = 0;
+    while (i < q.size()) {
+      const size_t j = q.find(',', i);
+      v.push_back(std::atoi(q.substr(i, j == std::string::npos ? std::string::npos : j - i).c_str()));
+      if (j == std::string::npos) break;
+      i = j + 1;
+    }
+    return v;
+  };
+  if (parts.size() > 0) t.xpk = std::atoi(parts[0].c_str());
+  if (parts.size() > 1) t.rot = ints(parts[1]);
+  if (parts.size() > 2) t.cadd = ints(parts[2]);
+  if (parts.size() > 3) t.order = ints(parts[3]);
+  return t;
+}
+
 void build_gram_table(ctf_ctx* c, int NT, int M, int L) {
   struct Grp { int m, m2, d, alo, cnt; };
+  const GramTune tune = gram_tune();
   std::vector<Grp> gs;
   for (int m = 0; m < M; ++m)
     for (int m2 = m; m2 < M; ++m2)
@@ -274,6 +313,11 @@ void build_gram_table(ctf_ctx* c, int NT, int M, int L) {
   // sorted by lag count (descending): a warp spans at most two adjacent counts
   std::stable_sort(gs.begin(), gs.end(), [](const Grp& a, const Grp& b) { return a.cnt > b.cnt; });
   const int ng = (int)gs.size();
+  if ((int)tune.order.size() == ng) {
+    std::vector<Grp> g2;
+    for (int i : tune.order) g2.push_back(gs[(size_t)i]);
+    gs = g2;
+  }
   if (ng > NT) throw CtfError(CTF_ERR_UNSUPPORTED, "gram kernel: more lag groups than threads");
   long total = 0;
   for (const auto& g : gs) total += g.cnt;
@@ -301,12 +345,14 @@ void build_gram_table(ctf_ctx* c, int NT, int M, int L) {
   int t = 0;
   for (int g = 0; g < ng; ++g) {
     const int want_n = th[(size_t)g];
-    const int clen = ((len + want_n - 1) / want_n) | 1;
+    const int clen = (((len + want_n - 1) / want_n) | 1) + ((int)tune.cadd.size() == ng ? 2 * tune.cadd[(size_t)g] : 0);
     const int n = (len + clen - 1) / clen;
+    const int rot = (int)tune.rot.size() == ng ? tune.rot[(size_t)g] % n : 0;
     const int t0 = t;
     for (int i = 0; i < want_n; ++i) {
       if (i < n) {
-        tab[(size_t)t] = make_int4(g, U0 + i * clen, U0 + std::min(len, (i + 1) * clen), 0);
+        const int k = (i + rot) % n;  // chunk k of the group (the reduction sums in thread order)
+        tab[(size_t)t] = make_int4(g, U0 + k * clen, U0 + std::min(len, (k + 1) * clen), 0);
       } else {
         tab[(size_t)t] = make_int4(-1, 0, 0, 0);
       }
@@ -398,7 +444,7 @@ void plan_sweep(ctf_ctx* c) {
       const int UB = ctf::kGramUB, NA = 2 * L - 1;
       const int U0 = -(L - 1), U1 = U0 + c->T + 2 * (L - 1) + UB;
       cand.xoff = 2 * L;
-      cand.xp = cand.xoff + std::max(TP, U1) + 2 * L + UB;
+      cand.xp = cand.xoff + std::max(TP, U1) + 2 * L + UB + gram_tune().xpk;
       const int gloff = 2 * L + 2;
       const int glp = gloff + std::max(TP, U1) + 2 * L + UB;
       cand.off_x = (int)take((size_t)M * cand.xp * cs);

@@ -31,6 +31,9 @@
 #include "ctf_cluster.cuh"
 #include "ctf_kernels.cuh"
 
+#ifndef CTF_FS_LAMKB
+#define CTF_FS_LAMKB 20
+#endif
 namespace ctf {
 
 template <typename Real, int R, int L, int FT, int NT, int CS, int RREG, int RG, bool AG = false>
@@ -277,16 +280,16 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
       Real v = Real(0);
       if (tau >= 0 && tau < T) {
         Real lam = Real(0);
-        int kk = k0;
-        for (; kk + 4 <= k1; kk += 4) {  // four loads in flight, same summation order
-          const Real v0 = __ldg(Vg + (size_t)kk * T + tau), v1 = __ldg(Vg + (size_t)(kk + 1) * T + tau);
-          const Real v2 = __ldg(Vg + (size_t)(kk + 2) * T + tau), v3 = __ldg(Vg + (size_t)(kk + 3) * T + tau);
-          lam = fma(Bs[kk], v0, lam);
-          lam = fma(Bs[kk + 1], v1, lam);
-          lam = fma(Bs[kk + 2], v2, lam);
-          lam = fma(Bs[kk + 3], v3, lam);
+        // KB loads in flight (one L2 round trip for K <= KB), same summation order
+        constexpr int KB = CTF_FS_LAMKB;
+        for (int kk = k0; kk < k1; kk += KB) {
+          Real vq[KB];
+#pragma unroll
+          for (int q = 0; q < KB; ++q) vq[q] = (kk + q < k1) ? __ldg(Vg + (size_t)(kk + q) * T + tau) : Real(0);
+#pragma unroll
+          for (int q = 0; q < KB; ++q)
+            if (kk + q < k1) lam = fma(Bs[kk + q], vq[q], lam);
         }
-        for (; kk < k1; ++kk) lam = fma(Bs[kk], __ldg(Vg + (size_t)kk * T + tau), lam);
         lam = fmax(lam, floor_abs);
         v = Real(1) / lam;
         if (p.has_prev && jl >= 0) logsum += (double)min(L, T - tau) * (double)log(lam);

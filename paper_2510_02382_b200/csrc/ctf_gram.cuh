@@ -30,6 +30,12 @@
 #pragma once
 #include "ctf_kernels.cuh"
 
+#ifndef CTF_LAMV
+#define CTF_LAMV 20
+#endif
+#ifndef CTF_LAMV3  // the same for the 3-CTA/SM (80-register) cfg1 variant
+#define CTF_LAMV3 10
+#endif
 namespace ctf {
 
 // Gram task table (host-built, global memory), int4 entries:
@@ -153,6 +159,11 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
   constexpr int NS = gram_ns<Real, N, R>();
   constexpr int LT1 = L > 1 ? L - 1 : 1;
   constexpr int CPB = 16 / (int)sizeof(R2);  // complex values per 16-byte load
+  // V columns of the lambda phase loaded at once (fp32, one CTA per SM)
+  constexpr int LAMV = !F32                                         ? 0
+                       : gram_min_blocks<Real, NT, M * L>() == 1 ? CTF_LAMV
+                       : (M == 2 && L == 5)                       ? CTF_LAMV3  // measured (cfg1); others spill
+                                                                  : 0;
   static_assert(D <= 32, "one lane per stacked channel in the covariance steps");
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -172,7 +183,8 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
   Real* Bs = reinterpret_cast<Real*>(smem + p.off_b);
   double* dred = reinterpret_cast<double*>(smem + p.off_d);
   __shared__ int s_bad, s_badrow;
-  __shared__ double s_logmu, s_dprod;
+  __shared__ double s_logmu;
+  __shared__ Real fac_s[R];  // (1 - z_r) of the ISS steps (determinant lemma)
   constexpr int kNoRow = 1 << 30;
 
   const size_t tile = (size_t)mix * p.FL + bin;
@@ -210,6 +222,27 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
     s_badrow = kNoRow;
     s_logmu = mu ? p.logmu[mix] : 0.0;
   }
+  // W and B of the tile: loads issued before the x tile's (their latency
+  // overlaps; stored to shared memory below)
+  const bool wb1 = R * D <= NT && SK <= NT;
+  R2 wpre;
+  Real bpre = Real(0);
+  wpre.x = wpre.y = Real(0);
+  double mw = 0.0, mb = 0.0;  // pending rescale factors of this thread's W and B entries
+  if (wb1) {
+    if (tid < R * D) {
+      wpre = Wg[tid];
+      if (mu) mw = mu[tid % R];
+    }
+    if (tid < SK) {
+      bpre = Bg[tid];
+      int nb = 0;
+#pragma unroll
+      for (int n = 1; n < N; ++n) nb += tid >= p.koff[n] ? 1 : 0;
+      if (mu) mb = mu[p.row0[nb]];
+    }
+  }
+  const bool lam4 = (T % 4 == 0 && 4 * NT >= T);
   // ---- prologue: zero-padded x tile, W and B with the pending rescale
   if ((T * M) % CPB == 0) {
     // the bin's T x M complex block is contiguous: 16-byte loads, all in
@@ -247,14 +280,45 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
       xs[i] = (t >= 0 && t < T) ? xg[(size_t)t * M + m] : z;
     }
   }
-  for (int i = tid; i < R * D; i += NT) Wb[i] = Wg[i];
-  for (int i = tid; i < SK; i += NT) Bs[i] = Bg[i];
-  __shared__ Real s_imu[R];  // fp32: 1 / mu_r of the pending rescale (1 where none)
-  if (F32 && warp == 0 && lane < R) s_imu[lane] = (mu && mu[lane] != 0.0) ? (Real)(1.0 / mu[lane]) : Real(1);
-  __syncthreads();
   // pending rescale (estimator.cpp:399-411): W rows / mu_r, B_n / mu_row0^2
   // floored; fp64 divides exactly like the reference, fp32 multiplies by
   // the rounded reciprocal
+  if (wb1) {  // one W and one B entry per thread: rescaled in registers
+    if (tid < R * D) {
+      R2 w = wpre;
+      if (mu && mw != 0.0) {
+        if constexpr (F32) {
+          const float im = (float)(1.0 / mw);
+          w.x *= im;
+          w.y *= im;
+        } else {
+          w.x /= mw;
+          w.y /= mw;
+        }
+      }
+      Wb[tid] = w;
+      if (p.has_prev && !cfinite(w)) s_bad = 1;
+    }
+    if (tid < SK) {
+      Real b = bpre;
+      if (mu && mb != 0.0) {  // estimator.cpp:405-406: silent row, no rescale
+        if constexpr (F32) {
+          const float im = (float)(1.0 / mb);
+          b = fmaxf(b * (im * im), floor_abs);
+        } else {
+          b = fmax(b / (mb * mb), (double)floor_abs);
+        }
+      }
+      Bs[tid] = b;
+    }
+  } else {
+    for (int i = tid; i < R * D; i += NT) Wb[i] = Wg[i];
+    for (int i = tid; i < SK; i += NT) Bs[i] = Bg[i];
+  }
+  __shared__ Real s_imu[R];  // fp32: 1 / mu_r of the pending rescale (1 where none)
+  if (!wb1) {
+  if (F32 && warp == 0 && lane < R) s_imu[lane] = (mu && mu[lane] != 0.0) ? (Real)(1.0 / mu[lane]) : Real(1);
+  __syncthreads();
   for (int i = tid; i < R * D; i += NT) {
     R2 w = Wb[i];
     if (mu) {
@@ -285,6 +349,7 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
         }
       }
     }
+  }
   __syncthreads();
   CTF_PHASE(1);
   if (p.has_prev && s_bad) {  // check_all_finite on W (estimator.cpp:494-496)
@@ -293,6 +358,7 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
   }
   // ---- lambda = max(B V, floor) -> 1/lambda (zero outside [0, T)), log term
   double logsum = 0.0;
+  const int t4 = tid * 4;
   for (int n = 0; n < N; ++n) {
     Real* il = invl + n * p.lp;
     for (int i = tid; i < p.lp; i += NT) {
@@ -300,13 +366,31 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
       if (s < 0 || s >= T) il[i] = Real(0);
     }
     const int k0 = p.koff[n], k1 = p.koff[n + 1];
-    if (T % 4 == 0 && 4 * NT >= T) {
+    if (lam4) {
       // four consecutive frames per thread, 16-byte V loads
-      const int t4 = tid * 4;
       if (t4 < T) {
         Real lam[4] = {Real(0), Real(0), Real(0), Real(0)};
+        int kst = k0;
+        if constexpr (LAMV > 0) {
+          // fp32: LAMV of the source's V columns loaded at once (one L2
+          // round trip; the rest, if any, by the loop below)
+          float4 vv[LAMV > 0 ? LAMV : 1];
+#pragma unroll
+          for (int q = 0; q < LAMV; ++q)
+            if (k0 + q < k1) vv[q] = __ldg(reinterpret_cast<const float4*>(Vg + (size_t)(k0 + q) * T + t4));
+#pragma unroll
+          for (int q = 0; q < LAMV; ++q)
+            if (k0 + q < k1) {
+              const float b = Bs[k0 + q];
+              lam[0] = fmaf(b, vv[q].x, lam[0]);
+              lam[1] = fmaf(b, vv[q].y, lam[1]);
+              lam[2] = fmaf(b, vv[q].z, lam[2]);
+              lam[3] = fmaf(b, vv[q].w, lam[3]);
+            }
+          kst = min(k1, k0 + LAMV);
+        }
 #pragma unroll 8
-        for (int kk = k0; kk < k1; ++kk) {
+        for (int kk = kst; kk < k1; ++kk) {
           const Real b = Bs[kk];
           const Real* vr = Vg + (size_t)kk * T + t4;
           if constexpr (F32) {
@@ -772,7 +856,7 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
   } else {
   // ---- R covariance-domain ISS steps (estimator.cpp:556-579, 275-302)
   R2* piv = zs;     // 2 x (D + LT1): pivot W row and tail, double-buffered by step parity
-  Real* fac = red;  // (1 - z_r) per row, multiplied in row order at the end
+  Real* fac = fac_s;  // (1 - z_r) per row, multiplied in row order at the end
   constexpr int PV = D + LT1;
   if (rowk[0] == 0) {
     if (hl < D) piv[hl] = wreg[0];
@@ -792,7 +876,10 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
       const int row = rowk[k];
       if (rowvk[k]) {
         if (!(den > Real(0)) || !isfinite(den)) {  // estimator.cpp:451-454
-          if (hl == 0) atomicMin(&s_badrow, row);
+          // (step, row) key: the first failing step, its lowest row; checked
+          // once after the sweep (the steps after a failure change nothing
+          // that is written out)
+          if (hl == 0) atomicMin(&s_badrow, r * 64 + row);
         } else if (row == r) {
           if constexpr (F32)
             z.x = 1.f - sqrtf((float)T) * rsqrtf(den);
@@ -820,19 +907,14 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
       }
     }
     __syncthreads();
-    if (s_badrow != kNoRow) {
-      if (tid == 0) record_err<Real>(p.err, mix, err_key(p.iteration, kPhSweep, gbin, r, s_badrow));
-      return;
-    }
+  }
+  if (s_badrow != kNoRow) {
+    if (tid == 0) record_err<Real>(p.err, mix, err_key(p.iteration, kPhSweep, gbin, s_badrow >> 6, s_badrow & 63));
+    return;
   }
 #pragma unroll
   for (int k = 0; k < KR; ++k)
     if (rowvk[k] && hl < D) Wb[hl * R + rowk[k]] = wreg[k];
-  if (tid == 0) {
-    double dp = 1.0;
-    for (int r = 0; r < R; ++r) dp *= (double)fac[r];
-    s_dprod = dp;
-  }
   __syncthreads();
   }
   R2* Wf = Wb;  // W' (column-major R x D) for the demix
@@ -996,7 +1078,12 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
     for (int w = 0; w < NW; ++w) s += (double)red[w * 32 + tid];
     p.rowpow[tile * R + tid] = s;
   }
-  if (tid == 0) p.logdet[tile] = IP ? s_iplogdet : logdet + log(s_dprod);
+  if (tid == 0) {
+    double dp = 1.0;  // prod_r (1 - z_r) in row order (determinant lemma)
+    if (!IP)
+      for (int r = 0; r < R; ++r) dp *= (double)fac_s[r];
+    p.logdet[tile] = IP ? s_iplogdet : logdet + log(dp);
+  }
   for (int i = tid; i < R * D; i += NT) Wg[i] = Wf[i];
   CTF_PHASE(9);
 }

@@ -5,11 +5,11 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2510_02382_b200 import _lib
-_lib.LIB_PATH = os.path.join(ROOT, "tools", "phase", "libctfiss.so")
+_lib.LIB_PATH = os.environ.get("CTF_DEV_LIB") or os.path.join(ROOT, "tools", "phase", "libctfiss.so")
 from paper_2510_02382_b200 import Session, synth_mixtures
 import argparse
 ap = argparse.ArgumentParser(); ap.add_argument("--cfg", type=int, default=1); a = ap.parse_args()
-B, F, T, M, N, L, K = {1: (64, 513, 1000, 2, 2, 5, 10), 3: (8, 2049, 1000, 4, 4, 8, 20)}[a.cfg]
+B, F, T, M, N, L, K = {1: (64, 513, 1000, 2, 2, 5, 10), 2: (16, 1025, 2000, 3, 3, 4, 20), 3: (8, 2049, 1000, 4, 4, 8, 20)}[a.cfg]
 x = synth_mixtures(B, F, T, M, N, L, K, 0.6, 1, precision="f32")
 s = Session(x, [L] * N, [K] * N, stack_taps=L, iterations=4, precision="f32")
 print(s.describe())
