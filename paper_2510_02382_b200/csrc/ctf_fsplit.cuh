@@ -229,6 +229,31 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
   // z of "step -1" (zero update in the first pass)
   for (int i = tid; i < R * CH / (int)sizeof(Real); i += NT)
     reinterpret_cast<Real*>(inZ + (size_t)R * CH)[i] = Real(0);
+  // own W columns, B and the pending rescale factors: loads issued before the
+  // x tile's so their latency overlaps (rescaled and stored below)
+  constexpr int WPT = (R * DC + NT - 1) / NT;
+  R2 wv[WPT];
+  double mv[WPT];
+#pragma unroll
+  for (int t = 0; t < WPT; ++t) {
+    const int e = tid + t * NT, q = e % R, col = c * DC + e / R;
+    wv[t] = czero<Real>();
+    mv[t] = 0.0;
+    if (e < R * DC && col < R) {
+      wv[t] = Wg[(size_t)col * R + q];
+      if (mu) mv[t] = mu[q];
+    }
+  }
+  const bool b1 = SK <= NT;
+  Real bv = Real(0);
+  double mbv = 0.0;
+  if (b1 && tid < SK) {
+    bv = Bg[tid];
+    int nb = 0;
+#pragma unroll
+    for (int n = 1; n < N; ++n) nb += tid >= p.koff[n] ? 1 : 0;
+    if (mu) mbv = mu[nb * L];
+  }
   // ---- prologue: x tile with its halo, own W columns and B with the pending rescale
   {
     // all of the thread's loads in flight before the transposing stores
@@ -246,28 +271,36 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
       if (e < XP * M) xs[m * XP + i] = xv[t];
     }
   }
-  for (int e = tid; e < R * DC; e += NT) {
-    const int q = e % R, i = e / R, col = c * DC + i;
-    R2 w = czero<Real>();
-    if (col < R) {
-      w = Wg[(size_t)col * R + q];
-      if (mu) {
-        const double m = mu[q];
-        if (m != 0.0) {
+#pragma unroll
+  for (int t = 0; t < WPT; ++t) {
+    const int e = tid + t * NT, col = c * DC + e / R;
+    if (e < R * DC) {
+      R2 w = wv[t];
+      if (col < R) {
+        const double m = mv[t];
+        if (mu && m != 0.0) {
           w.x = (Real)((double)w.x / m);
           w.y = (Real)((double)w.y / m);
         }
+        if (p.has_prev && !cfinite(w)) s_wbad = 1;
       }
-      if (p.has_prev && !cfinite(w)) s_wbad = 1;
+      Wsl[e] = w;
     }
-    Wsl[e] = w;
   }
-  for (int n = 0; n < N; ++n) {
-    const double m0 = mu ? mu[n * L] : 0.0;
-    for (int i = p.koff[n] + tid; i < p.koff[n + 1]; i += NT) {
-      Real b = Bg[i];
-      if (m0 != 0.0) b = (Real)fmax((double)b / (m0 * m0), (double)floor_abs);
-      Bs[i] = b;
+  if (b1) {
+    if (tid < SK) {
+      Real b = bv;
+      if (mbv != 0.0) b = (Real)fmax((double)b / (mbv * mbv), (double)floor_abs);
+      Bs[tid] = b;
+    }
+  } else {
+    for (int n = 0; n < N; ++n) {
+      const double m0 = mu ? mu[n * L] : 0.0;
+      for (int i = p.koff[n] + tid; i < p.koff[n + 1]; i += NT) {
+        Real b = Bg[i];
+        if (m0 != 0.0) b = (Real)fmax((double)b / (m0 * m0), (double)floor_abs);
+        Bs[i] = b;
+      }
     }
   }
   cluster_sync_all();  // mbarriers initialised cluster-wide; Bs, inZ visible in the CTA
@@ -727,39 +760,48 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
 #pragma unroll
         for (int k = 0; k < FT; ++k) en[k] = eown[q][k];
     });
-    for (int kb = k0; kb < k1; kb += 16) {
-      Real a[32];
+    // KW bases per pass: 10 when K is a multiple of 10 (BASELINE K = 20: no
+    // idle lanes), else 16; numerators at [0, KW), denominators at [16, 16 + KW)
+    auto mub = [&](auto kw) {
+      constexpr int KW = decltype(kw)::value;
+      for (int kb = k0; kb < k1; kb += KW) {
+        Real a[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) a[i] = Real(0);
+        for (int i = 0; i < 32; ++i) a[i] = Real(0);
 #pragma unroll
-      for (int k = 0; k < FT; ++k) {
-        const int jl = tid + k * NT, tau = j0 + jl;
-        const Real ilv = il[jl];
-        const Real an = en[k] * (ilv * ilv);
-        const Real bn = (tau < T) ? ilv * (Real)min(L, T - tau) : Real(0);
-        if (tau < T) {
+        for (int k = 0; k < FT; ++k) {
+          const int jl = tid + k * NT, tau = j0 + jl;
+          const Real ilv = il[jl];
+          const Real an = en[k] * (ilv * ilv);
+          const Real bn = (tau < T) ? ilv * (Real)min(L, T - tau) : Real(0);
+          if (tau < T) {
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const Real v = __ldg(Vg + (size_t)min(kb + q, k1 - 1) * T + tau);
-            a[q] = fma(an, v, a[q]);
-            a[16 + q] = fma(bn, v, a[16 + q]);
+            for (int q = 0; q < KW; ++q) {
+              const Real v = __ldg(Vg + (size_t)min(kb + q, k1 - 1) * T + tau);
+              a[q] = fma(an, v, a[q]);
+              a[16 + q] = fma(bn, v, a[16 + q]);
+            }
           }
         }
-      }
-      warp_reduce_scatter(a, lane);
-      __syncthreads();  // previous pass's reads of red are done
-      red[(size_t)warp * 32 + lane] = a[0];
-      __syncthreads();
-      if (tid < 16 && kb + tid < k1) {
-        Real num = Real(0), den = Real(0);
-        for (int w = 0; w < NW; ++w) {
-          num += red[(size_t)w * 32 + tid];
-          den += red[(size_t)w * 32 + 16 + tid];
+        warp_reduce_scatter(a, lane);
+        __syncthreads();  // previous pass's reads of red are done
+        red[(size_t)warp * 32 + lane] = a[0];
+        __syncthreads();
+        if (tid < KW && kb + tid < k1) {
+          Real num = Real(0), den = Real(0);
+          for (int w = 0; w < NW; ++w) {
+            num += red[(size_t)w * 32 + tid];
+            den += red[(size_t)w * 32 + 16 + tid];
+          }
+          exmub[2 * (kb + tid)] = (double)num;
+          exmub[2 * (kb + tid) + 1] = (double)den;
         }
-        exmub[2 * (kb + tid)] = (double)num;
-        exmub[2 * (kb + tid) + 1] = (double)den;
       }
-    }
+    };
+    if ((k1 - k0) % 10 == 0)
+      mub(std::integral_constant<int, 10>{});
+    else
+      mub(std::integral_constant<int, 16>{});
   }
   cluster_sync_all();  // MU-B partials published
 
