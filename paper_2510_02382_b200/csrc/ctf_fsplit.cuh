@@ -170,6 +170,13 @@ template <int V> __device__ __forceinline__ void warp_reduce_scatter_fast(double
 // AG: every CTA gathers all CS partials of every row and derives all R
 // coefficients itself (one DSMEM hop per step, CS x 3R values received)
 // instead of the owner scheme (two hops, 3R values)
+#ifdef CTF_PHASE_TIMING
+__device__ unsigned long long g_fphase[4096 * 12];  // dev instrumentation: clock64 per phase, CTA 0 tid 0
+#define CTF_FPHASE(k) \
+  if (c == 0 && tid == 0 && tile < 4096) g_fphase[tile * 12 + (k)] = clock64();
+#else
+#define CTF_FPHASE(k)
+#endif
 template <typename Real, int R, int L, int FT, int NT, int CS, int RREG, int RG, int MINB, bool AG = false>
 __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
   using R2 = typename Cplx<Real>::T;
@@ -204,6 +211,7 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
   __shared__ int s_wbad;
 
   const size_t tile = (size_t)mix * p.FL + bin;
+  CTF_FPHASE(0);
   const R2* xg = reinterpret_cast<const R2*>(p.x) + tile * (size_t)T * M;
   R2* Wg = reinterpret_cast<R2*>(p.W) + tile * (size_t)R * R;
   Real* Bg = reinterpret_cast<Real*>(p.Bf) + tile * SK;
@@ -304,33 +312,53 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
     }
   }
   cluster_sync_all();  // mbarriers initialised cluster-wide; Bs, inZ visible in the CTA
+  CTF_FPHASE(1);
   // ---- lambda = max(B V, floor) -> 1/lambda over the frames j0 - LOFF .. j0 + TC
   double logsum = 0.0;
   for (int n = 0; n < N; ++n) {
     const int k0 = p.koff[n], k1 = p.koff[n + 1];
-    for (int i = tid; i < LP; i += NT) {
-      const int jl = i - LOFF, tau = j0 + jl;
-      Real v = Real(0);
-      if (tau >= 0 && tau < T) {
-        Real lam = Real(0);
-        // KB loads in flight (one L2 round trip for K <= KB), same summation order
-        constexpr int KB = CTF_FS_LAMKB;
-        for (int kk = k0; kk < k1; kk += KB) {
-          Real vq[KB];
+    // ITB of the thread's IT frames x KB columns in flight at once (all IT
+    // frames when that stays within 64 registers: one L2 round trip per
+    // source for K <= KB); same summation order per frame
+    constexpr int KB = CTF_FS_LAMKB, IT = (LP + NT - 1) / NT, ITB = IT * KB <= 64 ? IT : 1;
+#pragma unroll 1
+    for (int it0 = 0; it0 < IT; it0 += ITB) {
+      Real lamv[ITB];
 #pragma unroll
-          for (int q = 0; q < KB; ++q) vq[q] = (kk + q < k1) ? __ldg(Vg + (size_t)(kk + q) * T + tau) : Real(0);
+      for (int it = 0; it < ITB; ++it) lamv[it] = Real(0);
+      for (int kk = k0; kk < k1; kk += KB) {
+        Real vq[ITB][KB];
+#pragma unroll
+        for (int it = 0; it < ITB; ++it) {
+          const int i = tid + (it0 + it) * NT, tau = j0 + i - LOFF;
+          const bool ok = i < LP && tau >= 0 && tau < T;
+#pragma unroll
+          for (int q = 0; q < KB; ++q) vq[it][q] = (ok && kk + q < k1) ? __ldg(Vg + (size_t)(kk + q) * T + tau) : Real(0);
+        }
+#pragma unroll
+        for (int it = 0; it < ITB; ++it)
 #pragma unroll
           for (int q = 0; q < KB; ++q)
-            if (kk + q < k1) lam = fma(Bs[kk + q], vq[q], lam);
-        }
-        lam = fmax(lam, floor_abs);
-        v = Real(1) / lam;
-        if (p.has_prev && jl >= 0) logsum += (double)min(L, T - tau) * (double)log(lam);
+            if (kk + q < k1) lamv[it] = fma(Bs[kk + q], vq[it][q], lamv[it]);
       }
-      invl[n * LP + i] = v;
+#pragma unroll
+      for (int it = 0; it < ITB; ++it) {
+        const int i = tid + (it0 + it) * NT;
+        if (i < LP) {
+          const int jl = i - LOFF, tau = j0 + jl;
+          Real v = Real(0);
+          if (tau >= 0 && tau < T) {
+            const Real lam = fmax(lamv[it], floor_abs);
+            v = Real(1) / lam;
+            if (p.has_prev && jl >= 0) logsum += (double)min(L, T - tau) * (double)log(lam);
+          }
+          invl[n * LP + i] = v;
+        }
+      }
     }
   }
   __syncthreads();
+  CTF_FPHASE(2);
 
   // ---- Y = (W / mu) x~ for the own frames (estimator.cpp:555), 4 rows per
   // chunk: the chunk's rescaled W rows staged column-major in shared memory
@@ -408,6 +436,7 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
     });
     __syncthreads();  // wst (the reduction buffer) is reused by the objective sums
   }
+  CTF_FPHASE(3);
 
   // ISS weights: w_p(j) = 1/lambda_{n_p}(j - l_p), row P = (P / L, P % L)
   const Real* wsrc[N];
@@ -482,6 +511,7 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
     return;
   }
 
+  CTF_FPHASE(4);
   // ---- ISS sweep (estimator.cpp:556-579). The pass of step r applies step
   // r-1's update (y_p -= z_p y_{r-1}) and accumulates step r's sums.
   R2 pv[FT];
@@ -673,6 +703,7 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
     return;
   }
 
+  CTF_FPHASE(5);
   // ---- epilogue: last step's update, row-power partials, |y|^2 of the first
   // HL frames for the previous CTA's delayed energies
   {
@@ -715,6 +746,7 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
     ex[4 + tid] = s;
   }
   cluster_sync_all();  // halos and row-power partials published
+  CTF_FPHASE(6);
 
   // delayed energies E_n(tau) = sum_{l<L, tau+l<T} |y_{nL+l}(tau+l)|^2 (estimator.cpp:321-332)
   Real eown[N][FT];
@@ -804,6 +836,7 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
       mub(std::integral_constant<int, 16>{});
   }
   cluster_sync_all();  // MU-B partials published
+  CTF_FPHASE(7);
 
   if (c == 0) {
     for (int k = tid; k < SK; k += NT) {
@@ -827,6 +860,7 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
     if (col < R) Wg[(size_t)col * R + q] = Wf[e];
   }
   cluster_sync_all();  // CTA 0's remote reads done before any CTA exits
+  CTF_FPHASE(8);
 }
 
 }  // namespace ctf

@@ -11,3 +11,10 @@ std::vector<SweepVariant> sweep_variants_fsplit_f32() {
           CTF_FSA(float, 1, 32, 8, 2, 128, 4, 16, 8, 3)};
 }
 }  // namespace ctf
+#ifdef CTF_PHASE_TIMING
+// dev instrumentation (builds with -DCTF_PHASE_TIMING only): clock64 of the
+// cluster's CTA 0 at the phase boundaries of fsplit_kernel, tiles < 4096
+extern "C" int ctf_debug_fsplit_phases(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, ctf::g_fphase, sizeof(unsigned long long) * 4096 * 12);
+}
+#endif
