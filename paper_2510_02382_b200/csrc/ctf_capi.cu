@@ -1150,6 +1150,36 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host,
   CK(cudaMemsetAsync(c->chk.p, 0, c->chk.n * 8, c->stream));
   CK(cudaMemsetAsync(c->E.p, 0, c->E.n, c->stream));
 
+  // random_factors with mt19937_64(seed + b) (model.cpp:189-208, estimator.cpp:532-533),
+  // drawn on host threads while x is uploaded and its mean power reduced
+  std::vector<double> hb((size_t)c->B * c->FL * c->SK), hv((size_t)c->B * c->SK * c->T);
+  // one independent mt19937_64 stream per mixture: threads over mixtures
+  struct Pool {
+    std::vector<std::thread> t;
+    void join_all() {
+      for (auto& th : t)
+        if (th.joinable()) th.join();
+    }
+    ~Pool() { join_all(); }  // also on the error paths below
+  } pool;
+  const int nth = std::max(1, std::min<int>(c->B, (int)std::thread::hardware_concurrency()));
+  for (int w = 0; w < nth; ++w) pool.t.emplace_back([&, w] {
+  for (int b = w; b < c->B; b += nth) {
+    std::mt19937_64 rng(prob->seed + (uint64_t)b);
+    std::uniform_real_distribution<double> uni(0.1, 1.0);
+    for (int n = 0; n < c->N; ++n) {
+      const int K = c->bases[n];
+      for (int i = 0; i < c->F; ++i)
+        for (int k = 0; k < K; ++k) {
+          const double v = uni(rng);
+          if (i >= c->lo && i < c->hi) hb[((size_t)b * c->FL + (i - c->lo)) * c->SK + c->koff[n] + k] = v;
+        }
+      for (int k = 0; k < K; ++k)
+        for (int j = 0; j < c->T; ++j) hv[((size_t)b * c->SK + c->koff[n] + k) * c->T + j] = uni(rng);
+    }
+  }
+  });
+
   // x: this rank's bins of every mixture, converted to the compute precision
   const size_t xs_in = prob->x_precision == CTF_F32 ? 8 : 16;
   const size_t per_mix = (size_t)c->FL * c->T * c->Mx;  // complex per mixture (local)
@@ -1207,28 +1237,7 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host,
   c->it_sweep_ms.clear();
   c->it_mu_ms.clear();
 
-  // random_factors with mt19937_64(seed + b) (model.cpp:189-208, estimator.cpp:532-533)
-  std::vector<double> hb((size_t)c->B * c->FL * c->SK), hv((size_t)c->B * c->SK * c->T);
-  // one independent mt19937_64 stream per mixture: threads over mixtures
-  const int nth = std::max(1, std::min<int>(c->B, (int)std::thread::hardware_concurrency()));
-  std::vector<std::thread> pool;
-  for (int w = 0; w < nth; ++w) pool.emplace_back([&, w] {
-  for (int b = w; b < c->B; b += nth) {
-    std::mt19937_64 rng(prob->seed + (uint64_t)b);
-    std::uniform_real_distribution<double> uni(0.1, 1.0);
-    for (int n = 0; n < c->N; ++n) {
-      const int K = c->bases[n];
-      for (int i = 0; i < c->F; ++i)
-        for (int k = 0; k < K; ++k) {
-          const double v = uni(rng);
-          if (i >= c->lo && i < c->hi) hb[((size_t)b * c->FL + (i - c->lo)) * c->SK + c->koff[n] + k] = v;
-        }
-      for (int k = 0; k < K; ++k)
-        for (int j = 0; j < c->T; ++j) hv[((size_t)b * c->SK + c->koff[n] + k) * c->T + j] = uni(rng);
-    }
-  }
-  });
-  for (auto& t : pool) t.join();
+  pool.join_all();  // the initial factors (drawn on host threads while x was uploaded)
   upload_real(c, c->Bf.p, hb.data(), hb.size());
   upload_real(c, c->V.p, hv.data(), hv.size());
   // W = I (model.cpp:221-227)
