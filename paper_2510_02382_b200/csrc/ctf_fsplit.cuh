@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
           Real v = Real(0);
           if (tau >= 0 && tau < T) {
             const Real lam = fmax(lamv[it], floor_abs);
-            v = Real(1) / lam;
+            v = rcp_rn(lam);
             if (p.has_prev && jl >= 0) logsum += (double)min(L, T - tau) * (double)log(lam);
           }
           invl[n * LP + i] = v;

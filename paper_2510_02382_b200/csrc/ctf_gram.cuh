@@ -131,11 +131,8 @@ __device__ __forceinline__ void gram_block(const typename Cplx<Real>::T* __restr
   if (u < u1) gram_step<Real, CNT, NS, UB, true>(x1, x2, w0, lp, u, u1, wv, acc);
 }
 
-// 1/x correctly rounded (same value as the division, no slow path) and the
-// objective's log term: MUFU-based in fp32 (abs. error ~1e-6, far inside the
-// fp32 cost tolerance), exact in fp64.
-__device__ __forceinline__ float rcp_rn(float x) { return __frcp_rn(x); }
-__device__ __forceinline__ double rcp_rn(double x) { return 1.0 / x; }
+// The objective's log term: MUFU-based in fp32 (abs. error ~1e-6, far inside
+// the fp32 cost tolerance), exact in fp64 (rcp_rn: ctf_kernels.cuh).
 __device__ __forceinline__ float log_fast(float x) { return __logf(x); }
 __device__ __forceinline__ double log_fast(double x) { return log(x); }
 

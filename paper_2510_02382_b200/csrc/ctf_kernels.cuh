@@ -112,6 +112,10 @@ template <typename V> __device__ __forceinline__ void cmsub(V& acc, V a, V b) { 
   acc.y = fma(-a.x, b.y, acc.y);
   acc.y = fma(-a.y, b.x, acc.y);
 }
+// 1/x correctly rounded: the same value as the IEEE division 1/x, without
+// its slow-path sequence (fp32: MUFU + Newton fixup); fp64 divides
+__device__ __forceinline__ float rcp_rn(float x) { return __frcp_rn(x); }
+__device__ __forceinline__ double rcp_rn(double x) { return 1.0 / x; }
 template <typename V> __device__ __forceinline__ auto cnorm(V a) -> decltype(a.x) { return fma(a.x, a.x, a.y * a.y); }
 template <typename V> __device__ __forceinline__ bool cfinite(V a) { return isfinite(a.x) && isfinite(a.y); }
 template <typename Real> __device__ __forceinline__ typename Cplx<Real>::T czero() {
@@ -474,7 +478,7 @@ __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(c
       Real v = Real(0);
       if (tau < T) {
         const Real l = fmax(lam[k], floor_abs);
-        v = Real(1) / l;
+        v = rcp_rn(l);
         if (p.has_prev) logsum += (double)min(Ln, T - tau) * (double)log(l);
       }
       il[p.loff + tau] = v;
@@ -963,7 +967,7 @@ __global__ void __launch_bounds__(128) muv_partial_kernel(const MuvParams p) {
           lb = fma(Bsh[k * nbp + i + 1], v[k], lb);
         }
       }
-      const Real ila = Real(1) / fmax(la, floor_abs), ilb = Real(1) / fmax(lb, floor_abs);
+      const Real ila = rcp_rn(fmax(la, floor_abs)), ilb = rcp_rn(fmax(lb, floor_abs));
       const Real ana = ecur[u] * (ila * ila), bna = ila * cnt;
       const Real anb = ecur[u + 1] * (ilb * ilb), bnb = ilb * cnt;
 #pragma unroll
