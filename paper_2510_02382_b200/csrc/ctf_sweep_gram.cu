@@ -5,7 +5,9 @@ namespace ctf {
 #define GF(...) CTF_GR(float, 1, __VA_ARGS__)
 #define GD(...) CTF_GR(double, 0, __VA_ARGS__)
 std::vector<SweepVariant> sweep_variants_gram_f32() {
-#ifdef CTF_GRAM_DEV  // dev builds (tools/dev_build.sh): only the variant being tuned
+#if defined(CTF_GRAM_DEV) && defined(CTF_DEV_F64)
+  return {};
+#elif defined(CTF_GRAM_DEV)  // dev builds (tools/dev_build.sh): only the variant being tuned
   return {GF(CTF_DEV_M, CTF_DEV_L, CTF_DEV_NT, CTF_DEV_FT)};
 #else
   return {GF(2, 2, 128, 4), GF(2, 2, 256, 4), GF(2, 3, 128, 4), GF(2, 3, 256, 4),
@@ -14,7 +16,9 @@ std::vector<SweepVariant> sweep_variants_gram_f32() {
 #endif
 }
 std::vector<SweepVariant> sweep_variants_gram_f64() {
-#ifdef CTF_GRAM_DEV
+#if defined(CTF_GRAM_DEV) && defined(CTF_DEV_F64)  // dev build of one fp64 variant
+  return {GD(CTF_DEV_M, CTF_DEV_L, CTF_DEV_NT, CTF_DEV_FT)};
+#elif defined(CTF_GRAM_DEV)
   return {};
 #else
   return {GD(2, 2, 128, 4), GD(2, 2, 256, 4), GD(2, 3, 128, 4), GD(2, 3, 256, 4),

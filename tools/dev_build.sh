@@ -1,7 +1,8 @@
 #!/bin/bash
 # Dev build for A/B timing of one gram_kernel variant: ctf_sweep_gram.cu with
 # only that variant (CTF_GRAM_DEV="M L NT FT", default "2 5 256 4"; fp64/IP lists empty), linked
-# with the regular objects into tools/dev/<name>/libctfiss.so. Use it with
+# with the regular objects into tools/dev/<name>/libctfiss.so (-DCTF_DEV_F64: the
+# fp64 variant of that shape instead). Use it with
 #   CTF_DEV_LIB=tools/dev/<name>/libctfiss.so python tools/prof_cfg.py ...
 # Extra nvcc flags (e.g. -DCTF_PHASE_TIMING) after the name.
 set -e
