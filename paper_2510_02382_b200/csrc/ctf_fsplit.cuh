@@ -31,6 +31,9 @@
 #include "ctf_cluster.cuh"
 #include "ctf_kernels.cuh"
 
+#ifndef CTF_FS_ITB  // frames per batch when all of them would exceed 64 registers
+#define CTF_FS_ITB 2
+#endif
 #ifndef CTF_FS_LAMKB
 #define CTF_FS_LAMKB 20
 #endif
@@ -320,7 +323,7 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
     // ITB of the thread's IT frames x KB columns in flight at once (all IT
     // frames when that stays within 64 registers: one L2 round trip per
     // source for K <= KB); same summation order per frame
-    constexpr int KB = CTF_FS_LAMKB, IT = (LP + NT - 1) / NT, ITB = IT * KB <= 64 ? IT : 1;
+    constexpr int KB = CTF_FS_LAMKB, IT = (LP + NT - 1) / NT, ITB = IT * KB <= 64 ? IT : CTF_FS_ITB;
 #pragma unroll 1
     for (int it0 = 0; it0 < IT; it0 += ITB) {
       Real lamv[ITB];
