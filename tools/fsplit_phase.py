@@ -12,14 +12,16 @@ B, F, T, M, N, L, K, dec = {3: (2, 2049, 1000, 4, 4, 8, 20, 0.8), 4: (2, 1025, 4
 x = synth_mixtures(B, F, T, M, N, L, K, dec, 1, precision="f32")
 s = Session(x, [L] * N, [K] * N, stack_taps=L, iterations=4, precision="f32")
 print(s.describe())
-s.iterate(3)
+s.iterate_async(3)  # no finalize pass (it would overwrite the first phases only)
+import torch; torch.cuda.synchronize()
 lib = _lib.load()
 buf = (C.c_ulonglong * (4096 * 12))()
 assert lib.ctf_debug_fsplit_phases(buf) == 0
 ph = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 12).astype(np.int64)[: B * F]
+bounds = [0, 1, 2, 3, 4, 5, 6, 7, 8]
 names = ["prologue", "lambda", "demix", "objective", "sweep", "epilogue", "mu_b", "tail"]
-d = np.diff(ph[:, :9], axis=1)
 tot = ph[:, 8] - ph[:, 0]
 print("CTA-0 cycles per bin: mean %.0f median %.0f" % (tot.mean(), np.median(tot)))
 for i, n in enumerate(names):
-    print(f"{n:10s} {d[:, i].mean():10.0f} cycles  {100 * d[:, i].mean() / tot.mean():5.1f} %")
+    d = ph[:, bounds[i + 1]] - ph[:, bounds[i]]
+    print(f"{n:16s} {d.mean():10.0f} cycles  {100 * d.mean() / tot.mean():5.1f} %")
