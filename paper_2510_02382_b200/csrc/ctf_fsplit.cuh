@@ -31,6 +31,12 @@
 #include "ctf_cluster.cuh"
 #include "ctf_kernels.cuh"
 
+#ifndef CTF_FS_DCR  // W rows per demix chunk (R = 32: cfg3; wider: cfg4)
+#define CTF_FS_DCR 8
+#endif
+#ifndef CTF_FS_DCR_WIDE
+#define CTF_FS_DCR_WIDE 12
+#endif
 #ifndef CTF_FS_ITB  // frames per batch when all of them would exceed 64 registers
 #define CTF_FS_ITB 2
 #endif
@@ -64,7 +70,7 @@ struct FsplitLayout {
   static constexpr size_t off_w = off_l + a16((size_t)M * LP * RB_);
   static constexpr size_t off_red = off_w + a16((size_t)2 * R * DC * CB_);
   static constexpr size_t off_a =
-      off_red + a16(mx((size_t)NW * mx(mx((size_t)NG * VP, (size_t)NG2 * 32), 16) * RB_, (size_t)4 * R * CB_));
+      off_red + a16(mx((size_t)NW * mx(mx((size_t)NG * VP, (size_t)NG2 * 32), 16) * RB_, (size_t)(R > 32 ? CTF_FS_DCR_WIDE : CTF_FS_DCR) * R * CB_));
   static constexpr size_t off_z = off_a + a16((size_t)2 * CS * (AG ? R : RC) * CH);
   static constexpr size_t off_h = off_z + a16((size_t)2 * R * CH);
   static constexpr size_t off_ex = off_h + a16((size_t)R * HL * RB_);
@@ -363,7 +369,7 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
   __syncthreads();
   CTF_FPHASE(2);
 
-  // ---- Y = (W / mu) x~ for the own frames (estimator.cpp:555), 4 rows per
+  // ---- Y = (W / mu) x~ for the own frames (estimator.cpp:555), CR rows per
   // chunk: the chunk's rescaled W rows staged column-major in shared memory
   // (the reduction buffer is free here), the next chunk prefetched into
   // registers; the stacked channel (m, l) is x_m(t - l) from the x tile
@@ -371,13 +377,14 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
   Y.sm = Ysm;
   Y.tp = TC;
   {
-    constexpr int NCH = (R + 3) / 4, WPT = (4 * R + NT - 1) / NT;
-    R2* wst = reinterpret_cast<R2*>(smem + LY::off_red);  // [R columns][4 rows]
+    constexpr int CR = R > 32 ? CTF_FS_DCR_WIDE : CTF_FS_DCR;  // rows per chunk
+    constexpr int NCH = (R + CR - 1) / CR, WPT = (CR * R + NT - 1) / NT;
+    R2* wst = reinterpret_cast<R2*>(smem + LY::off_red);  // [R columns][CR rows]
     R2 wpre[WPT];
     auto fetch = [&](int r0) {
 #pragma unroll
       for (int t = 0; t < WPT; ++t) {
-        const int e = tid + t * NT, cc = e >> 2, q = r0 + (e & 3);
+        const int e = tid + t * NT, cc = e / CR, q = r0 + (e % CR);
         R2 w = czero<Real>();
         if (cc < R && q < R) {
           w = Wg[(size_t)cc * R + q];
@@ -394,39 +401,39 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
     };
     fetch(0);
     static_for<0, NCH>([&](auto chunk) {
-      constexpr int r0 = decltype(chunk)::value * 4;
+      constexpr int r0 = decltype(chunk)::value * CR;
       __syncthreads();  // the previous chunk's reads of wst are done
 #pragma unroll
       for (int t = 0; t < WPT; ++t)
-        if (tid + t * NT < 4 * R) wst[tid + t * NT] = wpre[t];
+        if (tid + t * NT < CR * R) wst[tid + t * NT] = wpre[t];
       __syncthreads();
-      if constexpr (r0 + 4 < R) fetch(r0 + 4);
-      R2 acc[FT][4];
+      if constexpr (r0 + CR < R) fetch(r0 + CR);
+      R2 acc[FT][CR];
 #pragma unroll
       for (int k = 0; k < FT; ++k)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) acc[k][i] = czero<Real>();
+        for (int i = 0; i < CR; ++i) acc[k][i] = czero<Real>();
 #pragma unroll 4
       for (int cc = 0; cc < R; ++cc) {
         const int m = cc / L, l = cc - m * L;
         const R2* xrow = xs + m * XP + XOFF - l + tid;
-        R2 w[4];
+        R2 w[CR];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) w[i] = wst[cc * 4 + i];
+        for (int i = 0; i < CR; ++i) w[i] = wst[cc * CR + i];
 #pragma unroll
         for (int k = 0; k < FT; ++k) {
           const R2 xv = xrow[k * NT];
           if constexpr (std::is_same<Real, float>::value) {
             const float2 xn = make_float2(-xv.y, xv.x);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) acc[k][i] = ffma2s(xn, w[i].y, ffma2s(xv, w[i].x, acc[k][i]));
+            for (int i = 0; i < CR; ++i) acc[k][i] = ffma2s(xn, w[i].y, ffma2s(xv, w[i].x, acc[k][i]));
           } else {
 #pragma unroll
-            for (int i = 0; i < 4; ++i) cmac(acc[k][i], w[i], xv);
+            for (int i = 0; i < CR; ++i) cmac(acc[k][i], w[i], xv);
           }
         }
       }
-      static_for<0, 4>([&](auto ii) {
+      static_for<0, CR>([&](auto ii) {
         constexpr int P = r0 + decltype(ii)::value;
         if constexpr (P < R) {
 #pragma unroll
