@@ -5,8 +5,11 @@ Metric (BASELINE.json): TF-bin*iter/s of the ISS+NMF loop (one TF-bin = one
 (mixture, frequency bin, frame)); roofline fractions reported alongside.
 
 Workload at N=1: BASELINE configs[1] — 64 mixtures, M=N=2, L=5 (stacked
-D=10), F=513, T=1000, K=10, 100 iterations (--dtype f32 by default; f64 via
---dtype f64). Seeded synthetic mixtures from BASELINE's generator.
+D=10), F=513, T=1000, K=10, 100 iterations, in fp64 (complex128, the
+reference's arithmetic, types.hpp:10) — the headline `value`/`e2e`/`roofline`;
+configs[1] also asks for fp32, carried in the same line under "f32".
+cfg2-cfg4 (--cfg) are fp32 as BASELINE states. Seeded synthetic mixtures
+from BASELINE's generator.
 
   value : device-resident throughput — a "step" is one ISS+NMF iteration
           (estimator.cpp:548-654) over the whole batch with x already in HBM;
@@ -19,8 +22,14 @@ Multi-GPU (torchrun): frequency sharding (contiguous bin ranges), one NCCL
 all-reduce per iteration inside the library; strong scaling of the same
 workload; times are the max over ranks.
 
---impl reference times the CPU restatement of the reference (oracle/) on the
-host cores with all threads, one iteration of one mixture per step.
+--impl reference times the REFERENCE'S OWN CODE on the host cores: run()
+from /root/reference/proj/src compiled unmodified into oracle/_ref
+(oracle/Makefile.ref; kind "reference"), with config.threads = all host
+threads (its bin-parallel parallel_for), one run() of 2 iterations of one
+mixture per step (a bounded sample of the workload). If oracle/_ref did not
+travel, the restatement oracle/ctf_oracle.cpp stands in (kind "port").
+The reference arm never loads the product library (its inputs come from the
+generator copy inside libctf_ref.so).
 """
 from __future__ import annotations
 
@@ -174,43 +183,62 @@ def profile_traffic(kernel, prec, cfgn):
 
 
 # ---------------------------------------------------------------------------
-def cpu_reference_arm(args, cfgn, steps, warmup, sample_note=True):
-    """The reference's algorithm on the host cores: the oracle restatement
-    (proj/src/estimator.cpp:548-654), one iteration of one mixture per step."""
+def cpu_reference_arm(args, cfgn, steps, warmup):
+    """The reference on the host cores, bounded sample: one mixture of the
+    config (a bin subset for the large tiles so one step stays around a
+    second), each step one run() of 2 iterations (setup + 2 loop bodies,
+    estimator.cpp:513-657) through oracle/_ref — the reference's own sources.
+    Falls back to the restatement (oracle/ctf_oracle.cpp, kind "port") when
+    the reference build is not present."""
     from oracle import oracle as O
-    from paper_2510_02382_b200 import synth_mixtures
+    from oracle import ref as REF
+    kind = "reference" if REF.available() else "port"
     B, F, T, M, L, K, rho, iters = CFGS[cfgn]
     N = M
     threads = os.cpu_count() or 1
-    # bounded sample: all bins for cfg0/cfg1, a bin subset for the large
-    # tiles so one step (one iteration) stays around half a second
     R = M * L
     F = min(F, max(16, int(513 * (1000.0 / T) * (100.0 / (R * R)))))
-    raw = synth_mixtures(1, F, T, M, N, L, K, rho, args.seed)[0]
+    if kind == "reference":
+        raw = REF.synth_mixtures(1, F, T, M, N, L, K, rho, args.seed)[0]
+    else:
+        from paper_2510_02382_b200 import synth_mixtures
+        raw = synth_mixtures(1, F, T, M, N, L, K, rho, args.seed)[0]
     x = O.stack_observation(raw, L)
-    cfg = O.config([L] * N, [K] * N, iterations=1, seed=args.seed, threads=threads)
-    floor = 1e-10 * O.mean_power(x)
-    Bf, V = O.random_factors(cfg, F, T)
-    W = np.zeros((F, R, R), complex)
-    W[:] = np.eye(R)
+    per = 2
+    cfg = O.config([L] * N, [K] * N, iterations=per, seed=args.seed, threads=threads)
     times = []
-    for s in range(warmup + steps):
+    for st in range(warmup + steps):
         t0 = time.perf_counter()
-        W, Bf, V, _ = O.step(cfg, x, floor, W, Bf, V)
+        if kind == "reference":
+            REF.run(cfg, x)
+        else:
+            O.run(cfg, x)
         dt = time.perf_counter() - t0
-        if s >= warmup:
+        if st >= warmup:
             times.append(dt)
     sec = sum(times)
-    value = F * T * len(times) / sec
+    value = F * T * per * len(times) / sec
     try:
         model = [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")][0]
     except (OSError, IndexError):
         model = "unknown"
-    return {"value": value, "unit": "TF-bin*iter/s", "cores": threads, "kind": "port",
-            "sample": f"1 of {B} mixtures, {F} of {CFGS[cfgn][1]} bins, {len(times)} iterations of cfg{cfgn} "
-                      f"(T={T}, D={R}), "
-                      f"oracle/ctf_oracle.cpp with parallel_for over bins on {threads} threads ({model}); "
-                      f"{sec:.2f} s", "seconds": sec}
+    impl = ("oracle/_ref: the reference's run() (proj/src/*.cpp compiled unmodified, Eigen-API shim)"
+            if kind == "reference" else "oracle/ctf_oracle.cpp (restatement)")
+    return {"value": value, "unit": "TF-bin*iter/s", "cores": threads, "kind": kind,
+            "sample": f"1 of {B} mixtures, {F} of {CFGS[cfgn][1]} bins of cfg{cfgn} (T={T}, D={R}), "
+                      f"{len(times)} steps of one run() with {per} iterations; {impl}, "
+                      f"config.threads={threads} ({model}); {sec:.2f} s", "seconds": sec}
+
+
+def workload_config(cfgn, world, dtype):
+    """The config dict both arms print (identical, so the driver can pair them)."""
+    B, F, T, M, L, K, rho, iters = CFGS[cfgn]
+    D = M * L
+    return {"workload": f"BASELINE configs[{cfgn}]: {B} mixtures, M=N={M}, L={L} (D={D}), F={F}, T={T}, "
+                        f"K={K}, {iters} iterations, tap variance {rho}^l",
+            "mixtures": B, "bins": F, "frames": T, "mics": M, "taps": L, "bases": K, "iterations": iters,
+            "parallelism": f"freq-shard x{world}" if world > 1 else "1 GPU",
+            "l2": "inputs larger than L2 (x alone is %.0f MB)" % (B * F * T * M * (8 if dtype == "f32" else 16) / 1e6)}
 
 
 def main():
@@ -220,24 +248,24 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cfg", type=int, default=1)
-    ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
+    ap.add_argument("--dtype", default="auto", choices=["auto", "f32", "f64"],
+                    help="auto: f64 for cfg0/cfg1 (with the f32 line of cfg1 alongside), f32 for cfg2-4")
     ap.add_argument("--seed", type=int, default=20251002)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--unique", type=int, default=16,
                     help="distinct synthetic mixtures generated; the batch tiles them (seeds still differ per mixture)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-f32", action="store_true", help="cfg1: skip the fp32 line carried next to the fp64 headline")
     ap.add_argument("--no-frontend", action="store_true", help="skip the STFT/iSTFT front-end measurement")
     args = ap.parse_args()
     world, rank, local = dist_env()
+    if args.dtype == "auto":
+        args.dtype = "f64" if args.cfg <= 1 else "f32"
     B, F, T, M, L, K, rho, iters = CFGS[args.cfg]
     N, R = M, M * L
     D = R
-    config = {"workload": f"BASELINE configs[{args.cfg}]: {B} mixtures, M=N={M}, L={L} (D={D}), F={F}, T={T}, "
-                          f"K={K}, {iters} iterations, tap variance {rho}^l",
-              "mixtures": B, "bins": F, "frames": T, "mics": M, "taps": L, "bases": K, "iterations": iters,
-              "parallelism": f"freq-shard x{world}" if world > 1 else "1 GPU",
-              "l2": "inputs larger than L2 (x alone is %.0f MB)" % (B * F * T * M * (8 if args.dtype == "f32" else 16) / 1e6)}
+    config = workload_config(args.cfg, world, args.dtype)
 
     if args.impl == "reference":
         if rank != 0:
@@ -245,8 +273,8 @@ def main():
         ref = cpu_reference_arm(args, args.cfg, args.steps, args.warmup)
         line = {"metric": "TF-bin*iter/s of the ISS+NMF loop", "value": ref["value"], "unit": "TF-bin*iter/s",
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": 1e3 * ref["seconds"] / args.steps, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE configs generator, seeded)",
+                "ms_per_step": 1e3 * ref["seconds"] / args.steps, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE configs generator, seeded; no public dataset)",
                 "config": config, "impl": "reference",
                 "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")},
                 "e2e": {"value": ref["value"], "unit": "TF-bin*iter/s", "h2d_bytes_per_step": 0,
@@ -289,89 +317,99 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t[0])
 
-    prec = args.dtype
-    # BASELINE's generator, one seed per mixture; for large batches a set of
-    # `--unique` mixtures is generated and tiled over the batch (throughput
-    # does not depend on the content; init seeds stay distinct per mixture)
-    nu = min(B, max(1, args.unique)) if B > 64 else B
-    xu = synth_mixtures(nu, F, T, M, N, L, K, rho, args.seed, precision=prec)
-    x = xu if nu == B else np.ascontiguousarray(np.concatenate([xu] * ((B + nu - 1) // nu))[:B])
-    del xu
-    config["inputs"] = f"{nu} distinct synthetic mixtures" + ("" if nu == B else f" tiled to {B}")
-    s = Session(x, [L] * N, [K] * N, stack_taps=L, iterations=iters, precision=prec, seed=args.seed,
-                device=device, world_size=world, rank=rank, comm_id=comm_id)
-    desc = json.loads(s.describe())
-    stream = torch.cuda.ExternalStream(s.stream_ptr(), device=device)
+    def measure(prec, e2e_on, cpu_on):
+        """One precision of the workload: device-resident loop (value),
+        roofline of the dominant kernel, ctf_run() end to end (e2e)."""
+        # BASELINE's generator, one seed per mixture; for large batches a set of
+        # `--unique` mixtures is generated and tiled over the batch (throughput
+        # does not depend on the content; init seeds stay distinct per mixture)
+        nu = min(B, max(1, args.unique)) if B > 64 else B
+        xu = synth_mixtures(nu, F, T, M, N, L, K, rho, args.seed, precision=prec)
+        x = xu if nu == B else np.ascontiguousarray(np.concatenate([xu] * ((B + nu - 1) // nu))[:B])
+        del xu
+        inputs = f"{nu} distinct synthetic mixtures" + ("" if nu == B else f" tiled to {B}")
+        s = Session(x, [L] * N, [K] * N, stack_taps=L, iterations=iters, precision=prec, seed=args.seed,
+                    device=device, world_size=world, rank=rank, comm_id=comm_id if prec == args.dtype else new_comm_id())
+        desc = json.loads(s.describe())
+        stream = torch.cuda.ExternalStream(s.stream_ptr(), device=device)
 
-    # ---- device-resident loop: W warm-up iterations, then K timed iterations
-    s.iterate_async(max(args.warmup, 3))
-    torch.cuda.synchronize(device)
-    s.reset_timing()
-    barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(device) as clk:
+        # ---- device-resident loop: W warm-up iterations, then K timed iterations
+        s.iterate_async(max(args.warmup, 3))
         torch.cuda.synchronize(device)
+        s.reset_timing()
         barrier()
-        ev0.record(stream)
-        s.iterate_async(args.steps)
-        ev1.record(stream)
-        ev1.synchronize()
-        torch.cuda.synchronize(device)
-        barrier()
-    ms = ev0.elapsed_time(ev1)
-    timing = s.timing()  # per-kernel CUDA events on the library's stream
-    s.finalize()
-    ms = max_over_ranks(ms)
-    sweep_ms = max_over_ranks(timing.sweep_ms / max(1, timing.sweep_launches))
-    tfbins = B * F * T
-    value = tfbins * args.steps / (ms / 1e3)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with Clocks(device) as clk:
+            torch.cuda.synchronize(device)
+            barrier()
+            ev0.record(stream)
+            s.iterate_async(args.steps)
+            ev1.record(stream)
+            ev1.synchronize()
+            torch.cuda.synchronize(device)
+            barrier()
+        ms = ev0.elapsed_time(ev1)
+        timing = s.timing()  # per-kernel CUDA events on the library's stream
+        s.finalize()
+        ms = max_over_ranks(ms)
+        sweep_ms = max_over_ranks(timing.sweep_ms / max(1, timing.sweep_launches))
+        value = B * F * T * args.steps / (ms / 1e3)
 
-    # ---- roofline of the dominant kernel (the fused sweep kernel)
-    fl_sweep, fl_iter, fl_exec = flops_per_tfbin(R, D, N, K)
-    if desc["sweep_kernel"].startswith("gram_kernel"):
-        fl_exec = gram_executed_flops(M, N, L, K, R, D, T)
-    p32, p64 = peak_probe(device) if rank == 0 else (None, None)
-    peak = p32 if prec == "f32" else p64
-    local_bins = s.bin_range[1] - s.bin_range[0]
-    units_per_launch = B * local_bins * T
-    achieved = fl_sweep * units_per_launch / (sweep_ms / 1e3) / 1e12
-    traffic_per_tfbin = profile_traffic(desc["sweep_kernel"].split("<")[0], prec, args.cfg)
+        # ---- roofline of the dominant kernel (the fused iteration kernel)
+        fl_sweep, fl_iter, fl_exec = flops_per_tfbin(R, D, N, K)
+        if desc["sweep_kernel"].startswith("gram_kernel"):
+            fl_exec = gram_executed_flops(M, N, L, K, R, D, T)
+        peak = peaks[0] if prec == "f32" else peaks[1]
+        local_bins = s.bin_range[1] - s.bin_range[0]
+        units_per_launch = B * local_bins * T
+        achieved = fl_sweep * units_per_launch / (sweep_ms / 1e3) / 1e12
+        traffic_per_tfbin = profile_traffic(desc["sweep_kernel"].split("<")[0], prec, args.cfg)
+        c = 8 if prec == "f32" else 16
+        streamed = desc["sweep_kernel"].startswith("stream_kernel")
+        bpt = bytes_per_tfbin(M, N, K, R, D, T, F, c)
+        if streamed:  # SURVEY §8(d) streamed sweep: every step reads and writes the R x T tile
+            bpt = 2 * M * c + R * c + 2 * R * R * c + bpt - M * c
+        roofline = {"bound": "fp32-cuda-core" if prec == "f32" else "fp64-cuda-core",
+                    "bound_note": ("compute-bound on the CUDA-core FMA pipes: neither HBM-bound (the hbm sub-object "
+                                   "shows a few % of HBM) nor a tensor-core contraction (each ISS step is R "
+                                   "differently weighted inner products; the fp32/fp64 tolerances rule out "
+                                   "bf16/tf32), so the peak is the FFMA2/DFMA chain rate measured in this run"),
+                    "achieved": achieved,
+                    "peak": peak, "unit": "TFLOP/s", "frac": (achieved / peak) if peak else None,
+                    "traffic": traffic_per_tfbin * units_per_launch if traffic_per_tfbin else None,
+                    "kernel": desc["sweep_kernel"], "kernel_ms": sweep_ms,
+                    "flops_per_tfbin": fl_sweep, "units_per_launch": units_per_launch,
+                    "flops_note": "algorithmic (SURVEY 8(d): 20R^2 + 16RD + 8NK for the sweep kernel's share)",
+                    "executed_flops_per_tfbin": fl_exec,
+                    "executed_tflops": fl_exec * units_per_launch / (sweep_ms / 1e3) / 1e12,
+                    "peak_source": "in-run FFMA2/DFMA chain probe (tools/peak.cu); MEASURED_PEAKS.json has no CUDA-core peak",
+                    "hbm": {"achieved": bpt * units_per_launch / (sweep_ms / 1e3) / 1e9, "peak": hbm_peak,
+                            "unit": "GB/s",
+                            "note": ("streamed tile: bytes are the tile's read+write per step; when the per-CTA "
+                                     "scratch fits L2 (cfg3) the traffic is served by L2 and frac can exceed 1")
+                            if streamed else "resident tile: x read once, E written, W/B/V amortised",
+                            "frac": bpt * units_per_launch / (sweep_ms / 1e3) / 1e9 / hbm_peak,
+                            "bytes_per_tfbin": bpt, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"}}
+        out = {"value": value, "ms_per_step": ms / args.steps, "roofline": roofline, "inputs": inputs,
+               "gpu_launches": int(timing.launches), "clocks": clk.summary(),
+               "kernels": {"sweep_ms_per_iteration": sweep_ms, "mu_ms_per_iteration": timing.mu_ms / args.steps,
+                           "variant": desc}}
+        bin_range = s.bin_range
+        s.close()
+        out["e2e"] = None
+        if e2e_on:
+            out["e2e"] = run_e2e(args, LB, x, prec, device, world, rank, new_comm_id(), barrier, max_over_ranks,
+                                 bin_range, (B, F, T, M, N, L, K, R, D, iters, c))
+        del x
+        return out
+
     mp = measured_peaks()
     hbm_peak = mp.get("hbm_gbs", 6650.0)
-    c = 8 if prec == "f32" else 16
-    streamed = desc["sweep_kernel"].startswith("stream_kernel")
-    bpt = bytes_per_tfbin(M, N, K, R, D, T, F, c)
-    if streamed:  # SURVEY §8(d) streamed sweep: every step reads and writes the R x T tile
-        bpt = 2 * M * c + R * c + 2 * R * R * c + bpt - M * c
-    roofline = {"bound": "fp32-cuda-core" if prec == "f32" else "fp64-cuda-core",
-                "bound_note": ("compute-bound on the CUDA-core FMA pipes: neither HBM-bound (the hbm sub-object "
-                               "shows a few % of HBM) nor a tensor-core contraction (each ISS step is R "
-                               "differently weighted inner products; the fp32/fp64 tolerances rule out "
-                               "bf16/tf32), so the peak is the FFMA2/DFMA chain rate measured in this run"),
-                "achieved": achieved,
-                "peak": peak, "unit": "TFLOP/s", "frac": (achieved / peak) if peak else None,
-                "traffic": traffic_per_tfbin * units_per_launch if traffic_per_tfbin else None,
-                "kernel": desc["sweep_kernel"], "kernel_ms": sweep_ms,
-                "flops_per_tfbin": fl_sweep, "units_per_launch": units_per_launch,
-                "flops_note": "algorithmic (SURVEY 8(d): 20R^2 + 16RD + 8NK for the sweep kernel's share)",
-                "executed_flops_per_tfbin": fl_exec,
-                "executed_tflops": fl_exec * units_per_launch / (sweep_ms / 1e3) / 1e12,
-                "peak_source": "in-run FFMA2/DFMA chain probe (tools/peak.cu); MEASURED_PEAKS.json has no CUDA-core peak",
-                "hbm": {"achieved": bpt * units_per_launch / (sweep_ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
-                        "note": ("streamed tile: bytes are the tile's read+write per step; when the per-CTA "
-                                 "scratch fits L2 (cfg3) the traffic is served by L2 and frac can exceed 1")
-                        if streamed else "resident tile: x read once, E written, W/B/V amortised",
-                        "frac": bpt * units_per_launch / (sweep_ms / 1e3) / 1e9 / hbm_peak,
-                        "bytes_per_tfbin": bpt, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"}}
-    gpu_launches = int(timing.launches)
-
-    # ---- end to end through the public C-ABI call with host buffers
-    s.close()
-    e2e = None
-    if not args.no_e2e:
-        e2e = run_e2e(args, LB, x, prec, device, world, rank, new_comm_id(), barrier, max_over_ranks, s.bin_range,
-                      (B, F, T, M, N, L, K, R, D, iters, c))
-    del x
+    peaks = peak_probe(device) if rank == 0 else (None, None)
+    main_m = measure(args.dtype, not args.no_e2e, True)
+    extra = None
+    if args.cfg == 1 and args.dtype == "f64" and not args.no_f32:  # configs[1] asks for both precisions
+        extra = measure("f32", not args.no_e2e, False)
     frontend = None
     if rank == 0 and not args.no_frontend:
         frontend = bench_frontend(args, LB, device, B, M, T, hbm_peak)
@@ -381,16 +419,21 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_reference_arm(args, args.cfg, steps=8, warmup=1)
             cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
-        clocks = clk.summary()
-        line = {"metric": "TF-bin*iter/s of the ISS+NMF loop", "value": value, "unit": "TF-bin*iter/s",
-                "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps,
-                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": prec,
+        line = {"metric": "TF-bin*iter/s of the ISS+NMF loop", "value": main_m["value"], "unit": "TF-bin*iter/s",
+                "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
+                "ms_per_step": main_m["ms_per_step"],
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": args.dtype,
                 "data": "synthetic (BASELINE configs generator, seeded; no public dataset)", "config": config,
-                "roofline": roofline, "cpu_baseline": cpu,
-                "e2e": e2e,
-                "gpu_launches": gpu_launches, "clocks": clocks, "frontend": frontend,
-                "kernels": {"sweep_ms_per_iteration": sweep_ms, "mu_ms_per_iteration": timing.mu_ms / args.steps,
-                            "variant": desc}}
+                "inputs": main_m["inputs"], "roofline": main_m["roofline"], "cpu_baseline": cpu,
+                "e2e": main_m["e2e"], "gpu_launches": main_m["gpu_launches"], "clocks": main_m["clocks"],
+                "frontend": frontend, "kernels": main_m["kernels"]}
+        if extra is not None:
+            line["f32"] = {"value": extra["value"], "unit": "TF-bin*iter/s", "ms_per_step": extra["ms_per_step"],
+                           "e2e": extra["e2e"], "roofline": {k: extra["roofline"][k] for k in
+                                                             ("achieved", "peak", "unit", "frac", "kernel",
+                                                              "kernel_ms", "executed_tflops")},
+                           "gpu_launches": extra["gpu_launches"], "clocks": extra["clocks"],
+                           "note": "BASELINE configs[1] fp32 run (same workload, complex64 inputs, fp32 compute)"}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

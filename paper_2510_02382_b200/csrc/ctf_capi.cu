@@ -1087,6 +1087,8 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host,
   c->R = c->D;
   c->N = prob->num_sources;
   c->real_size = prob->precision == CTF_F32 ? 4 : 8;
+  // evaluated identically on every rank, so all ranks fail before the first collective
+  if (c->F < c->world) throw CtfError(CTF_ERR_CONFIG, "more ranks than frequency bins");
   ctf_shard_range(c->F, c->world, c->rank, &c->lo, &c->hi);
   c->FL = c->hi - c->lo;
   if (c->FL < 1) throw CtfError(CTF_ERR_CONFIG, "more ranks than frequency bins");
@@ -1364,6 +1366,10 @@ int ctf_set_state(ctf_ctx* c, const double* W, const double* Bh, const double* V
   return guarded(err, [&] {
     if (!c || !c->ready) throw CtfError(CTF_ERR_CONFIG, "ctf_setup has not been called");
     CK(cudaSetDevice(c->device));
+    // a deferred rescale/objective of an async iteration applies to the
+    // state as it stands before any factor is replaced (W or B kept as NULL
+    // must not miss its rescale)
+    if (c->pending) iterate_impl(c, 0, true);
     if (W) {
       std::vector<double> w((size_t)c->B * plane_stride(c) * 2);
       const size_t per = (size_t)c->R * c->D * 2;
@@ -1372,9 +1378,16 @@ int ctf_set_state(ctf_ctx* c, const double* W, const double* Bh, const double* V
       upload_real(c, c->W.p, w.data(), w.size());
       // exact log|det W| for the externally supplied state (estimator.cpp:41-53)
       const int nb = c->B * c->FL;
-      const size_t smem = (size_t)c->R * c->R * 2 * c->real_size;
-      if (c->real_size == 4) ctf::logdet_kernel<float><<<nb, 32, smem, c->stream>>>(c->W.p, c->logdet.p, c->R, nb);
-      else ctf::logdet_kernel<double><<<nb, 32, smem, c->stream>>>(c->W.p, c->logdet.p, c->R, nb);
+      const size_t smem = (size_t)c->R * c->R * 2 * c->real_size;  // fp64 R = 60: 57,600 B > the 48 KiB default
+      if (c->real_size == 4) {
+        CK(cudaFuncSetAttribute((const void*)ctf::logdet_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+        ctf::logdet_kernel<float><<<nb, 32, smem, c->stream>>>(c->W.p, c->logdet.p, c->R, nb);
+      } else {
+        CK(cudaFuncSetAttribute((const void*)ctf::logdet_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+        ctf::logdet_kernel<double><<<nb, 32, smem, c->stream>>>(c->W.p, c->logdet.p, c->R, nb);
+      }
       CK(cudaGetLastError());
     }
     if (Bh) {  // [B][N] F x K_n column-major -> [B][FL][SK]

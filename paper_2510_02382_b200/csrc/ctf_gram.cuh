@@ -1053,12 +1053,13 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
     __syncthreads();  // Pq is rewritten by the next group
   }
   CTF_PHASE(8);
-  // check_all_finite on Y (estimator.cpp:497-499): a non-finite estimate
-  // makes its row's power sum non-finite
-  bool ybad = false;
+  // check_all_finite (estimator.cpp:494-499): W' first (code 1), then Y
+  // (code 2; a non-finite estimate makes its row's power sum non-finite)
+  bool ybad = false, wbad = false;
 #pragma unroll
   for (int i = 0; i < R; ++i) ybad |= !isfinite(rp[i]);
-  if (ybad) s_bad = 1;
+  for (int i = tid; i < R * D; i += NT) wbad |= !cfinite(Wf[i]);
+  if (ybad || wbad) atomicOr(&s_bad, (wbad ? 2 : 0) | (ybad ? 1 : 0));
   // row powers (estimator.cpp:391-397)
   Real rr[32];
 #pragma unroll
@@ -1067,7 +1068,7 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
   red[warp * 32 + lane] = rr[0];
   __syncthreads();
   if (s_bad) {
-    if (tid == 0) record_err<Real>(p.err, mix, err_key(p.iteration, kPhFinite, gbin, 0, 2));
+    if (tid == 0) record_err<Real>(p.err, mix, err_key(p.iteration, kPhFinite, gbin, 0, (s_bad & 2) ? 1 : 2));
     return;
   }
   if (tid < R) {

@@ -24,28 +24,38 @@ def rel(a, b):
     return float(np.linalg.norm(np.ravel(a - b)) / max(np.linalg.norm(np.ravel(b)), 1e-300))
 
 
-def gpu_history(x, taps, bases, iters, precision, seed, stack_taps):
+def gpu_history(x, taps, bases, iters, precision, seed, stack_taps, images=False):
     """State after every iteration: one ctf_iterate(1) per step (each call
     ends with the trailing rescale + objective, so the state equals the
-    reference's after that many iterations)."""
+    reference's after that many iterations). images=True also records the
+    separated signals the GPU projects back after every iteration
+    (ctf_project_back, wiener.cpp:11-49)."""
     s = Session(x, taps, bases, stack_taps=stack_taps, iterations=iters, precision=precision, seed=seed)
     hist = []
     for _ in range(iters):
         s.iterate(1)
         W, B, V, obj = s.download_raw()
-        hist.append((W, B, V, obj))
+        hist.append((W, B, V, obj, s.project_back() if images else None))
     s.close()
     return hist
 
 
-def check_history(hist, ref, b, tol, what=""):
+def check_history(hist, ref, b, tol, what="", x=None, taps=None, bases=None):
+    """W, B, V and the objective after every iteration; with x given also the
+    separated signals (the GPU's projected-back images against the images the
+    reference state yields, reconstruct_images wiener.cpp:11-49)."""
     F = ref["hist_W"].shape[1]
-    for it, (W, B, V, obj) in enumerate(hist):
+    for it, (W, B, V, obj, img) in enumerate(hist):
         eW = rel(W[b], ref["hist_W"][it].reshape(F, -1))
         eB = rel(B[b], ref["hist_B"][it])
         eV = rel(V[b], ref["hist_V"][it])
         eo = abs(obj[b, it] - ref["objective"][it]) / abs(ref["objective"][it])
-        assert max(eW, eB, eV, eo) <= tol, f"{what} it={it + 1}: W={eW:.2e} B={eB:.2e} V={eV:.2e} obj={eo:.2e}"
+        eY = 0.0
+        if x is not None and img is not None:
+            want = O.reconstruct_images(O.config(taps, bases), ref["hist_W"][it], x)
+            eY = rel(img[:, b], want)
+        assert max(eW, eB, eV, eo, eY) <= tol, \
+            f"{what} it={it + 1}: W={eW:.2e} B={eB:.2e} V={eV:.2e} obj={eo:.2e} images={eY:.2e}"
 
 
 # ---------------------------------------------------------------------------
@@ -58,8 +68,36 @@ def test_golden_fixtures_fp64(name):
         xin, st = raw[None], c["L"]
     else:
         xin, st = x[None], 1
-    hist = gpu_history(xin, taps, bases, c["iters"], "f64", c["seed"], st)
-    check_history(hist, {k: g[k] for k in g.files}, 0, 1e-9, name)
+    hist = gpu_history(xin, taps, bases, c["iters"], "f64", c["seed"], st, images=True)
+    check_history(hist, {k: g[k] for k in g.files}, 0, 1e-9, name, x=x, taps=taps, bases=bases)
+
+
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_cfg0_full_against_reference_fixture(precision):
+    """BASELINE configs[0] at full size against the fixture the reference's
+    own code produced (oracle/_ref): fp64 1e-9 on W, B, V at the checkpoints
+    and on the objective after every one of the 100 iterations; fp32 1e-4
+    relative L2 at the checkpoints and 1e-3 on the final cost."""
+    from tests.test_golden import load_case
+    mg, c, raw, x, taps, bases, g = load_case("cfg0_full")
+    assert mg.digest(raw) == str(g["x_sha256"])
+    F = c["F"]
+    xin = raw[None] if precision == "f64" else raw[None].astype(np.complex64)
+    s = Session(xin, taps, bases, stack_taps=c["L"], iterations=c["iters"], precision=precision, seed=c["seed"])
+    done = 0
+    tol = 1e-9 if precision == "f64" else 1e-4
+    for k in g["checkpoints"]:
+        s.iterate(int(k) - done)
+        done = int(k)
+        W, B, V, obj = s.download_raw()
+        errs = (rel(W[0], g[f"W_{k}"].reshape(F, -1)), rel(B[0], g[f"B_{k}"]), rel(V[0], g[f"V_{k}"]))
+        assert max(errs) <= tol, (precision, k, errs)
+    s.close()
+    eobj = np.abs(obj[0] - g["objective"]) / np.abs(g["objective"])
+    if precision == "f64":
+        assert eobj.max() <= 1e-9, eobj.max()
+    else:
+        assert eobj[-1] <= 1e-3, eobj[-1]
 
 
 def test_cfg0_full_100_iterations_fp64_every_iteration():
@@ -80,7 +118,7 @@ def test_cfg0_fp32_tolerances():
                 O.stack_observation(raw[0], L), history=True)
     hist = gpu_history(raw.astype(np.complex64), [L] * N, [K] * N, iters, "f32", seed, L)
     worst = 0.0
-    for it, (W, B, V, obj) in enumerate(hist):
+    for it, (W, B, V, obj, _) in enumerate(hist):
         e = max(rel(W[0], ref["hist_W"][it].reshape(F, -1)), rel(B[0], ref["hist_B"][it]),
                 rel(V[0], ref["hist_V"][it]))
         worst = max(worst, e)
@@ -104,7 +142,7 @@ def test_fp32_trajectory_cfg_geometries(M, L, T, K, rho):
     kern = json.loads(s.describe())["sweep_kernel"]
     s.close()
     hist = gpu_history(raw.astype(np.complex64), [L] * M, [K] * M, iters, "f32", seed, L)
-    for it, (W, B, V, obj) in enumerate(hist):
+    for it, (W, B, V, obj, _) in enumerate(hist):
         e = max(rel(W[0], ref["hist_W"][it].reshape(F, -1)), rel(B[0], ref["hist_B"][it]),
                 rel(V[0], ref["hist_V"][it]))
         assert e <= 1e-4, f"{kern} it={it + 1}: {e:.2e}"
@@ -614,7 +652,7 @@ def test_ip_rule_fp32_tolerance_and_iss_vs_ip():
     ref = O.run(O.config([L] * M, [K] * M, iterations=iters, seed=seed, threads=NPROC, rule="ip"),
                 O.stack_observation(raw[0], L), history=True)
     hist = _ip_history(raw.astype(np.complex64), L, K, iters, "f32", seed)
-    for it, (W, B, V, obj) in enumerate(hist):
+    for it, (W, B, V, obj, _) in enumerate(hist):
         e = max(rel(W[0], ref["hist_W"][it].reshape(F, -1)), rel(B[0], ref["hist_B"][it]),
                 rel(V[0], ref["hist_V"][it]))
         assert e <= 1e-4, f"it={it + 1}: {e:.2e}"
@@ -716,7 +754,7 @@ def test_covariance_kernel_odd_frame_counts(M, L, T, prec):
                 O.stack_observation(raw[0], L), history=True)
     hist = gpu_history(x, [L] * M, [K] * M, iters, prec, seed, L)
     tol = 1e-9 if prec == "f64" else 1e-4
-    for it, (W, B, V, obj) in enumerate(hist):
+    for it, (W, B, V, obj, _) in enumerate(hist):
         e = max(rel(W[0], ref["hist_W"][it].reshape(F, -1)), rel(B[0], ref["hist_B"][it]),
                 rel(V[0], ref["hist_V"][it]))
         assert e <= tol, f"it={it + 1}: {e:.2e}"
