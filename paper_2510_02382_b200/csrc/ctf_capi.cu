@@ -162,6 +162,15 @@ struct ctf_ctx {
   int kmax = 0, chunk_bins = 0, nchunk = 0;
   int stream_grid = 0;
   int cluster_size = 0;
+  // conditioning fallback of the covariance-domain kernel: the frame-domain
+  // variant that re-runs the bins it hands over (SweepParams::fb_mode)
+  bool has_fb = false;
+  ctf::SweepVariant fbv{};
+  ctf::SweepParams sp_fb{};
+  size_t fb_smem = 0;
+  int fb_nt = 0, fb_grid = 0;
+  double fb_theta = 0.0;
+  DevBuf<int> fb_list, fb_count;
   // device buffers
   DevBuf<unsigned char> x, W, Bf, V, E, part, packed, scratch, cpivot, cwpivot;
   DevBuf<double> cpart;
@@ -376,7 +385,6 @@ void plan_sweep(ctf_ctx* c) {
   CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
   max_smem -= 1024;  // static shared memory of the kernel + reserve
   const size_t rs = c->real_size, cs = 2 * rs;
-  bool found = false;
   int force[5] = {0, 0, -1, 0, -1};
   if (const char* env = std::getenv("CTF_SWEEP_VARIANT"))
     std::sscanf(env, "%d,%d,%d,%d,%d", &force[0], &force[1], &force[2], &force[3], &force[4]);
@@ -384,19 +392,22 @@ void plan_sweep(ctf_ctx* c) {
   if (const char* env = std::getenv("CTF_SWEEP_KIND")) force_kind = std::atoi(env);
   int force_ag = -1;  // frame-split exchange: 0 owner scheme, 1 all-gather
   if (const char* env = std::getenv("CTF_FSPLIT_AG")) force_ag = std::atoi(env);
-  ctf::SweepVariant best{};
-  size_t best_smem = 0;
-  int best_nt = 0, best_rank = 0;
   const int lmax = std::max(1, *std::max_element(c->taps, c->taps + c->N));
   const int loff = ((lmax + 3) / 4) * 4;
-  const int want_chk = c->prob.checks != 0;
-  const int want_ip = c->prob.update_rule == CTF_RULE_IP;
+  const bool want_chk = c->prob.checks != 0;
+  const bool want_ip = c->prob.update_rule == CTF_RULE_IP;
+  // best variant of kind only_kind (< 0: any) for the problem; pins: honour
+  // the CTF_SWEEP_VARIANT / CTF_FSPLIT_AG profiling pins
+  auto search = [&](int only_kind, bool chk, bool ip, bool pins, ctf::SweepVariant& best, size_t& best_smem,
+                    int& best_nt, ctf::SweepParams& best_sp, int& best_TP) {
+  bool found = false;
+  int best_rank = 0;
   for (const auto& v : vars) {
-    if (v.chk != want_chk) continue;  // CheckOptions runs on the instrumented variants only
-    if (v.ip != want_ip) continue;    // the IP rule runs on the covariance-domain IP variants only
-    if (force_kind >= 0 && v.kind != force_kind) continue;
-    if (force_ag >= 0 && v.kind == 5 && v.ag != force_ag) continue;
-    if (force[0] && (v.rmax != force[0] || v.ft != force[1] || v.rreg != force[2] || v.maxt != force[3] ||
+    if (v.chk != (int)chk) continue;  // CheckOptions runs on the instrumented variants only
+    if (v.ip != (int)ip) continue;    // the IP rule runs on the covariance-domain IP variants only
+    if (only_kind >= 0 && v.kind != only_kind) continue;
+    if (pins && force_ag >= 0 && v.kind == 5 && v.ag != force_ag) continue;
+    if (pins && force[0] && (v.rmax != force[0] || v.ft != force[1] || v.rreg != force[2] || v.maxt != force[3] ||
                      (force[4] >= 0 && v.exact != force[4])))
       continue;
     const int nt = v.maxt;  // exact CTA size of the variant
@@ -582,7 +593,7 @@ void plan_sweep(ctf_ctx* c) {
                      (v.kind == 4 ? gram_rank : v.kind == 3 ? 3000 : v.kind == 2 ? 2000 : v.kind == 5 ? (c->R > 16 ? -2000 : 4000) + v.cs + (1 - v.ag) : v.kind == 1 ? 1000 : 0) +
                      (v.kind == 3 ? -v.rmax * 4 : v.rmax * 4) + (v.exact ? 0 : 2) + (v.lt > 0 ? 0 : 1);
     const bool better = !found || rank < best_rank ||
-                        (rank == best_rank && (TP < c->TP || (TP == c->TP && nt < best_nt)));
+                        (rank == best_rank && (TP < best_TP || (TP == best_TP && nt < best_nt)));
     if (better) {
       found = true;
       best = v;
@@ -593,10 +604,17 @@ void plan_sweep(ctf_ctx* c) {
         cand.loff = loff;
         cand.lp = loff + TP;
       }
-      c->TP = TP;
-      c->sp = cand;
+      best_TP = TP;
+      best_sp = cand;
     }
   }
+  return found;
+  };
+  ctf::SweepVariant best{};
+  size_t best_smem = 0;
+  int best_nt = 0, best_TP = 0;
+  const bool found = search(force_kind, want_chk, want_ip, true, best, best_smem, best_nt, c->sp, best_TP);
+  c->TP = best_TP;
   if (!found && want_ip)
     throw CtfError(CTF_ERR_CONFIG,
                    "update rule 'ip' on the GPU runs on the covariance-domain kernel: it needs the stacked "
@@ -643,11 +661,11 @@ void plan_sweep(ctf_ctx* c) {
     const char* env = std::getenv("CTF_PREFETCH");
     if (!(env && std::atoi(env) == 0)) c->sp.pf_stride = std::max(1, per_sm) * nsm;
   }
-  ctf::SweepParams& sp = c->sp;
+  auto finish = [&](ctf::SweepParams& sp, int TP) {
   sp.FL = c->FL;
   sp.bin_lo = c->lo;
   sp.T = c->T;
-  sp.TP = c->TP;
+  sp.TP = TP;
   sp.Mx = c->Mx;
   sp.Ls = c->Ls;
   sp.D = c->D;
@@ -669,6 +687,31 @@ void plan_sweep(ctf_ctx* c) {
   for (int ch = 0; ch < c->D && ch < ctf::kMaxRows; ++ch) {
     const int m = ch / c->Ls, l = ch - m * c->Ls;
     sp.xcol[ch] = m * sp.xp + sp.xoff - l;
+  }
+  sp.fb_mode = 0;
+  };
+  finish(c->sp, c->TP);
+  // Conditioning fallback (SweepParams::fb_mode): the ISS covariance-domain
+  // kernel hands bins whose Gram form is ill-conditioned in this precision to
+  // the best frame-domain variant for the same problem (kappa threshold: fp32
+  // 64, healthy bins measure 5-17; fp64 1e7). CTF_GRAM_FALLBACK=0 disables it.
+  c->has_fb = false;
+  const char* fb_env = std::getenv("CTF_GRAM_FALLBACK");
+  if (best.kind == 4 && !want_ip && !want_chk && !(fb_env && std::atoi(fb_env) == 0)) {
+    int fb_TP = 0;
+    if (search(0, false, false, false, c->fbv, c->fb_smem, c->fb_nt, c->sp_fb, fb_TP)) {
+      c->has_fb = true;
+      finish(c->sp_fb, fb_TP);
+      c->sp_fb.pf_stride = 0;
+      c->fb_theta = c->real_size == 4 ? 64.0 : 1e7;
+      if (const char* th = std::getenv("CTF_GRAM_FALLBACK_THETA")) c->fb_theta = std::atof(th);
+      CK(cudaFuncSetAttribute((const void*)c->fbv.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)c->fb_smem));
+      int per_sm = 0, nsm = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c->fbv.fn, c->fb_nt, c->fb_smem));
+      CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+      c->fb_grid = std::max(1, std::min(std::max(1, per_sm) * nsm, c->B * c->FL));
+    }
   }
 }
 
@@ -906,6 +949,7 @@ void launch_apply(ctf_ctx* c, int mode, int obj_slot, int do_v) {
 template <class Real>
 void run_body(ctf_ctx* c, bool do_sweep) {
   ctf::SweepParams sp = c->sp;
+  auto fill = [&](ctf::SweepParams& sp) {
   sp.x = c->x.p;
   sp.W = c->W.p;
   sp.Bf = c->Bf.p;
@@ -923,6 +967,11 @@ void run_body(ctf_ctx* c, bool do_sweep) {
   sp.iteration = c->done + 1;
   sp.do_sweep = do_sweep ? 1 : 0;
   sp.has_prev = c->pending ? 1 : 0;
+  sp.fb_list = c->fb_list.p;
+  sp.fb_count = c->fb_count.p;
+  sp.fb_theta = c->fb_theta;
+  };
+  fill(sp);
   const int obj_slot = c->pending ? c->done - 1 : -1;
 
   cudaEvent_t e0 = take_event(c), e1 = take_event(c), e2 = take_event(c);
@@ -971,7 +1020,19 @@ void run_body(ctf_ctx* c, bool do_sweep) {
     st.ngroups = (c->R + c->sv.rreg - 1) / c->sv.rreg;
     c->sv.sfn<<<c->stream_grid, c->NT, c->sweep_smem, c->stream>>>(st);
   } else if (c->sv.kind == 4) {
+    if (c->has_fb) {
+      CK(cudaMemsetAsync(c->fb_count.p, 0, sizeof(int), c->stream));
+      sp.fb_mode = 1;
+    }
     c->sv.gfn<<<dim3(c->FL, c->B), c->NT, c->sweep_smem, c->stream>>>(sp, c->gtab.p);
+    if (c->has_fb) {  // the bins the Gram form handed over, in the frame domain
+      CK(cudaGetLastError());
+      ctf::SweepParams fp = c->sp_fb;
+      fill(fp);
+      fp.fb_mode = 2;
+      c->fbv.fn<<<c->fb_grid, c->fb_nt, c->fb_smem, c->stream>>>(fp);
+      c->timing.launches += 1;
+    }
   } else {
     c->sv.fn<<<dim3(c->FL, c->B), c->NT, c->sweep_smem, c->stream>>>(sp);
   }
@@ -1134,6 +1195,10 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host,
   c->mp_part.alloc((size_t)c->B * c->FL);
   c->err.alloc((size_t)c->B);
   c->chk.alloc((size_t)c->B * 2);
+  if (c->has_fb) {
+    c->fb_list.alloc((size_t)c->B * c->FL);
+    c->fb_count.alloc(1);
+  }
   if (c->sv.kind == 2) c->scratch.alloc((size_t)c->stream_grid * c->R * c->TP * cs);
   else c->scratch.free();
   if (c->sv.kind == 3) {
@@ -1451,13 +1516,15 @@ int ctf_describe(ctf_ctx* c, char* buf, int len) {
   std::snprintf(buf, (size_t)len,
                 "{\"sweep_kernel\": \"%s<%s,RMAX=%d,FT=%d,%s=%d,NT=%d,EXACT=%d>\", \"threads\": %d, "
                 "\"smem_bytes\": %zu, \"grid\": [%d, %d], \"muv_chunks\": %d, \"bins\": [%d, %d], "
-                "\"world\": %d, \"rank\": %d, \"collective\": \"%s\", \"cluster\": %d}",
+                "\"world\": %d, \"rank\": %d, \"collective\": \"%s\", \"cluster\": %d, "
+                "\"gram_fallback\": %s, \"fallback_theta\": %g, \"fallback_kernel\": \"sweep_kernel<RMAX=%d,FT=%d,RREG=%d,NT=%d>\"}",
                 c->sv.kind == 5 ? "fsplit_kernel" : c->sv.kind == 4 ? "gram_kernel" : c->sv.kind == 3 ? "cluster_kernel" : c->sv.kind == 2 ? "stream_kernel" : c->sv.kind ? "rowwarp_kernel" : "sweep_kernel",
                 c->real_size == 4 ? "f32" : "f64", c->sv.rmax, c->sv.ft,
                 c->sv.kind == 4 ? "M" : (c->sv.kind == 3 || c->sv.kind == 5) ? "RREG" : c->sv.kind == 2 ? "RG" : c->sv.kind ? "WPR" : "RREG", c->sv.rreg, c->sv.maxt, c->sv.exact, c->NT,
                 c->sweep_smem, c->FL, c->B, c->nchunk, c->lo, c->hi, c->world, c->rank,
                 c->group ? "host-group" : c->comm ? "nccl" : "none",
-                (c->sv.kind == 3 || c->sv.kind == 5) ? c->cluster_size : 1);
+                (c->sv.kind == 3 || c->sv.kind == 5) ? c->cluster_size : 1, c->has_fb ? "true" : "false",
+                c->fb_theta, c->fbv.rmax, c->fbv.ft, c->fbv.rreg, c->fbv.maxt);
   return CTF_OK;
 }
 
@@ -1618,10 +1685,13 @@ void compute_images(ctf_ctx* c, int mode, DevBuf<double>& out) {
     ip.ntaps[n] = c->taps[n];
   }
   const size_t cs = 2 * (size_t)c->real_size;
-  const size_t smem = (size_t)(2 * c->R * c->R + c->R * c->D) * cs + (size_t)c->Mx * (c->Ls - 1 + c->T) * cs;
+  const size_t smem_mats = (size_t)(2 * c->R * c->R + c->R * c->D) * cs;
+  const size_t smem_x = (size_t)c->Mx * (c->Ls - 1 + c->T) * cs;
   int max_smem = 0;
   CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
-  if (smem > (size_t)max_smem) throw CtfError(CTF_ERR_UNSUPPORTED, "projection-back tile exceeds shared memory");
+  if (smem_mats > (size_t)max_smem) throw CtfError(CTF_ERR_UNSUPPORTED, "projection-back tile exceeds shared memory");
+  ip.stage_x = smem_mats + smem_x <= (size_t)max_smem ? 1 : 0;  // cfg4 (6 x 4009 frames): x read from global
+  const size_t smem = ip.stage_x ? smem_mats + smem_x : smem_mats;
   CK(cudaMemsetAsync(c->err.p, 0xFF, c->err.n * 8, c->stream));
   if (c->real_size == 4) {
     CK(cudaFuncSetAttribute((const void*)ctf::image_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
   Real* red = reinterpret_cast<Real*>(smem + p.off_red);  // 32 * NW
   Real* Bs = reinterpret_cast<Real*>(smem + p.off_b);
   double* dred = reinterpret_cast<double*>(smem + p.off_d);
-  __shared__ int s_bad, s_badrow;
+  __shared__ int s_bad, s_badrow, s_fb;
   __shared__ double s_logmu;
   __shared__ Real fac_s[R];  // (1 - z_r) of the ISS steps (determinant lemma)
   constexpr int kNoRow = 1 << 30;
@@ -216,6 +216,7 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
 
   if (tid == 0) {
     s_bad = 0;
+    s_fb = 0;
     s_badrow = kNoRow;
     s_logmu = mu ? p.logmu[mix] : 0.0;
   }
@@ -639,6 +640,28 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
       const int rr = rowvk[k] ? rowk[k] : 0;
       row_sums(k, Wb + rr, R, Yt + rr * LT1, nre, nim, den);
       if (hl == 0 && rowvk[k]) red[rowk[k]] = den;
+      if constexpr (!WIDE && !IP) {
+        // conditioning of the Gram form for this row: the quadratic form
+        // w^H Q w = sum_t |y(t)|^2 / lambda cancels when lambda is small
+        // where |x| is not (NMF activations near the floor); its rounding
+        // error grows with kappa = sum_c |w_c|^2 Q(c,c) / w^H Q w, while the
+        // frame-domain sums (sweep_kernel) do not. Over fb_theta: the bin is
+        // handed to the frame-domain kernel (fb_mode 1).
+        if (p.fb_mode == 1) {
+          Real qd = Real(0);
+#pragma unroll
+          for (int c = 0; c < D; ++c)
+            if (c == hl) qd = creg[c].x;
+          Real a = Real(0);
+          if (rowvk[k] && hl < D) {
+            const R2 w = Wb[hl * R + rr];
+            a = (w.x * w.x + w.y * w.y) * qd;
+          }
+#pragma unroll
+          for (int o = LPR / 2; o >= 1; o >>= 1) a += __shfl_xor_sync(kFull, a, o);
+          if (hl == 0 && rowvk[k] && !((double)a <= p.fb_theta * (double)den)) s_fb = 1;
+        }
+      }
     }
     double v1[1] = {logsum};
     block_sum_d<1>(v1, dred, lane, warp, NW);  // contains __syncthreads: red visible after
@@ -650,6 +673,11 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
       return;
     }
     if (tid == 0) p.objbin[tile] = v1[0] + quad - 2.0 * (double)T * logdet;
+    if (s_fb) {  // (visible after block_sum_d's barrier) nothing of this bin is written but objbin,
+                 // which the frame-domain kernel recomputes
+      if (tid == 0) p.fb_list[atomicAdd(p.fb_count, 1)] = (int)tile;
+      return;
+    }
   }
 
   if (!p.do_sweep) {  // finalize pass: write the rescaled state and stop

@@ -74,6 +74,17 @@ struct SweepParams {
   int chk_flags;
   unsigned long long* chk;  // [mix][2]
   int pf_stride;  // > 0: prefetch into L2 the tiles of work item (mix*FL + bin) + pf_stride
+  // Conditioning fallback of the covariance-domain kernel (ctf_gram.cuh):
+  // fb_mode 1 (gram_kernel): a bin whose weighted covariance is too
+  // ill-conditioned for the Gram form in this precision (kappa estimate
+  // sum_c |w_rc|^2 Q_r(c,c) / (w_r^H Q_r w_r) > fb_theta for some row) writes
+  // nothing but appends its work item (mix*FL + bin) to fb_list;
+  // fb_mode 2 (sweep_kernel, the frame-domain form): the CTAs run exactly the
+  // listed items (grid-stride over *fb_count).
+  int fb_mode;
+  int* fb_list;
+  int* fb_count;
+  double fb_theta;
 };
 
 // L2 prefetch of a contiguous block (bulk async, no registers or smem).
@@ -372,8 +383,26 @@ template <typename Real> constexpr int sweep_min_blocks(int nt) {
 // per source with immediate offsets.
 // CHECK: CheckOptions instrumentation (exact recomputation of det W after
 // every step by a warp LU, and of each updated row's weighted power).
+template <typename Real, int RMAX, int FT, int RREG, int NT, bool EXACT, int LT, bool CHECK>
+__device__ __forceinline__ void sweep_body(const SweepParams& p, const int bin, const int mix);
+
 template <typename Real, int RMAX, int FT, int RREG, int NT, bool EXACT, int LT = 0, bool CHECK = false>
 __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(const SweepParams p) {
+  if (p.fb_mode != 2) {  // one work item per CTA: (bin, mixture) = (blockIdx.x, blockIdx.y)
+    sweep_body<Real, RMAX, FT, RREG, NT, EXACT, LT, CHECK>(p, blockIdx.x, blockIdx.y);
+    return;
+  }
+  // conditioning fallback of the covariance-domain kernel: the listed items
+  const int cnt = *p.fb_count;
+  for (int w = blockIdx.x; w < cnt; w += gridDim.x) {
+    const int t = p.fb_list[w];
+    __syncthreads();  // shared memory of the previous item
+    sweep_body<Real, RMAX, FT, RREG, NT, EXACT, LT, CHECK>(p, t % p.FL, t / p.FL);
+  }
+}
+
+template <typename Real, int RMAX, int FT, int RREG, int NT, bool EXACT, int LT, bool CHECK>
+__device__ __forceinline__ void sweep_body(const SweepParams& p, const int bin, const int mix) {
   using R2 = typename Cplx<Real>::T;
   constexpr int RS = RMAX - RREG;
   constexpr int NV = 3 * RMAX;
@@ -384,7 +413,6 @@ __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(c
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT >> 5;
-  const int bin = blockIdx.x, mix = blockIdx.y;
   const int gbin = p.bin_lo + bin;
   // EXACT: R == D == RMAX is a compile-time constant (no row guards).
   const int R = EXACT ? RMAX : p.R, D = EXACT ? RMAX : p.D;
@@ -1125,6 +1153,7 @@ struct ImageParams {
   double* out;       // double2 [n][mix][FL][T][Dout]
   unsigned long long* err;
   int FL, bin_lo, T, Mx, Ls, D, R, N, nmix, current_only;
+  int stage_x;  // 1: the x tile is staged in shared memory; 0: read from global (tiles over 227 KB)
   int row0[kMaxSources], ntaps[kMaxSources];
 };
 
@@ -1151,13 +1180,15 @@ __global__ void __launch_bounds__(256) image_kernel(const ImageParams p) {
     H[i] = czero<Real>();
     if (r == c) H[i].x = Real(1);
   }
-  for (int i = tid; i < p.Mx * xp; i += blockDim.x) {
-    const int m = i / xp, t = i - m * xp - xoff;
-    if (t < 0) xs[i] = czero<Real>();
-  }
-  for (int e = tid; e < T * p.Mx; e += blockDim.x) {
-    const int t = e / p.Mx, m = e - t * p.Mx;
-    xs[m * xp + xoff + t] = xg[e];
+  if (p.stage_x) {
+    for (int i = tid; i < p.Mx * xp; i += blockDim.x) {
+      const int m = i / xp, t = i - m * xp - xoff;
+      if (t < 0) xs[i] = czero<Real>();
+    }
+    for (int e = tid; e < T * p.Mx; e += blockDim.x) {
+      const int t = e / p.Mx, m = e - t * p.Mx;
+      xs[m * xp + xoff + t] = xg[e];
+    }
   }
   __syncthreads();
   if (tid < 32) {
@@ -1224,7 +1255,10 @@ __global__ void __launch_bounds__(256) image_kernel(const ImageParams p) {
       R2 acc = czero<Real>();
       for (int c = 0; c < D; ++c) {
         const int m = c / p.Ls, l = c - m * p.Ls;
-        cmac(acc, Wsm[c * R + r], xs[m * xp + xoff + j - l]);
+        R2 xv;
+        if (p.stage_x) xv = xs[m * xp + xoff + j - l];
+        else xv = j >= l ? xg[(size_t)(j - l) * p.Mx + m] : czero<Real>();
+        cmac(acc, Wsm[c * R + r], xv);
       }
       y[r] = acc;
     }

@@ -626,7 +626,7 @@ def _ip_history(raw, L, K, iters, precision, seed):
     hist = []
     for _ in range(iters):
         s.iterate(1)
-        hist.append(s.download_raw())
+        hist.append(tuple(s.download_raw()) + (None,))
     s.close()
     return hist
 
@@ -775,3 +775,24 @@ def test_zero_iterations_returns_the_initial_state(precision):
     assert rel(W[0], ref["W"].reshape(F, -1)) == 0.0
     tol = 0.0 if precision == "f64" else 1e-7
     assert rel(B[0], ref["B"]) <= tol and rel(V[0], ref["V"]) <= tol
+
+
+@pytest.mark.parametrize("precision,tol,theta", [("f64", 1e-9, "0"), ("f64", 1e-9, "6"), ("f32", 1e-4, "0"),
+                                                 ("f32", 1e-4, "6")])
+def test_gram_conditioning_fallback(monkeypatch, precision, tol, theta):
+    """The covariance-domain kernel hands ill-conditioned bins to the
+    frame-domain kernel (SweepParams::fb_mode). theta 0 forces every bin over
+    from iteration 2 on, theta 6 a data-dependent subset: the trajectory
+    still matches the oracle after every iteration."""
+    monkeypatch.setenv("CTF_GRAM_FALLBACK_THETA", theta)
+    F, T, M, L, K, iters, seed = 9, 300, 2, 5, 4, 6, 2
+    raw = synth_mixtures(1, F, T, M, M, L, K, 0.6, 99)
+    ref = O.run(O.config([L] * M, [K] * M, iterations=iters, seed=seed, threads=NPROC),
+                O.stack_observation(raw[0], L), history=True)
+    x = raw if precision == "f64" else raw.astype(np.complex64)
+    s = Session(x, [L] * M, [K] * M, stack_taps=L, iterations=iters, precision=precision, seed=seed)
+    d = json.loads(s.describe())
+    s.close()
+    assert "gram_kernel" in d["sweep_kernel"] and d["gram_fallback"] is True, d
+    hist = gpu_history(x, [L] * M, [K] * M, iters, precision, seed, L)
+    check_history(hist, ref, 0, tol, f"fallback theta={theta}")
