@@ -630,6 +630,30 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
     den = cd.x;
   };
 
+  // conditioning of the Gram form for row slot k (pre-sweep W): the
+  // quadratic form w^H Q w = sum_t |y(t)|^2 / lambda cancels when lambda is
+  // small where |x| is not (NMF activations near the floor); its rounding
+  // error grows with kappa = sum_c |w_c|^2 Q(c,c) / w^H Q w, while the
+  // frame-domain sums (sweep_kernel) do not. Over fb_theta the bin is handed
+  // to the frame-domain kernel (fb_mode 1). Warp-uniform (every lane calls it).
+  auto cond_check = [&](int k, int rr, Real den) {
+    if constexpr (!WIDE && !IP) {
+      if (p.fb_mode == 1) {
+        Real qd = Real(0);
+#pragma unroll
+        for (int c = 0; c < D; ++c)
+          if (c == hl) qd = creg[c].x;
+        Real a = Real(0);
+        if (rowvk[k] && hl < D) {
+          const R2 w = Wb[hl * R + rr];
+          a = (w.x * w.x + w.y * w.y) * qd;
+        }
+#pragma unroll
+        for (int o = LPR / 2; o >= 1; o >>= 1) a += __shfl_xor_sync(kFull, a, o);
+        if (hl == 0 && rowvk[k] && !((double)a <= p.fb_theta * (double)den)) s_fb = 1;
+      }
+    }
+  };
   double logdet = p.logdet[tile] - s_logmu;
   if (p.has_prev) {
     // objective of the previous iteration (estimator.cpp:55-77): quadratic
@@ -640,28 +664,7 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
       const int rr = rowvk[k] ? rowk[k] : 0;
       row_sums(k, Wb + rr, R, Yt + rr * LT1, nre, nim, den);
       if (hl == 0 && rowvk[k]) red[rowk[k]] = den;
-      if constexpr (!WIDE && !IP) {
-        // conditioning of the Gram form for this row: the quadratic form
-        // w^H Q w = sum_t |y(t)|^2 / lambda cancels when lambda is small
-        // where |x| is not (NMF activations near the floor); its rounding
-        // error grows with kappa = sum_c |w_c|^2 Q(c,c) / w^H Q w, while the
-        // frame-domain sums (sweep_kernel) do not. Over fb_theta: the bin is
-        // handed to the frame-domain kernel (fb_mode 1).
-        if (p.fb_mode == 1) {
-          Real qd = Real(0);
-#pragma unroll
-          for (int c = 0; c < D; ++c)
-            if (c == hl) qd = creg[c].x;
-          Real a = Real(0);
-          if (rowvk[k] && hl < D) {
-            const R2 w = Wb[hl * R + rr];
-            a = (w.x * w.x + w.y * w.y) * qd;
-          }
-#pragma unroll
-          for (int o = LPR / 2; o >= 1; o >>= 1) a += __shfl_xor_sync(kFull, a, o);
-          if (hl == 0 && rowvk[k] && !((double)a <= p.fb_theta * (double)den)) s_fb = 1;
-        }
-      }
+      cond_check(k, rr, den);
     }
     double v1[1] = {logsum};
     block_sum_d<1>(v1, dred, lane, warp, NW);  // contains __syncthreads: red visible after
@@ -673,11 +676,19 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
       return;
     }
     if (tid == 0) p.objbin[tile] = v1[0] + quad - 2.0 * (double)T * logdet;
-    if (s_fb) {  // (visible after block_sum_d's barrier) nothing of this bin is written but objbin,
-                 // which the frame-domain kernel recomputes
-      if (tid == 0) p.fb_list[atomicAdd(p.fb_count, 1)] = (int)tile;
-      return;
+  } else if (!WIDE && !IP && p.fb_mode == 1) {  // first loop body after a finalize: check only
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      Real nre, nim, den;
+      const int rr = rowvk[k] ? rowk[k] : 0;
+      row_sums(k, Wb + rr, R, Yt + rr * LT1, nre, nim, den);
+      cond_check(k, rr, den);
     }
+    __syncthreads();
+  }
+  if (s_fb) {  // nothing of this bin is written (but objbin, which the frame-domain kernel recomputes)
+    if (tid == 0) p.fb_list[atomicAdd(p.fb_count, 1)] = (int)tile;
+    return;
   }
 
   if (!p.do_sweep) {  // finalize pass: write the rescaled state and stop
