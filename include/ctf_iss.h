@@ -293,6 +293,45 @@ int ctf_write_factors(const char* path, int num_sources, int bins, int frames, c
 int ctf_read_factors(const char* path, int* num_sources, int* bins, int* frames, int32_t* bases /* [16] */,
                      double* floor_abs, double* B /* NULL: header only */, double* V, ctf_err* err);
 
+/* ---- Op-level entries: the reference's individual estimator operations
+ * (proj/include/ctfmnmf/estimator.hpp:56-117, model.hpp:86-88) on the GPU in
+ * fp64, for drivers that run the loop piece by piece the way the reference's
+ * own unit tests do (test_estimator.cpp). Shapes come from a ctf_problem
+ * (num_bins F, num_frames T, num_sources, taps_per_source, bases_per_source;
+ * R = D = sum of taps: the already-stacked observation). Layouts:
+ *   W [F] column-major R x D complex;  Y [F] column-major R x T complex
+ *   x [F][T][D] complex;  B / V as ctf_download (one mixture);
+ *   lambda [N] column-major F x T doubles.
+ * mem = CTF_MEM_HOST: host pointers (copied in/out, the call synchronises);
+ * CTF_MEM_DEVICE: device pointers on the context's device, stream-ordered on
+ * ctf_stream(ctx). Errors use the reference's texts and codes. */
+#define CTF_MEM_HOST 0
+#define CTF_MEM_DEVICE 1
+/* demix, estimator.cpp:304-311: Y_i = W_i x_i */
+int ctf_op_demix(ctf_ctx* ctx, int F, int R, int D, int T, const double* W, const double* x, double* Y, int mem,
+                 ctf_err* err);
+/* compute_psd for every source, model.cpp:210-215 */
+int ctf_op_compute_psd(ctf_ctx* ctx, const ctf_problem* prob, const double* B, const double* V, double floor_abs,
+                       double* lambda, int mem, ctf_err* err);
+/* iss_sweep, estimator.cpp:505-511 (steering :434-462, step :476-484) on
+ * every bin; W and Y updated in place. Degeneracy: the lowest failing bin. */
+int ctf_op_iss_sweep(ctf_ctx* ctx, const ctf_problem* prob, double* W, double* Y, const double* lambda, int mem,
+                     ctf_err* err);
+/* mu_update_bases / mu_update_activations for one source,
+ * estimator.cpp:313-346 / :348-382 (all taps contribute) */
+int ctf_op_mu_update_bases(ctf_ctx* ctx, const ctf_problem* prob, double* B, const double* V, double floor_abs,
+                           const double* Y, int source, int mem, ctf_err* err);
+int ctf_op_mu_update_activations(ctf_ctx* ctx, const ctf_problem* prob, const double* B, double* V, double floor_abs,
+                                 const double* Y, int source, int mem, ctf_err* err);
+/* rescale, estimator.cpp:384-412: W, B and Y in place */
+int ctf_op_rescale(ctf_ctx* ctx, const ctf_problem* prob, double* W, double* B, double floor_abs, double* Y, int mem,
+                   ctf_err* err);
+/* log_abs_det of num_bins R x R matrices, estimator.cpp:41-53 */
+int ctf_op_log_abs_det(ctf_ctx* ctx, int R, int num_bins, const double* W, double* out, int mem, ctf_err* err);
+/* objective_from_parts, estimator.cpp:55-77 (out: one double) */
+int ctf_op_objective_from_parts(ctf_ctx* ctx, const ctf_problem* prob, const double* W, const double* lambda,
+                                const double* Y, double* out, int mem, ctf_err* err);
+
 /* Synthetic generator of BASELINE.json configs (host code, no GPU):
  * mixture b uses mt19937_64(base_seed + b); see DESIGN.md for draw order.
  * x_out: [B][F][T][M] complex (double if out_precision == CTF_F64, float

@@ -17,6 +17,7 @@ CTF_OK, CTF_ERR_CONFIG, CTF_ERR_IO, CTF_ERR_DEGENERACY, CTF_ERR_CUDA, CTF_ERR_UN
 CTF_F64, CTF_F32 = 0, 1
 CTF_RULE_IP, CTF_RULE_ISS = 0, 1
 CTF_IMAGES_FULL, CTF_IMAGES_CURRENT_FRAME = 0, 1
+CTF_MEM_HOST, CTF_MEM_DEVICE = 0, 1
 
 
 class CtfErr(C.Structure):
@@ -99,6 +100,16 @@ SIGNATURES = {
     "ctf_reset_timing": (C.c_int, [_P]),
     "ctf_run": (C.c_int, [_P, C.POINTER(CtfProblem), _P, _D, _D, _D, _D, _E]),
     "ctf_project_back": (C.c_int, [_P, C.c_int, _D, _E]),
+    "ctf_op_demix": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, _D, _D, _D, C.c_int, _E]),
+    "ctf_op_compute_psd": (C.c_int, [_P, C.POINTER(CtfProblem), _D, _D, C.c_double, _D, C.c_int, _E]),
+    "ctf_op_iss_sweep": (C.c_int, [_P, C.POINTER(CtfProblem), _D, _D, _D, C.c_int, _E]),
+    "ctf_op_mu_update_bases": (C.c_int, [_P, C.POINTER(CtfProblem), _D, _D, C.c_double, _D, C.c_int, C.c_int,
+                                         _E]),
+    "ctf_op_mu_update_activations": (C.c_int, [_P, C.POINTER(CtfProblem), _D, _D, C.c_double, _D, C.c_int,
+                                               C.c_int, _E]),
+    "ctf_op_rescale": (C.c_int, [_P, C.POINTER(CtfProblem), _D, _D, C.c_double, _D, C.c_int, _E]),
+    "ctf_op_log_abs_det": (C.c_int, [_P, C.c_int, C.c_int, _D, _D, C.c_int, _E]),
+    "ctf_op_objective_from_parts": (C.c_int, [_P, C.POINTER(CtfProblem), _D, _D, _D, _D, C.c_int, _E]),
     "ctf_synth_mixtures": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
                                      C.c_uint64, C.c_int, _P, C.c_int, _E]),
 }

@@ -343,5 +343,179 @@ NmfFactors read_factors(const std::string& path) {  // container.cpp:144-165
   return f;
 }
 
+// ---- op-level API ---------------------------------------------------------
+namespace {
+
+ctf_problem op_problem(const CtfConfig& config, int F, int T) {
+  if (config.num_sources < 1 || config.num_sources > CTF_MAX_SOURCES) throw ConfigError("n_sources must be in [1, 16]");
+  ctf_problem p{};
+  p.num_mixtures = 1;
+  p.num_bins = F;
+  p.num_frames = T;
+  p.num_sources = config.num_sources;
+  p.stack_taps = 1;
+  p.num_mics = config.total_taps();
+  for (int n = 0; n < config.num_sources; ++n) {
+    p.taps_per_source[n] = config.taps_per_source[static_cast<size_t>(n)];
+    p.bases_per_source[n] =
+        n < static_cast<int>(config.bases_per_source.size()) ? config.bases_per_source[static_cast<size_t>(n)] : 1;
+  }
+  return p;
+}
+
+std::vector<double> pack(const std::vector<CMatrix>& mats) {
+  std::vector<double> out;
+  for (const auto& m : mats)
+    for (const auto& v : m.data) {
+      out.push_back(v.real());
+      out.push_back(v.imag());
+    }
+  return out;
+}
+
+void unpack(const std::vector<double>& buf, std::vector<CMatrix>& mats) {
+  size_t k = 0;
+  for (auto& m : mats)
+    for (auto& v : m.data) {
+      v = Complex(buf[k], buf[k + 1]);
+      k += 2;
+    }
+}
+
+std::vector<double> pack_factors(const std::vector<RMatrix>& fs) {
+  std::vector<double> out;
+  for (const auto& f : fs) out.insert(out.end(), f.data.begin(), f.data.end());
+  return out;
+}
+
+void unpack_factors(const std::vector<double>& buf, std::vector<RMatrix>& fs) {
+  size_t k = 0;
+  for (auto& f : fs)
+    for (auto& v : f.data) v = buf[k++];
+}
+
+CtfConfig factors_config(const NmfFactors& f, const CtfConfig* base) {
+  CtfConfig c = base ? *base : CtfConfig{};
+  c.num_sources = static_cast<int>(f.bases.size());
+  c.bases_per_source.clear();
+  for (const auto& b : f.bases) c.bases_per_source.push_back(b.cols);
+  if (!base) c.taps_per_source.assign(f.bases.size(), 1);
+  return c;
+}
+
+template <class Fn>
+void op_call(const GpuOptions& gpu, Fn&& fn) {
+  Ctx ctx(gpu.device);
+  ctf_err e{};
+  if (fn(ctx.c, &e) != CTF_OK) rethrow(e);
+}
+
+}  // namespace
+
+double log_abs_det(const CMatrix& m, const GpuOptions& gpu) {  // estimator.cpp:41-53
+  const std::vector<double> w = pack({m});
+  double out = 0.0;
+  op_call(gpu, [&](ctf_ctx* c, ctf_err* e) { return ctf_op_log_abs_det(c, m.rows, 1, w.data(), &out, CTF_MEM_HOST, e); });
+  return out;
+}
+
+double objective_from_parts(const std::vector<CMatrix>& demixing, const std::vector<RMatrix>& lambdas,
+                            const DelayedEstimates& estimates, const CtfConfig& config, const GpuOptions& gpu) {
+  const int F = estimates.num_bins(), T = estimates.num_frames();
+  const ctf_problem p = op_problem(config, F, T);
+  const std::vector<double> w = pack(demixing), y = pack(estimates.bins), l = pack_factors(lambdas);
+  double out = 0.0;
+  op_call(gpu, [&](ctf_ctx* c, ctf_err* e) {
+    return ctf_op_objective_from_parts(c, &p, w.data(), l.data(), y.data(), &out, CTF_MEM_HOST, e);
+  });
+  return out;
+}
+
+void iss_sweep(CMatrix& demixing_bin, CMatrix& estimates_bin, const std::vector<RMatrix>& lambdas,
+               const CtfConfig& config, int bin, const GpuOptions& gpu) {  // estimator.cpp:505-511
+  const int T = estimates_bin.cols;
+  const ctf_problem p = op_problem(config, 1, T);
+  std::vector<double> lam;  // row `bin` of every lambda_n as a 1 x T matrix
+  for (const auto& l : lambdas)
+    for (int j = 0; j < T; ++j) lam.push_back(l(bin, j));
+  std::vector<CMatrix> w{demixing_bin}, y{estimates_bin};
+  std::vector<double> wb = pack(w), yb = pack(y);
+  Ctx ctx(gpu.device);
+  ctf_err e{};
+  if (ctf_op_iss_sweep(ctx.c, &p, wb.data(), yb.data(), lam.data(), CTF_MEM_HOST, &e) != CTF_OK) {
+    if (e.code == CTF_ERR_DEGENERACY) throw DegeneracyError(e.msg, -1, bin, e.row);
+    rethrow(e);
+  }
+  unpack(wb, w);
+  unpack(yb, y);
+  demixing_bin = w[0];
+  estimates_bin = y[0];
+}
+
+DelayedEstimates demix(const std::vector<CMatrix>& demixing, const MixtureSpectrogram& x, const GpuOptions& gpu) {
+  const int F = x.num_bins(), T = x.num_frames(), D = x.num_channels();
+  const int R = demixing.empty() ? 0 : demixing[0].rows;
+  std::vector<double> w = pack(demixing), xx = flatten(x), y((size_t)F * R * T * 2);
+  op_call(gpu, [&](ctf_ctx* c, ctf_err* e) {
+    return ctf_op_demix(c, F, R, D, T, w.data(), xx.data(), y.data(), CTF_MEM_HOST, e);
+  });
+  DelayedEstimates out;
+  out.bins.assign(static_cast<size_t>(F), CMatrix(R, T));
+  unpack(y, out.bins);
+  return out;
+}
+
+RMatrix compute_psd(const NmfFactors& factors, int source, const GpuOptions& gpu) {  // model.cpp:210-215
+  const int F = factors.bases[0].rows, T = factors.activations[0].cols;
+  const CtfConfig cfg = factors_config(factors, nullptr);
+  const ctf_problem p = op_problem(cfg, F, T);
+  const std::vector<double> b = pack_factors(factors.bases), v = pack_factors(factors.activations);
+  std::vector<double> lam((size_t)factors.bases.size() * F * T);
+  op_call(gpu, [&](ctf_ctx* c, ctf_err* e) {
+    return ctf_op_compute_psd(c, &p, b.data(), v.data(), factors.floor, lam.data(), CTF_MEM_HOST, e);
+  });
+  RMatrix out(F, T);
+  std::copy(lam.begin() + (size_t)source * F * T, lam.begin() + (size_t)(source + 1) * F * T, out.data.begin());
+  return out;
+}
+
+void mu_update_bases(NmfFactors& factors, const DelayedEstimates& estimates, int source, const CtfConfig& config,
+                     const GpuOptions& gpu) {  // estimator.cpp:313-346
+  const int F = estimates.num_bins(), T = estimates.num_frames();
+  const ctf_problem p = op_problem(factors_config(factors, &config), F, T);
+  std::vector<double> b = pack_factors(factors.bases);
+  const std::vector<double> v = pack_factors(factors.activations), y = pack(estimates.bins);
+  op_call(gpu, [&](ctf_ctx* c, ctf_err* e) {
+    return ctf_op_mu_update_bases(c, &p, b.data(), v.data(), factors.floor, y.data(), source, CTF_MEM_HOST, e);
+  });
+  unpack_factors(b, factors.bases);
+}
+
+void mu_update_activations(NmfFactors& factors, const DelayedEstimates& estimates, int source,
+                           const CtfConfig& config, const GpuOptions& gpu) {  // estimator.cpp:348-382
+  const int F = estimates.num_bins(), T = estimates.num_frames();
+  const ctf_problem p = op_problem(factors_config(factors, &config), F, T);
+  const std::vector<double> b = pack_factors(factors.bases), y = pack(estimates.bins);
+  std::vector<double> v = pack_factors(factors.activations);
+  op_call(gpu, [&](ctf_ctx* c, ctf_err* e) {
+    return ctf_op_mu_update_activations(c, &p, b.data(), v.data(), factors.floor, y.data(), source, CTF_MEM_HOST, e);
+  });
+  unpack_factors(v, factors.activations);
+}
+
+void rescale(std::vector<CMatrix>& demixing, NmfFactors& factors, DelayedEstimates& estimates,
+             const CtfConfig& config, const GpuOptions& gpu) {  // estimator.cpp:384-412
+  const int F = estimates.num_bins(), T = estimates.num_frames();
+  if (F == 0 || T == 0) return;
+  const ctf_problem p = op_problem(factors_config(factors, &config), F, T);
+  std::vector<double> w = pack(demixing), b = pack_factors(factors.bases), y = pack(estimates.bins);
+  op_call(gpu, [&](ctf_ctx* c, ctf_err* e) {
+    return ctf_op_rescale(c, &p, w.data(), b.data(), factors.floor, y.data(), CTF_MEM_HOST, e);
+  });
+  unpack(w, demixing);
+  unpack_factors(b, factors.bases);
+  unpack(y, estimates.bins);
+}
+
 }  // namespace b200
 }  // namespace ctfmnmf

@@ -163,6 +163,29 @@ Spectrogram read_spectrogram(const std::string& path);
 void write_factors(const std::string& path, const NmfFactors& factors);
 NmfFactors read_factors(const std::string& path);
 
+// ---- op-level API (estimator.hpp:15-23, 56-117; model.hpp:86-88) on the GPU
+// (fp64, the ctf_op_* entries of include/ctf_iss.h), for drivers that run the
+// loop piece by piece the way test_estimator.cpp does.
+struct DelayedEstimates {  // estimator.hpp:15-23: one R x T matrix per bin
+  std::vector<CMatrix> bins;
+  int num_bins() const { return static_cast<int>(bins.size()); }
+  int num_rows() const { return bins.empty() ? 0 : bins[0].rows; }
+  int num_frames() const { return bins.empty() ? 0 : bins[0].cols; }
+};
+double log_abs_det(const CMatrix& m, const GpuOptions& gpu = {});
+double objective_from_parts(const std::vector<CMatrix>& demixing, const std::vector<RMatrix>& lambdas,
+                            const DelayedEstimates& estimates, const CtfConfig& config, const GpuOptions& gpu = {});
+void iss_sweep(CMatrix& demixing_bin, CMatrix& estimates_bin, const std::vector<RMatrix>& lambdas,
+               const CtfConfig& config, int bin, const GpuOptions& gpu = {});
+DelayedEstimates demix(const std::vector<CMatrix>& demixing, const MixtureSpectrogram& x, const GpuOptions& gpu = {});
+RMatrix compute_psd(const NmfFactors& factors, int source, const GpuOptions& gpu = {});
+void mu_update_bases(NmfFactors& factors, const DelayedEstimates& estimates, int source, const CtfConfig& config,
+                     const GpuOptions& gpu = {});
+void mu_update_activations(NmfFactors& factors, const DelayedEstimates& estimates, int source,
+                           const CtfConfig& config, const GpuOptions& gpu = {});
+void rescale(std::vector<CMatrix>& demixing, NmfFactors& factors, DelayedEstimates& estimates,
+             const CtfConfig& config, const GpuOptions& gpu = {});
+
 // wiener.hpp:22-24: inverse STFT of one source image; ref_channel < 0 keeps all.
 TimeSignal image_to_signal(const MixtureSpectrogram& image, const Spectrogram& meta, int ref_channel = -1,
                            const GpuOptions& gpu = {});
