@@ -462,7 +462,12 @@ void plan_sweep(ctf_ctx* c) {
       cand.off_l = (int)take((size_t)c->N * glp * rs);
       cand.off_y = (int)take((size_t)c->N * (M * (M + 1) / 2) * NA * NA * cs);  // Hermitian half of the Gram
       const int NS = (c->real_size == 4 && c->R <= 16) ? c->N : 1;  // sources per Gram pass (gram_ns) and demix group
-      cand.off_e = (int)take(std::max((size_t)NS * NA * (nt + 1) * cs, (size_t)NS * L * TP * rs));
+      size_t ebytes = std::max((size_t)NS * NA * (nt + 1) * cs, (size_t)NS * L * TP * rs);
+      if (v.tc) {  // two stages of the tcgen05 Gram operands (ctf_gram.cuh GramTC)
+        const int NG = M * L + (M * (M - 1) / 2) * NA, TILES = (NG + 127) / 128, NP = (M * NA + 15) / 16 * 16;
+        ebytes = std::max(ebytes, (size_t)2 * (2 * 2 * (2 * TILES * 128 * 32) + 2 * 2 * NP * 32));
+      }
+      cand.off_e = (int)take(ebytes);
       cand.off_w = (int)take((size_t)c->R * c->D * cs);
       cand.off_z = (int)take((size_t)(2 * c->R * std::max(1, L - 1) + 2 * (c->D + std::max(1, L - 1))) * cs);
       cand.off_red = (int)take((size_t)32 * NW * rs);
@@ -589,7 +594,10 @@ void plan_sweep(ctf_ctx* c) {
     const int gram_rank = (c->real_size == 8 && c->R <= 4 && !want_ip) ? 500 : -1000;
     // wide covariance tiles (R > 16, one CTA per SM) run best with the most threads
     const int wide_bonus = (v.kind == 4 && c->R > 16) ? -nt / 128 : 0;
-    const int rank = wide_bonus +
+    // tcgen05 Gram: preferred with CTF_GRAM_TC=1, else ranked just after its CUDA-core twin
+    const char* tc_env = std::getenv("CTF_GRAM_TC");
+    const int tc_rank = v.tc ? ((tc_env && std::atoi(tc_env)) ? -6000 : 50) : 0;
+    const int rank = wide_bonus + tc_rank +
                      (v.kind == 4 ? gram_rank : v.kind == 3 ? 3000 : v.kind == 2 ? 2000 : v.kind == 5 ? (c->R > 16 ? -2000 : 4000) + v.cs + (1 - v.ag) : v.kind == 1 ? 1000 : 0) +
                      (v.kind == 3 ? -v.rmax * 4 : v.rmax * 4) + (v.exact ? 0 : 2) + (v.lt > 0 ? 0 : 1);
     const bool better = !found || rank < best_rank ||

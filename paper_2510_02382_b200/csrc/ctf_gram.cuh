@@ -29,6 +29,7 @@
 // Y = W' x~ for the delayed energies, row powers and MU-B.
 #pragma once
 #include "ctf_kernels.cuh"
+#include "ctf_tc.cuh"
 
 #ifndef CTF_LAMV
 #define CTF_LAMV 20
@@ -145,8 +146,35 @@ template <typename Real, int NT, int R> constexpr int gram_min_blocks() {
   return R > 16 ? 1 : std::is_same<Real, float>::value ? (NT <= 256 ? 3 : 1) : (NT <= 256 ? 2 : 1);
 }
 
+// Tensor-core Gram (TC = true, fp32): the lag correlations as one real GEMM
+// per bin on tcgen05 (kind::tf32, 3xTF32 split for fp32 accuracy),
+//   C[(g, re|im)][(n, a)] = sum_u P_g(u) w_n(u - a),  P_g = x_m conj(x_m'(. + d)),
+// rows = the NG (m, m', d) groups' real and imaginary parts (A, K-major:
+// frames contiguous), columns = source x lag a in [-(L-1), L-1] (B, K-major),
+// K = the frames. Products and weights are formed by all threads into a
+// double-buffered shared-memory stage of KC frames (hi and lo tf32 parts);
+// one thread issues the 3 x (re, im) MMAs of a stage into TMEM and commits
+// them to the stage's mbarrier, which the producers wait on before refilling
+// it. The accumulators are read back with tcgen05.ld into the same Gram
+// table the CUDA-core path builds, so the steps are unchanged.
+template <int M, int L> struct GramTC {
+  static constexpr int NA = 2 * L - 1;
+  static constexpr int NG = M * L + (M * (M - 1) / 2) * NA;  // (m <= m', d) groups
+  static constexpr int TILES = (NG + 127) / 128;              // 128-row MMA tiles per re / im part
+  static constexpr int NC = M * NA;                           // columns (sources = mics)
+  static constexpr int NP = (NC + 15) / 16 * 16;              // MMA N
+  static constexpr int KC = 16;                               // frames per stage
+  static constexpr int KS = KC / 8;                           // K-steps per stage
+  static constexpr int ASTEP = 2 * TILES * 128 * 32;          // bytes of one A K-step (re and im rows)
+  static constexpr int BSTEP = NP * 32;
+  static constexpr int STAGE = 2 * KS * ASTEP + 2 * KS * BSTEP;  // hi + lo
+  // [2 sets (chunk parity)] x [2 terms] x [2 TILES tiles (re, im)] x NP columns
+  static constexpr int TCOLS = 8 * TILES * NP <= 128 ? 128 : 8 * TILES * NP <= 256 ? 256 : 512;
+  static constexpr size_t bytes() { return (size_t)2 * STAGE; }
+};
+
 // IP: the iterative-projection rule in place of the ISS steps.
-template <typename Real, int M, int L, int NT, int FT, bool IP = false>
+template <typename Real, int M, int L, int NT, int FT, bool IP = false, bool TC = false>
 __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
     gram_kernel(const SweepParams p, const int4* __restrict__ gtab) {
   using R2 = typename Cplx<Real>::T;
@@ -453,6 +481,172 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
     Yt[r * LT1 + jj] = y;
   }
 
+  if constexpr (TC) {
+    static_assert(F32 && !IP, "tensor-core Gram: fp32 ISS only");
+    using TCL = GramTC<M, L>;
+    static_assert(TCL::TILES == 1 && NT == 512 && TCL::NP == 64, "readout mapping: 16 warps x (32 lanes, 16 columns)");
+    __shared__ __align__(8) uint64_t s_mbar[2];
+    __shared__ uint32_t s_tmem;
+    unsigned char* stage0 = reinterpret_cast<unsigned char*>(part);  // 2 stages of TCL::STAGE bytes
+    const int ng = gtab[NT].x;
+    const int U0 = -(L - 1), len = T + 2 * (L - 1);
+    const int nch = (len + TCL::KC - 1) / TCL::KC;
+    if (warp == 0) tc::tmem_alloc(&s_tmem, TCL::TCOLS);
+    if (tid == 0) {
+      tc::mbar_init(&s_mbar[0], 1);
+      tc::mbar_init(&s_mbar[1], 1);
+    }
+    // rows past the groups and columns past the sources stay zero in both stages
+    for (int i = tid; i < 2 * TCL::STAGE / 16; i += NT) reinterpret_cast<float4*>(stage0)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    // this thread's production tasks, the same every stage: A (group, frame
+    // quad) or B (column, frame quad); their x / weight bases and stage offsets
+    constexpr int QPC = TCL::KC / 4;  // frame quads per stage
+    constexpr int MAXT = 2;           // tasks per thread (NG*QPC + NC*QPC <= 2*NT)
+    static_assert(TCL::NG * QPC + TCL::NC * QPC <= MAXT * NT, "production tasks per thread");
+    const R2* tx1[MAXT];
+    const R2* tx2[MAXT];
+    int toff[MAXT], toff2[MAXT], tkind[MAXT];  // kind 0 none, 1 A, 2 B
+#pragma unroll
+    for (int i = 0; i < MAXT; ++i) {
+      const int e = tid + i * NT;
+      tkind[i] = 0;
+      tx1[i] = tx2[i] = xs;
+      toff[i] = toff2[i] = 0;
+      if (e < ng * QPC) {
+        const int g = e % ng, q = e / ng;
+        const int4 gp = gtab[NT + 1 + 2 * g];
+        tkind[i] = 1;
+        tx1[i] = xs + gp.x * p.xp + p.xoff + 4 * q;
+        tx2[i] = xs + gp.y * p.xp + p.xoff + gp.z + 4 * q;
+        toff[i] = (q >> 1) * (TCL::ASTEP / 4) + tc::kmaj(g, (q & 1) * 4);
+        toff2[i] = (q >> 1) * (TCL::ASTEP / 4) + tc::kmaj(TCL::TILES * 128 + g, (q & 1) * 4);
+      } else if (e < ng * QPC + TCL::NC * QPC) {
+        const int e2 = e - ng * QPC;
+        const int j = e2 % TCL::NC, q = e2 / TCL::NC;
+        const int n = j / NA, a = j - n * NA - (L - 1);
+        tkind[i] = 2;
+        tx1[i] = reinterpret_cast<const R2*>(invl + n * p.lp + p.loff + 4 * q - a);  // (weights, read as Real)
+        toff[i] = (q >> 1) * (TCL::BSTEP / 4) + tc::kmaj(j, (q & 1) * 4);
+      }
+    }
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = s_tmem;
+    constexpr uint32_t idesc = tc::idesc_tf32(128, TCL::NP);
+    // TMEM columns: [set (chunk parity)][term: hi*hi, hi*lo + lo*hi][tile: re, im][NP]
+    auto tcol = [](int set, int term, int tile) { return (uint32_t)(((set * 2 + term) * 2 + tile) * TCL::NP); };
+    // readout mapping: warp w holds lanes 32 (w % 4) .. +31 (groups), columns 16 (w / 4) .. +15;
+    // the per-chunk partials are summed here in fp32 (round to nearest) so the
+    // tensor-core accumulation spans only one stage (2 K-steps)
+    float sre[16], sim[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) sre[i] = sim[i] = 0.f;
+    const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    const uint32_t col0 = (uint32_t)(16 * (warp >> 2));
+    auto readout = [&](int set) {
+      float h[16], c[16];
+      tc::tmem_ld16(tmem + lane_base + tcol(set, 0, 0) + col0, h);
+      tc::tmem_ld16(tmem + lane_base + tcol(set, 1, 0) + col0, c);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) sre[i] += h[i] + c[i];
+      tc::tmem_ld16(tmem + lane_base + tcol(set, 0, 1) + col0, h);
+      tc::tmem_ld16(tmem + lane_base + tcol(set, 1, 1) + col0, c);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) sim[i] += h[i] + c[i];
+    };
+    for (int c = 0; c < nch; ++c) {
+      const int st = c & 1;
+      unsigned char* sb = stage0 + st * TCL::STAGE;
+      float* ahi = reinterpret_cast<float*>(sb);
+      float* alo = reinterpret_cast<float*>(sb + TCL::KS * TCL::ASTEP);
+      float* bhi = reinterpret_cast<float*>(sb + 2 * TCL::KS * TCL::ASTEP);
+      float* blo = reinterpret_cast<float*>(sb + 2 * TCL::KS * TCL::ASTEP + TCL::KS * TCL::BSTEP);
+      const int u0 = U0 + c * TCL::KC;
+      // (stage st was last read by the MMAs of chunk c-2, waited for in the readout of iteration c-1)
+#pragma unroll
+      for (int i = 0; i < MAXT; ++i) {
+        if (tkind[i] == 1) {
+          const R2* x1 = tx1[i] + u0;
+          const R2* x2 = tx2[i] + u0;
+          float4 rh, rl, ih, il;
+          float* prh = &rh.x;
+          float* prl = &rl.x;
+          float* pih = &ih.x;
+          float* pil = &il.x;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const R2 v = Ops::mulc(x1[k], x2[k]);
+            tc::split_tf32(v.x, prh[k], prl[k]);
+            tc::split_tf32(v.y, pih[k], pil[k]);
+          }
+          *reinterpret_cast<float4*>(ahi + toff[i]) = rh;
+          *reinterpret_cast<float4*>(alo + toff[i]) = rl;
+          *reinterpret_cast<float4*>(ahi + toff2[i]) = ih;
+          *reinterpret_cast<float4*>(alo + toff2[i]) = il;
+        } else if (tkind[i] == 2) {
+          const Real* w = reinterpret_cast<const Real*>(tx1[i]) + u0;
+          float4 hv, lv;
+          tc::split_tf32(w[0], hv.x, lv.x);
+          tc::split_tf32(w[1], hv.y, lv.y);
+          tc::split_tf32(w[2], hv.z, lv.z);
+          tc::split_tf32(w[3], hv.w, lv.w);
+          *reinterpret_cast<float4*>(bhi + toff[i]) = hv;
+          *reinterpret_cast<float4*>(blo + toff[i]) = lv;
+        }
+      }
+      tc::fence_async_smem();
+      tc::fence_before_sync();
+      __syncthreads();  // stage c written; the readout of chunk c-2's set finished
+      if (tid == 0) {
+        tc::fence_after_sync();
+#pragma unroll
+        for (int ks = 0; ks < TCL::KS; ++ks)
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            const unsigned char* ah = reinterpret_cast<const unsigned char*>(ahi) + ks * TCL::ASTEP + t * 4096;
+            const unsigned char* al = reinterpret_cast<const unsigned char*>(alo) + ks * TCL::ASTEP + t * 4096;
+            const unsigned char* bh = reinterpret_cast<const unsigned char*>(bhi) + ks * TCL::BSTEP;
+            const unsigned char* bl = reinterpret_cast<const unsigned char*>(blo) + ks * TCL::BSTEP;
+            tc::mma_tf32(tmem + tcol(st, 0, t), tc::desc(ah), tc::desc(bh), idesc, ks > 0);
+            tc::mma_tf32(tmem + tcol(st, 1, t), tc::desc(ah), tc::desc(bl), idesc, ks > 0);
+            tc::mma_tf32(tmem + tcol(st, 1, t), tc::desc(al), tc::desc(bh), idesc, true);
+          }
+        tc::commit(&s_mbar[st]);
+      }
+      if (c >= 1) {  // partials of chunk c-1 (its MMAs overlap this chunk's production)
+        tc::mbar_wait(&s_mbar[st ^ 1], ((c - 1) >> 1) & 1);
+        tc::fence_after_sync();
+        readout(st ^ 1);
+      }
+    }
+    tc::mbar_wait(&s_mbar[(nch - 1) & 1], ((nch - 1) >> 1) & 1);
+    tc::fence_after_sync();
+    readout((nch - 1) & 1);
+    CTF_PHASE(3);
+    const int g = 32 * (warp & 3) + lane;
+    if (g < ng) {
+      const int4 h0 = gtab[NT + 1 + 2 * g], h1 = gtab[NT + 2 + 2 * g];
+      const int m = h0.x, m2 = h0.y, d = h0.z, alo = h0.w, cnt = h1.x;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int j = (int)col0 + i;
+        if (j >= TCL::NC) continue;
+        const int n = j / NA, a = j - n * NA - (L - 1);
+        if (a < alo || a >= alo + cnt) continue;
+        R2 v;
+        v.x = sre[i];
+        v.y = sim[i];
+        G[gidx(n, m, m2, a, a + d)] = v;
+        if (m == m2 && d != 0) {
+          v.y = -v.y;
+          G[gidx(n, m, m, a + d, a)] = v;
+        }
+      }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc(tmem, TCL::TCOLS);
+  } else {
   // ---- Gram: this thread's (m, m', d) task over frames [u0, u1), NS
   // sources per pass. The lag count is made warp-uniform (groups are sorted
   // by it, so a warp spans at most two adjacent counts): no divergent code
@@ -508,6 +702,7 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
       }
       __syncthreads();
     }
+  }
   }
   CTF_PHASE(4);
 

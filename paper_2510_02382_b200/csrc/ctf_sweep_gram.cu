@@ -7,12 +7,15 @@ namespace ctf {
 std::vector<SweepVariant> sweep_variants_gram_f32() {
 #if defined(CTF_GRAM_DEV) && defined(CTF_DEV_F64)
   return {};
+#elif defined(CTF_GRAM_DEV) && defined(CTF_DEV_TC)  // dev build of the tcgen05-Gram variant
+  return {CTF_GRT(float, 1, CTF_DEV_M, CTF_DEV_L, CTF_DEV_NT, CTF_DEV_FT)};
 #elif defined(CTF_GRAM_DEV)  // dev builds (tools/dev_build.sh): only the variant being tuned
   return {GF(CTF_DEV_M, CTF_DEV_L, CTF_DEV_NT, CTF_DEV_FT)};
 #else
   return {GF(2, 2, 128, 4), GF(2, 2, 256, 4), GF(2, 3, 128, 4), GF(2, 3, 256, 4),
           GF(2, 5, 256, 4), GF(2, 5, 512, 4), GF(3, 4, 256, 4), GF(3, 4, 512, 4),
-          GF(4, 8, 256, 4), GF(4, 8, 512, 2)};  // wide tiles (BASELINE cfg3): warp per row, Gram table reads
+          GF(4, 8, 256, 4), GF(4, 8, 512, 2),  // wide tiles (BASELINE cfg3): warp per row, Gram table reads
+          CTF_GRT(float, 1, 4, 8, 512, 2)};     // the same with the tcgen05 Gram
 #endif
 }
 std::vector<SweepVariant> sweep_variants_gram_f64() {

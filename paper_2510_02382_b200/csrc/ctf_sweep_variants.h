@@ -29,6 +29,7 @@ struct SweepVariant {
   int cs = 0;   // kind 5: CTAs per cluster (frame split)
   size_t (*fbytes)(int) = nullptr;  // kind 5: dynamic shared memory for SK bases
   int ag = 0;   // kind 5: all-gather exchange (every CTA derives every z)
+  int tc = 0;   // kind 4: tensor-core (tcgen05) Gram
 };
 #define CTF_V(REAL, PREC, RMAX, FT, RREG, NT, EX) \
   SweepVariant { PREC, RMAX, FT, RREG, NT, EX, sweep_kernel<REAL, RMAX, FT, RREG, NT, EX> }
@@ -61,6 +62,12 @@ struct SweepVariant {
 #define CTF_GR(REAL, PREC, M, L, NT, FT)                                                                 \
   SweepVariant {                                                                                         \
     PREC, (M) * (L), FT, M, NT, 1, nullptr, 4, L, nullptr, nullptr, 0, gram_kernel<REAL, M, L, NT, FT>   \
+  }
+// gram_kernel with the tcgen05 Gram (fp32)
+#define CTF_GRT(REAL, PREC, M, L, NT, FT)                                                                        \
+  SweepVariant {                                                                                                \
+    PREC, (M) * (L), FT, M, NT, 1, nullptr, 4, L, nullptr, nullptr, 0, gram_kernel<REAL, M, L, NT, FT, false, true>, \
+        0, 0, nullptr, 0, 1                                                                                     \
   }
 #define CTF_GRI(REAL, PREC, M, L, NT, FT)                                                                   \
   SweepVariant {                                                                                            \

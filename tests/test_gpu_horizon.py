@@ -84,3 +84,27 @@ def test_fp64_cfg1_shape_full_bins_20_iterations():
     img = s.project_back()
     s.close()
     assert rel(img[:, 0], O.reconstruct_images(O.config(taps, bases), ref["W"], x)) <= 1e-9
+
+
+def test_tensor_core_gram_variant_cfg3(monkeypatch):
+    """The tcgen05 Gram variant of the covariance-domain kernel (3xTF32 split,
+    per-stage TMEM partials summed in fp32; CTF_GRAM_TC=1 selects it, the
+    frame-split kernel stays the default for this tile) on the cfg3 geometry:
+    1e-4 relative L2 after every one of 20 iterations."""
+    monkeypatch.setenv("CTF_SWEEP_KIND", "4")
+    monkeypatch.setenv("CTF_GRAM_TC", "1")
+    M, L, T, K, rho, F, iters, seed = 4, 8, 1000, 20, 0.8, 9, 20, 12
+    raw = synth_mixtures(1, F, T, M, M, L, K, rho, 4242 + M * L)
+    ref = O.run(O.config([L] * M, [K] * M, iterations=iters, seed=seed, threads=NPROC),
+                O.stack_observation(raw[0], L), history=True)
+    s = Session(raw.astype(np.complex64), [L] * M, [K] * M, stack_taps=L, iterations=iters, precision="f32",
+                seed=seed)
+    d = json.loads(s.describe())
+    assert "gram_kernel" in d["sweep_kernel"] and d["smem_bytes"] > 210000, d  # the TC variant's stage buffers
+    for it in range(iters):
+        s.iterate(1)
+        W, B, V, obj = s.download_raw()
+        e = max(rel(W[0], ref["hist_W"][it].reshape(F, -1)), rel(B[0], ref["hist_B"][it]),
+                rel(V[0], ref["hist_V"][it]))
+        assert e <= 1e-4, f"it={it + 1}: {e:.2e}"
+    s.close()
