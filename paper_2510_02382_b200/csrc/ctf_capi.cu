@@ -420,6 +420,7 @@ void plan_sweep(ctf_ctx* c) {
       return o;
     };
     ctf::SweepParams cand = c->sp;
+    int fs_sms = 0;  // kind 5: SMs covered by co-resident clusters
     if (v.kind == 0) {
       if (v.rmax < c->R || (v.exact && v.rmax != c->R)) continue;
       if (v.lt > 0) {
@@ -535,6 +536,12 @@ void plan_sweep(ctf_ctx* c) {
         cudaGetLastError();
         continue;
       }
+      // SMs the co-resident clusters cover (GPC packing: 8-CTA clusters leave
+      // 28 of 148 SMs idle, 9-CTA ones 13): the planner prefers the most
+      int per_sm = 1, nsm = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v.fn, nt, off));
+      CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+      fs_sms = std::min(nsm, nclusters * CS / std::max(1, per_sm));
     } else if (v.kind == 2) {  // streamed: any R <= 64, tile in global scratch
       if (c->R > v.rmax) continue;
       TP = nt * v.ft;
@@ -598,7 +605,7 @@ void plan_sweep(ctf_ctx* c) {
     const char* tc_env = std::getenv("CTF_GRAM_TC");
     const int tc_rank = v.tc ? ((tc_env && std::atoi(tc_env)) ? -6000 : 50) : 0;
     const int rank = wide_bonus + tc_rank +
-                     (v.kind == 4 ? gram_rank : v.kind == 3 ? 3000 : v.kind == 2 ? 2000 : v.kind == 5 ? (c->R > 16 ? -2000 : 4000) + v.cs + (1 - v.ag) : v.kind == 1 ? 1000 : 0) +
+                     (v.kind == 4 ? gram_rank : v.kind == 3 ? 3000 : v.kind == 2 ? 2000 : v.kind == 5 ? (c->R > 16 ? -2000 - 10 * fs_sms : 4000) + v.cs + (1 - v.ag) : v.kind == 1 ? 1000 : 0) +
                      (v.kind == 3 ? -v.rmax * 4 : v.rmax * 4) + (v.exact ? 0 : 2) + (v.lt > 0 ? 0 : 1);
     const bool better = !found || rank < best_rank ||
                         (rank == best_rank && (TP < best_TP || (TP == best_TP && nt < best_nt)));

@@ -9,6 +9,10 @@ std::vector<SweepVariant> sweep_variants_fsplit_f32() {
           // all-gather exchange variants (one DSMEM hop per step)
           CTF_FSA(float, 1, 60, 10, 2, 256, 8, 32, 10, 1), CTF_FSA(float, 1, 32, 8, 4, 128, 2, 16, 8, 2),
           CTF_FSA(float, 1, 32, 8, 2, 128, 4, 16, 8, 3)};
+// (measured and dropped: cfg4 over 9-CTA clusters, NT = 224 — 15 co-resident
+// clusters cover 135 SMs instead of 120 (tools/cluster_probe.cu) but the
+// cluster count, not the SM count, bounds the bins in flight and each bin's
+// 60-step chain is latency-bound: 202.8 vs 201.2 ms per 8 mixtures)
 }
 }  // namespace ctf
 #ifdef CTF_PHASE_TIMING
