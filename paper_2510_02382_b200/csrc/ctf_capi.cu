@@ -463,6 +463,7 @@ void plan_sweep(ctf_ctx* c) {
       cand.off_l = (int)take((size_t)c->N * glp * rs);
       cand.off_y = (int)take((size_t)c->N * (M * (M + 1) / 2) * NA * NA * cs);  // Hermitian half of the Gram
       const int NS = (c->real_size == 4 && c->R <= 16) ? c->N : 1;  // sources per Gram pass (gram_ns) and demix group
+      // (dev builds with -DCTF_GRAM_NS64 must size this from gram_ns as well)
       size_t ebytes = std::max((size_t)NS * NA * (nt + 1) * cs, (size_t)NS * L * TP * rs);
       if (v.tc) {  // two stages of the tcgen05 Gram operands (ctf_gram.cuh GramTC)
         const int NG = M * L + (M * (M - 1) / 2) * NA, TILES = (NG + 127) / 128, NP = (M * NA + 15) / 16 * 16;

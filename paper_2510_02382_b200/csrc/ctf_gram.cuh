@@ -139,8 +139,11 @@ __device__ __forceinline__ double log_fast(double x) { return log(x); }
 
 // Sources accumulated per Gram pass: all of them in fp32 (the conj products
 // are shared); one at a time in fp64 (register budget, half the partials).
+#ifndef CTF_GRAM_NS64
+#define CTF_GRAM_NS64 1
+#endif
 template <typename Real, int N, int R> constexpr int gram_ns() {
-  return (std::is_same<Real, float>::value && R <= 16) ? N : 1;
+  return (std::is_same<Real, float>::value && R <= 16) ? N : (R <= 16 && N % CTF_GRAM_NS64 == 0 ? CTF_GRAM_NS64 : 1);
 }
 template <typename Real, int NT, int R> constexpr int gram_min_blocks() {
   return R > 16 ? 1 : std::is_same<Real, float>::value ? (NT <= 256 ? 3 : 1) : (NT <= 256 ? 2 : 1);
@@ -1166,7 +1169,12 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
 #pragma unroll
   for (int g0 = 0; g0 < N; g0 += NSD) {  // unrolled: the row-power register index is static
     // FB frames per pass would share the W loads
-    constexpr int FB = 1;  // 2 shares the W loads but spills at the 80-register budget (measured slower)
+    // frames per demix pass: 2 share the W loads (fp64: half the broadcast
+    // shared-memory wavefronts); fp32 at its 80-register budget spills with 2
+#ifndef CTF_GRAM_FB64
+#define CTF_GRAM_FB64 2
+#endif
+    constexpr int FB = F32 ? 1 : CTF_GRAM_FB64;
 #pragma unroll 1
     for (int k = 0; k < FT; k += FB) {
       R2 acc[FB][GR];
