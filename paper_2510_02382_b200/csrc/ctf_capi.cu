@@ -57,6 +57,8 @@ struct NcclApi {
   int (*CommInitRank)(NcclComm*, int, NcclUid, int) = nullptr;
   int (*AllReduce)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
   int (*CommDestroy)(NcclComm) = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(int) = nullptr;
   bool load() {
     if (h) return true;
@@ -71,6 +73,8 @@ struct NcclApi {
     AllReduce = (decltype(AllReduce))dlsym(h, "ncclAllReduce");
     CommDestroy = (decltype(CommDestroy))dlsym(h, "ncclCommDestroy");
     GetErrorString = (decltype(GetErrorString))dlsym(h, "ncclGetErrorString");
+    GroupStart = (decltype(GroupStart))dlsym(h, "ncclGroupStart");
+    GroupEnd = (decltype(GroupEnd))dlsym(h, "ncclGroupEnd");
     return GetUniqueId && CommInitRank && AllReduce && CommDestroy;
   }
 };
@@ -171,6 +175,17 @@ struct ctf_ctx {
   int fb_nt = 0, fb_grid = 0;
   double fb_theta = 0.0;
   DevBuf<int> fb_list, fb_count;
+  // pipelined collective loop (world > 1): the mixtures in nmc chunks; the
+  // all-reduce of chunk k runs on comm_stream while chunk k+1 sweeps, and
+  // its apply is deferred to just before chunk k's next sweep
+  int nmc = 1;
+  cudaStream_t comm_stream = nullptr;
+  std::vector<cudaEvent_t> ev_red, ev_ar;
+  struct Deferred {
+    bool on = false;
+    int obj_slot = -1, do_v = 0;
+  };
+  std::vector<Deferred> deferred;
   // device buffers
   DevBuf<unsigned char> x, W, Bf, V, E, part, packed, scratch, cpivot, cwpivot;
   DevBuf<double> cpart;
@@ -816,8 +831,9 @@ void download_real(ctf_ctx* c, double* dst, const void* src, size_t n) {
   CK(cudaStreamSynchronize(c->stream));
 }
 
-void allreduce(ctf_ctx* c, void* buf, size_t count, int dtype, int op) {
+void allreduce(ctf_ctx* c, void* buf, size_t count, int dtype, int op, cudaStream_t st = nullptr) {
   if (!c->collective() || count == 0) return;
+  if (!st) st = c->stream;
   if (c->group) {  // host exchange, fixed rank order (deterministic)
     const size_t es = dtype == kNcclFloat ? 4 : 8;
     ctf_group* g = c->group;
@@ -850,7 +866,7 @@ void allreduce(ctf_ctx* c, void* buf, size_t count, int dtype, int op) {
     CK(cudaStreamSynchronize(c->stream));
     return;
   }
-  const int rc = g_nccl.AllReduce(buf, buf, count, dtype, op, c->comm, c->stream);
+  const int rc = g_nccl.AllReduce(buf, buf, count, dtype, op, c->comm, st);
   if (rc != 0)
     throw CtfError(CTF_ERR_CUDA, std::string("ncclAllReduce failed: ") +
                                      (g_nccl.GetErrorString ? g_nccl.GetErrorString(rc) : "?"));
@@ -899,8 +915,9 @@ void check_errors(ctf_ctx* c) {
 }
 
 template <class Real>
-void launch_muv(ctf_ctx* c) {
+void launch_muv(ctf_ctx* c, int m0, int m1) {
   ctf::MuvParams mp{};
+  mp.mix0 = m0;
   mp.Bf = c->Bf.p;
   mp.V = c->V.p;
   mp.E = c->E.p;
@@ -914,7 +931,7 @@ void launch_muv(ctf_ctx* c) {
   mp.chunk_bins = c->chunk_bins;
   for (int n = 0; n <= c->N; ++n) mp.koff[n] = c->koff[n];
   for (int n = 0; n < c->N; ++n) mp.ntaps[n] = c->taps[n];
-  dim3 grid((c->T + 127) / 128, c->B * c->N, c->nchunk);
+  dim3 grid((c->T + 127) / 128, (m1 - m0) * c->N, c->nchunk);
   const size_t smem = (size_t)((c->chunk_bins + 7) / 8 * 8) * c->kmax * sizeof(Real);
   switch (c->kmax) {
     case 4: ctf::muv_partial_kernel<Real, 4><<<grid, 128, smem, c->stream>>>(mp); break;
@@ -930,8 +947,9 @@ void launch_muv(ctf_ctx* c) {
 }
 
 template <class Real>
-void launch_apply(ctf_ctx* c, int mode, int obj_slot, int do_v) {
+void launch_apply(ctf_ctx* c, int mode, int obj_slot, int do_v, int m0, int m1) {
   ctf::ApplyParams ap{};
+  ap.mix0 = m0;
   ap.part = c->part.p;
   ap.packed = c->packed.p;
   ap.V = c->V.p;
@@ -956,14 +974,15 @@ void launch_apply(ctf_ctx* c, int mode, int obj_slot, int do_v) {
   ap.do_v = do_v;
   const size_t plane = (size_t)c->SK * c->T;
   const int bx = do_v ? (int)std::min<size_t>((plane + 255) / 256, 64) : 1;
-  ctf::reduce_apply_kernel<Real><<<dim3(bx, c->B), 256, 0, c->stream>>>(ap);
+  ctf::reduce_apply_kernel<Real><<<dim3(bx, m1 - m0), 256, 0, c->stream>>>(ap);
   CK(cudaGetLastError());
 }
 
 // One loop body (estimator.cpp:553-654) or, with do_sweep = false, the
 // trailing rescale + objective of the last completed iteration.
+// The iteration kernel (+ its fallback) for mixtures [m0, m1).
 template <class Real>
-void run_body(ctf_ctx* c, bool do_sweep) {
+void launch_sweep(ctf_ctx* c, bool do_sweep, int m0, int m1) {
   ctf::SweepParams sp = c->sp;
   auto fill = [&](ctf::SweepParams& sp) {
   sp.x = c->x.p;
@@ -986,12 +1005,11 @@ void run_body(ctf_ctx* c, bool do_sweep) {
   sp.fb_list = c->fb_list.p;
   sp.fb_count = c->fb_count.p;
   sp.fb_theta = c->fb_theta;
+  sp.mix0 = m0;
+  sp.nmix = c->B;
   };
   fill(sp);
-  const int obj_slot = c->pending ? c->done - 1 : -1;
-
-  cudaEvent_t e0 = take_event(c), e1 = take_event(c), e2 = take_event(c);
-  CK(cudaEventRecord(e0, c->stream));
+  const int nm = m1 - m0;
   if (c->sv.kind == 3) {
     ctf::ClusterParams cl{};
     cl.s = sp;
@@ -1002,7 +1020,7 @@ void run_body(ctf_ctx* c, bool do_sweep) {
     cl.CS = c->cluster_size;
     CK(cudaMemsetAsync(c->cbad.p, 0, c->cbad.n * sizeof(int), c->stream));
     cudaLaunchConfig_t lc{};
-    lc.gridDim = dim3(c->FL * c->cluster_size, c->B);
+    lc.gridDim = dim3(c->FL * c->cluster_size, nm);
     lc.blockDim = dim3(c->NT);
     lc.dynamicSmemBytes = c->sweep_smem;
     lc.stream = c->stream;
@@ -1016,7 +1034,7 @@ void run_body(ctf_ctx* c, bool do_sweep) {
     CK(cudaLaunchKernelEx(&lc, c->sv.cfn, cl));
   } else if (c->sv.kind == 5) {
     cudaLaunchConfig_t lc{};
-    lc.gridDim = dim3(c->FL * c->cluster_size, c->B);
+    lc.gridDim = dim3(c->FL * c->cluster_size, nm);
     lc.blockDim = dim3(c->NT);
     lc.dynamicSmemBytes = c->sweep_smem;
     lc.stream = c->stream;
@@ -1028,7 +1046,7 @@ void run_body(ctf_ctx* c, bool do_sweep) {
     lc.attrs = at;
     lc.numAttrs = 1;
     CK(cudaLaunchKernelEx(&lc, c->sv.fn, sp));
-  } else if (c->sv.kind == 2) {
+  } else if (c->sv.kind == 2) {  // persistent over all work items (never chunked)
     ctf::StreamParams st{};
     st.s = sp;
     st.scratch = c->scratch.p;
@@ -1040,7 +1058,7 @@ void run_body(ctf_ctx* c, bool do_sweep) {
       CK(cudaMemsetAsync(c->fb_count.p, 0, sizeof(int), c->stream));
       sp.fb_mode = 1;
     }
-    c->sv.gfn<<<dim3(c->FL, c->B), c->NT, c->sweep_smem, c->stream>>>(sp, c->gtab.p);
+    c->sv.gfn<<<dim3(c->FL, nm), c->NT, c->sweep_smem, c->stream>>>(sp, c->gtab.p);
     if (c->has_fb) {  // the bins the Gram form handed over, in the frame domain
       CK(cudaGetLastError());
       ctf::SweepParams fp = c->sp_fb;
@@ -1050,25 +1068,92 @@ void run_body(ctf_ctx* c, bool do_sweep) {
       c->timing.launches += 1;
     }
   } else {
-    c->sv.fn<<<dim3(c->FL, c->B), c->NT, c->sweep_smem, c->stream>>>(sp);
+    c->sv.fn<<<dim3(c->FL, nm), c->NT, c->sweep_smem, c->stream>>>(sp);
   }
   CK(cudaGetLastError());
-  CK(cudaEventRecord(e1, c->stream));
   c->timing.sweep_launches += 1;
   c->timing.launches += 1;
-  if (do_sweep) {
-    launch_muv<Real>(c);
-    c->timing.launches += 1;
-  }
-  if (c->collective()) {
-    launch_apply<Real>(c, 0, obj_slot, do_sweep ? 1 : 0);
-    if (do_sweep) allreduce(c, c->packed.p, (size_t)c->B * 2 * c->SK * c->T, sizeof(Real) == 4 ? kNcclFloat : kNcclDouble, kNcclSum);
-    allreduce(c, c->packed_d.p, (size_t)c->B * (c->R + 1), kNcclDouble, kNcclSum);
-    launch_apply<Real>(c, 1, obj_slot, do_sweep ? 1 : 0);
-    c->timing.launches += 2;
+}
+
+// Applies the deferred V update / rescale of mixture chunk k (after its all-reduce).
+template <class Real>
+void apply_deferred(ctf_ctx* c, int k) {
+  auto& d = c->deferred[(size_t)k];
+  if (!d.on) return;
+  const int m0 = k * c->B / c->nmc, m1 = (k + 1) * c->B / c->nmc;
+  CK(cudaStreamWaitEvent(c->stream, c->ev_ar[(size_t)k], 0));
+  launch_apply<Real>(c, 1, d.obj_slot, d.do_v, m0, m1);
+  c->timing.launches += 1;
+  d.on = false;
+}
+
+template <class Real>
+void flush_deferred(ctf_ctx* c) {
+  for (int k = 0; k < c->nmc && k < (int)c->deferred.size(); ++k) apply_deferred<Real>(c, k);
+}
+
+// One loop body (estimator.cpp:553-654) or, with do_sweep = false, the
+// trailing rescale + objective of the last completed iteration.
+template <class Real>
+void run_body(ctf_ctx* c, bool do_sweep) {
+  const int obj_slot = c->pending ? c->done - 1 : -1;
+  const int do_v = do_sweep ? 1 : 0;
+  cudaEvent_t e0 = take_event(c), e1 = take_event(c), e2 = take_event(c);
+  CK(cudaEventRecord(e0, c->stream));
+  if (c->nmc > 1) {
+    // pipelined over mixture chunks: chunk k's all-reduce (comm_stream)
+    // overlaps chunk k+1's sweep; its apply runs just before chunk k's next
+    // sweep (the only consumer of the updated V / mu of those mixtures)
+    const int kNccl = sizeof(Real) == 4 ? kNcclFloat : kNcclDouble;
+    for (int k = 0; k < c->nmc; ++k) {
+      const int m0 = k * c->B / c->nmc, m1 = (k + 1) * c->B / c->nmc;
+      apply_deferred<Real>(c, k);
+      launch_sweep<Real>(c, do_sweep, m0, m1);
+      if (do_sweep) {
+        launch_muv<Real>(c, m0, m1);
+        c->timing.launches += 1;
+      }
+      launch_apply<Real>(c, 0, obj_slot, do_v, m0, m1);
+      c->timing.launches += 1;
+      const size_t nv = (size_t)(m1 - m0) * 2 * c->SK * c->T, nd = (size_t)(m1 - m0) * (c->R + 1);
+      Real* pv = reinterpret_cast<Real*>(c->packed.p) + (size_t)m0 * 2 * c->SK * c->T;
+      double* pd = c->packed_d.p + (size_t)m0 * (c->R + 1);
+      if (c->group) {  // in-process exchange: synchronous on the compute stream
+        if (do_sweep) allreduce(c, pv, nv, kNccl, kNcclSum);
+        allreduce(c, pd, nd, kNcclDouble, kNcclSum);
+        CK(cudaEventRecord(c->ev_ar[(size_t)k], c->stream));
+      } else {  // NCCL on the communication stream, both sums in one group
+        CK(cudaEventRecord(c->ev_red[(size_t)k], c->stream));
+        CK(cudaStreamWaitEvent(c->comm_stream, c->ev_red[(size_t)k], 0));
+        if (g_nccl.GroupStart) g_nccl.GroupStart();
+        if (do_sweep) allreduce(c, pv, nv, kNccl, kNcclSum, c->comm_stream);
+        allreduce(c, pd, nd, kNcclDouble, kNcclSum, c->comm_stream);
+        if (g_nccl.GroupEnd && g_nccl.GroupEnd() != 0) throw CtfError(CTF_ERR_CUDA, "ncclGroupEnd failed");
+        CK(cudaEventRecord(c->ev_ar[(size_t)k], c->comm_stream));
+      }
+      c->deferred[(size_t)k] = {true, obj_slot, do_v};
+    }
   } else {
-    launch_apply<Real>(c, 2, obj_slot, do_sweep ? 1 : 0);
-    c->timing.launches += 1;
+    launch_sweep<Real>(c, do_sweep, 0, c->B);
+  }
+  CK(cudaEventRecord(e1, c->stream));
+  if (c->nmc <= 1) {
+    if (do_sweep) {
+      launch_muv<Real>(c, 0, c->B);
+      c->timing.launches += 1;
+    }
+    if (c->collective()) {
+      launch_apply<Real>(c, 0, obj_slot, do_v, 0, c->B);
+      if (c->comm && g_nccl.GroupStart) g_nccl.GroupStart();
+      if (do_sweep) allreduce(c, c->packed.p, (size_t)c->B * 2 * c->SK * c->T, sizeof(Real) == 4 ? kNcclFloat : kNcclDouble, kNcclSum);
+      allreduce(c, c->packed_d.p, (size_t)c->B * (c->R + 1), kNcclDouble, kNcclSum);
+      if (c->comm && g_nccl.GroupEnd && g_nccl.GroupEnd() != 0) throw CtfError(CTF_ERR_CUDA, "ncclGroupEnd failed");
+      launch_apply<Real>(c, 1, obj_slot, do_v, 0, c->B);
+      c->timing.launches += 2;
+    } else {
+      launch_apply<Real>(c, 2, obj_slot, do_v, 0, c->B);
+      c->timing.launches += 1;
+    }
   }
   CK(cudaEventRecord(e2, c->stream));
   if (do_sweep) {
@@ -1139,6 +1224,9 @@ void iterate_impl(ctf_ctx* c, int n, bool finalize) {
     if (c->real_size == 4) run_body<float>(c, false);
     else run_body<double>(c, false);
   }
+  // the deferred applies of the pipelined loop (mixture chunks) complete here
+  if (c->real_size == 4) flush_deferred<float>(c);
+  else flush_deferred<double>(c);
   if (finalize) {
     collect_timing(c);
     check_errors(c);
@@ -1215,6 +1303,26 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host,
     c->fb_list.alloc((size_t)c->B * c->FL);
     c->fb_count.alloc(1);
   }
+  // pipelined collective loop: two mixture chunks by default (CTF_MIX_CHUNKS
+  // overrides; 1 = the unchunked reduce -> all-reduce -> apply). Kernels with
+  // a per-launch mixture offset only (not the persistent streamed kernel) and
+  // not with CheckOptions (their maxima are reduced per iteration).
+  c->nmc = 1;
+  if (c->collective() && c->B >= 2 && c->sv.kind != 2 && c->prob.checks == 0) {
+    c->nmc = 2;
+    if (const char* env = std::getenv("CTF_MIX_CHUNKS")) c->nmc = std::max(1, std::min(c->B, std::atoi(env)));
+  }
+  if (c->nmc > 1) {
+    if (!c->comm_stream) CK(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    while ((int)c->ev_red.size() < c->nmc) {
+      cudaEvent_t a, b;
+      CK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+      c->ev_red.push_back(a);
+      c->ev_ar.push_back(b);
+    }
+  }
+  c->deferred.assign((size_t)c->nmc, ctf_ctx::Deferred{});
   if (c->sv.kind == 2) c->scratch.alloc((size_t)c->stream_grid * c->R * c->TP * cs);
   else c->scratch.free();
   if (c->sv.kind == 3) {
@@ -1383,7 +1491,11 @@ void ctf_close(ctf_ctx* c) {
   for (auto& pr : c->ev_mu) c->ev_pool.push_back(pr.second);
   for (auto& pr : c->ev_fin) c->ev_pool.push_back(pr.first), c->ev_pool.push_back(pr.second);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
+  for (auto e : c->ev_red) cudaEventDestroy(e);
+  for (auto e : c->ev_ar) cudaEventDestroy(e);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -1533,14 +1645,15 @@ int ctf_describe(ctf_ctx* c, char* buf, int len) {
                 "{\"sweep_kernel\": \"%s<%s,RMAX=%d,FT=%d,%s=%d,NT=%d,EXACT=%d>\", \"threads\": %d, "
                 "\"smem_bytes\": %zu, \"grid\": [%d, %d], \"muv_chunks\": %d, \"bins\": [%d, %d], "
                 "\"world\": %d, \"rank\": %d, \"collective\": \"%s\", \"cluster\": %d, "
-                "\"gram_fallback\": %s, \"fallback_theta\": %g, \"fallback_kernel\": \"sweep_kernel<RMAX=%d,FT=%d,RREG=%d,NT=%d>\"}",
+                "\"gram_fallback\": %s, \"fallback_theta\": %g, \"fallback_kernel\": \"sweep_kernel<RMAX=%d,FT=%d,RREG=%d,NT=%d>\", "
+                "\"mix_chunks\": %d}",
                 c->sv.kind == 5 ? "fsplit_kernel" : c->sv.kind == 4 ? "gram_kernel" : c->sv.kind == 3 ? "cluster_kernel" : c->sv.kind == 2 ? "stream_kernel" : c->sv.kind ? "rowwarp_kernel" : "sweep_kernel",
                 c->real_size == 4 ? "f32" : "f64", c->sv.rmax, c->sv.ft,
                 c->sv.kind == 4 ? "M" : (c->sv.kind == 3 || c->sv.kind == 5) ? "RREG" : c->sv.kind == 2 ? "RG" : c->sv.kind ? "WPR" : "RREG", c->sv.rreg, c->sv.maxt, c->sv.exact, c->NT,
                 c->sweep_smem, c->FL, c->B, c->nchunk, c->lo, c->hi, c->world, c->rank,
                 c->group ? "host-group" : c->comm ? "nccl" : "none",
                 (c->sv.kind == 3 || c->sv.kind == 5) ? c->cluster_size : 1, c->has_fb ? "true" : "false",
-                c->fb_theta, c->fbv.rmax, c->fbv.ft, c->fbv.rreg, c->fbv.maxt);
+                c->fb_theta, c->fbv.rmax, c->fbv.ft, c->fbv.rreg, c->fbv.maxt, c->nmc);
   return CTF_OK;
 }
 

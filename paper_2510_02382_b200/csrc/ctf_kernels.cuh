@@ -85,6 +85,9 @@ struct SweepParams {
   int* fb_list;
   int* fb_count;
   double fb_theta;
+  // mixture range of this launch: blockIdx.y + mix0 (mixture chunks of the
+  // pipelined multi-GPU loop); nmix = all mixtures of the context
+  int mix0, nmix;
 };
 
 // L2 prefetch of a contiguous block (bulk async, no registers or smem).
@@ -98,7 +101,7 @@ __device__ __forceinline__ void prefetch_next_tile(const SweepParams& p, int bin
                                                    size_t wbytes) {
   if (p.pf_stride <= 0 || threadIdx.x != 0) return;
   const size_t w = (size_t)mix * p.FL + bin + p.pf_stride;
-  if (w >= (size_t)gridDim.y * p.FL) return;
+  if (w >= (size_t)p.nmix * p.FL) return;
   prefetch_l2(reinterpret_cast<const unsigned char*>(p.x) + w * xbytes, (unsigned)xbytes);
   prefetch_l2(reinterpret_cast<const unsigned char*>(p.W) + w * wbytes, (unsigned)wbytes);
 }
@@ -389,7 +392,7 @@ __device__ __forceinline__ void sweep_body(const SweepParams& p, const int bin, 
 template <typename Real, int RMAX, int FT, int RREG, int NT, bool EXACT, int LT = 0, bool CHECK = false>
 __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(const SweepParams p) {
   if (p.fb_mode != 2) {  // one work item per CTA: (bin, mixture) = (blockIdx.x, blockIdx.y)
-    sweep_body<Real, RMAX, FT, RREG, NT, EXACT, LT, CHECK>(p, blockIdx.x, blockIdx.y);
+    sweep_body<Real, RMAX, FT, RREG, NT, EXACT, LT, CHECK>(p, blockIdx.x, blockIdx.y + p.mix0);
     return;
   }
   // conditioning fallback of the covariance-domain kernel: the listed items
@@ -932,6 +935,7 @@ struct MuvParams {
   void* part;      // Real [chunk][mix][2][SK][T]
   const double* floor_abs;
   int FL, T, N, SK, nmix, chunk_bins;
+  int mix0;  // mixture of blockIdx.y / N == 0
   int koff[kMaxSources + 1], ntaps[kMaxSources];
 };
 
@@ -943,7 +947,7 @@ template <typename Real, int KMAX>
 __global__ void __launch_bounds__(128) muv_partial_kernel(const MuvParams p) {
   constexpr int G = 8;
   const int tau = blockIdx.x * blockDim.x + threadIdx.x;
-  const int mix = blockIdx.y / p.N, n = blockIdx.y - mix * p.N;
+  const int mix = blockIdx.y / p.N + p.mix0, n = blockIdx.y % p.N;
   const int chunk = blockIdx.z;
   const int i0 = chunk * p.chunk_bins, i1 = min(p.FL, i0 + p.chunk_bins);
   const int nb = i1 - i0, nbp = (nb + G - 1) / G * G;
@@ -1041,6 +1045,7 @@ struct ApplyParams {
   const double* floor_abs;
   unsigned long long* err;
   int nchunk, nmix, SK, T, FL, R, F_total, max_iters;
+  int mix0;             // mixture of blockIdx.y == 0 (mixture-chunk launches)
   int obj_slot;         // iteration index (0-based) whose objective is summed, -1 if none
   int mode;             // 0 = reduce to packed, 1 = apply from packed, 2 = reduce+apply (world 1)
   int do_v;             // 0 for the objective-only finalize pass
@@ -1048,7 +1053,7 @@ struct ApplyParams {
 
 template <typename Real>
 __global__ void __launch_bounds__(256) reduce_apply_kernel(const ApplyParams p) {
-  const int mix = blockIdx.y;
+  const int mix = blockIdx.y + p.mix0;
   const size_t plane = (size_t)p.SK * p.T;
   if (p.do_v) {
     for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < plane; e += (size_t)gridDim.x * blockDim.x) {

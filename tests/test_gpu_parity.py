@@ -437,8 +437,9 @@ def _sharded_run(raw, L, K, iters, precision, seed, world):
 @pytest.mark.parametrize("precision,tol", [("f64", 1e-12), ("f32", 2e-5)])
 def test_frequency_sharded_contexts_match_single_context(precision, tol):
     """The world > 1 path (shard ranges, packed all-reduce of MU-V sums, row
-    powers, objective, mean power, error words) reproduces the world = 1 run."""
-    B, F, T, M, L, K, iters, seed = 2, 37, 300, 2, 3, 4, 4, 6
+    powers, objective, mean power, error words) reproduces the world = 1 run;
+    with three mixtures the pipelined loop runs two uneven mixture chunks."""
+    B, F, T, M, L, K, iters, seed = 3, 37, 300, 2, 3, 4, 4, 6
     raw = synth_mixtures(B, F, T, M, M, L, K, 0.6, 31)
     if precision == "f32":
         raw = raw.astype(np.complex64)
@@ -460,15 +461,17 @@ def test_frequency_sharded_contexts_match_single_context(precision, tol):
         assert sorted(covered)[0][0] == 0 and sorted(covered)[-1][1] == F
 
 
-@pytest.mark.parametrize("precision,tol", [("f64", 1e-12), ("f32", 1e-5)])
-def test_nccl_single_rank_communicator(monkeypatch, precision, tol):
+@pytest.mark.parametrize("precision,tol,chunks,use_async", [("f64", 1e-12, "1", False), ("f32", 1e-5, "1", False),
+                                                          ("f64", 1e-12, "2", False), ("f64", 1e-12, "3", True),
+                                                          ("f32", 1e-5, "2", True)])
+def test_nccl_single_rank_communicator(monkeypatch, precision, tol, chunks, use_async):
     """The NCCL exchange itself on one GPU: a single-rank communicator
     (CTF_NCCL_SINGLE_RANK=1) drives the reduce -> ncclAllReduce -> apply path
     (packed MU-V sums, row powers, objective, mean power, error words) and must
     reproduce the plain world = 1 run."""
     from paper_2510_02382_b200 import _lib
     import ctypes
-    B, F, T, M, L, K, iters, seed = 2, 37, 300, 2, 3, 4, 4, 6
+    B, F, T, M, L, K, iters, seed = 3, 37, 300, 2, 3, 4, 4, 6
     raw = synth_mixtures(B, F, T, M, M, L, K, 0.6, 31)
     if precision == "f32":
         raw = raw.astype(np.complex64)
@@ -476,14 +479,20 @@ def test_nccl_single_rank_communicator(monkeypatch, precision, tol):
     s.iterate(iters)
     ref = s.download_raw()
     s.close()
+    monkeypatch.setenv("CTF_MIX_CHUNKS", chunks)
     lib = _lib.load()
     uid, err = (ctypes.c_uint8 * 128)(), _lib.CtfErr()
     assert lib.ctf_comm_unique_id(uid, ctypes.byref(err)) == 0, err.msg
     monkeypatch.setenv("CTF_NCCL_SINGLE_RANK", "1")
     s = Session(raw, [L] * M, [K] * M, stack_taps=L, iterations=iters, precision=precision, seed=seed,
                 comm_id=bytes(uid))
-    assert json.loads(s.describe())["collective"] == "nccl"
-    s.iterate(iters)
+    d = json.loads(s.describe())
+    assert d["collective"] == "nccl" and d["mix_chunks"] == int(chunks), d
+    if use_async:  # the benchmark form: n loop bodies, then the trailing finalize
+        s.iterate_async(iters)
+        s.finalize()
+    else:
+        s.iterate(iters)
     got = s.download_raw()
     s.close()
     for a, b in zip(got, ref):
