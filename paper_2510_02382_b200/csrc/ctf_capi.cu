@@ -179,7 +179,11 @@ struct ctf_ctx {
   // all-reduce of chunk k runs on comm_stream while chunk k+1 sweeps, and
   // its apply is deferred to just before chunk k's next sweep
   int nmc = 1;
+  std::vector<int> mix_split;  // chunk k = mixtures [mix_split[k], mix_split[k+1])
   cudaStream_t comm_stream = nullptr;
+  cudaStream_t stream2 = nullptr;  // odd chunks: their sweeps overlap the even chunks' tails
+  cudaEvent_t ev_join = nullptr;
+  cudaStream_t chunk_stream(int k) const { return (k & 1) && stream2 ? stream2 : stream; }
   std::vector<cudaEvent_t> ev_red, ev_ar;
   struct Deferred {
     bool on = false;
@@ -839,8 +843,8 @@ void allreduce(ctf_ctx* c, void* buf, size_t count, int dtype, int op, cudaStrea
     ctf_group* g = c->group;
     auto& mine = g->slots[(size_t)c->rank];
     mine.resize(count * es);
-    CK(cudaMemcpyAsync(mine.data(), buf, count * es, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpyAsync(mine.data(), buf, count * es, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
     g->barrier();
     std::vector<unsigned char> out(count * es);
     for (size_t i = 0; i < count; ++i) {
@@ -862,8 +866,8 @@ void allreduce(ctf_ctx* c, void* buf, size_t count, int dtype, int op, cudaStrea
       }
     }
     g->barrier();  // every rank has read every slot
-    CK(cudaMemcpyAsync(buf, out.data(), count * es, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpyAsync(buf, out.data(), count * es, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
     return;
   }
   const int rc = g_nccl.AllReduce(buf, buf, count, dtype, op, c->comm, st);
@@ -915,7 +919,7 @@ void check_errors(ctf_ctx* c) {
 }
 
 template <class Real>
-void launch_muv(ctf_ctx* c, int m0, int m1) {
+void launch_muv(ctf_ctx* c, int m0, int m1, cudaStream_t st) {
   ctf::MuvParams mp{};
   mp.mix0 = m0;
   mp.Bf = c->Bf.p;
@@ -934,20 +938,20 @@ void launch_muv(ctf_ctx* c, int m0, int m1) {
   dim3 grid((c->T + 127) / 128, (m1 - m0) * c->N, c->nchunk);
   const size_t smem = (size_t)((c->chunk_bins + 7) / 8 * 8) * c->kmax * sizeof(Real);
   switch (c->kmax) {
-    case 4: ctf::muv_partial_kernel<Real, 4><<<grid, 128, smem, c->stream>>>(mp); break;
-    case 10: ctf::muv_partial_kernel<Real, 10><<<grid, 128, smem, c->stream>>>(mp); break;
-    case 12: ctf::muv_partial_kernel<Real, 12><<<grid, 128, smem, c->stream>>>(mp); break;
-    case 20: ctf::muv_partial_kernel<Real, 20><<<grid, 128, smem, c->stream>>>(mp); break;
-    case 8: ctf::muv_partial_kernel<Real, 8><<<grid, 128, smem, c->stream>>>(mp); break;
-    case 16: ctf::muv_partial_kernel<Real, 16><<<grid, 128, smem, c->stream>>>(mp); break;
-    case 24: ctf::muv_partial_kernel<Real, 24><<<grid, 128, smem, c->stream>>>(mp); break;
-    default: ctf::muv_partial_kernel<Real, 32><<<grid, 128, smem, c->stream>>>(mp); break;
+    case 4: ctf::muv_partial_kernel<Real, 4><<<grid, 128, smem, st>>>(mp); break;
+    case 10: ctf::muv_partial_kernel<Real, 10><<<grid, 128, smem, st>>>(mp); break;
+    case 12: ctf::muv_partial_kernel<Real, 12><<<grid, 128, smem, st>>>(mp); break;
+    case 20: ctf::muv_partial_kernel<Real, 20><<<grid, 128, smem, st>>>(mp); break;
+    case 8: ctf::muv_partial_kernel<Real, 8><<<grid, 128, smem, st>>>(mp); break;
+    case 16: ctf::muv_partial_kernel<Real, 16><<<grid, 128, smem, st>>>(mp); break;
+    case 24: ctf::muv_partial_kernel<Real, 24><<<grid, 128, smem, st>>>(mp); break;
+    default: ctf::muv_partial_kernel<Real, 32><<<grid, 128, smem, st>>>(mp); break;
   }
   CK(cudaGetLastError());
 }
 
 template <class Real>
-void launch_apply(ctf_ctx* c, int mode, int obj_slot, int do_v, int m0, int m1) {
+void launch_apply(ctf_ctx* c, int mode, int obj_slot, int do_v, int m0, int m1, cudaStream_t st) {
   ctf::ApplyParams ap{};
   ap.mix0 = m0;
   ap.part = c->part.p;
@@ -974,7 +978,7 @@ void launch_apply(ctf_ctx* c, int mode, int obj_slot, int do_v, int m0, int m1) 
   ap.do_v = do_v;
   const size_t plane = (size_t)c->SK * c->T;
   const int bx = do_v ? (int)std::min<size_t>((plane + 255) / 256, 64) : 1;
-  ctf::reduce_apply_kernel<Real><<<dim3(bx, m1 - m0), 256, 0, c->stream>>>(ap);
+  ctf::reduce_apply_kernel<Real><<<dim3(bx, m1 - m0), 256, 0, st>>>(ap);
   CK(cudaGetLastError());
 }
 
@@ -982,7 +986,7 @@ void launch_apply(ctf_ctx* c, int mode, int obj_slot, int do_v, int m0, int m1) 
 // trailing rescale + objective of the last completed iteration.
 // The iteration kernel (+ its fallback) for mixtures [m0, m1).
 template <class Real>
-void launch_sweep(ctf_ctx* c, bool do_sweep, int m0, int m1) {
+void launch_sweep(ctf_ctx* c, bool do_sweep, int m0, int m1, int k, cudaStream_t st) {
   ctf::SweepParams sp = c->sp;
   auto fill = [&](ctf::SweepParams& sp) {
   sp.x = c->x.p;
@@ -1002,8 +1006,8 @@ void launch_sweep(ctf_ctx* c, bool do_sweep, int m0, int m1) {
   sp.iteration = c->done + 1;
   sp.do_sweep = do_sweep ? 1 : 0;
   sp.has_prev = c->pending ? 1 : 0;
-  sp.fb_list = c->fb_list.p;
-  sp.fb_count = c->fb_count.p;
+  sp.fb_list = c->fb_list.p ? c->fb_list.p + (size_t)m0 * c->FL : nullptr;  // chunk k's tiles
+  sp.fb_count = c->fb_count.p ? c->fb_count.p + k : nullptr;
   sp.fb_theta = c->fb_theta;
   sp.mix0 = m0;
   sp.nmix = c->B;
@@ -1018,12 +1022,12 @@ void launch_sweep(ctf_ctx* c, bool do_sweep, int m0, int m1) {
     cl.part = c->cpart.p;
     cl.bad = c->cbad.p;
     cl.CS = c->cluster_size;
-    CK(cudaMemsetAsync(c->cbad.p, 0, c->cbad.n * sizeof(int), c->stream));
+    CK(cudaMemsetAsync(c->cbad.p, 0, c->cbad.n * sizeof(int), st));
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(c->FL * c->cluster_size, nm);
     lc.blockDim = dim3(c->NT);
     lc.dynamicSmemBytes = c->sweep_smem;
-    lc.stream = c->stream;
+    lc.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = c->cluster_size;
@@ -1037,7 +1041,7 @@ void launch_sweep(ctf_ctx* c, bool do_sweep, int m0, int m1) {
     lc.gridDim = dim3(c->FL * c->cluster_size, nm);
     lc.blockDim = dim3(c->NT);
     lc.dynamicSmemBytes = c->sweep_smem;
-    lc.stream = c->stream;
+    lc.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = c->cluster_size;
@@ -1047,28 +1051,28 @@ void launch_sweep(ctf_ctx* c, bool do_sweep, int m0, int m1) {
     lc.numAttrs = 1;
     CK(cudaLaunchKernelEx(&lc, c->sv.fn, sp));
   } else if (c->sv.kind == 2) {  // persistent over all work items (never chunked)
-    ctf::StreamParams st{};
-    st.s = sp;
-    st.scratch = c->scratch.p;
-    st.nwork = c->B * c->FL;
-    st.ngroups = (c->R + c->sv.rreg - 1) / c->sv.rreg;
-    c->sv.sfn<<<c->stream_grid, c->NT, c->sweep_smem, c->stream>>>(st);
+    ctf::StreamParams stp{};
+    stp.s = sp;
+    stp.scratch = c->scratch.p;
+    stp.nwork = c->B * c->FL;
+    stp.ngroups = (c->R + c->sv.rreg - 1) / c->sv.rreg;
+    c->sv.sfn<<<c->stream_grid, c->NT, c->sweep_smem, st>>>(stp);
   } else if (c->sv.kind == 4) {
     if (c->has_fb) {
-      CK(cudaMemsetAsync(c->fb_count.p, 0, sizeof(int), c->stream));
+      CK(cudaMemsetAsync(c->fb_count.p, 0, sizeof(int), st));
       sp.fb_mode = 1;
     }
-    c->sv.gfn<<<dim3(c->FL, nm), c->NT, c->sweep_smem, c->stream>>>(sp, c->gtab.p);
+    c->sv.gfn<<<dim3(c->FL, nm), c->NT, c->sweep_smem, st>>>(sp, c->gtab.p);
     if (c->has_fb) {  // the bins the Gram form handed over, in the frame domain
       CK(cudaGetLastError());
       ctf::SweepParams fp = c->sp_fb;
       fill(fp);
       fp.fb_mode = 2;
-      c->fbv.fn<<<c->fb_grid, c->fb_nt, c->fb_smem, c->stream>>>(fp);
+      c->fbv.fn<<<c->fb_grid, c->fb_nt, c->fb_smem, st>>>(fp);
       c->timing.launches += 1;
     }
   } else {
-    c->sv.fn<<<dim3(c->FL, nm), c->NT, c->sweep_smem, c->stream>>>(sp);
+    c->sv.fn<<<dim3(c->FL, nm), c->NT, c->sweep_smem, st>>>(sp);
   }
   CK(cudaGetLastError());
   c->timing.sweep_launches += 1;
@@ -1080,9 +1084,10 @@ template <class Real>
 void apply_deferred(ctf_ctx* c, int k) {
   auto& d = c->deferred[(size_t)k];
   if (!d.on) return;
-  const int m0 = k * c->B / c->nmc, m1 = (k + 1) * c->B / c->nmc;
-  CK(cudaStreamWaitEvent(c->stream, c->ev_ar[(size_t)k], 0));
-  launch_apply<Real>(c, 1, d.obj_slot, d.do_v, m0, m1);
+  const int m0 = c->mix_split[(size_t)k], m1 = c->mix_split[(size_t)k + 1];
+  const cudaStream_t st = c->chunk_stream(k);
+  CK(cudaStreamWaitEvent(st, c->ev_ar[(size_t)k], 0));
+  launch_apply<Real>(c, 1, d.obj_slot, d.do_v, m0, m1, st);
   c->timing.launches += 1;
   d.on = false;
 }
@@ -1090,6 +1095,10 @@ void apply_deferred(ctf_ctx* c, int k) {
 template <class Real>
 void flush_deferred(ctf_ctx* c) {
   for (int k = 0; k < c->nmc && k < (int)c->deferred.size(); ++k) apply_deferred<Real>(c, k);
+  if (c->stream2) {  // the odd chunks' work joins the context stream
+    CK(cudaEventRecord(c->ev_join, c->stream2));
+    CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+  }
 }
 
 // One loop body (estimator.cpp:553-654) or, with do_sweep = false, the
@@ -1105,25 +1114,30 @@ void run_body(ctf_ctx* c, bool do_sweep) {
     // overlaps chunk k+1's sweep; its apply runs just before chunk k's next
     // sweep (the only consumer of the updated V / mu of those mixtures)
     const int kNccl = sizeof(Real) == 4 ? kNcclFloat : kNcclDouble;
+    if (c->stream2) {  // the odd chunks start after everything queued before this body
+      CK(cudaEventRecord(c->ev_join, c->stream));
+      CK(cudaStreamWaitEvent(c->stream2, c->ev_join, 0));
+    }
     for (int k = 0; k < c->nmc; ++k) {
-      const int m0 = k * c->B / c->nmc, m1 = (k + 1) * c->B / c->nmc;
+      const int m0 = c->mix_split[(size_t)k], m1 = c->mix_split[(size_t)k + 1];
+      const cudaStream_t st = c->chunk_stream(k);
       apply_deferred<Real>(c, k);
-      launch_sweep<Real>(c, do_sweep, m0, m1);
+      launch_sweep<Real>(c, do_sweep, m0, m1, k, st);
       if (do_sweep) {
-        launch_muv<Real>(c, m0, m1);
+        launch_muv<Real>(c, m0, m1, st);
         c->timing.launches += 1;
       }
-      launch_apply<Real>(c, 0, obj_slot, do_v, m0, m1);
+      launch_apply<Real>(c, 0, obj_slot, do_v, m0, m1, st);
       c->timing.launches += 1;
       const size_t nv = (size_t)(m1 - m0) * 2 * c->SK * c->T, nd = (size_t)(m1 - m0) * (c->R + 1);
       Real* pv = reinterpret_cast<Real*>(c->packed.p) + (size_t)m0 * 2 * c->SK * c->T;
       double* pd = c->packed_d.p + (size_t)m0 * (c->R + 1);
-      if (c->group) {  // in-process exchange: synchronous on the compute stream
-        if (do_sweep) allreduce(c, pv, nv, kNccl, kNcclSum);
-        allreduce(c, pd, nd, kNcclDouble, kNcclSum);
-        CK(cudaEventRecord(c->ev_ar[(size_t)k], c->stream));
+      if (c->group) {  // in-process exchange: synchronous on the chunk's stream
+        if (do_sweep) allreduce(c, pv, nv, kNccl, kNcclSum, st);
+        allreduce(c, pd, nd, kNcclDouble, kNcclSum, st);
+        CK(cudaEventRecord(c->ev_ar[(size_t)k], st));
       } else {  // NCCL on the communication stream, both sums in one group
-        CK(cudaEventRecord(c->ev_red[(size_t)k], c->stream));
+        CK(cudaEventRecord(c->ev_red[(size_t)k], st));
         CK(cudaStreamWaitEvent(c->comm_stream, c->ev_red[(size_t)k], 0));
         if (g_nccl.GroupStart) g_nccl.GroupStart();
         if (do_sweep) allreduce(c, pv, nv, kNccl, kNcclSum, c->comm_stream);
@@ -1133,25 +1147,29 @@ void run_body(ctf_ctx* c, bool do_sweep) {
       }
       c->deferred[(size_t)k] = {true, obj_slot, do_v};
     }
+    if (c->stream2) {  // e1 / e2 on the context stream cover the odd chunks too
+      CK(cudaEventRecord(c->ev_join, c->stream2));
+      CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+    }
   } else {
-    launch_sweep<Real>(c, do_sweep, 0, c->B);
+    launch_sweep<Real>(c, do_sweep, 0, c->B, 0, c->stream);
   }
   CK(cudaEventRecord(e1, c->stream));
   if (c->nmc <= 1) {
     if (do_sweep) {
-      launch_muv<Real>(c, 0, c->B);
+      launch_muv<Real>(c, 0, c->B, c->stream);
       c->timing.launches += 1;
     }
     if (c->collective()) {
-      launch_apply<Real>(c, 0, obj_slot, do_v, 0, c->B);
+      launch_apply<Real>(c, 0, obj_slot, do_v, 0, c->B, c->stream);
       if (c->comm && g_nccl.GroupStart) g_nccl.GroupStart();
       if (do_sweep) allreduce(c, c->packed.p, (size_t)c->B * 2 * c->SK * c->T, sizeof(Real) == 4 ? kNcclFloat : kNcclDouble, kNcclSum);
       allreduce(c, c->packed_d.p, (size_t)c->B * (c->R + 1), kNcclDouble, kNcclSum);
       if (c->comm && g_nccl.GroupEnd && g_nccl.GroupEnd() != 0) throw CtfError(CTF_ERR_CUDA, "ncclGroupEnd failed");
-      launch_apply<Real>(c, 1, obj_slot, do_v, 0, c->B);
+      launch_apply<Real>(c, 1, obj_slot, do_v, 0, c->B, c->stream);
       c->timing.launches += 2;
     } else {
-      launch_apply<Real>(c, 2, obj_slot, do_v, 0, c->B);
+      launch_apply<Real>(c, 2, obj_slot, do_v, 0, c->B, c->stream);
       c->timing.launches += 1;
     }
   }
@@ -1314,6 +1332,9 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host,
   }
   if (c->nmc > 1) {
     if (!c->comm_stream) CK(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    if (!c->stream2) CK(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
+    if (!c->ev_join) CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    if (c->has_fb) c->fb_count.alloc((size_t)c->nmc);
     while ((int)c->ev_red.size() < c->nmc) {
       cudaEvent_t a, b;
       CK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
@@ -1323,6 +1344,27 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host,
     }
   }
   c->deferred.assign((size_t)c->nmc, ctf_ctx::Deferred{});
+  // chunk boundaries at whole waves of the one-CTA-per-bin kernels (a split
+  // in the middle of a wave would add a partial wave per chunk): chunk k ends
+  // at the mixture whose CTAs fill about k/nmc of the waves
+  c->mix_split.assign((size_t)c->nmc + 1, 0);
+  for (int k = 0; k <= c->nmc; ++k) c->mix_split[(size_t)k] = k * c->B / c->nmc;
+  if (c->nmc > 1 && (c->sv.kind == 0 || c->sv.kind == 4)) {
+    int per_sm = 0, nsm = 0;
+    if (c->sv.kind == 4)
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c->sv.gfn, c->NT, c->sweep_smem));
+    else
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c->sv.fn, c->NT, c->sweep_smem));
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+    const long slots = (long)std::max(1, per_sm) * nsm;
+    const long waves = ((long)c->B * c->FL + slots - 1) / slots;
+    for (int k = 1; k < c->nmc; ++k) {
+      const long target = (waves * k / c->nmc) * slots;  // CTAs of the first k chunks
+      int m = (int)(target / c->FL);
+      m = std::max(c->mix_split[(size_t)k - 1] + 1, std::min(m, c->B - (c->nmc - k)));
+      c->mix_split[(size_t)k] = m;
+    }
+  }
   if (c->sv.kind == 2) c->scratch.alloc((size_t)c->stream_grid * c->R * c->TP * cs);
   else c->scratch.free();
   if (c->sv.kind == 3) {
@@ -1492,6 +1534,9 @@ void ctf_close(ctf_ctx* c) {
   for (auto& pr : c->ev_fin) c->ev_pool.push_back(pr.first), c->ev_pool.push_back(pr.second);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
+  if (c->stream2) cudaStreamSynchronize(c->stream2);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->stream2) cudaStreamDestroy(c->stream2);
   for (auto e : c->ev_red) cudaEventDestroy(e);
   for (auto e : c->ev_ar) cudaEventDestroy(e);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
