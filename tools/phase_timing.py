@@ -8,10 +8,10 @@ from paper_2510_02382_b200 import _lib
 _lib.LIB_PATH = os.environ.get("CTF_DEV_LIB") or os.path.join(ROOT, "tools", "phase", "libctfiss.so")
 from paper_2510_02382_b200 import Session, synth_mixtures
 import argparse
-ap = argparse.ArgumentParser(); ap.add_argument("--cfg", type=int, default=1); a = ap.parse_args()
+ap = argparse.ArgumentParser(); ap.add_argument("--cfg", type=int, default=1); ap.add_argument("--prec", default="f32"); a = ap.parse_args()
 B, F, T, M, N, L, K = {1: (64, 513, 1000, 2, 2, 5, 10), 2: (16, 1025, 2000, 3, 3, 4, 20), 3: (8, 2049, 1000, 4, 4, 8, 20)}[a.cfg]
-x = synth_mixtures(B, F, T, M, N, L, K, 0.6, 1, precision="f32")
-s = Session(x, [L] * N, [K] * N, stack_taps=L, iterations=4, precision="f32")
+x = synth_mixtures(B, F, T, M, N, L, K, 0.6, 1, precision=a.prec)
+s = Session(x, [L] * N, [K] * N, stack_taps=L, iterations=4, precision=a.prec)
 print(s.describe())
 s.iterate_async(3)
 import torch; torch.cuda.synchronize()
