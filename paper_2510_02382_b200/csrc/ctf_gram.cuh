@@ -145,8 +145,27 @@ __device__ __forceinline__ double log_fast(double x) { return log(x); }
 template <typename Real, int N, int R> constexpr int gram_ns() {
   return (std::is_same<Real, float>::value && R <= 16) ? N : (R <= 16 && N % CTF_GRAM_NS64 == 0 ? CTF_GRAM_NS64 : 1);
 }
+// Sources accumulated per Gram pass over the frames (NSG >= gram_ns, a
+// multiple of it): fp64 two-source shapes share each conj product between
+// both sources (the second source's partials wait in registers while the
+// first's are reduced: the partial buffer holds gram_ns sources).
+#ifndef CTF_GRAM_NSG64
+#define CTF_GRAM_NSG64 2
+#endif
+template <typename Real, int N, int R> constexpr int gram_nsg() {
+  return (!std::is_same<Real, float>::value && R <= 16 && N == CTF_GRAM_NSG64) ? N : gram_ns<Real, N, R>();
+}
+#ifndef CTF_GRAM_UB2  // frames per register block when two fp64 sources share the products
+#define CTF_GRAM_UB2 1
+#endif
+#ifndef CTF_GRAM_RCP64
+#define CTF_GRAM_RCP64 1
+#endif
+#ifndef CTF_GRAM_MINB64
+#define CTF_GRAM_MINB64 2
+#endif
 template <typename Real, int NT, int R> constexpr int gram_min_blocks() {
-  return R > 16 ? 1 : std::is_same<Real, float>::value ? (NT <= 256 ? 3 : 1) : (NT <= 256 ? 2 : 1);
+  return R > 16 ? 1 : std::is_same<Real, float>::value ? (NT <= 256 ? 3 : 1) : (NT <= 256 ? CTF_GRAM_MINB64 : 1);
 }
 
 // Tensor-core Gram (TC = true, fp32): the lag correlations as one real GEMM
@@ -664,46 +683,65 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
     const R2* x1 = xs + g0.x * p.xp + p.xoff;
     const R2* x2 = xs + g0.y * p.xp + p.xoff + g0.z;
     const int ng = gtab[NT].x;
-    for (int n0 = 0; n0 < N; n0 += NS) {
+    constexpr int NSG = gram_nsg<Real, N, R>();  // sources per pass over the frames
+    constexpr int NSP = NS;                      // sources whose partials fit the buffer at once
+    static_assert(NSG % NSP == 0, "partial groups");
+    R2 keep[NSG > NSP ? NSG - NSP : 1][NA];  // partials of the later source groups, in registers
+    for (int n0 = 0; n0 < N; n0 += NSG) {
       const Real* w0 = invl + n0 * p.lp + p.loff - g0.w;
       static_for<L, NA + 1>([&](auto cc) {
         constexpr int C = decltype(cc)::value;
         if (cmax == C) {
-          R2 acc[NS][C];
+          R2 acc[NSG][C];
 #pragma unroll
-          for (int n = 0; n < NS; ++n)
+          for (int n = 0; n < NSG; ++n)
 #pragma unroll
             for (int j = 0; j < C; ++j) acc[n][j].x = acc[n][j].y = Real(0);
-          if (active) gram_block<Real, C, NS, kGramUB>(x1, x2, w0, p.lp, tk.y, tk.z, acc);
+          if (active)
+            gram_block<Real, C, NSG, (NSG > NSP ? CTF_GRAM_UB2 : kGramUB)>(x1, x2, w0, p.lp, tk.y, tk.z, acc);
 #pragma unroll
-          for (int n = 0; n < NS; ++n)
+          for (int n = 0; n < NSP; ++n)
 #pragma unroll
             for (int j = 0; j < C; ++j)
               if (j < cnt) part[(size_t)(n * NA + j) * (NT + 1) + tid] = acc[n][j];
+#pragma unroll
+          for (int n = NSP; n < NSG; ++n)
+#pragma unroll
+            for (int j = 0; j < C; ++j) keep[n - NSP][j] = acc[n][j];
         }
       });
-      __syncthreads();
-      CTF_PHASE(3);
-      for (int e = tid; e < ng * NS * NA; e += NT) {
-        const int g = e / (NS * NA), rr = e - g * (NS * NA), n = rr / NA, j = rr - n * NA;
-        const int4 h0 = gtab[NT + 1 + 2 * g], h1 = gtab[NT + 2 + 2 * g];
-        if (j >= h1.x) continue;
-        R2 sum;
-        sum.x = sum.y = Real(0);
-        const R2* pr = part + (size_t)(n * NA + j) * (NT + 1);
-        for (int t = h1.y; t < h1.z; ++t) {
-          sum.x += pr[t].x;
-          sum.y += pr[t].y;
+#pragma unroll
+      for (int s0 = 0; s0 < NSG; s0 += NSP) {
+        if (s0 > 0) {  // the next source group's partials from registers (lags >= cmax are never read)
+#pragma unroll
+          for (int n = 0; n < NSP; ++n)
+#pragma unroll
+            for (int j = 0; j < NA; ++j)
+              if (j < cnt) part[(size_t)(n * NA + j) * (NT + 1) + tid] = keep[s0 - NSP + n][j];
         }
-        const int m = h0.x, m2 = h0.y, d = h0.z, a = h0.w + j, b = a + d;
-        G[gidx(n0 + n, m, m2, a, b)] = sum;  // groups have m <= m2
-        if (m == m2 && d != 0) {              // the mirrored lag of the same mic
-          R2 mir = sum;
-          mir.y = -sum.y;
-          G[gidx(n0 + n, m, m, b, a)] = mir;
+        __syncthreads();
+        CTF_PHASE(3);
+        for (int e = tid; e < ng * NSP * NA; e += NT) {
+          const int g = e / (NSP * NA), rr = e - g * (NSP * NA), n = rr / NA, j = rr - n * NA;
+          const int4 h0 = gtab[NT + 1 + 2 * g], h1 = gtab[NT + 2 + 2 * g];
+          if (j >= h1.x) continue;
+          R2 sum;
+          sum.x = sum.y = Real(0);
+          const R2* pr = part + (size_t)(n * NA + j) * (NT + 1);
+          for (int t = h1.y; t < h1.z; ++t) {
+            sum.x += pr[t].x;
+            sum.y += pr[t].y;
+          }
+          const int m = h0.x, m2 = h0.y, d = h0.z, a = h0.w + j, b = a + d;
+          G[gidx(n0 + s0 + n, m, m2, a, b)] = sum;  // groups have m <= m2
+          if (m == m2 && d != 0) {                   // the mirrored lag of the same mic
+            R2 mir = sum;
+            mir.y = -sum.y;
+            G[gidx(n0 + s0 + n, m, m, b, a)] = mir;
+          }
         }
+        __syncthreads();
       }
-      __syncthreads();
     }
   }
   }
@@ -1123,6 +1161,10 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
         } else {
           if constexpr (F32) {
             const float inv = __frcp_rn(den);
+            z.x = nre * inv;
+            z.y = nim * inv;
+          } else if constexpr (CTF_GRAM_RCP64) {  // one division (rounding differs by <= 1 ulp)
+            const double inv = 1.0 / den;
             z.x = nre * inv;
             z.y = nim * inv;
           } else {
