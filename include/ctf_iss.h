@@ -202,8 +202,13 @@ int ctf_describe(ctf_ctx* ctx, char* buf, int len);
 /* Absolute PSD floor per mixture (factors.floor, estimator.cpp:529). */
 int ctf_psd_floor(ctf_ctx* ctx, double* floor_out /* [B] */);
 /* Per-iteration phase times (OptimizationTrace demix_ms / mu_ms /
- * rescale_ms, estimator.hpp:25-40) from CUDA events; rescale is fused into
- * the next sweep and reported as 0. Arrays of ctf_iterations_done() entries. */
+ * rescale_ms, estimator.hpp:25-40, timed as at estimator.cpp:623-653) from
+ * CUDA events: demix_ms = the fused sweep kernel (ISS steps, demix, MU-B),
+ * mu_ms = the MU-V partials, rescale_ms = the reduce/apply kernel that forms
+ * mu_r from the row powers, applies V and the objective (the division of W
+ * and B by mu is fused into the next sweep's prologue). With mixture chunks
+ * (multi-rank pipelining) the apply is inside mu_ms and rescale_ms is 0.
+ * Arrays of ctf_iterations_done() entries. */
 int ctf_trace_ms(ctf_ctx* ctx, double* demix_ms, double* mu_ms, double* rescale_ms);
 
 /* OptimizationTrace check fields (estimator.hpp:31-34) per mixture, for a

@@ -208,9 +208,10 @@ struct ctf_ctx {
   DevBuf<double2> stft_spec;
   // timing
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_sweep, ev_mu, ev_fin;
+  std::vector<cudaEvent_t> ev_rs;  // per iteration: between MU-V and the reduce/apply kernel (null when chunked)
   std::vector<cudaEvent_t> ev_pool;
   ctf_timing timing{};
-  std::vector<double> it_sweep_ms, it_mu_ms;  // per completed iteration
+  std::vector<double> it_sweep_ms, it_mu_ms, it_rs_ms;  // per completed iteration
   std::vector<double> floors;
 };
 
@@ -464,6 +465,10 @@ void plan_sweep(ctf_ctx* c) {
       cand.off_z = (int)take((size_t)NW * v.rmax * cs);
       cand.off_b = (int)take((size_t)c->SK * rs);
       cand.off_d = (int)take((size_t)NW * 4 * sizeof(double));
+      if (v.ip) {  // IP rule: square W, warp solve (ip_solve_row)
+        if (c->R != c->D || c->D > 32) continue;
+        cand.off_ip = (int)take((size_t)(3 * c->D * c->D + 2 * c->D) * cs);
+      }
     } else if (v.kind == 4) {  // covariance-domain (Gram) kernel: stacked equal taps, M = N
       const int M = v.rreg, L = v.lt;
       if (c->Mx != M || c->N != M || c->Ls != L || c->R != v.rmax || c->D != v.rmax) continue;
@@ -652,8 +657,8 @@ void plan_sweep(ctf_ctx* c) {
   c->TP = best_TP;
   if (!found && want_ip)
     throw CtfError(CTF_ERR_CONFIG,
-                   "update rule 'ip' on the GPU runs on the covariance-domain kernel: it needs the stacked "
-                   "observation (stack_taps = taps of every source), num_sources == num_mics and a compiled "
+                   "update rule 'ip' on the GPU needs a square demixing matrix (sum of taps == channels) with "
+                   "R <= 16 and T <= 2048 frames (frame-domain IP variants), or a compiled covariance-domain "
                    "(mics, taps) pair");
   if (!found && want_chk)
     throw CtfError(CTF_ERR_UNSUPPORTED, "CheckOptions need a resident tile (R <= 16, T <= 2048)");
@@ -662,6 +667,8 @@ void plan_sweep(ctf_ctx* c) {
                                             " T=" + std::to_string(c->T));
   c->sv = best;
   c->NT = best_nt;
+  if (const char* pad = std::getenv("CTF_SMEM_PAD"))  // measurement aid: lower the CTAs per SM
+    best_smem += (size_t)std::atoi(pad);
   c->sweep_smem = best_smem;
   if (best.kind == 3) {
     CK(cudaFuncSetAttribute((const void*)best.cfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)best_smem));
@@ -1155,10 +1162,13 @@ void run_body(ctf_ctx* c, bool do_sweep) {
     launch_sweep<Real>(c, do_sweep, 0, c->B, 0, c->stream);
   }
   CK(cudaEventRecord(e1, c->stream));
+  cudaEvent_t ers = nullptr;  // OptimizationTrace::rescale_ms starts here (mu, V apply, objective)
   if (c->nmc <= 1) {
     if (do_sweep) {
       launch_muv<Real>(c, 0, c->B, c->stream);
       c->timing.launches += 1;
+      ers = take_event(c);
+      CK(cudaEventRecord(ers, c->stream));
     }
     if (c->collective()) {
       launch_apply<Real>(c, 0, obj_slot, do_v, 0, c->B, c->stream);
@@ -1177,6 +1187,7 @@ void run_body(ctf_ctx* c, bool do_sweep) {
   if (do_sweep) {
     c->ev_sweep.push_back({e0, e1});
     c->ev_mu.push_back({e1, e2});
+    c->ev_rs.push_back(ers);
     c->done += 1;
     c->pending = true;
   } else {
@@ -1200,19 +1211,26 @@ void collect_timing(ctf_ctx* c) {
   };
   // ev_sweep and ev_mu share events; collect times first, then recycle once
   for (size_t i = 0; i < c->ev_sweep.size(); ++i) {
-    float a = 0.f, b = 0.f;
+    float a = 0.f, b = 0.f, r = 0.f;
     CK(cudaEventElapsedTime(&a, c->ev_sweep[i].first, c->ev_sweep[i].second));
     CK(cudaEventElapsedTime(&b, c->ev_mu[i].first, c->ev_mu[i].second));
+    const cudaEvent_t ers = i < c->ev_rs.size() ? c->ev_rs[i] : nullptr;
+    if (ers) {
+      CK(cudaEventElapsedTime(&r, ers, c->ev_mu[i].second));
+      c->ev_pool.push_back(ers);
+    }
     c->timing.sweep_ms += a;
     c->timing.mu_ms += b;
     c->it_sweep_ms.push_back(a);
-    c->it_mu_ms.push_back(b);
+    c->it_mu_ms.push_back(b - r);
+    c->it_rs_ms.push_back(r);
     c->ev_pool.push_back(c->ev_sweep[i].first);
     c->ev_pool.push_back(c->ev_sweep[i].second);
     c->ev_pool.push_back(c->ev_mu[i].second);
   }
   c->ev_sweep.clear();
   c->ev_mu.clear();
+  c->ev_rs.clear();
   drain(c->ev_fin, c->timing.finalize_ms);
 }
 
@@ -1469,6 +1487,7 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host,
   c->floors = floors;
   c->it_sweep_ms.clear();
   c->it_mu_ms.clear();
+  c->it_rs_ms.clear();
 
   pool.join_all();  // the initial factors (drawn on host threads while x was uploaded)
   upload_real(c, c->Bf.p, hb.data(), hb.size());
@@ -1531,6 +1550,9 @@ void ctf_close(ctf_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto& pr : c->ev_sweep) c->ev_pool.push_back(pr.first), c->ev_pool.push_back(pr.second);
   for (auto& pr : c->ev_mu) c->ev_pool.push_back(pr.second);
+  for (auto e : c->ev_rs)
+    if (e) c->ev_pool.push_back(e);
+  c->ev_rs.clear();
   for (auto& pr : c->ev_fin) c->ev_pool.push_back(pr.first), c->ev_pool.push_back(pr.second);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
@@ -1720,7 +1742,7 @@ int ctf_trace_ms(ctf_ctx* c, double* demix_ms, double* mu_ms, double* rescale_ms
   for (size_t i = 0; i < n; ++i) {
     if (demix_ms) demix_ms[i] = c->it_sweep_ms[off + i];
     if (mu_ms) mu_ms[i] = c->it_mu_ms[off + i];
-    if (rescale_ms) rescale_ms[i] = 0.0;
+    if (rescale_ms) rescale_ms[i] = c->it_rs_ms[off + i];
   }
   return CTF_OK;
 }

@@ -165,7 +165,7 @@ template <typename Real, int N, int R> constexpr int gram_nsg() {
 #define CTF_GRAM_MINB64 2
 #endif
 template <typename Real, int NT, int R> constexpr int gram_min_blocks() {
-  return R > 16 ? 1 : std::is_same<Real, float>::value ? (NT <= 256 ? 3 : 1) : (NT <= 256 ? CTF_GRAM_MINB64 : 1);
+  return R > 16 ? 1 : std::is_same<Real, float>::value ? (NT <= 256 ? 3 : 1) : (NT <= 256 ? CTF_GRAM_MINB64 : NT <= 384 ? 2 : 1);
 }
 
 // Tensor-core Gram (TC = true, fp32): the lag correlations as one real GEMM
@@ -977,112 +977,7 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
       }
       __syncthreads();
       if (warp == 0) {
-        auto attempt = [&](Real load) -> bool {
-          // A = W (h + load I) = W h + load W, rhs e_r
-          for (int e = lane; e < D * (D + 1); e += 32) {
-            const int i = e % D, j = e / D;
-            R2 acc;
-            acc.x = acc.y = Real(0);
-            if (j < D) {
-              for (int k = 0; k < D; ++k) cmac(acc, Wb[i + k * R], cov[k + j * D]);
-              acc.x += load * Wb[i + j * R].x;
-              acc.y += load * Wb[i + j * R].y;
-            } else {
-              acc.x = (i == r) ? Real(1) : Real(0);
-            }
-            A[i + j * D] = acc;
-          }
-          __syncwarp();
-          double minp = INFINITY, maxp = 0.0;
-          for (int c = 0; c < D; ++c) {
-            // pivot: largest |a| in column c at or below the diagonal, lowest row on ties
-            Real best = Real(-1);
-            int prow = D;
-            if (lane >= c && lane < D) {
-              const R2 v = A[lane + c * D];
-              best = sqrt(cnorm(v));
-              prow = lane;
-            }
-#pragma unroll
-            for (int o = 16; o >= 1; o >>= 1) {
-              const Real ob = __shfl_xor_sync(kFull, best, o);
-              const int orow = __shfl_xor_sync(kFull, prow, o);
-              if (ob > best || (ob == best && orow < prow)) {
-                best = ob;
-                prow = orow;
-              }
-            }
-            minp = fmin(minp, (double)best);
-            maxp = fmax(maxp, (double)best);
-            if (prow != c)
-              for (int j = lane; j <= D; j += 32) {
-                const R2 t = A[c + j * D];
-                A[c + j * D] = A[prow + j * D];
-                A[prow + j * D] = t;
-              }
-            __syncwarp();
-            if (!(best > Real(0))) continue;
-            const R2 piv = A[c + c * D];
-            const Real ip2 = Real(1) / cnorm(piv);
-            const int w = D - c;  // rows c+1..D-1 x columns c+1..D
-            for (int e = lane; e < (w - 1) * w; e += 32) {
-              const int rr = c + 1 + e % (w - 1), j = c + 1 + e / (w - 1);
-              const R2 arc = A[rr + c * D];
-              R2 f;  // a(r, c) / a(c, c)
-              f.x = (arc.x * piv.x + arc.y * piv.y) * ip2;
-              f.y = (arc.y * piv.x - arc.x * piv.y) * ip2;
-              cmsub(A[rr + j * D], f, A[c + j * D]);
-            }
-            __syncwarp();
-          }
-          if (!(minp > 1e-13 * maxp)) return false;
-          if (lane == 0)
-            for (int rr = D - 1; rr >= 0; --rr) {
-              R2 acc = A[rr + D * D];
-              for (int j = rr + 1; j < D; ++j) cmsub(acc, A[rr + j * D], sol[j]);
-              const R2 d = A[rr + rr * D];
-              const Real id = Real(1) / cnorm(d);
-              R2 q;
-              q.x = (acc.x * d.x + acc.y * d.y) * id;
-              q.y = (acc.y * d.x - acc.x * d.y) * id;
-              sol[rr] = q;
-            }
-          __syncwarp();
-          bool fin = true;
-          if (lane < D) fin = cfinite(sol[lane]);
-          return __all_sync(kFull, fin);
-        };
-        bool ok = attempt(Real(0));
-        if (!ok) {
-          Real tr = Real(0);
-          for (int i = 0; i < D; ++i) tr += cov[i + i * D].x;
-          ok = attempt(Real(1e-10) * tr / (Real)D);
-        }
-        int err = 0;
-        if (!ok) {
-          err = 1;  // singular system after diagonal loading
-        } else {
-          // scale against the unloaded covariance: norm2 = Re(u^H h u)
-          Real part_n = Real(0);
-          if (lane < D) {
-            R2 wgt;
-            wgt.x = wgt.y = Real(0);
-            for (int j = 0; j < D; ++j) cmac(wgt, cov[lane + j * D], sol[j]);
-            const R2 u = sol[lane];
-            part_n = u.x * wgt.x + u.y * wgt.y;
-          }
-          for (int o = 16; o >= 1; o >>= 1) part_n += __shfl_xor_sync(kFull, part_n, o);
-          if (!(part_n > Real(0)) || !isfinite(part_n)) {
-            err = 2;  // nonpositive row power
-          } else if (lane < D) {
-            const Real sc = Real(1) / sqrt(part_n);
-            const R2 u = sol[lane];
-            R2 wv;
-            wv.x = u.x * sc;
-            wv.y = -u.y * sc;
-            Wb[r + lane * R] = wv;
-          }
-        }
+        const int err = ip_solve_row<Real>(Wb, R, D, r, cov, A, sol, lane);
         if (lane == 0 && err) s_iperr = err;
       }
       __syncthreads();

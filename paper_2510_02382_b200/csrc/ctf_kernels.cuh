@@ -64,6 +64,7 @@ struct SweepParams {
   int loff, lp;   // 1/lambda: N rows of lp = loff + TP, at [n*lp + loff + tau]
   double* logdet;           // [mix][FL] log|det W| (pre-rescale after a sweep)
   int off_y, off_x, off_e, off_l, off_w, off_red, off_z, off_b, off_d;  // smem byte offsets
+  int off_ip;  // IP-rule scratch of the frame-domain kernel (3 D x D + 2 D complex)
   int woff[kMaxRows];  // per row p: n_p*lp + loff - l_p (weight index base)
   int xcol[kMaxRows];  // per stacked channel c = m*Ls + l: m*xp + xoff - l (x tile offset)
   int srcr[kMaxRows];  // source of each row
@@ -363,6 +364,126 @@ __device__ __forceinline__ void record_err(unsigned long long* err, int mix, uns
   atomicMin(err + mix, key);
 }
 
+// One row of the IP rule (estimator.cpp:103-273, ip_update): solve
+// (W h) u = e_r by LU with partial pivoting (pivot-ratio singularity probe
+// 1e-13 on |pivot|, i.e. 1e-26 on |pivot|^2 as ip_update_small; one retry
+// with 1e-10 tr(h)/D diagonal loading), then W[r, :] = conj(u) / sqrt(u^H h u)
+// with the unloaded h. W column-major R x D (R == D <= 32), h (cov) D x D,
+// A scratch D x (D+1), sol D, all in shared memory. Called by one whole warp;
+// returns 0, 1 (singular after loading) or 2 (nonpositive row power).
+template <typename Real>
+__device__ int ip_solve_row(typename Cplx<Real>::T* Wb, int R, int D, int r, const typename Cplx<Real>::T* cov,
+                            typename Cplx<Real>::T* A, typename Cplx<Real>::T* sol, int lane) {
+  using R2 = typename Cplx<Real>::T;
+  auto attempt = [&](Real load) -> bool {
+    // A = W (h + load I) = W h + load W, rhs e_r
+    for (int e = lane; e < D * (D + 1); e += 32) {
+      const int i = e % D, j = e / D;
+      R2 acc;
+      acc.x = acc.y = Real(0);
+      if (j < D) {
+        for (int k = 0; k < D; ++k) cmac(acc, Wb[i + k * R], cov[k + j * D]);
+        acc.x += load * Wb[i + j * R].x;
+        acc.y += load * Wb[i + j * R].y;
+      } else {
+        acc.x = (i == r) ? Real(1) : Real(0);
+      }
+      A[i + j * D] = acc;
+    }
+    __syncwarp();
+    double minp = INFINITY, maxp = 0.0;
+    for (int c = 0; c < D; ++c) {
+      // pivot: largest |a| in column c at or below the diagonal, lowest row on ties
+      Real best = Real(-1);
+      int prow = D;
+      if (lane >= c && lane < D) {
+        const R2 v = A[lane + c * D];
+        best = sqrt(cnorm(v));
+        prow = lane;
+      }
+  #pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        const Real ob = __shfl_xor_sync(kFull, best, o);
+        const int orow = __shfl_xor_sync(kFull, prow, o);
+        if (ob > best || (ob == best && orow < prow)) {
+          best = ob;
+          prow = orow;
+        }
+      }
+      minp = fmin(minp, (double)best);
+      maxp = fmax(maxp, (double)best);
+      if (prow != c)
+        for (int j = lane; j <= D; j += 32) {
+          const R2 t = A[c + j * D];
+          A[c + j * D] = A[prow + j * D];
+          A[prow + j * D] = t;
+        }
+      __syncwarp();
+      if (!(best > Real(0))) continue;
+      const R2 piv = A[c + c * D];
+      const Real ip2 = Real(1) / cnorm(piv);
+      const int w = D - c;  // rows c+1..D-1 x columns c+1..D
+      for (int e = lane; e < (w - 1) * w; e += 32) {
+        const int rr = c + 1 + e % (w - 1), j = c + 1 + e / (w - 1);
+        const R2 arc = A[rr + c * D];
+        R2 f;  // a(r, c) / a(c, c)
+        f.x = (arc.x * piv.x + arc.y * piv.y) * ip2;
+        f.y = (arc.y * piv.x - arc.x * piv.y) * ip2;
+        cmsub(A[rr + j * D], f, A[c + j * D]);
+      }
+      __syncwarp();
+    }
+    if (!(minp > 1e-13 * maxp)) return false;
+    if (lane == 0)
+      for (int rr = D - 1; rr >= 0; --rr) {
+        R2 acc = A[rr + D * D];
+        for (int j = rr + 1; j < D; ++j) cmsub(acc, A[rr + j * D], sol[j]);
+        const R2 d = A[rr + rr * D];
+        const Real id = Real(1) / cnorm(d);
+        R2 q;
+        q.x = (acc.x * d.x + acc.y * d.y) * id;
+        q.y = (acc.y * d.x - acc.x * d.y) * id;
+        sol[rr] = q;
+      }
+    __syncwarp();
+    bool fin = true;
+    if (lane < D) fin = cfinite(sol[lane]);
+    return __all_sync(kFull, fin);
+  };
+  bool ok = attempt(Real(0));
+  if (!ok) {
+    Real tr = Real(0);
+    for (int i = 0; i < D; ++i) tr += cov[i + i * D].x;
+    ok = attempt(Real(1e-10) * tr / (Real)D);
+  }
+  int err = 0;
+  if (!ok) {
+    err = 1;  // singular system after diagonal loading
+  } else {
+    // scale against the unloaded covariance: norm2 = Re(u^H h u)
+    Real part_n = Real(0);
+    if (lane < D) {
+      R2 wgt;
+      wgt.x = wgt.y = Real(0);
+      for (int j = 0; j < D; ++j) cmac(wgt, cov[lane + j * D], sol[j]);
+      const R2 u = sol[lane];
+      part_n = u.x * wgt.x + u.y * wgt.y;
+    }
+    for (int o = 16; o >= 1; o >>= 1) part_n += __shfl_xor_sync(kFull, part_n, o);
+    if (!(part_n > Real(0)) || !isfinite(part_n)) {
+      err = 2;  // nonpositive row power
+    } else if (lane < D) {
+      const Real sc = Real(1) / sqrt(part_n);
+      const R2 u = sol[lane];
+      R2 wv;
+      wv.x = u.x * sc;
+      wv.y = -u.y * sc;
+      Wb[r + lane * R] = wv;
+    }
+  }
+  return err;
+}
+
 // ---------------------------------------------------------------------------
 // The fused per-bin iteration kernel.
 //
@@ -386,13 +507,18 @@ template <typename Real> constexpr int sweep_min_blocks(int nt) {
 // per source with immediate offsets.
 // CHECK: CheckOptions instrumentation (exact recomputation of det W after
 // every step by a warp LU, and of each updated row's weighted power).
-template <typename Real, int RMAX, int FT, int RREG, int NT, bool EXACT, int LT, bool CHECK>
+// IPR: the IP rule (estimator.cpp:580-606) in place of the ISS steps, for any
+// layout (pre-stacked or unequal taps; R == D): per row the weighted
+// covariance from the x tile, a warp LU solve (ip_solve_row) and the
+// frame-sum refinement, then Y = W' x~ recomputed for the epilogue.
+template <typename Real, int RMAX, int FT, int RREG, int NT, bool EXACT, int LT, bool CHECK, bool IPR>
 __device__ __forceinline__ void sweep_body(const SweepParams& p, const int bin, const int mix);
 
-template <typename Real, int RMAX, int FT, int RREG, int NT, bool EXACT, int LT = 0, bool CHECK = false>
+template <typename Real, int RMAX, int FT, int RREG, int NT, bool EXACT, int LT = 0, bool CHECK = false,
+          bool IPR = false>
 __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(const SweepParams p) {
   if (p.fb_mode != 2) {  // one work item per CTA: (bin, mixture) = (blockIdx.x, blockIdx.y)
-    sweep_body<Real, RMAX, FT, RREG, NT, EXACT, LT, CHECK>(p, blockIdx.x, blockIdx.y + p.mix0);
+    sweep_body<Real, RMAX, FT, RREG, NT, EXACT, LT, CHECK, IPR>(p, blockIdx.x, blockIdx.y + p.mix0);
     return;
   }
   // conditioning fallback of the covariance-domain kernel: the listed items
@@ -400,11 +526,11 @@ __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(c
   for (int w = blockIdx.x; w < cnt; w += gridDim.x) {
     const int t = p.fb_list[w];
     __syncthreads();  // shared memory of the previous item
-    sweep_body<Real, RMAX, FT, RREG, NT, EXACT, LT, CHECK>(p, t % p.FL, t / p.FL);
+    sweep_body<Real, RMAX, FT, RREG, NT, EXACT, LT, CHECK, IPR>(p, t % p.FL, t / p.FL);
   }
 }
 
-template <typename Real, int RMAX, int FT, int RREG, int NT, bool EXACT, int LT, bool CHECK>
+template <typename Real, int RMAX, int FT, int RREG, int NT, bool EXACT, int LT, bool CHECK, bool IPR>
 __device__ __forceinline__ void sweep_body(const SweepParams& p, const int bin, const int mix) {
   using R2 = typename Cplx<Real>::T;
   constexpr int RS = RMAX - RREG;
@@ -564,6 +690,93 @@ __device__ __forceinline__ void sweep_body(const SweepParams& p, const int bin, 
     return;
   }
 
+  double dprod = 1.0;  // prod_r (1 - z_r): det W' = det W prod_r (1 - z_r)
+  double c_det = 0.0, c_norm = 0.0;  // CHECK maxima
+  Real lastn = Real(0);  // CHECK: weighted power of the last updated row
+  double ip_logdet = 0.0;  // IPR: exact log|det W'|
+  if constexpr (IPR) {
+    // ---- IP rule (estimator.cpp:580-606): per row r = (n, l) the weighted
+    // covariance h = (Q + Q^H) / 2, Q = sum_{j>=l} x~(j) x~(j)^H / lambda_n(j-l)
+    // / T (compute_weighted_covariance :89-101) from the x tile, the solve,
+    // then w_r /= sqrt(sum_{j>=l} |w_r x~(j)|^2 / lambda_n(j-l) / T)
+    // (steering_row_power, :596-602).
+    static_assert(!CHECK, "CheckOptions with the IP rule run in the covariance-domain variants");
+    R2* qm = reinterpret_cast<R2*>(smem + p.off_ip);  // D x D raw Q / T
+    R2* cov = qm + D * D;                              // D x D h
+    R2* A = cov + D * D;                               // D x (D+1)
+    R2* sol = A + D * (D + 1);                         // D
+    __shared__ int s_iperr;
+    if (tid == 0) s_iperr = 0;
+    for (int r = 0; r < R; ++r) {
+      const Real* wr = invl + p.woff[r];  // weight of row r at frame j: wr[j] (zero for j < l)
+      for (int e = tid; e < D * D; e += NT) {
+        const int a = e % D, b = e / D;
+        const R2* xa = xs + p.xcol[a];
+        const R2* xb = xs + p.xcol[b];
+        R2 v = czero<Real>();
+        for (int j = 0; j < T; ++j) {
+          const R2 u = xa[j], t = xb[j];
+          const Real w = wr[j];
+          v.x = fma(fma(u.x, t.x, u.y * t.y), w, v.x);
+          v.y = fma(fma(u.y, t.x, -u.x * t.y), w, v.y);
+        }
+        v.x /= (Real)T;
+        v.y /= (Real)T;
+        qm[a + b * D] = v;
+      }
+      __syncthreads();
+      for (int e = tid; e < D * D; e += NT) {
+        const int a = e % D, b = e / D;
+        const R2 u = qm[a + b * D], t = qm[b + a * D];
+        R2 h;
+        h.x = Real(0.5) * (u.x + t.x);
+        h.y = Real(0.5) * (u.y - t.y);
+        cov[a + b * D] = h;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        const int err = ip_solve_row<Real>(Wb, R, D, r, cov, A, sol, lane);
+        if (lane == 0 && err) s_iperr = err;
+      }
+      __syncthreads();
+      if (s_iperr) {
+        if (tid == 0) record_err<Real>(p.err, mix, err_key(p.iteration, kPhSweep, gbin, r, s_iperr));
+        return;
+      }
+      double pw = 0.0;
+#pragma unroll
+      for (int k = 0; k < FT; ++k) {
+        const int j = tid + k * NT;
+        if (j < T) {
+          R2 y = czero<Real>();
+          for (int c = 0; c < D; ++c) cmac(y, Wb[r + c * R], xs[p.xcol[c] + j]);
+          pw += (double)(cnorm(y) * wr[j]);
+        }
+      }
+      double v1[1] = {pw};
+      block_sum_d<1>(v1, dred, lane, warp, NW);
+      const double power = v1[0] / T;
+      if (power > 0.0 && isfinite(power) && tid < D) {
+        R2 w = Wb[r + tid * R];
+        w.x = (Real)((double)w.x / sqrt(power));
+        w.y = (Real)((double)w.y / sqrt(power));
+        Wb[r + tid * R] = w;
+      }
+      __syncthreads();
+    }
+    if (warp == 0) {  // exact log|det W'| (no determinant lemma for IP)
+      R2* Acp = qm;
+      for (int i = lane; i < R * D; i += 32) Acp[i] = Wb[i];
+      __syncwarp();
+      double out = 0.0;
+      const int st = warp_logdet<Real>(Acp, R, lane, out);
+      if (lane == 0) dred[0] = st == 4 ? -INFINITY : out;
+    }
+    __syncthreads();
+    ip_logdet = dred[0];
+    __syncthreads();
+    demix_tile<Real, RMAX, FT, RREG, EXACT>(Y, xs, Wb, p, tid, NT, R, D);  // Y = W' x~ (estimator.cpp:607)
+  } else {
   // ---- ISS sweep (estimator.cpp:556-579): step r computes z from the
   // current Y, then Y -= z y_r and W -= z w_r. The pass of step r applies
   // step r-1's update and accumulates step r's sums in one sweep over Y.
@@ -582,10 +795,9 @@ __device__ __forceinline__ void sweep_body(const SweepParams& p, const int bin, 
   for (int k = 0; k < FT; ++k) pv[k] = czero<Real>();
   if (lane < RMAX) zs[warp * RMAX + lane] = czero<Real>();  // pass 0 applies a zero update
   __syncwarp();
-  double dprod = 1.0;  // prod_r (1 - z_r): det W' = det W prod_r (1 - z_r)
   // CHECK: det of the current W (log-magnitude, phase; warp 0), and the
   // running maxima of both errors (tid 0)
-  double c_lm = 0.0, c_ph = 0.0, c_det = 0.0, c_norm = 0.0;
+  double c_lm = 0.0, c_ph = 0.0;
   int c_ok = 0;
   R2* cscr = xs;  // the x tile is dead during the sweep
   auto check_det = [&](const R2* Wcur, double zr, bool compare) {
@@ -761,7 +973,6 @@ __device__ __forceinline__ void sweep_body(const SweepParams& p, const int bin, 
   // (estimator.cpp:607); here the last step's update is applied to the
   // running Y instead (same values up to rounding, one R x T pass instead of
   // an R x D x T product).
-  Real lastn = Real(0);  // CHECK: weighted power of the last updated row
   {
     const R2* zw = zs + warp * RMAX;
 #pragma unroll
@@ -786,8 +997,9 @@ __device__ __forceinline__ void sweep_body(const SweepParams& p, const int bin, 
       });
     }
   }
+  }
   __syncthreads();  // xs is dead: reuse the region for |y|^2 of register rows and E
-  const R2* Wf = Wb + (R & 1) * R * D;
+  const R2* Wf = IPR ? Wb : Wb + (R & 1) * R * D;
 
   // row powers (estimator.cpp:391-397) and |y|^2 export
   {
@@ -831,7 +1043,7 @@ __device__ __forceinline__ void sweep_body(const SweepParams& p, const int bin, 
       if (p.chk_flags & 1) chk_max(p.chk + (size_t)mix * 2, c_det);
     }
   }
-  if (tid == 0) p.logdet[tile] = logdet + log(dprod);
+  if (tid == 0) p.logdet[tile] = IPR ? ip_logdet : logdet + log(dprod);
   // delayed energies E_n(tau) = sum_{l<L_n, tau+l<T} |y_{row0+l}(tau+l)|^2
   Real* Eg = reinterpret_cast<Real*>(p.E);
   for (int n = 0; n < N; ++n) {

@@ -19,6 +19,7 @@ std::vector<SweepVariant> sweep_variants_gram_f64();
 std::vector<SweepVariant> sweep_variants_gram_ip();
 std::vector<SweepVariant> sweep_variants_check_f64();
 std::vector<SweepVariant> sweep_variants_fsplit_f32();
+std::vector<SweepVariant> sweep_variants_ip_frame();
 const std::vector<SweepVariant>& sweep_variants_f32() {
   static const std::vector<SweepVariant> v = [] {
     auto a = sweep_variants_rowwarp_f32();
@@ -37,6 +38,8 @@ const std::vector<SweepVariant>& sweep_variants_f32() {
     auto gr = sweep_variants_gram_f32();
     a.insert(a.end(), gr.begin(), gr.end());
     for (const auto& v : sweep_variants_gram_ip())
+      if (v.prec == 1) a.push_back(v);
+    for (const auto& v : sweep_variants_ip_frame())
       if (v.prec == 1) a.push_back(v);
     auto fs = sweep_variants_fsplit_f32();
     a.insert(a.end(), fs.begin(), fs.end());
@@ -62,6 +65,8 @@ const std::vector<SweepVariant>& sweep_variants_f64() {
     auto gr = sweep_variants_gram_f64();
     a.insert(a.end(), gr.begin(), gr.end());
     for (const auto& v : sweep_variants_gram_ip())
+      if (v.prec == 0) a.push_back(v);
+    for (const auto& v : sweep_variants_ip_frame())
       if (v.prec == 0) a.push_back(v);
     return a;
   }();

@@ -48,6 +48,14 @@ struct SweepVariant {
 #define CTF_VCHK3(REAL, PREC, RMAX, FT, RREG)                                           \
   CTF_VCHK(REAL, PREC, RMAX, FT, RREG, 128), CTF_VCHK(REAL, PREC, RMAX, FT, RREG, 256), \
       CTF_VCHK(REAL, PREC, RMAX, FT, RREG, 512)
+// IP rule on the frame-domain kernel (any layout, runtime R == D <= RMAX)
+#define CTF_VIP(REAL, PREC, RMAX, FT, RREG, NT)                                                                  \
+  SweepVariant {                                                                                              \
+    PREC, RMAX, FT, RREG, NT, 0, sweep_kernel<REAL, RMAX, FT, RREG, NT, false, 0, false, true>, 0, 0, nullptr, \
+        nullptr, 0, nullptr, 1                                                                                \
+  }
+#define CTF_VIP3(REAL, PREC, RMAX, FT, RREG) \
+  CTF_VIP(REAL, PREC, RMAX, FT, RREG, 128), CTF_VIP(REAL, PREC, RMAX, FT, RREG, 256), CTF_VIP(REAL, PREC, RMAX, FT, RREG, 512)
 // one (RMAX, FT, RREG) at the three CTA sizes
 #define CTF_V3(REAL, PREC, RMAX, FT, RREG, EX) \
   CTF_V(REAL, PREC, RMAX, FT, RREG, 128, EX), CTF_V(REAL, PREC, RMAX, FT, RREG, 256, EX), \

@@ -220,6 +220,9 @@ def test_run_api_prestacked_general_config():
     B0 = ref["B"][:F * 2].reshape(2, F).T
     assert rel(res.bases[0], B0) <= 1e-9
     assert len(res.trace.demix_ms) == 7 and all(t > 0 for t in res.trace.demix_ms)
+    # OptimizationTrace phases (estimator.cpp:623-653): every phase timed, rescale = the mu/apply kernel
+    assert len(res.trace.mu_ms) == 7 and all(t > 0 for t in res.trace.mu_ms)
+    assert len(res.trace.rescale_ms) == 7 and all(t > 0 for t in res.trace.rescale_ms)
 
 
 def test_check_options_hooks():
@@ -315,8 +318,8 @@ def test_errors_match_reference_semantics():
         run(cfg, np.zeros((4, 4, 10), complex))
     with pytest.raises(ConfigError):  # bad tap split
         run(CtfConfig(2, 4, [1, 2], [3, 3], iterations=2), g.standard_normal((4, 4, 10)) + 0j)
-    with pytest.raises(ConfigError):  # IP on a pre-stacked observation: outside the covariance kernel layout
-        run(CtfConfig(2, 4, [2, 2], [3, 3], iterations=2, update_rule="ip"), g.standard_normal((4, 4, 10)) + 0j)
+    with pytest.raises(ConfigError):  # IP needs a square demixing matrix (taps sum to the channels)
+        run(CtfConfig(2, 5, [2, 2], [3, 3], iterations=2, update_rule="ip"), g.standard_normal((4, 5, 10)) + 0j)
     x = g.standard_normal((2, 4, 10)) + 1j * g.standard_normal((2, 4, 10))
     x[1, 2, 3] = np.nan
     with pytest.raises(DegeneracyError) as e:
@@ -670,10 +673,37 @@ def test_ip_rule_fp32_tolerance_and_iss_vs_ip():
     assert abs(ip - iss) / abs(iss) < 0.05
 
 
+@pytest.mark.parametrize("precision,tol", [("f64", 1e-9), ("f32", 1e-4)])
+@pytest.mark.parametrize("taps,bases", [([2, 2], [3, 3]), ([2, 3], [2, 4]), ([1, 2, 1], [2, 3, 2])])
+def test_ip_rule_general_layouts_every_iteration(taps, bases, precision, tol):
+    """IP rule on layouts the covariance-domain kernel does not cover: a
+    pre-stacked observation (equal and unequal taps per source, the
+    reference's general CtfConfig), served by the frame-domain IP variant
+    (weighted covariance from the x tile, ip_solve_row, frame-sum refinement,
+    estimator.cpp:580-606, 89-273) against the oracle's IP run after every
+    iteration."""
+    g = np.random.default_rng(31 + len(taps) + sum(taps))
+    F, T, iters, seed = 11, 160, 6, 9
+    D = sum(taps)
+    xm = (g.standard_normal((F, T, D)) + 1j * g.standard_normal((F, T, D))).astype(np.complex128)
+    x = xm[None] if precision == "f64" else xm[None].astype(np.complex64)
+    s = Session(x, taps, bases, stack_taps=1, iterations=iters, precision=precision, seed=seed, update_rule="ip")
+    assert json.loads(s.describe())["sweep_kernel"].startswith("sweep_kernel"), s.describe()
+    ref = O.run(O.config(taps, bases, iterations=iters, seed=seed, threads=NPROC, rule="ip"), xm, history=True)
+    for it in range(iters):
+        s.iterate(1)
+        W, B, V, obj = s.download_raw()
+        e = max(rel(W[0], ref["hist_W"][it].reshape(F, -1)), rel(B[0], ref["hist_B"][it]),
+                rel(V[0], ref["hist_V"][it]))
+        eo = abs(obj[0, it] - ref["objective"][it]) / abs(ref["objective"][it])
+        assert e <= tol and eo <= tol, f"taps={taps} {precision} it={it + 1}: {e:.2e} obj {eo:.2e}"
+    s.close()
+
+
 def test_ip_rule_errors_and_run_api():
     """run(config with update_rule='ip') on a stacked observation; the IP rule
-    with CheckOptions or on a pre-stacked layout is refused with ConfigError /
-    unsupported, never silently run on another path."""
+    with CheckOptions is refused (unsupported), never silently run on another
+    path."""
     M, L, T, K, F = 2, 2, 120, 3, 9
     raw = synth_mixtures(1, F, T, M, M, L, K, 0.6, 5)
     cfg = CtfConfig(M, M * L, [L] * M, [K] * M, iterations=3, update_rule="ip", seed=2)
