@@ -661,7 +661,7 @@ void plan_sweep(ctf_ctx* c) {
                    "R <= 16 and T <= 2048 frames (frame-domain IP variants), or a compiled covariance-domain "
                    "(mics, taps) pair");
   if (!found && want_chk)
-    throw CtfError(CTF_ERR_UNSUPPORTED, "CheckOptions need a resident tile (R <= 16, T <= 2048)");
+    throw CtfError(CTF_ERR_UNSUPPORTED, "CheckOptions need R <= 64 and T <= 4096 (instrumented frame-domain and streamed kernels)");
   if (!found)
     throw CtfError(CTF_ERR_UNSUPPORTED, "no compiled sweep kernel for R=" + std::to_string(c->R) +
                                             " T=" + std::to_string(c->T));
@@ -1383,7 +1383,8 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host,
       c->mix_split[(size_t)k] = m;
     }
   }
-  if (c->sv.kind == 2) c->scratch.alloc((size_t)c->stream_grid * c->R * c->TP * cs);
+  if (c->sv.kind == 2)  // per-CTA tile slots (+ the CheckOptions LU scratch)
+    c->scratch.alloc((size_t)c->stream_grid * ((size_t)c->R * c->TP + (c->sv.chk ? (size_t)c->R * c->D : 0)) * cs);
   else c->scratch.free();
   if (c->sv.kind == 3) {
     const size_t tiles = (size_t)c->B * c->FL;

@@ -24,7 +24,12 @@ struct StreamParams {
   int ngroups;         // ceil(R / RG)
 };
 
-template <typename Real, int FT, int RG, int NT, int MINB = 1>
+// CHECK: CheckOptions instrumentation for any R <= 64 (estimator.cpp:556-577):
+// log|det W| recomputed by a warp LU after every step and compared with the
+// determinant lemma det W' = det W (1 - z_r), and the updated pivot row's
+// weighted power sum_j |y_r'(j)|^2 / lambda / T compared with 1; per-mixture
+// maxima in p.chk (the LU works on a copy of W after the CTA's tile slot).
+template <typename Real, int FT, int RG, int NT, int MINB = 1, bool CHECK = false>
 __global__ void __launch_bounds__(NT, MINB) stream_kernel(const StreamParams sp) {
   using R2 = typename Cplx<Real>::T;
   constexpr int NW = NT / 32;
@@ -43,7 +48,8 @@ __global__ void __launch_bounds__(NT, MINB) stream_kernel(const StreamParams sp)
   R2* xst = reinterpret_cast<R2*>(smem + p.off_x);        // one microphone: xoff + TP (demix stage)
   __shared__ int s_bad, s_badrow;
   __shared__ double s_logmu;
-  R2* Yg = reinterpret_cast<R2*>(sp.scratch) + (size_t)blockIdx.x * R * TP;
+  // per-CTA slot: the R x TP tile (+ CHECK: R x D LU scratch)
+  R2* Yg = reinterpret_cast<R2*>(sp.scratch) + (size_t)blockIdx.x * ((size_t)R * TP + (CHECK ? (size_t)R * D : 0));
 
   for (int work = blockIdx.x; work < sp.nwork; work += gridDim.x) {
     const int mix = work / p.FL, bin = work - mix * p.FL;
@@ -188,6 +194,25 @@ __global__ void __launch_bounds__(NT, MINB) stream_kernel(const StreamParams sp)
     double* onemz = dred + NW * 4;
     __syncthreads();
     bool aborted = false;
+    // CHECK: det of the current W (warp 0: log-magnitude, phase) and maxima (tid 0)
+    double c_lm = 0.0, c_ph = 0.0, c_det = 0.0, c_norm = 0.0;
+    int c_ok = 0;
+    R2* cscr = Yg + (size_t)R * TP;  // (global, L2-resident: check mode only)
+    auto check_det = [&](const R2* Wcur, double zr, bool compare) {
+      if (warp == 0) {
+        for (int i = lane; i < R * D; i += 32) cscr[i] = Wcur[i];
+        __syncwarp();
+        double lm, ph;
+        const int st = warp_logdet<Real>(cscr, R, lane, lm, &ph);
+        if (compare && c_ok && st != 4) c_det = fmax(c_det, det_lemma_error(c_lm, c_ph, lm, ph, zr));
+        c_ok = st != 4;
+        c_lm = lm;
+        c_ph = ph;
+      }
+    };
+    if constexpr (CHECK) {
+      if (p.chk_flags & 1) check_det(Wb, 0.0, false);
+    }
     for (int r = 0; r < R; ++r) {
       R2 yr[FT];
       Real ar2[FT];
@@ -288,6 +313,35 @@ __global__ void __launch_bounds__(NT, MINB) stream_kernel(const StreamParams sp)
         R2 w = Wo[e];
         cmsub(w, zsh[q], Wo[c * R + r]);
         Wn[e] = w;
+      }
+      if constexpr (CHECK) {
+        if (p.chk_flags & 2) {  // steering_row_power of the updated row r (estimator.cpp:571-576)
+          const R2 zr2 = zsh[r];
+          const int wo = p.woff[r];
+          Real q = Real(0);
+#pragma unroll
+          for (int k = 0; k < FT; ++k) {
+            const int j = tid + k * NT;
+            R2 y = yr[k];
+            cmsub(y, zr2, yr[k]);
+            if (j < T) q = fma(cnorm(y), invl[wo + j], q);
+          }
+          double v1[1] = {(double)q};
+          block_sum_d<1>(v1, dred, lane, warp, NW);
+          if (tid == 0) c_norm = fmax(c_norm, fabs(v1[0] / T - 1.0));
+        }
+        if (p.chk_flags & 1) {
+          __syncthreads();  // W' complete
+          check_det(Wn, (double)zsh[r].x, true);
+        }
+      }
+    }
+    if constexpr (CHECK) {
+      if (!aborted) {
+        if (tid == 0) {
+          if (p.chk_flags & 2) chk_max(p.chk + (size_t)mix * 2 + 1, c_norm);
+          if (p.chk_flags & 1) chk_max(p.chk + (size_t)mix * 2, c_det);
+        }
       }
     }
     if (aborted) continue;

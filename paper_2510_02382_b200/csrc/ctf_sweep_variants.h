@@ -63,6 +63,9 @@ struct SweepVariant {
 // stream_kernel: any R <= 64 in groups of RG rows, FT frames per thread
 #define CTF_ST(REAL, PREC, FT, RG, NT, MINB) \
   SweepVariant { PREC, 64, FT, RG, NT, 0, nullptr, 2, 0, stream_kernel<REAL, FT, RG, NT, MINB> }
+// stream_kernel with the CheckOptions instrumentation (any R <= 64)
+#define CTF_STC(REAL, PREC, FT, RG, NT) \
+  SweepVariant { PREC, 64, FT, RG, NT, 0, nullptr, 2, 0, stream_kernel<REAL, FT, RG, NT, 1, true>, nullptr, 1 }
 // cluster_kernel: R = CS * RB rows over a cluster of CS CTAs
 #define CTF_CL(REAL, PREC, RB, FT, RREG, NT) \
   SweepVariant { PREC, RB, FT, RREG, NT, 0, nullptr, 3, 0, nullptr, cluster_kernel<REAL, RB, FT, RREG, NT> }

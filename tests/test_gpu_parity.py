@@ -251,6 +251,32 @@ def test_check_options_hooks():
     assert r32.trace.max_det_lemma_error < 1e-3 and r32.trace.max_normalization_error < 1e-3
 
 
+@pytest.mark.parametrize("M,L,T,K,F,iters", [(4, 8, 1000, 20, 3, 3), (6, 10, 600, 16, 2, 2), (3, 6, 300, 4, 3, 4)])
+def test_check_options_wide_tiles(M, L, T, K, F, iters):
+    """CheckOptions for R > 16 (BASELINE cfg3 R = 32, cfg4 R = 60, and R = 18):
+    the instrumented streamed kernel recomputes det W by a warp LU after every
+    step and the updated row's weighted power (estimator.cpp:556-577) ->
+    checked_updates = iterations * F * R, the det-lemma and normalization
+    errors at the oracle's order, and the same state as the plain run (fp64)."""
+    R = M * L
+    raw = synth_mixtures(1, F, T, M, M, L, K, 0.7, 23)
+    s = Session(raw, [L] * M, [K] * M, stack_taps=L, iterations=iters, precision="f64", seed=3, checks=3)
+    assert "stream_kernel" in s.describe(), s.describe()
+    s.iterate(iters)
+    det, nrm, cnt = s.check_stats()
+    W = s.download_raw()[0]
+    s.close()
+    assert int(cnt[0]) == iters * F * R
+    odet, onrm, ocnt = O.run_checked(O.config([L] * M, [K] * M, iterations=iters, seed=3, threads=NPROC),
+                                     O.stack_observation(raw[0], L))
+    assert ocnt == iters * F * R
+    assert 0.0 <= det[0] < 1e-9 and 0.0 < nrm[0] < 1e-8, (det[0], nrm[0], odet, onrm)
+    plain = Session(raw, [L] * M, [K] * M, stack_taps=L, iterations=iters, precision="f64", seed=3)
+    plain.iterate(iters)
+    assert rel(W, plain.download_raw()[0]) <= 1e-10
+    plain.close()
+
+
 def test_check_options_sharded_max_over_ranks():
     """With frequency shards the check maxima are reduced over ranks (host group)."""
     import threading
