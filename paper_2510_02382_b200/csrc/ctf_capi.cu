@@ -488,7 +488,13 @@ void plan_sweep(ctf_ctx* c) {
       cand.off_y = (int)take((size_t)c->N * (M * (M + 1) / 2) * NA * NA * cs);  // Hermitian half of the Gram
       const int NS = (c->real_size == 4 && c->R <= 16) ? c->N : 1;  // sources per Gram pass (gram_ns) and demix group
       // (dev builds with -DCTF_GRAM_NS64 must size this from gram_ns as well)
-      size_t ebytes = std::max((size_t)NS * NA * (nt + 1) * cs, (size_t)NS * L * TP * rs);
+      // partials of NSP sources at a time; |y|^2 rows of a source group, or
+      // (ctf::gram_ereg: fp32 long-frame variants) only the energy halo
+      const bool ereg = c->real_size == 4 && v.ft >= 8;
+      const int NSP = ereg ? 1 : NS;
+      const size_t LH = std::max(1, L - 1);  // halo [warp][frame pass][source][l-1][lane]
+      size_t ebytes = std::max((size_t)NSP * NA * (nt + 1) * cs,
+                               ereg ? (size_t)NW * v.ft * NS * LH * LH * rs : (size_t)NS * L * TP * rs);
       if (v.tc) {  // two stages of the tcgen05 Gram operands (ctf_gram.cuh GramTC)
         const int NG = M * L + (M * (M - 1) / 2) * NA, TILES = (NG + 127) / 128, NP = (M * NA + 15) / 16 * 16;
         ebytes = std::max(ebytes, (size_t)2 * (2 * 2 * (2 * TILES * 128 * 32) + 2 * 2 * NP * 32));

@@ -164,8 +164,14 @@ template <typename Real, int N, int R> constexpr int gram_nsg() {
 #ifndef CTF_GRAM_MINB64
 #define CTF_GRAM_MINB64 2
 #endif
-template <typename Real, int NT, int R> constexpr int gram_min_blocks() {
-  return R > 16 ? 1 : std::is_same<Real, float>::value ? (NT <= 256 ? 3 : 1) : (NT <= 256 ? CTF_GRAM_MINB64 : NT <= 384 ? 2 : 1);
+// fp32 long-frame variants (FT >= 8, BASELINE cfg2 T = 2000) at 256 threads:
+// two CTAs per SM (EREG energies + one-source partial buffer keep them under
+// half the shared memory)
+template <typename Real> constexpr bool gram_ereg(int FT) { return std::is_same<Real, float>::value && FT >= 8; }
+template <typename Real, int NT, int R, int FT = 4> constexpr int gram_min_blocks() {
+  return R > 16 ? 1
+         : std::is_same<Real, float>::value ? (NT <= 256 ? (FT >= 8 ? 2 : 3) : 1)
+                                            : (NT <= 256 ? CTF_GRAM_MINB64 : NT <= 384 ? 2 : 1);
 }
 
 // Tensor-core Gram (TC = true, fp32): the lag correlations as one real GEMM
@@ -197,18 +203,19 @@ template <int M, int L> struct GramTC {
 
 // IP: the iterative-projection rule in place of the ISS steps.
 template <typename Real, int M, int L, int NT, int FT, bool IP = false, bool TC = false>
-__global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
+__global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L, FT>())
     gram_kernel(const SweepParams p, const int4* __restrict__ gtab) {
   using R2 = typename Cplx<Real>::T;
   using Ops = GOps<Real>;
   constexpr bool F32 = std::is_same<Real, float>::value;
   constexpr int N = M, R = M * L, D = M * L, NA = 2 * L - 1, NW = NT / 32;
   constexpr int NS = gram_ns<Real, N, R>();
+  constexpr bool EREG = gram_ereg<Real>(FT);  // E_n in registers (no |y|^2 rows in shared memory)
   constexpr int LT1 = L > 1 ? L - 1 : 1;
   constexpr int CPB = 16 / (int)sizeof(R2);  // complex values per 16-byte load
   // V columns of the lambda phase loaded at once (fp32, one CTA per SM)
   constexpr int LAMV = !F32                                         ? 0
-                       : gram_min_blocks<Real, NT, M * L>() == 1 ? CTF_LAMV
+                       : gram_min_blocks<Real, NT, M * L, FT>() == 1 ? CTF_LAMV
                        : (M == 2 && L == 5)                       ? CTF_LAMV3  // measured (cfg1); others spill
                                                                   : 0;
   static_assert(D <= 32, "one lane per stacked channel in the covariance steps");
@@ -222,7 +229,7 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
   Real* invl = reinterpret_cast<Real*>(smem + p.off_l);  // N rows of lp: w_n(s) at [n*lp + loff + s]
   R2* G = reinterpret_cast<R2*>(smem + p.off_y);       // [n][m][m'][a][b]
   R2* part = reinterpret_cast<R2*>(smem + p.off_e);    // [n*NA + j][NT + 1] Gram partials (NS sources)
-  Real* Pq = reinterpret_cast<Real*>(smem + p.off_e);  // [l][TP] |y|^2 of one source; row 0 then E_n
+  Real* Pq = reinterpret_cast<Real*>(smem + p.off_e);  // [l][TP] |y|^2 of one source; row 0 then E_n (!EREG)
   R2* Wb = reinterpret_cast<R2*>(smem + p.off_w);      // R x D (column-major)
   R2* Yt = reinterpret_cast<R2*>(smem + p.off_z);      // R x LT1 tail frames
   R2* zs = Yt + 2 * R * LT1;                           // 2 x (D + LT1) pivot buffers
@@ -684,7 +691,7 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
     const R2* x2 = xs + g0.y * p.xp + p.xoff + g0.z;
     const int ng = gtab[NT].x;
     constexpr int NSG = gram_nsg<Real, N, R>();  // sources per pass over the frames
-    constexpr int NSP = NS;                      // sources whose partials fit the buffer at once
+    constexpr int NSP = EREG ? 1 : NS;           // sources whose partials fit the buffer at once
     static_assert(NSG % NSP == 0, "partial groups");
     R2 keep[NSG > NSP ? NSG - NSP : 1][NA];  // partials of the later source groups, in registers
     for (int n0 = 0; n0 < N; n0 += NSG) {
@@ -1112,6 +1119,90 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
 #define CTF_GRAM_FB64 2
 #endif
     constexpr int FB = F32 ? 1 : CTF_GRAM_FB64;
+    Real ereg[NSD][EREG ? FT : 1];  // EREG: E_n of this thread's frames
+    if constexpr (EREG) {
+    // E_n(tau) in registers: the row-(n,l) term |y|^2 at tau + l comes from
+    // lane + l of the same warp by a shuffle, or, past the warp's last lane,
+    // from the next warp's first L-1 lanes (frame k) / warp 0's (frame k+1)
+    // through a small halo buffer; terms are added in l order as before.
+    constexpr int LH = L > 1 ? L - 1 : 1;
+    Real* halo = reinterpret_cast<Real*>(smem + p.off_e);  // [warp][k][source][l-1][lane < L-1]
+    auto hidx = [&](int w, int kk, int s, int l, int ln) { return (((w * FT + kk) * NSD + s) * LH + (l - 1)) * LH + ln; };
+#pragma unroll
+    for (int k = 0; k < FT; k += FB) {
+      asm volatile("" ::: "memory");  // one frame pass at a time (registers)
+      R2 acc[FB][GR];
+#pragma unroll
+      for (int f = 0; f < FB; ++f)
+#pragma unroll
+        for (int i = 0; i < GR; ++i) acc[f][i].x = acc[f][i].y = Real(0);
+#pragma unroll
+      for (int m = 0; m < M; ++m)
+#pragma unroll
+        for (int l1 = 0; l1 < L; ++l1) {
+          R2 xv[FB];
+#pragma unroll
+          for (int f = 0; f < FB; ++f) xv[f] = xs[m * p.xp + p.xoff + tid + (k + f) * NT - l1];
+          const R2* wc = Wf + (m * L + l1) * R + g0 * L;
+          if constexpr (F32 && GR % 2 == 0) {  // W pairs with 16-byte loads
+            const float4* w4 = reinterpret_cast<const float4*>(wc);
+#pragma unroll
+            for (int i = 0; i < GR; i += 2) {
+              const float4 w = w4[i / 2];
+#pragma unroll
+              for (int f = 0; f < FB; ++f) {
+                acc[f][i] = Ops::mac(make_float2(w.x, w.y), xv[f], acc[f][i]);
+                acc[f][i + 1] = Ops::mac(make_float2(w.z, w.w), xv[f], acc[f][i + 1]);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < GR; ++i)
+#pragma unroll
+              for (int f = 0; f < FB; ++f) acc[f][i] = Ops::mac(wc[i], xv[f], acc[f][i]);
+          }
+        }
+#pragma unroll
+      for (int f = 0; f < FB; ++f) {
+        const int j = tid + (k + f) * NT;
+        Real q[GR];
+#pragma unroll
+        for (int i = 0; i < GR; ++i) {
+          q[i] = (j < T) ? cnorm(acc[f][i]) : Real(0);
+          rp[g0 * L + i] += q[i];
+        }
+#pragma unroll
+        for (int s = 0; s < NSD; ++s) {
+          Real e = q[s * L];
+#pragma unroll
+          for (int l = 1; l < L; ++l) {
+            const Real v = __shfl_down_sync(kFull, q[s * L + l], l);
+            if (lane + l < 32) e += v;
+            if (lane < L - 1) halo[hidx(warp, k + f, s, l, lane)] = q[s * L + l];
+          }
+          ereg[s][k + f] = e;
+        }
+      }
+    }
+    __syncthreads();  // halo complete
+    CTF_PHASE(7);
+#pragma unroll
+    for (int s = 0; s < NSD; ++s)
+#pragma unroll
+      for (int k = 0; k < FT; ++k) {
+        const int tau = tid + k * NT;
+#pragma unroll
+        for (int l = 1; l < L; ++l)
+          if (lane + l >= 32) {  // frame tau + l belongs to the next warp (or warp 0 at frame k + 1)
+            const int t2 = tid + l;
+            Real v = Real(0);
+            if (t2 < NT) v = halo[hidx(t2 >> 5, k, s, l, t2 & 31)];
+            else if (k + 1 < FT) v = halo[hidx(0, k + 1, s, l, t2 - NT)];
+            ereg[s][k] += v;
+          }
+        if (tau < T) Eg[(((size_t)mix * N + g0 + s) * p.FL + bin) * T + tau] = ereg[s][k];
+      }
+    } else {
 #pragma unroll 1
     for (int k = 0; k < FT; k += FB) {
       R2 acc[FB][GR];
@@ -1172,6 +1263,7 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
         if (tau < T) Eg[(((size_t)mix * N + n) * p.FL + bin) * T + tau] = e;
       }
     }
+    }
     __syncthreads();  // red is shared by the MU-B passes below
 #pragma unroll
     for (int n = g0; n < g0 + NSD; ++n) {
@@ -1194,7 +1286,7 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
           for (int k = 0; k < FT; ++k) {
             const int tau = tid + k * NT;
             const Real ilv = il[tau];
-            const Real an = En[tau] * (ilv * ilv);
+            const Real an = (EREG ? ereg[n - g0][EREG ? k : 0] : En[tau]) * (ilv * ilv);
             const Real bn = (tau < T) ? ilv * (Real)min(L, T - tau) : Real(0);
 #pragma unroll
             for (int q = 0; q < KW; ++q) {
@@ -1229,7 +1321,7 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L>())
       else
         mub(std::integral_constant<int, 16>{});
     }
-    __syncthreads();  // Pq is rewritten by the next group
+    __syncthreads();  // Pq / the halo is rewritten by the next group
   }
   CTF_PHASE(8);
   // check_all_finite (estimator.cpp:494-499): W' first (code 1), then Y

@@ -14,6 +14,7 @@ std::vector<SweepVariant> sweep_variants_gram_f32() {
 #else
   return {GF(2, 2, 128, 4), GF(2, 2, 256, 4), GF(2, 3, 128, 4), GF(2, 3, 256, 4),
           GF(2, 5, 256, 4), GF(2, 5, 512, 4), GF(3, 4, 256, 4), GF(3, 4, 512, 4),
+          GF(3, 4, 256, 8),  // cfg2 (T = 2000) at two CTAs per SM
           GF(4, 8, 256, 4), GF(4, 8, 512, 2),  // wide tiles (BASELINE cfg3): warp per row, Gram table reads
           CTF_GRT(float, 1, 4, 8, 512, 2)};     // the same with the tcgen05 Gram
 #endif
