@@ -948,18 +948,26 @@ void launch_muv(ctf_ctx* c, int m0, int m1, cudaStream_t st) {
   mp.chunk_bins = c->chunk_bins;
   for (int n = 0; n <= c->N; ++n) mp.koff[n] = c->koff[n];
   for (int n = 0; n < c->N; ++n) mp.ntaps[n] = c->taps[n];
-  dim3 grid((c->T + 127) / 128, (m1 - m0) * c->N, c->nchunk);
+  // KS = 2 (bases split over half-warps) for K >= 16: half the registers,
+  // twice the resident warps (CTF_MUV_KS=1|2 pins it for measurement)
+  int ks = 1;
+  if (const char* e = std::getenv("CTF_MUV_KS")) ks = std::atoi(e) == 2 && c->kmax % 2 == 0 ? 2 : 1;
+  dim3 grid(ks == 2 ? (c->T + 63) / 64 : (c->T + 127) / 128, (m1 - m0) * c->N, c->nchunk);
   const size_t smem = (size_t)((c->chunk_bins + 7) / 8 * 8) * c->kmax * sizeof(Real);
+#define CTF_MUV(KM)                                                                  \
+  (ks == 2 ? ctf::muv_partial_kernel<Real, KM, 2><<<grid, 128, smem, st>>>(mp)     \
+           : ctf::muv_partial_kernel<Real, KM, 1><<<grid, 128, smem, st>>>(mp))
   switch (c->kmax) {
-    case 4: ctf::muv_partial_kernel<Real, 4><<<grid, 128, smem, st>>>(mp); break;
-    case 10: ctf::muv_partial_kernel<Real, 10><<<grid, 128, smem, st>>>(mp); break;
-    case 12: ctf::muv_partial_kernel<Real, 12><<<grid, 128, smem, st>>>(mp); break;
-    case 20: ctf::muv_partial_kernel<Real, 20><<<grid, 128, smem, st>>>(mp); break;
-    case 8: ctf::muv_partial_kernel<Real, 8><<<grid, 128, smem, st>>>(mp); break;
-    case 16: ctf::muv_partial_kernel<Real, 16><<<grid, 128, smem, st>>>(mp); break;
-    case 24: ctf::muv_partial_kernel<Real, 24><<<grid, 128, smem, st>>>(mp); break;
-    default: ctf::muv_partial_kernel<Real, 32><<<grid, 128, smem, st>>>(mp); break;
+    case 4: CTF_MUV(4); break;
+    case 10: CTF_MUV(10); break;
+    case 12: CTF_MUV(12); break;
+    case 20: CTF_MUV(20); break;
+    case 8: CTF_MUV(8); break;
+    case 16: CTF_MUV(16); break;
+    case 24: CTF_MUV(24); break;
+    default: CTF_MUV(32); break;
   }
+#undef CTF_MUV
   CK(cudaGetLastError());
 }
 

@@ -131,6 +131,14 @@ template <typename V> __device__ __forceinline__ void cmsub(V& acc, V a, V b) { 
 // its slow-path sequence (fp32: MUFU + Newton fixup); fp64 divides
 __device__ __forceinline__ float rcp_rn(float x) { return __frcp_rn(x); }
 __device__ __forceinline__ double rcp_rn(double x) { return 1.0 / x; }
+// 1/x for the MU-V weights: fp32 MUFU approximation + one Newton step (within
+// ~1 ulp of rcp_rn, 3 instructions instead of its fixup sequence); fp64 exact.
+__device__ __forceinline__ float rcp_fast(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return fmaf(r, fmaf(-x, r, 1.f), r);
+}
+__device__ __forceinline__ double rcp_fast(double x) { return 1.0 / x; }
 template <typename V> __device__ __forceinline__ auto cnorm(V a) -> decltype(a.x) { return fma(a.x, a.x, a.y * a.y); }
 template <typename V> __device__ __forceinline__ bool cfinite(V a) { return isfinite(a.x) && isfinite(a.y); }
 template <typename Real> __device__ __forceinline__ typename Cplx<Real>::T czero() {
@@ -1154,16 +1162,23 @@ struct MuvParams {
 // Bins are processed in groups of 8 with no per-bin guards (the B chunk is
 // zero-padded to whole groups; a padded bin has b = 0 and E = 0, so it adds
 // exactly 0), which lets the lambda' FMA chains of different bins overlap;
-// fp32 computes lambda' for two bins per FFMA2.
-template <typename Real, int KMAX>
+// fp32 computes lambda' for two bins per FFMA2. KS = 2 splits a frame's K
+// bases over the two half-warps (lanes l and l ^ 16 share the frame): each
+// forms lambda' over its half and the halves are exchanged by one shuffle
+// (the sum is the same on both lanes), halving the v / num / den registers.
+template <typename Real, int KMAX, int KS = 1>
 __global__ void __launch_bounds__(128) muv_partial_kernel(const MuvParams p) {
   constexpr int G = 8;
-  const int tau = blockIdx.x * blockDim.x + threadIdx.x;
+  constexpr int KPT = KMAX / KS;  // bases per thread
+  static_assert(KS == 1 || (KS == 2 && KMAX % 2 == 0), "k split");
+  const int lane = threadIdx.x & 31, half = KS == 2 ? lane >> 4 : 0;
+  const int tau = KS == 2 ? blockIdx.x * 64 + (threadIdx.x >> 5) * 16 + (lane & 15) : blockIdx.x * blockDim.x + threadIdx.x;
   const int mix = blockIdx.y / p.N + p.mix0, n = blockIdx.y % p.N;
   const int chunk = blockIdx.z;
   const int i0 = chunk * p.chunk_bins, i1 = min(p.FL, i0 + p.chunk_bins);
   const int nb = i1 - i0, nbp = (nb + G - 1) / G * G;
   const int k0 = p.koff[n], K = p.koff[n + 1] - k0;
+  const int kb0 = half * KPT;  // this thread's first base (within the source)
   extern __shared__ __align__(16) unsigned char smem[];
   Real* Bsh = reinterpret_cast<Real*>(smem);  // [k][bin] (bins padded to nbp)
   const Real* Bg = reinterpret_cast<const Real*>(p.Bf) + (size_t)mix * p.FL * p.SK;
@@ -1172,24 +1187,27 @@ __global__ void __launch_bounds__(128) muv_partial_kernel(const MuvParams p) {
     Bsh[e] = (k < K && i < nb) ? Bg[(size_t)(i0 + i) * p.SK + k0 + k] : Real(0);
   }
   __syncthreads();
-  if (tau >= p.T) return;
+  const bool valid = tau < p.T;
+  if (KS == 1 && !valid) return;
+  const int tc = valid ? tau : 0;  // (KS = 2: lanes past T join the shuffles with zero data)
   const Real floor_abs = (Real)p.floor_abs[mix];
-  const Real cnt = (Real)min(p.ntaps[n], p.T - tau);
-  const Real* Vg = reinterpret_cast<const Real*>(p.V) + ((size_t)mix * p.SK + k0) * p.T + tau;
-  Real v[KMAX], num[KMAX], den[KMAX];
+  const Real cnt = (Real)min(p.ntaps[n], p.T - tc);
+  const Real* Vg = reinterpret_cast<const Real*>(p.V) + ((size_t)mix * p.SK + k0 + kb0) * p.T + tc;
+  Real v[KPT], num[KPT], den[KPT];
 #pragma unroll
-  for (int k = 0; k < KMAX; ++k) {
-    v[k] = (k < K) ? Vg[(size_t)k * p.T] : Real(0);
+  for (int k = 0; k < KPT; ++k) {
+    v[k] = (valid && kb0 + k < K) ? Vg[(size_t)k * p.T] : Real(0);
     num[k] = Real(0);
     den[k] = Real(0);
   }
-  const Real* Eg = reinterpret_cast<const Real*>(p.E) + (((size_t)mix * p.N + n) * p.FL) * p.T + tau;
+  const Real* Eg = reinterpret_cast<const Real*>(p.E) + (((size_t)mix * p.N + n) * p.FL) * p.T + tc;
+  const Real* Bk = Bsh + kb0 * nbp;
   Real ecur[G], enext[G];
 #pragma unroll
-  for (int u = 0; u < G; ++u) ecur[u] = (u < nb) ? Eg[(size_t)(i0 + u) * p.T] : Real(0);
+  for (int u = 0; u < G; ++u) ecur[u] = (valid && u < nb) ? Eg[(size_t)(i0 + u) * p.T] : Real(0);
   for (int g = 0; g < nbp; g += G) {
 #pragma unroll
-    for (int u = 0; u < G; ++u) enext[u] = (g + G + u < nb) ? Eg[(size_t)(i0 + g + G + u) * p.T] : Real(0);
+    for (int u = 0; u < G; ++u) enext[u] = (valid && g + G + u < nb) ? Eg[(size_t)(i0 + g + G + u) * p.T] : Real(0);
 #pragma unroll
     for (int u = 0; u < G; u += 2) {
       // keep the B reads of one bin pair from being hoisted across the group
@@ -1200,23 +1218,27 @@ __global__ void __launch_bounds__(128) muv_partial_kernel(const MuvParams p) {
       if constexpr (std::is_same<Real, float>::value) {
         float2 l2 = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int k = 0; k < KMAX; ++k) l2 = ffma2s(*reinterpret_cast<const float2*>(Bsh + k * nbp + i), v[k], l2);
+        for (int k = 0; k < KPT; ++k) l2 = ffma2s(*reinterpret_cast<const float2*>(Bk + k * nbp + i), v[k], l2);
         la = l2.x;
         lb = l2.y;
       } else {
         la = lb = Real(0);
 #pragma unroll
-        for (int k = 0; k < KMAX; ++k) {
-          la = fma(Bsh[k * nbp + i], v[k], la);
-          lb = fma(Bsh[k * nbp + i + 1], v[k], lb);
+        for (int k = 0; k < KPT; ++k) {
+          la = fma(Bk[k * nbp + i], v[k], la);
+          lb = fma(Bk[k * nbp + i + 1], v[k], lb);
         }
       }
-      const Real ila = rcp_rn(fmax(la, floor_abs)), ilb = rcp_rn(fmax(lb, floor_abs));
+      if constexpr (KS == 2) {
+        la += __shfl_xor_sync(kFull, la, 16);
+        lb += __shfl_xor_sync(kFull, lb, 16);
+      }
+      const Real ila = rcp_fast(fmax(la, floor_abs)), ilb = rcp_fast(fmax(lb, floor_abs));
       const Real ana = ecur[u] * (ila * ila), bna = ila * cnt;
       const Real anb = ecur[u + 1] * (ilb * ilb), bnb = ilb * cnt;
 #pragma unroll
-      for (int k = 0; k < KMAX; ++k) {
-        const Real ba = Bsh[k * nbp + i], bb = Bsh[k * nbp + i + 1];
+      for (int k = 0; k < KPT; ++k) {
+        const Real ba = Bk[k * nbp + i], bb = Bk[k * nbp + i + 1];
         if constexpr (std::is_same<Real, float>::value) {
           float2 t = ffma2s(make_float2(ana, bna), ba, make_float2(num[k], den[k]));
           t = ffma2s(make_float2(anb, bnb), bb, t);
@@ -1233,10 +1255,11 @@ __global__ void __launch_bounds__(128) muv_partial_kernel(const MuvParams p) {
 #pragma unroll
     for (int u = 0; u < G; ++u) ecur[u] = enext[u];
   }
-  Real* out = reinterpret_cast<Real*>(p.part) + (((size_t)chunk * p.nmix + mix) * 2 * p.SK + k0) * p.T + tau;
+  if (!valid) return;
+  Real* out = reinterpret_cast<Real*>(p.part) + (((size_t)chunk * p.nmix + mix) * 2 * p.SK + k0 + kb0) * p.T + tau;
 #pragma unroll
-  for (int k = 0; k < KMAX; ++k)
-    if (k < K) {
+  for (int k = 0; k < KPT; ++k)
+    if (kb0 + k < K) {
       out[(size_t)k * p.T] = num[k];
       out[(size_t)(p.SK + k) * p.T] = den[k];
     }
