@@ -1080,7 +1080,7 @@ void launch_sweep(ctf_ctx* c, bool do_sweep, int m0, int m1, int k, cudaStream_t
     c->sv.sfn<<<c->stream_grid, c->NT, c->sweep_smem, st>>>(stp);
   } else if (c->sv.kind == 4) {
     if (c->has_fb) {
-      CK(cudaMemsetAsync(c->fb_count.p, 0, sizeof(int), st));
+      CK(cudaMemsetAsync(c->fb_count.p + k, 0, sizeof(int), st));  // chunk k's list
       sp.fb_mode = 1;
     }
     c->sv.gfn<<<dim3(c->FL, nm), c->NT, c->sweep_smem, st>>>(sp, c->gtab.p);

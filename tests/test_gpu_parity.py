@@ -490,16 +490,21 @@ def test_frequency_sharded_contexts_match_single_context(precision, tol):
         assert sorted(covered)[0][0] == 0 and sorted(covered)[-1][1] == F
 
 
-@pytest.mark.parametrize("precision,tol,chunks,use_async", [("f64", 1e-12, "1", False), ("f32", 1e-5, "1", False),
-                                                          ("f64", 1e-12, "2", False), ("f64", 1e-12, "3", True),
-                                                          ("f32", 1e-5, "2", True)])
-def test_nccl_single_rank_communicator(monkeypatch, precision, tol, chunks, use_async):
+@pytest.mark.parametrize("precision,tol,chunks,use_async,theta", [
+    ("f64", 1e-12, "1", False, None), ("f32", 1e-5, "1", False, None), ("f64", 1e-12, "2", False, None),
+    ("f64", 1e-12, "3", True, None), ("f32", 1e-5, "2", True, None),
+    ("f64", 1e-12, "3", True, "0"), ("f32", 1e-5, "2", False, "0")])
+def test_nccl_single_rank_communicator(monkeypatch, precision, tol, chunks, use_async, theta):
     """The NCCL exchange itself on one GPU: a single-rank communicator
     (CTF_NCCL_SINGLE_RANK=1) drives the reduce -> ncclAllReduce -> apply path
     (packed MU-V sums, row powers, objective, mean power, error words) and must
-    reproduce the plain world = 1 run."""
+    reproduce the plain world = 1 run. theta "0": every bin takes the
+    conditioning fallback from iteration 2 on, each mixture chunk with its own
+    fallback list."""
     from paper_2510_02382_b200 import _lib
     import ctypes
+    if theta is not None:
+        monkeypatch.setenv("CTF_GRAM_FALLBACK_THETA", theta)
     B, F, T, M, L, K, iters, seed = 3, 37, 300, 2, 3, 4, 4, 6
     raw = synth_mixtures(B, F, T, M, M, L, K, 0.6, 31)
     if precision == "f32":
