@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(const ClusterParams cp) 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int CS = cp.CS;
   const int c = (int)cluster_ctarank();
-  const int bin = blockIdx.x / CS, mix = blockIdx.y + p.mix0;
+  const int bin = blockIdx.x / CS, mix = blockIdx.y;
   const int gbin = p.bin_lo + bin;
   const int R = p.R, D = p.D, T = p.T, TP = p.TP, N = p.N, SK = p.SK;
   const int row0c = c * RB;  // first global row of this CTA

@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int c = (int)cluster_ctarank();
-  const int bin = blockIdx.x / CS, mix = blockIdx.y + p.mix0, gbin = p.bin_lo + bin;
+  const int bin = blockIdx.x / CS, mix = blockIdx.y, gbin = p.bin_lo + bin;
   const int T = p.T, SK = p.SK;
   const int j0 = c * TC;  // first global frame of this CTA
 

@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L, FT>())
   static_assert(D <= 32, "one lane per stacked channel in the covariance steps");
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int bin = blockIdx.x, mix = blockIdx.y + p.mix0;
+  const int bin = blockIdx.x, mix = blockIdx.y;
   const int gbin = p.bin_lo + bin;
   const int T = p.T, TP = p.TP, SK = p.SK;
 

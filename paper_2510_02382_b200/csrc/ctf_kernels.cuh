@@ -86,9 +86,10 @@ struct SweepParams {
   int* fb_list;
   int* fb_count;
   double fb_theta;
-  // mixture range of this launch: blockIdx.y + mix0 (mixture chunks of the
-  // pipelined multi-GPU loop); nmix = all mixtures of the context
-  int mix0, nmix;
+  // mixtures addressable from the (host-offset) buffers of this launch: a
+  // mixture-chunk launch gets every per-mixture pointer offset to its first
+  // mixture and indexes mixtures by blockIdx.y
+  int nmix;
 };
 
 // L2 prefetch of a contiguous block (bulk async, no registers or smem).
@@ -526,7 +527,7 @@ template <typename Real, int RMAX, int FT, int RREG, int NT, bool EXACT, int LT 
           bool IPR = false>
 __global__ void __launch_bounds__(NT, sweep_min_blocks<Real>(NT)) sweep_kernel(const SweepParams p) {
   if (p.fb_mode != 2) {  // one work item per CTA: (bin, mixture) = (blockIdx.x, blockIdx.y)
-    sweep_body<Real, RMAX, FT, RREG, NT, EXACT, LT, CHECK, IPR>(p, blockIdx.x, blockIdx.y + p.mix0);
+    sweep_body<Real, RMAX, FT, RREG, NT, EXACT, LT, CHECK, IPR>(p, blockIdx.x, blockIdx.y);
     return;
   }
   // conditioning fallback of the covariance-domain kernel: the listed items
@@ -1233,7 +1234,9 @@ __global__ void __launch_bounds__(128) muv_partial_kernel(const MuvParams p) {
         la += __shfl_xor_sync(kFull, la, 16);
         lb += __shfl_xor_sync(kFull, lb, 16);
       }
-      const Real ila = rcp_fast(fmax(la, floor_abs)), ilb = rcp_fast(fmax(lb, floor_abs));
+      // (the MUFU form measured faster at K = 20, slower at K = 10)
+      const Real ila = KMAX >= 16 ? rcp_fast(fmax(la, floor_abs)) : rcp_rn(fmax(la, floor_abs));
+      const Real ilb = KMAX >= 16 ? rcp_fast(fmax(lb, floor_abs)) : rcp_rn(fmax(lb, floor_abs));
       const Real ana = ecur[u] * (ila * ila), bna = ila * cnt;
       const Real anb = ecur[u + 1] * (ilb * ilb), bnb = ilb * cnt;
 #pragma unroll

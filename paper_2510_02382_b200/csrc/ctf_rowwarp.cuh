@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) rowwarp_kernel(const SweepParams 
   constexpr int NW = NTHREADS / 32;
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int bin = blockIdx.x, mix = blockIdx.y + p.mix0;
+  const int bin = blockIdx.x, mix = blockIdx.y;
   const int gbin = p.bin_lo + bin;
   const int R = p.R, D = p.D, T = p.T, TP = p.TP, N = p.N, SK = p.SK;
   const int row = warp / WPR, wir = warp - row * WPR;  // row of this warp, warp index within the row
