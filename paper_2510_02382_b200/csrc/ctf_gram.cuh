@@ -158,6 +158,9 @@ template <typename Real, int N, int R> constexpr int gram_nsg() {
 #ifndef CTF_GRAM_UB2  // frames per register block when two fp64 sources share the products
 #define CTF_GRAM_UB2 1
 #endif
+#ifndef CTF_GRAM_SPLITWIDE
+#define CTF_GRAM_SPLITWIDE 1
+#endif
 #ifndef CTF_GRAM_RCP64
 #define CTF_GRAM_RCP64 1
 #endif
@@ -699,22 +702,30 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L, FT>())
       static_for<L, NA + 1>([&](auto cc) {
         constexpr int C = decltype(cc)::value;
         if (cmax == C) {
-          R2 acc[NSG][C];
+          // the widest lag window of the fp64 two-source pass runs one source
+          // per pass over the frames (its accumulators would spill)
+          constexpr int NSGC = (!F32 && NSG > NSP && C == NA && CTF_GRAM_SPLITWIDE) ? NSP : NSG;
+          constexpr int UBC = NSGC > NSP ? CTF_GRAM_UB2 : kGramUB;
 #pragma unroll
-          for (int n = 0; n < NSG; ++n)
+          for (int s = 0; s < NSG; s += NSGC) {
+            R2 acc[NSGC][C];
 #pragma unroll
-            for (int j = 0; j < C; ++j) acc[n][j].x = acc[n][j].y = Real(0);
-          if (active)
-            gram_block<Real, C, NSG, (NSG > NSP ? CTF_GRAM_UB2 : kGramUB)>(x1, x2, w0, p.lp, tk.y, tk.z, acc);
+            for (int n = 0; n < NSGC; ++n)
 #pragma unroll
-          for (int n = 0; n < NSP; ++n)
+              for (int j = 0; j < C; ++j) acc[n][j].x = acc[n][j].y = Real(0);
+            if (active) gram_block<Real, C, NSGC, UBC>(x1, x2, w0 + s * p.lp, p.lp, tk.y, tk.z, acc);
 #pragma unroll
-            for (int j = 0; j < C; ++j)
-              if (j < cnt) part[(size_t)(n * NA + j) * (NT + 1) + tid] = acc[n][j];
+            for (int n = 0; n < NSGC; ++n) {
+              if (s + n < NSP) {
 #pragma unroll
-          for (int n = NSP; n < NSG; ++n)
+                for (int j = 0; j < C; ++j)
+                  if (j < cnt) part[(size_t)((s + n) * NA + j) * (NT + 1) + tid] = acc[n][j];
+              } else {
 #pragma unroll
-            for (int j = 0; j < C; ++j) keep[n - NSP][j] = acc[n][j];
+                for (int j = 0; j < C; ++j) keep[(s + n - NSP) < 0 ? 0 : s + n - NSP][j] = acc[n][j];
+              }
+            }
+          }
         }
       });
 #pragma unroll
