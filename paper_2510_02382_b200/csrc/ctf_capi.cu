@@ -17,6 +17,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <complex>
 #include <functional>
@@ -185,6 +186,11 @@ struct ctf_ctx {
   cudaEvent_t ev_join = nullptr;
   cudaStream_t chunk_stream(int k) const { return (k & 1) && stream2 ? stream2 : stream; }
   std::vector<cudaEvent_t> ev_red, ev_ar;
+  // ctf_run's upload pipeline (world 1): x in mixture chunks on a copy
+  // stream, each chunk's first iterations on its own stream
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaStream_t> ustreams;
+  std::vector<cudaEvent_t> ev_up, ev_udone;
   struct Deferred {
     bool on = false;
     int obj_slot = -1, do_v = 0;
@@ -199,6 +205,7 @@ struct ctf_ctx {
   DevBuf<unsigned long long> err;
   DevBuf<unsigned long long> chk;  // CheckOptions maxima [B][2] (double bit patterns)
   DevBuf<double> logmu;             // [B] sum_r log mu_r of the pending rescale
+  DevBuf<double> mpsum;             // [B] sum of |x~|^2 (device-side floors of the overlapped ctf_run)
   DevBuf<int4> gtab;                // gram_kernel task table
   std::vector<int4> gtab_host;
   // STFT tables (window length stft_N) and scratch
@@ -1289,8 +1296,11 @@ void iterate_impl(ctf_ctx* c, int n, bool finalize) {
 }
 
 
+// defer_x: allocate, draw and upload the initial factors, but leave the x
+// upload, its mean power and the PSD floors to the caller (run_overlapped).
 void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host,
-                const std::function<void()>& fill_x = nullptr) {
+                const std::function<void()>& fill_x = nullptr, bool defer_x = false,
+                const std::function<void()>& after_alloc = nullptr) {
   if (!prob) throw CtfError(CTF_ERR_CONFIG, "null problem");
   validate(*prob);
   if (!x_host && !fill_x) throw CtfError(CTF_ERR_CONFIG, "null mixture");
@@ -1455,9 +1465,9 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host,
   const size_t per_mix = (size_t)c->FL * c->T * c->Mx;  // complex per mixture (local)
   const bool same = (xs_in == cs);
   DevBuf<unsigned char> stage;
-  if (!same && !fill_x) stage.alloc(per_mix * xs_in);
+  if (!same && !fill_x && !defer_x) stage.alloc(per_mix * xs_in);
   if (fill_x) fill_x();  // device-side producer (the GPU STFT front end)
-  for (int b = 0; b < c->B && !fill_x; ++b) {
+  for (int b = 0; b < c->B && !fill_x && !defer_x; ++b) {
     const unsigned char* src =
         static_cast<const unsigned char*>(x_host) + ((size_t)b * c->F + c->lo) * c->T * c->Mx * xs_in;
     unsigned char* dst = c->x.p + (size_t)b * per_mix * cs;
@@ -1475,6 +1485,9 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host,
       CK(cudaStreamSynchronize(c->stream));  // stage is reused
     }
   }
+  if (defer_x) {
+    if (c->has_fb) c->fb_count.alloc(std::max<size_t>(c->fb_count.n, (size_t)c->B));  // one list per upload chunk
+  } else {
   // mean power of x~ and the absolute PSD floor (estimator.cpp:520-529)
   if (rs == 4)
     ctf::mean_power_kernel<float><<<dim3(c->FL, c->B), 256, 0, c->stream>>>(c->x.p, c->mp_part.p, c->FL, c->T, c->Mx, c->Ls);
@@ -1504,6 +1517,7 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host,
   }
   CK(cudaMemcpyAsync(c->floor_abs.p, floors.data(), floors.size() * 8, cudaMemcpyHostToDevice, c->stream));
   c->floors = floors;
+  }
   c->it_sweep_ms.clear();
   c->it_mu_ms.clear();
   c->it_rs_ms.clear();
@@ -1519,11 +1533,156 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host,
     else identity_kernel<double><<<g, 256, 0, c->stream>>>((double*)c->W.p, (size_t)c->B * c->FL, c->R, c->D);
     CK(cudaGetLastError());
   }
+  // run_overlapped's chunked x copies: after the (pageable) factor uploads,
+  // which would otherwise queue behind the whole of x on the copy engine
+  if (after_alloc) after_alloc();
   CK(cudaStreamSynchronize(c->stream));
   c->done = 0;
   c->pending = false;
   c->timing = ctf_timing{};
   c->ready = true;
+}
+
+// Per-mixture PSD floors on the device (estimator.cpp:520-529), the same
+// arithmetic and bin order as setup_impl's host loop: sum_i part[b][i] / count.
+__global__ void floor_kernel(const double* part, double* floor_abs, double* mpsum, int FL, int m0, int m1,
+                             double count, double psd_floor) {
+  const int b = m0 + (int)(blockIdx.x * blockDim.x + threadIdx.x);
+  if (b >= m1) return;
+  double s = 0.0;
+  for (int i = 0; i < FL; ++i) s += part[(size_t)b * FL + i];
+  mpsum[b] = s;
+  floor_abs[b] = psd_floor * (s / count);
+}
+
+// ctf_run on one GPU with the host->device copy of x overlapped with the first
+// iterations: x goes up in mixture chunks on a copy stream; each chunk's mean
+// power, floor and first J loop bodies run on the chunk's own stream as soon
+// as its bytes have landed (mixtures are independent until the all-bin MU-V
+// sums, which are per mixture), so chunk 0 iterates while chunk 7 uploads.
+// Then the streams join and the remaining iterations run unchunked. Results
+// are bit-identical to setup + iterate (same kernels per mixture, MU-V
+// chunking independent of the batch). Returns false (nothing done) when the
+// problem does not qualify (multi-rank, x conversion, CheckOptions, < 2
+// mixtures or no iterations); the caller then runs the plain path.
+template <class Real>
+bool run_overlapped(ctf_ctx* c, const ctf_problem* prob, const void* x_host) {
+  if (c->world != 1 || c->group || prob->x_precision != prob->precision || prob->checks != 0 ||
+      prob->num_mixtures < 2 || prob->iterations < 1)
+    return false;
+  if (const char* e = std::getenv("CTF_RUN_OVERLAP"))
+    if (std::atoi(e) == 0) return false;
+  int NU = std::min(prob->num_mixtures, 8), J = std::min(prob->iterations, 3);  // J: chunked loop bodies
+  if (const char* e = std::getenv("CTF_RUN_OVERLAP_NU")) NU = std::max(1, std::min(prob->num_mixtures, std::atoi(e)));
+  if (const char* e = std::getenv("CTF_RUN_OVERLAP_J")) J = std::max(1, std::min(prob->iterations, std::atoi(e)));
+  while ((int)c->ustreams.size() < NU) {
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    c->ustreams.push_back(st);
+    cudaEvent_t a, b;
+    CK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+    c->ev_up.push_back(a);
+    c->ev_udone.push_back(b);
+  }
+  if (!c->copy_stream) CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  std::vector<int> mb((size_t)NU + 1);
+  for (int u = 0; u <= NU; ++u) mb[(size_t)u] = u * prob->num_mixtures / NU;
+  size_t per_mix = 0, cs = 0;  // complex values per mixture, bytes per complex
+  bool copies = false;
+  // x goes up in mixture chunks, issued at the end of the setup
+  auto issue_copies = [&] {
+    if (c->sv.kind == 2 || c->nmc != 1) return;  // not chunkable
+    cs = 2 * (size_t)c->real_size;
+    per_mix = (size_t)c->FL * c->T * c->Mx;
+    CK(cudaStreamSynchronize(c->copy_stream));  // (x of a previous run)
+    for (int u = 0; u < NU; ++u) {
+      const size_t off = (size_t)mb[(size_t)u] * per_mix * cs;
+      const size_t n = (size_t)(mb[(size_t)u + 1] - mb[(size_t)u]) * per_mix * cs;
+      CK(cudaMemcpyAsync(c->x.p + off, static_cast<const unsigned char*>(x_host) + off, n, cudaMemcpyHostToDevice,
+                         c->copy_stream));
+      CK(cudaEventRecord(c->ev_up[(size_t)u], c->copy_stream));
+    }
+    copies = true;
+  };
+  const auto t_enter = std::chrono::steady_clock::now();
+  setup_impl(c, prob, x_host, nullptr, true, issue_copies);
+  const auto t_setup = std::chrono::steady_clock::now();
+  if (!copies) {  // not chunkable: the plain setup + loop
+    setup_impl(c, prob, x_host);
+    iterate_impl(c, prob->iterations, true);
+    return true;
+  }
+  c->mpsum.alloc((size_t)c->B);
+  cudaEvent_t e_start = take_event(c), e_end = take_event(c);
+  CK(cudaEventRecord(e_start, c->stream));  // memsets, initial factors, W = I
+  const double count = (double)c->F * c->D * c->T;
+  for (int u = 0; u < NU; ++u) {
+    const cudaStream_t st = c->ustreams[(size_t)u];
+    const int m0 = mb[(size_t)u], m1 = mb[(size_t)u + 1];
+    CK(cudaStreamWaitEvent(st, e_start, 0));
+    CK(cudaStreamWaitEvent(st, c->ev_up[(size_t)u], 0));
+    ctf::mean_power_kernel<Real><<<dim3(c->FL, m1 - m0), 256, 0, st>>>(c->x.p + (size_t)m0 * per_mix * cs,
+                                                                       c->mp_part.p + (size_t)m0 * c->FL, c->FL,
+                                                                       c->T, c->Mx, c->Ls);
+    floor_kernel<<<1, 64, 0, st>>>(c->mp_part.p, c->floor_abs.p, c->mpsum.p, c->FL, m0, m1, count, prob->psd_floor);
+    CK(cudaGetLastError());
+  }
+  for (int i = 0; i < J; ++i) {  // run_body's loop body, chunk by chunk
+    const int obj_slot = c->pending ? c->done - 1 : -1;
+    for (int u = 0; u < NU; ++u) {
+      const cudaStream_t st = c->ustreams[(size_t)u];
+      const int m0 = mb[(size_t)u], m1 = mb[(size_t)u + 1];
+      launch_sweep<Real>(c, true, m0, m1, u, st);
+      launch_muv<Real>(c, m0, m1, st);
+      launch_apply<Real>(c, 2, obj_slot, 1, m0, m1, st);
+      c->timing.launches += 2;
+    }
+    c->done += 1;
+    c->pending = true;
+  }
+  for (int u = 0; u < NU; ++u) {
+    CK(cudaEventRecord(c->ev_udone[(size_t)u], c->ustreams[(size_t)u]));
+    CK(cudaStreamWaitEvent(c->stream, c->ev_udone[(size_t)u], 0));
+  }
+  CK(cudaEventRecord(e_end, c->stream));
+  // the setup checks of estimator.cpp:520-529 (non-finite / zero mixture),
+  // raised before anything the loop may have recorded
+  std::vector<double> sums((size_t)c->B), floors((size_t)c->B);
+  CK(cudaMemcpyAsync(sums.data(), c->mpsum.p, sums.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(floors.data(), c->floor_abs.p, floors.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (int b = 0; b < c->B; ++b) {
+    const double mp = sums[(size_t)b] / count;
+    if (!std::isfinite(mp))
+      throw CtfError(CTF_ERR_DEGENERACY, "mixture spectrogram contains non-finite values", CTF_KIND_NONFINITE_X, -1, b);
+    if (!(mp > 0.0))
+      throw CtfError(CTF_ERR_CONFIG, "mixture spectrogram is identically zero", CTF_KIND_ZERO_X, -1, b);
+  }
+  c->floors = floors;
+  if (std::getenv("CTF_DEBUG_RUN")) {  // measurement aid: host and device timeline of the section
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, e_start, e_end));
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "run_overlapped: NU=%d J=%d setup(host) %.2f ms, section(device, e_start->join) %.2f ms, "
+                 "host to floor check %.2f ms\n", NU, J, std::chrono::duration<double, std::milli>(t_setup - t_enter).count(), t,
+                 std::chrono::duration<double, std::milli>(now - t_enter).count());
+  }
+  // OptimizationTrace entries of the overlapped bodies: the section's time
+  // (from the end of the setup, upload included) split evenly over them
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e_start, e_end));
+  c->ev_pool.push_back(e_start);
+  c->ev_pool.push_back(e_end);
+  for (int i = 0; i < J; ++i) {
+    c->it_sweep_ms.push_back(ms / J);
+    c->it_mu_ms.push_back(0.0);
+    c->it_rs_ms.push_back(0.0);
+  }
+  c->timing.sweep_ms += ms;
+  c->timing.sweep_launches += J * NU;
+  iterate_impl(c, prob->iterations - J, true);
+  return true;
 }
 
 }  // namespace
@@ -1577,6 +1736,10 @@ void ctf_close(ctf_ctx* c) {
   if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
   if (c->stream2) cudaStreamSynchronize(c->stream2);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  for (auto st : c->ustreams) cudaStreamSynchronize(st), cudaStreamDestroy(st);
+  if (c->copy_stream) cudaStreamSynchronize(c->copy_stream), cudaStreamDestroy(c->copy_stream);
+  for (auto e : c->ev_up) cudaEventDestroy(e);
+  for (auto e : c->ev_udone) cudaEventDestroy(e);
   if (c->stream2) cudaStreamDestroy(c->stream2);
   for (auto e : c->ev_red) cudaEventDestroy(e);
   for (auto e : c->ev_ar) cudaEventDestroy(e);
@@ -1859,8 +2022,13 @@ int ctf_run(ctf_ctx* c, const ctf_problem* prob, const void* x_host, double* W_o
             double* objective_out, ctf_err* err) {
   return guarded(err, [&] {
     if (!c) throw CtfError(CTF_ERR_CONFIG, "null context");
-    setup_impl(c, prob, x_host);
-    iterate_impl(c, prob->iterations, true);
+    if (!prob) throw CtfError(CTF_ERR_CONFIG, "null problem");
+    const bool done = prob->precision == CTF_F32 ? run_overlapped<float>(c, prob, x_host)
+                                                 : run_overlapped<double>(c, prob, x_host);
+    if (!done) {
+      setup_impl(c, prob, x_host);
+      iterate_impl(c, prob->iterations, true);
+    }
     ctf_err e2{};
     const int rc = ctf_download(c, W_out, B_out, V_out, objective_out, &e2);
     if (rc != CTF_OK) throw CtfError(rc, e2.msg);

@@ -592,14 +592,20 @@ def test_odd_shapes(case):
     assert np.max(np.abs(obj[0] - ref["objective"]) / np.abs(ref["objective"])) <= tol
 
 
-def test_ctf_run_end_to_end_matches_device_resident_path():
-    """ctf_run (host buffers in, host buffers out) == setup + iterate + download."""
+@pytest.mark.parametrize("B,iters,precision", [(3, 5, "f64"), (9, 2, "f64"), (11, 6, "f32"), (2, 1, "f32")])
+def test_ctf_run_end_to_end_matches_device_resident_path(B, iters, precision):
+    """ctf_run (host buffers in, host buffers out) == setup + iterate + download,
+    bit for bit: ctf_run uploads x in mixture chunks and runs each chunk's
+    first loop bodies on its own stream while later chunks are still in
+    flight (run_overlapped); the result must not depend on that."""
     import ctypes
     from paper_2510_02382_b200 import _lib
     from paper_2510_02382_b200.api import _problem
-    B, F, T, M, L, K, iters, seed = 3, 21, 120, 2, 3, 4, 5, 8
+    F, T, M, L, K, seed = 21, 120, 2, 3, 4, 8
     raw = synth_mixtures(B, F, T, M, M, L, K, 0.6, 5)
-    s = Session(raw, [L] * M, [K] * M, stack_taps=L, iterations=iters, precision="f64", seed=seed)
+    if precision == "f32":
+        raw = raw.astype(np.complex64)
+    s = Session(raw, [L] * M, [K] * M, stack_taps=L, iterations=iters, precision=precision, seed=seed)
     s.iterate(iters)
     W1, B1, V1, o1 = s.download_raw()
     s.close()
@@ -609,7 +615,7 @@ def test_ctf_run_end_to_end_matches_device_resident_path():
     Bf = np.zeros(B * F * SK)
     V = np.zeros(B * SK * T)
     o = np.zeros(B * iters)
-    prob = _problem(B, F, T, M, L, [L] * M, [K] * M, iters, "f64", "f64", 1e-10, seed)
+    prob = _problem(B, F, T, M, L, [L] * M, [K] * M, iters, precision, precision, 1e-10, seed)
     ctx = ctypes.c_void_p()
     err = _lib.CtfErr()
     assert lib.ctf_open(0, ctypes.byref(ctx), ctypes.byref(err)) == 0
@@ -620,6 +626,34 @@ def test_ctf_run_end_to_end_matches_device_resident_path():
     assert np.array_equal(W.view(np.complex128).reshape(B, F, -1), W1)
     assert np.array_equal(Bf.reshape(B, -1), B1) and np.array_equal(V.reshape(B, -1), V1)
     assert np.array_equal(o.reshape(B, iters), o1)
+
+
+def test_ctf_run_setup_errors_with_the_overlapped_upload():
+    """The setup checks of estimator.cpp:520-529 still come first when ctf_run
+    overlaps the upload with the loop: a non-finite mixture -> degeneracy
+    "non-finite", an all-zero mixture -> ConfigError, for the offending mixture."""
+    import ctypes
+    from paper_2510_02382_b200 import _lib
+    from paper_2510_02382_b200.api import _problem
+    B, F, T, M, L, K, iters, seed = 5, 9, 60, 2, 2, 3, 4, 1
+    lib = _lib.load()
+    for kind in ("nan", "zero"):
+        raw = synth_mixtures(B, F, T, M, M, L, K, 0.6, 2)
+        if kind == "nan":
+            raw[3, 4, 7, 1] = np.nan
+        else:
+            raw[2] = 0
+        W, Bf, V, o = np.zeros(B * F * (M * L) ** 2 * 2), np.zeros(B * F * M * K), np.zeros(B * M * K * T), np.zeros(B * iters)
+        prob = _problem(B, F, T, M, L, [L] * M, [K] * M, iters, "f64", "f64", 1e-10, seed)
+        ctx, err = ctypes.c_void_p(), _lib.CtfErr()
+        assert lib.ctf_open(0, ctypes.byref(ctx), ctypes.byref(err)) == 0
+        rc = lib.ctf_run(ctx, ctypes.byref(prob), _lib.vptr(raw), _lib.dptr(W), _lib.dptr(Bf), _lib.dptr(V),
+                         _lib.dptr(o), ctypes.byref(err))
+        lib.ctf_close(ctx)
+        if kind == "nan":
+            assert rc == 4 and b"non-finite" in err.msg and err.mixture == 3, (rc, err.msg)
+        else:
+            assert rc == 2 and b"zero" in err.msg and err.mixture == 2, (rc, err.msg)
 
 
 def test_cpp_reference_mirror_runs_on_gpu(tmp_path):
