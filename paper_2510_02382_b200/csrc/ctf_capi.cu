@@ -419,6 +419,8 @@ void plan_sweep(ctf_ctx* c) {
   if (const char* env = std::getenv("CTF_SWEEP_KIND")) force_kind = std::atoi(env);
   int force_ag = -1;  // frame-split exchange: 0 owner scheme, 1 all-gather
   if (const char* env = std::getenv("CTF_FSPLIT_AG")) force_ag = std::atoi(env);
+  int force_pair = -1;  // frame-split: 1 two ISS steps per exchange, 0 one
+  if (const char* env = std::getenv("CTF_FSPLIT_PAIR")) force_pair = std::atoi(env);
   const int lmax = std::max(1, *std::max_element(c->taps, c->taps + c->N));
   const int loff = ((lmax + 3) / 4) * 4;
   const bool want_chk = c->prob.checks != 0;
@@ -434,6 +436,7 @@ void plan_sweep(ctf_ctx* c) {
     if (v.ip != (int)ip) continue;    // the IP rule runs on the covariance-domain IP variants only
     if (only_kind >= 0 && v.kind != only_kind) continue;
     if (pins && force_ag >= 0 && v.kind == 5 && v.ag != force_ag) continue;
+    if (pins && force_pair >= 0 && v.kind == 5 && v.pair != force_pair) continue;
     if (pins && force[0] && (v.rmax != force[0] || v.ft != force[1] || v.rreg != force[2] || v.maxt != force[3] ||
                      (force[4] >= 0 && v.exact != force[4])))
       continue;
@@ -627,6 +630,10 @@ void plan_sweep(ctf_ctx* c) {
     // (measured on B200: the cluster kernel is correct but slower than the
     // streamed one for cfg3/cfg4 so far, so it ranks last; CTF_SWEEP_KIND=3
     // selects it)
+    // step pairs (two ISS steps per pass and exchange) preferred for R <= 32
+    // (cfg3 41.86 vs 42.87 ms per 16 mixtures), one step per exchange for
+    // R = 60 (cfg4 203.2 vs 201.9 ms per 8: the 8R sums per pair cost more
+    // reduce-scatter than the halved exchanges save);
     // the frame-split cluster kernel (kind 5, only compiled for the wide
     // stacked tiles R = 32 / 60) first, the fewest CTAs per cluster and the
     // all-gather exchange preferred (cfg3 43.1 vs 44.6 ms per 16 mixtures
@@ -643,7 +650,7 @@ void plan_sweep(ctf_ctx* c) {
     const char* tc_env = std::getenv("CTF_GRAM_TC");
     const int tc_rank = v.tc ? ((tc_env && std::atoi(tc_env)) ? -6000 : 50) : 0;
     const int rank = wide_bonus + tc_rank +
-                     (v.kind == 4 ? gram_rank : v.kind == 3 ? 3000 : v.kind == 2 ? 2000 : v.kind == 5 ? (c->R > 16 ? -2000 - 10 * fs_sms : 4000) + v.cs + (1 - v.ag) : v.kind == 1 ? 1000 : 0) +
+                     (v.kind == 4 ? gram_rank : v.kind == 3 ? 3000 : v.kind == 2 ? 2000 : v.kind == 5 ? (c->R > 16 ? -2000 - 10 * fs_sms : 4000) + v.cs + (1 - v.ag) + (c->R <= 32 ? -v.pair : v.pair) : v.kind == 1 ? 1000 : 0) +
                      (v.kind == 3 ? -v.rmax * 4 : v.rmax * 4) + (v.exact ? 0 : 2) + (v.lt > 0 ? 0 : 1);
     const bool better = !found || rank < best_rank ||
                         (rank == best_rank && (TP < best_TP || (TP == best_TP && nt < best_nt)));
@@ -1895,14 +1902,15 @@ int ctf_describe(ctf_ctx* c, char* buf, int len) {
                 "\"smem_bytes\": %zu, \"grid\": [%d, %d], \"muv_chunks\": %d, \"bins\": [%d, %d], "
                 "\"world\": %d, \"rank\": %d, \"collective\": \"%s\", \"cluster\": %d, "
                 "\"gram_fallback\": %s, \"fallback_theta\": %g, \"fallback_kernel\": \"sweep_kernel<RMAX=%d,FT=%d,RREG=%d,NT=%d>\", "
-                "\"mix_chunks\": %d}",
+                "\"mix_chunks\": %d, \"exchange\": \"%s\"}",
                 c->sv.kind == 5 ? "fsplit_kernel" : c->sv.kind == 4 ? "gram_kernel" : c->sv.kind == 3 ? "cluster_kernel" : c->sv.kind == 2 ? "stream_kernel" : c->sv.kind ? "rowwarp_kernel" : "sweep_kernel",
                 c->real_size == 4 ? "f32" : "f64", c->sv.rmax, c->sv.ft,
                 c->sv.kind == 4 ? "M" : (c->sv.kind == 3 || c->sv.kind == 5) ? "RREG" : c->sv.kind == 2 ? "RG" : c->sv.kind ? "WPR" : "RREG", c->sv.rreg, c->sv.maxt, c->sv.exact, c->NT,
                 c->sweep_smem, c->FL, c->B, c->nchunk, c->lo, c->hi, c->world, c->rank,
                 c->group ? "host-group" : c->comm ? "nccl" : "none",
                 (c->sv.kind == 3 || c->sv.kind == 5) ? c->cluster_size : 1, c->has_fb ? "true" : "false",
-                c->fb_theta, c->fbv.rmax, c->fbv.ft, c->fbv.rreg, c->fbv.maxt, c->nmc);
+                c->fb_theta, c->fbv.rmax, c->fbv.ft, c->fbv.rreg, c->fbv.maxt, c->nmc,
+                c->sv.kind != 5 ? "none" : c->sv.pair ? "all-gather, step pairs" : c->sv.ag ? "all-gather" : "owner");
   return CTF_OK;
 }
 

@@ -45,7 +45,7 @@
 #endif
 namespace ctf {
 
-template <typename Real, int R, int L, int FT, int NT, int CS, int RREG, int RG, bool AG = false>
+template <typename Real, int R, int L, int FT, int NT, int CS, int RREG, int RG, bool AG = false, bool PAIR = false>
 struct FsplitLayout {
   static constexpr int M = R / L;  // mics == sources
   static constexpr int NW = NT / 32;
@@ -57,10 +57,13 @@ struct FsplitLayout {
   static constexpr int RC = (R + CS - 1) / CS;  // rows owned per CTA (max)
   static constexpr int DC = RC;                 // W columns per CTA
   static constexpr int NG = (R + RG - 1) / RG;  // row groups per pass
-  static constexpr int VP = ((3 * RG + 31) / 32) * 32;
+  static constexpr int NV = PAIR ? 8 : 3;  // sums per row and exchange: 3R per step, 8R per step pair
+  static constexpr int VP = ((NV * RG + 31) / 32) * 32;
   static constexpr int NG2 = (R + 31) / 32;  // row-power groups
   static constexpr int HL = L > 1 ? L - 1 : 1;
   static constexpr int CH = 4 * (int)sizeof(Real);  // bytes per DSMEM message
+  static constexpr int CHA = PAIR ? 2 * CH : CH;      // bytes per (row, CTA) partial
+  static constexpr int CHZ = PAIR ? 2 * CH : CH;      // bytes per row of the coefficient buffer
   static constexpr size_t RB_ = sizeof(Real), CB_ = 2 * sizeof(Real);
   static constexpr size_t a16(size_t b) { return (b + 15) & ~size_t(15); }
   static constexpr size_t mx(size_t a, size_t b) { return a > b ? a : b; }
@@ -71,8 +74,8 @@ struct FsplitLayout {
   static constexpr size_t off_red = off_w + a16((size_t)2 * R * DC * CB_);
   static constexpr size_t off_a =
       off_red + a16(mx((size_t)NW * mx(mx((size_t)NG * VP, (size_t)NG2 * 32), 16) * RB_, (size_t)(R > 32 ? CTF_FS_DCR_WIDE : CTF_FS_DCR) * R * CB_));
-  static constexpr size_t off_z = off_a + a16((size_t)2 * CS * (AG ? R : RC) * CH);
-  static constexpr size_t off_h = off_z + a16((size_t)2 * R * CH);
+  static constexpr size_t off_z = off_a + a16((size_t)2 * CS * (AG ? R : RC) * CHA);
+  static constexpr size_t off_h = off_z + a16((size_t)2 * R * CHZ);
   static constexpr size_t off_ex = off_h + a16((size_t)R * HL * RB_);
   static constexpr size_t off_bar = off_ex + a16((size_t)(8 + R) * 8);
   static constexpr size_t off_bs = off_bar + 64;
@@ -186,10 +189,13 @@ __device__ unsigned long long g_fphase[4096 * 12];  // dev instrumentation: cloc
 #else
 #define CTF_FPHASE(k)
 #endif
-template <typename Real, int R, int L, int FT, int NT, int CS, int RREG, int RG, int MINB, bool AG = false>
+template <typename Real, int R, int L, int FT, int NT, int CS, int RREG, int RG, int MINB, bool AG = false,
+          bool PAIR = false>
 __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
   using R2 = typename Cplx<Real>::T;
-  using LY = FsplitLayout<Real, R, L, FT, NT, CS, RREG, RG, AG>;
+  using LY = FsplitLayout<Real, R, L, FT, NT, CS, RREG, RG, AG, PAIR>;
+  static_assert(!PAIR || (AG && R % 2 == 0 && std::is_same<Real, float>::value),
+                "step pairs: all-gather exchange, even R, fp32");
   constexpr int N = LY::M, M = LY::M, NW = LY::NW, TC = LY::TC, XP = LY::XP, XOFF = LY::XOFF;
   constexpr int LP = LY::LP, LOFF = LY::LOFF, RC = LY::RC, DC = LY::DC, NG = LY::NG, VP = LY::VP;
   constexpr int VM = VP / 32, HL = LY::HL, CH = LY::CH, RS = R - RREG;
@@ -229,7 +235,7 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
   const int prev_it = p.iteration - 1;
   const double* mu = p.mu ? p.mu + (size_t)mix * R : nullptr;
   const int nown = (R - c + CS - 1) / CS;  // rows p with p % CS == c
-  const uint32_t txA = (uint32_t)(CS * (AG ? R : nown) * CH), txZ = (uint32_t)(R * CH);
+  const uint32_t txA = (uint32_t)(CS * (AG ? R : nown) * LY::CHA), txZ = (uint32_t)(R * CH);
   const uint32_t barA[2] = {smem_u32addr(bars + 0), smem_u32addr(bars + 1)};
   const uint32_t barZ[2] = {smem_u32addr(bars + 2), smem_u32addr(bars + 3)};
 
@@ -244,8 +250,8 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
     mbar_arm(barZ[1], txZ);
   }
   // z of "step -1" (zero update in the first pass)
-  for (int i = tid; i < R * CH / (int)sizeof(Real); i += NT)
-    reinterpret_cast<Real*>(inZ + (size_t)R * CH)[i] = Real(0);
+  for (int i = tid; i < R * LY::CHZ / (int)sizeof(Real); i += NT)
+    reinterpret_cast<Real*>(inZ + (size_t)R * LY::CHZ)[i] = Real(0);
   // own W columns, B and the pending rescale factors: loads issued before the
   // x tile's so their latency overlaps (rescaled and stored below)
   constexpr int WPT = (R * DC + NT - 1) / NT;
@@ -524,11 +530,207 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
   CTF_FPHASE(4);
   // ---- ISS sweep (estimator.cpp:556-579). The pass of step r applies step
   // r-1's update (y_p -= z_p y_{r-1}) and accumulates step r's sums.
-  R2 pv[FT];
+  R2 pv[FT], pc[FT];  // pivot row(s) of the previous step (pair: rows a and c at the pair's start)
 #pragma unroll
-  for (int k = 0; k < FT; ++k) pv[k] = czero<Real>();
+  for (int k = 0; k < FT; ++k) pv[k] = pc[k] = czero<Real>();
   double dprod = 1.0;  // prod_r (1 - z_r): det W' = det W prod_r (1 - z_r)
   int badrow = -1, badstep = 0;
+  if constexpr (PAIR) {
+    // Steps a = r and c = r + 1 in ONE pass and ONE exchange. With the rows
+    // y_p at the pair's start and w = w_p, the pass accumulates
+    //   S_pa = sum w y_p conj(y_a), S_pc = sum w y_p conj(y_c),
+    //   G_aa = sum w |y_a|^2, G_cc = sum w |y_c|^2, G_ac = sum w y_a conj(y_c);
+    // step a is z_p = S_pa / G_aa (estimator.cpp:442-458); step c acts on
+    // y_p' = y_p - z_p y_a and y_c' = y_c - z_c y_a, whose sums expand exactly:
+    //   numer'_p = S_pc - conj(z_c) S_pa - z_p G_ac + z_p conj(z_c) G_aa,
+    //   denom'_p = G_cc - 2 Re(z_c G_ac) + |z_c|^2 G_aa;
+    // and both updates apply at once (next pass): y_p -= alpha_p y_a + beta_p y_c,
+    // alpha_p = z_p - z'_p z_c, beta_p = z'_p (the same for W's rows).
+    constexpr int CHZ = LY::CHZ, CHA = LY::CHA;
+    for (int r = 0; r < R; r += 2) {
+      const int s2 = r >> 1, buf = s2 & 1;
+      const unsigned char* zprev = inZ + (size_t)(buf ^ 1) * R * CHZ;
+      auto coef = [&](int P) -> float4 { return *reinterpret_cast<const float4*>(zprev + (size_t)P * CHZ); };
+      R2 ya[FT], yc[FT];
+      float2 g1[FT], g2[FT];  // (|y_a|^2, |y_c|^2), y_a conj(y_c)
+      {
+        const float4 ca = coef(r), cc = coef(r + 1);
+#pragma unroll
+        for (int k = 0; k < FT; ++k) {
+          const int jl = tid + k * NT;
+          float2 u = Y.pick(k, jl, r), v = Y.pick(k, jl, r + 1);
+          const float2 pvs = make_float2(pv[k].y, -pv[k].x), pcs = make_float2(pc[k].y, -pc[k].x);
+          u = ffma2s(pv[k], -ca.x, u);
+          u = ffma2s(pvs, ca.y, u);
+          u = ffma2s(pc[k], -ca.z, u);
+          u = ffma2s(pcs, ca.w, u);
+          v = ffma2s(pv[k], -cc.x, v);
+          v = ffma2s(pvs, cc.y, v);
+          v = ffma2s(pc[k], -cc.z, v);
+          v = ffma2s(pcs, cc.w, v);
+          ya[k] = u;
+          yc[k] = v;
+          g1[k] = make_float2(cnorm(u), cnorm(v));
+          g2[k] = make_float2(fmaf(u.x, v.x, u.y * v.y), fmaf(u.y, v.x, -u.x * v.y));
+        }
+      }
+      static_for<0, NG>([&](auto gg) {
+        constexpr int g = decltype(gg)::value;
+        Real a[VP];
+#pragma unroll
+        for (int i = 0; i < VP; ++i) a[i] = Real(0);
+        static_for<0, RG>([&](auto qq) {
+          constexpr int q = decltype(qq)::value, P = g * RG + q;
+          if constexpr (P < R) {
+            const float4 cp = coef(P);
+            float2 q1a = make_float2(0.f, 0.f), q2a = q1a, q1c = q1a, q2c = q1a, gs1 = q1a, gs2 = q1a;
+#pragma unroll
+            for (int k = 0; k < FT; ++k) {
+              const int jl = tid + k * NT;
+              float2 y = Y.template get<P>(k, jl);
+              y = ffma2s(pv[k], -cp.x, y);
+              y = ffma2s(make_float2(pv[k].y, -pv[k].x), cp.y, y);
+              y = ffma2s(pc[k], -cp.z, y);
+              y = ffma2s(make_float2(pc[k].y, -pc[k].x), cp.w, y);
+              Y.template set<P>(k, jl, y);
+              const float w = weight(std::integral_constant<int, P>{}, k);
+              const float2 swa = fmul2s(ya[k], w), swc = fmul2s(yc[k], w);
+              q1a = ffma2s(y, swa.x, q1a);
+              q2a = ffma2s(y, swa.y, q2a);
+              q1c = ffma2s(y, swc.x, q1c);
+              q2c = ffma2s(y, swc.y, q2c);
+              gs1 = ffma2s(g1[k], w, gs1);
+              gs2 = ffma2s(g2[k], w, gs2);
+            }
+            a[q] = q1a.x + q2a.y;           // Re S_pa
+            a[RG + q] = q1a.y - q2a.x;      // Im S_pa
+            a[2 * RG + q] = q1c.x + q2c.y;  // Re S_pc
+            a[3 * RG + q] = q1c.y - q2c.x;  // Im S_pc
+            a[4 * RG + q] = gs1.x;          // G_aa
+            a[5 * RG + q] = gs1.y;          // G_cc
+            a[6 * RG + q] = gs2.x;          // Re G_ac
+            a[7 * RG + q] = gs2.y;          // Im G_ac
+          }
+        });
+        warp_reduce_scatter_fast(a, lane);
+        Real* rb = red + ((size_t)warp * NG + g) * VP;
+#pragma unroll
+        for (int i = 0; i < VM; ++i) rb[lane * VM + i] = a[i];
+      });
+#pragma unroll
+      for (int k = 0; k < FT; ++k) {
+        pv[k] = ya[k];
+        pc[k] = yc[k];
+      }
+      __syncthreads();
+      // this CTA's partial of row `tid` -> every CTA of the cluster
+      if (tid < R) {
+        const int g = tid / RG, q = tid - g * RG;
+        Real v8[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v8[i] = Real(0);
+        for (int w = 0; w < NW; ++w) {
+          const Real* rb = red + ((size_t)w * NG + g) * VP;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v8[i] += rb[i * RG + q];
+        }
+        const uint32_t la = smem_u32addr(inA + ((size_t)(buf * CS + c) * R + tid) * CHA);
+#pragma unroll 1
+        for (int dst = 0; dst < CS; ++dst) {
+          const uint32_t ra = dsmem_map(la, (uint32_t)dst), rbar = dsmem_map(barA[buf], (uint32_t)dst);
+          msg_send(ra, rbar, v8[0], v8[1], v8[2], v8[3]);
+          msg_send(ra + 16, rbar, v8[4], v8[5], v8[6], v8[7]);
+        }
+      }
+      mbar_wait_parity(barA[buf], (uint32_t)((s2 >> 1) & 1));
+      if (tid == 0) mbar_arm(barA[buf], txA);  // pair s2 + 2
+      if (tid < R) {  // both steps' coefficients of row `tid` from the CS partials in CTA order
+        Real v8[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v8[i] = Real(0);
+        Real sca_x = Real(0), sca_y = Real(0), gaa_c = Real(0);  // row c's step-a sums (z_c)
+        for (int q = 0; q < CS; ++q) {
+          const float4* e = reinterpret_cast<const float4*>(inA + ((size_t)(buf * CS + q) * R + tid) * CHA);
+          const float4 e0 = e[0], e1 = e[1];
+          v8[0] += e0.x;
+          v8[1] += e0.y;
+          v8[2] += e0.z;
+          v8[3] += e0.w;
+          v8[4] += e1.x;
+          v8[5] += e1.y;
+          v8[6] += e1.z;
+          v8[7] += e1.w;
+          const float4* ec = reinterpret_cast<const float4*>(inA + ((size_t)(buf * CS + q) * R + r + 1) * CHA);
+          const float4 c0 = ec[0], c1 = ec[1];
+          sca_x += c0.x;
+          sca_y += c0.y;
+          gaa_c += c1.x;
+        }
+        const Real gaa = v8[4];
+        const bool bad_a = !(gaa > Real(0)) || !isfinite(gaa);  // estimator.cpp:451-454
+        Real zx, zy = Real(0);
+        if (tid == r) {
+          zx = Real(1) - sqrt((Real)T / gaa);
+        } else {
+          zx = v8[0] / gaa;
+          zy = v8[1] / gaa;
+        }
+        const Real zcx = sca_x / gaa_c, zcy = sca_y / gaa_c;  // z_c of step a (row c is never the pivot a)
+        // numer' = S_pc - conj(z_c) S_pa - z_p G_ac + z_p conj(z_c) G_aa
+        const Real zzx = zx * zcx + zy * zcy, zzy = zy * zcx - zx * zcy;  // z_p conj(z_c)
+        const Real nx = v8[2] - (zcx * v8[0] + zcy * v8[1]) - (zx * v8[6] - zy * v8[7]) + zzx * gaa;
+        const Real ny = v8[3] - (zcx * v8[1] - zcy * v8[0]) - (zx * v8[7] + zy * v8[6]) + zzy * gaa;
+        // denom' = G_cc - 2 Re(z_c G_ac) + |z_c|^2 G_aa
+        const Real dn = v8[5] - Real(2) * (zcx * v8[6] - zcy * v8[7]) + (zcx * zcx + zcy * zcy) * gaa;
+        const bool bad_c = !(dn > Real(0)) || !isfinite(dn);
+        Real z2x, z2y = Real(0);
+        if (tid == r + 1) {
+          z2x = Real(1) - sqrt((Real)T / dn);
+        } else {
+          z2x = nx / dn;
+          z2y = ny / dn;
+        }
+        float4* zo = reinterpret_cast<float4*>(inZ + ((size_t)buf * R + tid) * CHZ);
+        // alpha = z_p - z'_p z_c, beta = z'_p
+        zo[0] = make_float4(zx - (z2x * zcx - z2y * zcy), zy - (z2x * zcy + z2y * zcx), z2x, z2y);
+        zo[1] = make_float4(bad_a ? Real(1) : Real(0), bad_c ? Real(1) : Real(0), tid == r ? zx : z2x, Real(0));
+      }
+      __syncthreads();
+      const unsigned char* zcur = inZ + (size_t)buf * R * CHZ;
+      auto flag = [&](int P, int i) -> bool {
+        return P < R && reinterpret_cast<const Real*>(zcur + (size_t)P * CHZ + CH)[i] != Real(0);
+      };
+      {
+        const unsigned ma1 = __ballot_sync(kFull, flag(lane, 0)), ma2 = __ballot_sync(kFull, flag(lane + 32, 0));
+        const unsigned mc1 = __ballot_sync(kFull, flag(lane, 1)), mc2 = __ballot_sync(kFull, flag(lane + 32, 1));
+        if (ma1 | ma2) {
+          badrow = ma1 ? __ffs(ma1) - 1 : 32 + __ffs(ma2) - 1;
+          badstep = r;
+          break;
+        }
+        if (mc1 | mc2) {
+          badrow = mc1 ? __ffs(mc1) - 1 : 32 + __ffs(mc2) - 1;
+          badstep = r + 1;
+          break;
+        }
+      }
+      const Real za = reinterpret_cast<const Real*>(zcur + (size_t)r * CHZ + CH)[2];
+      const Real zc2 = reinterpret_cast<const Real*>(zcur + (size_t)(r + 1) * CHZ + CH)[2];
+      dprod *= (double)(Real(1) - za);
+      dprod *= (double)(Real(1) - zc2);
+      // both steps on the own W columns: W -= alpha w_a + beta w_c (pair-start rows), ping-pong
+      const R2* Wo = Wsl + (size_t)(s2 & 1) * R * DC;
+      R2* Wn = Wsl + (size_t)((s2 + 1) & 1) * R * DC;
+      for (int e = tid; e < R * DC; e += NT) {
+        const int q = e % R, i = e / R;
+        const float4 cq = *reinterpret_cast<const float4*>(zcur + (size_t)q * CHZ);
+        R2 w = Wo[e];
+        cmsub(w, make_float2(cq.x, cq.y), Wo[i * R + r]);
+        cmsub(w, make_float2(cq.z, cq.w), Wo[i * R + r + 1]);
+        Wn[e] = w;
+      }
+    }
+  } else
   for (int r = 0; r < R; ++r) {
     const int buf = r & 1;
     const unsigned char* zprev = inZ + (size_t)(buf ^ 1) * R * CH;
@@ -717,7 +919,7 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
   // ---- epilogue: last step's update, row-power partials, |y|^2 of the first
   // HL frames for the previous CTA's delayed energies
   {
-    const unsigned char* zl = inZ + (size_t)((R - 1) & 1) * R * CH;
+    const unsigned char* zl = inZ + (PAIR ? (size_t)(((R - 2) >> 1) & 1) * R * LY::CHZ : (size_t)((R - 1) & 1) * R * CH);
     static_for<0, LY::NG2>([&](auto gg) {
       constexpr int g = decltype(gg)::value;
       Real a[32];
@@ -726,12 +928,18 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
       static_for<0, 32>([&](auto qq) {
         constexpr int q = decltype(qq)::value, P = g * 32 + q;
         if constexpr (P < R) {
-          const R2 zp = *reinterpret_cast<const R2*>(zl + (size_t)P * CH);
+          const R2 zp = *reinterpret_cast<const R2*>(zl + (size_t)P * LY::CHZ);
 #pragma unroll
           for (int k = 0; k < FT; ++k) {
             const int jl = tid + k * NT;
             R2 y = Y.template get<P>(k, jl);
-            if constexpr (std::is_same<Real, float>::value) {
+            if constexpr (PAIR) {
+              const R2 zb = *reinterpret_cast<const R2*>(zl + (size_t)P * LY::CHZ + 2 * sizeof(Real));
+              y = ffma2s(pv[k], -zp.x, y);
+              y = ffma2s(make_float2(pv[k].y, -pv[k].x), zp.y, y);
+              y = ffma2s(pc[k], -zb.x, y);
+              y = ffma2s(make_float2(pc[k].y, -pc[k].x), zb.y, y);
+            } else if constexpr (std::is_same<Real, float>::value) {
               y = ffma2s(pv[k], -zp.x, y);
               y = ffma2s(make_float2(pv[k].y, -pv[k].x), zp.y, y);
             } else {
@@ -864,7 +1072,7 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
     }
     if (tid == 0) p.logdet[tile] = logdet + log(dprod);
   }
-  const R2* Wf = Wsl + (size_t)(R & 1) * R * DC;
+  const R2* Wf = Wsl + (size_t)((PAIR ? R / 2 : R) & 1) * R * DC;
   for (int e = tid; e < R * DC; e += NT) {
     const int q = e % R, i = e / R, col = c * DC + i;
     if (col < R) Wg[(size_t)col * R + q] = Wf[e];

@@ -8,7 +8,10 @@ std::vector<SweepVariant> sweep_variants_fsplit_f32() {
           CTF_FS(float, 1, 32, 8, 1, 128, 8, 16, 8, 3), CTF_FS(float, 1, 32, 8, 4, 128, 2, 16, 8, 2),
           // all-gather exchange variants (one DSMEM hop per step)
           CTF_FSA(float, 1, 60, 10, 2, 256, 8, 32, 10, 1), CTF_FSA(float, 1, 32, 8, 4, 128, 2, 16, 8, 2),
-          CTF_FSA(float, 1, 32, 8, 2, 128, 4, 16, 8, 3)};
+          CTF_FSA(float, 1, 32, 8, 2, 128, 4, 16, 8, 3),
+          // step pairs (two ISS steps per pass and per exchange)
+          CTF_FSP(float, 1, 60, 10, 2, 256, 8, 32, 4, 1),
+          CTF_FSP(float, 1, 32, 8, 4, 128, 2, 16, 4, 2), CTF_FSP(float, 1, 32, 8, 2, 128, 4, 16, 4, 3)};
 // (measured and dropped: cfg4 over 9-CTA clusters, NT = 224 — 15 co-resident
 // clusters cover 135 SMs instead of 120 (tools/cluster_probe.cu) but the
 // cluster count, not the SM count, bounds the bins in flight and each bin's

@@ -30,6 +30,7 @@ struct SweepVariant {
   size_t (*fbytes)(int) = nullptr;  // kind 5: dynamic shared memory for SK bases
   int ag = 0;   // kind 5: all-gather exchange (every CTA derives every z)
   int tc = 0;   // kind 4: tensor-core (tcgen05) Gram
+  int pair = 0; // kind 5: two ISS steps per pass and exchange (all-gather only)
 };
 #define CTF_V(REAL, PREC, RMAX, FT, RREG, NT, EX) \
   SweepVariant { PREC, RMAX, FT, RREG, NT, EX, sweep_kernel<REAL, RMAX, FT, RREG, NT, EX> }
@@ -94,6 +95,12 @@ struct SweepVariant {
   SweepVariant {                                                                                                \
     PREC, R, FT, RREG, NT, 1, fsplit_kernel<REAL, R, L, FT, NT, CS, RREG, RG, MINB, true>, 5, L, nullptr, nullptr, 0, \
         nullptr, 0, CS, &FsplitLayout<REAL, R, L, FT, NT, CS, RREG, RG, true>::bytes, 1                         \
+  }
+// frame-split, all-gather, two ISS steps per pass / exchange (step pairs)
+#define CTF_FSP(REAL, PREC, R, L, FT, NT, CS, RREG, RG, MINB)                                                       \
+  SweepVariant {                                                                                                    \
+    PREC, R, FT, RREG, NT, 1, fsplit_kernel<REAL, R, L, FT, NT, CS, RREG, RG, MINB, true, true>, 5, L, nullptr,       \
+        nullptr, 0, nullptr, 0, CS, &FsplitLayout<REAL, R, L, FT, NT, CS, RREG, RG, true, true>::bytes, 1, 0, 1      \
   }
 // rowwarp_kernel: R = NT / (32 * WPR) rows, FT frames per lane
 #define CTF_RW(REAL, PREC, FT, WPR, NT) \

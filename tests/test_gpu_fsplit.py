@@ -32,25 +32,30 @@ def history(x, L, K, iters, seed):
     return d, out
 
 
-# (M, L, T, K, rho, F, iters, variant "rmax,ft,rreg,nt", cluster size, exchange: 0 owner, 1 all-gather)
+# (M, L, T, K, rho, F, iters, variant "rmax,ft,rreg,nt", cluster size, exchange: 0 owner, 1 all-gather,
+#  step pairs: 1 two ISS steps per pass and exchange)
 CASES = [
-    (4, 8, 1000, 20, 0.8, 9, 4, "32,2,16,128", 4, 0),
-    (4, 8, 1000, 20, 0.8, 5, 3, "32,2,16,256", 2, 0),
-    (4, 8, 1000, 20, 0.8, 5, 3, "32,1,16,128", 8, 0),
-    (4, 8, 1000, 20, 0.8, 5, 3, "32,4,16,128", 2, 0),
-    (6, 10, 4000, 16, 0.85, 2, 3, "60,2,24,128", 16, 0),
-    (6, 10, 4000, 16, 0.85, 2, 2, "60,2,32,256", 8, 0),
-    (4, 8, 1000, 20, 0.8, 5, 3, "32,4,16,128", 2, 1),
-    (4, 8, 1000, 20, 0.8, 9, 3, "32,2,16,128", 4, 1),
-    (6, 10, 4000, 16, 0.85, 2, 3, "60,2,32,256", 8, 1),
+    (4, 8, 1000, 20, 0.8, 9, 4, "32,2,16,128", 4, 0, 0),
+    (4, 8, 1000, 20, 0.8, 5, 3, "32,2,16,256", 2, 0, 0),
+    (4, 8, 1000, 20, 0.8, 5, 3, "32,1,16,128", 8, 0, 0),
+    (4, 8, 1000, 20, 0.8, 5, 3, "32,4,16,128", 2, 0, 0),
+    (6, 10, 4000, 16, 0.85, 2, 3, "60,2,24,128", 16, 0, 0),
+    (6, 10, 4000, 16, 0.85, 2, 2, "60,2,32,256", 8, 0, 0),
+    (4, 8, 1000, 20, 0.8, 5, 3, "32,4,16,128", 2, 1, 0),
+    (4, 8, 1000, 20, 0.8, 9, 3, "32,2,16,128", 4, 1, 0),
+    (6, 10, 4000, 16, 0.85, 2, 3, "60,2,32,256", 8, 1, 0),
+    (4, 8, 1000, 20, 0.8, 5, 4, "32,4,16,128", 2, 1, 1),
+    (4, 8, 1000, 20, 0.8, 9, 4, "32,2,16,128", 4, 1, 1),
+    (6, 10, 4000, 16, 0.85, 2, 3, "60,2,32,256", 8, 1, 1),
 ]
 
 
-@pytest.mark.parametrize("M,L,T,K,rho,F,iters,variant,cs,ag", CASES)
-def test_fsplit_fp32_every_iteration(M, L, T, K, rho, F, iters, variant, cs, ag, monkeypatch):
+@pytest.mark.parametrize("M,L,T,K,rho,F,iters,variant,cs,ag,pair", CASES)
+def test_fsplit_fp32_every_iteration(M, L, T, K, rho, F, iters, variant, cs, ag, pair, monkeypatch):
     monkeypatch.setenv("CTF_SWEEP_KIND", "5")
     monkeypatch.setenv("CTF_SWEEP_VARIANT", variant)
     monkeypatch.setenv("CTF_FSPLIT_AG", str(ag))
+    monkeypatch.setenv("CTF_FSPLIT_PAIR", str(pair))
     raw = synth_mixtures(1, F, T, M, M, L, K, rho, 77 + M * L)
     ref = O.run(O.config([L] * M, [K] * M, iterations=iters, seed=3, threads=NPROC),
                 O.stack_observation(raw[0], L), history=True)

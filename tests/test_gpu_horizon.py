@@ -36,8 +36,24 @@ CONFIGS = [
 
 @pytest.mark.parametrize("name,M,L,T,K,rho,F,iters,kernel,cs", CONFIGS)
 def test_fp32_full_horizon_default_kernel(name, M, L, T, K, rho, F, iters, kernel, cs):
-    for v in ("CTF_SWEEP_KIND", "CTF_SWEEP_VARIANT", "CTF_FSPLIT_AG"):
+    for v in ("CTF_SWEEP_KIND", "CTF_SWEEP_VARIANT", "CTF_FSPLIT_AG", "CTF_FSPLIT_PAIR"):
         assert v not in os.environ
+    _horizon(name, M, L, T, K, rho, F, iters, kernel, cs)
+
+
+@pytest.mark.parametrize("name,M,L,T,K,rho,F,iters,kernel,cs", CONFIGS[2:])
+@pytest.mark.parametrize("pair", [0, 1])
+def test_fp32_full_horizon_fsplit_step_pairs(name, M, L, T, K, rho, F, iters, kernel, cs, pair, monkeypatch):
+    """Both frame-split step schedules (one ISS step per exchange, and the
+    step pairs: two steps per pass from the expanded sums) over the full
+    horizon of cfg3 / cfg4."""
+    monkeypatch.setenv("CTF_SWEEP_KIND", "5")
+    monkeypatch.setenv("CTF_FSPLIT_AG", "1")
+    monkeypatch.setenv("CTF_FSPLIT_PAIR", str(pair))
+    _horizon(name, M, L, T, K, rho, F, iters, kernel, cs)
+
+
+def _horizon(name, M, L, T, K, rho, F, iters, kernel, cs):
     seed = 31
     raw = synth_mixtures(1, F, T, M, M, L, K, rho, 4242 + M * L)
     x = O.stack_observation(raw[0], L)
