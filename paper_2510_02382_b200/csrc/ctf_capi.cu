@@ -207,6 +207,11 @@ struct ctf_ctx {
   DevBuf<double> logmu;             // [B] sum_r log mu_r of the pending rescale
   DevBuf<double> mpsum;             // [B] sum of |x~|^2 (device-side floors of the overlapped ctf_run)
   DevBuf<int4> gtab;                // gram_kernel task table
+  // covariance-domain kernel: 1 / lambda [B][FL][N][T] and the objective's
+  // log term [B][FL] computed ahead of each loop body by lambda_kernel
+  bool lam_pre = false;
+  DevBuf<unsigned char> invl;
+  DevBuf<double> logsum;
   std::vector<int4> gtab_host;
   // STFT tables (window length stft_N) and scratch
   int stft_N = 0;
@@ -1022,6 +1027,53 @@ void launch_apply(ctf_ctx* c, int mode, int obj_slot, int do_v, int m0, int m1, 
 // The iteration kernel (+ its fallback) for mixtures [m0, m1).
 size_t plane_stride(const ctf_ctx* c) { return (size_t)c->FL * c->R * c->D; }
 
+// 1 / lambda and the objective's log term of mixtures [m0, m1) for the loop
+// body about to run (compute_psd with the pending rescale of B).
+template <class Real>
+void launch_lambda(ctf_ctx* c, int m0, int m1, cudaStream_t st) {
+  ctf::LambdaParams lp{};
+  const size_t mz = (size_t)m0, rs = c->real_size;
+  lp.Bf = c->Bf.p + mz * c->FL * c->SK * rs;
+  lp.V = c->V.p + mz * c->SK * c->T * rs;
+  lp.invl = c->invl.p + mz * c->FL * c->N * c->T * rs;
+  lp.logsum = c->logsum.p + mz * c->FL;
+  lp.mu = c->pending ? c->mu.p + mz * c->R : nullptr;
+  lp.floor_abs = c->floor_abs.p + mz;
+  lp.FL = c->FL;
+  lp.T = c->T;
+  lp.N = c->N;
+  lp.SK = c->SK;
+  lp.R = c->R;
+  lp.has_prev = c->pending ? 1 : 0;
+  for (int n = 0; n <= c->N; ++n) lp.koff[n] = c->koff[n];
+  for (int n = 0; n < c->N; ++n) {
+    lp.ntaps[n] = c->taps[n];
+    lp.row0[n] = c->row0[n];
+  }
+  constexpr int VEC = 16 / (int)sizeof(Real);
+  const dim3 grid((c->FL + ctf::kLambdaBins - 1) / ctf::kLambdaBins, m1 - m0);
+  const bool vec = c->T % VEC == 0;  // 16-byte V loads / stores (else one frame per thread)
+#define CTF_LAM(KM)                                                                                          \
+  {                                                                                                          \
+    const size_t sm = (size_t)ctf::kLambdaBins * c->N * ((KM + 3) / 4 * 4) * sizeof(Real);                   \
+    if (vec) ctf::lambda_kernel<Real, KM, VEC><<<grid, 256, sm, st>>>(lp);                                   \
+    else ctf::lambda_kernel<Real, KM, 1><<<grid, 256, sm, st>>>(lp);                                         \
+  }
+  switch (c->kmax) {
+    case 4: CTF_LAM(4); break;
+    case 8: CTF_LAM(8); break;
+    case 10: CTF_LAM(10); break;
+    case 12: CTF_LAM(12); break;
+    case 16: CTF_LAM(16); break;
+    case 20: CTF_LAM(20); break;
+    case 24: CTF_LAM(24); break;
+    default: CTF_LAM(32); break;
+  }
+#undef CTF_LAM
+  CK(cudaGetLastError());
+  c->timing.launches += 1;
+}
+
 template <class Real>
 void launch_sweep(ctf_ctx* c, bool do_sweep, int m0, int m1, int k, cudaStream_t st) {
   ctf::SweepParams sp = c->sp;
@@ -1101,6 +1153,13 @@ void launch_sweep(ctf_ctx* c, bool do_sweep, int m0, int m1, int k, cudaStream_t
     if (c->has_fb) {
       CK(cudaMemsetAsync(c->fb_count.p + k, 0, sizeof(int), st));  // chunk k's list
       sp.fb_mode = 1;
+    }
+    if (c->lam_pre) {
+      // (dev: CTF_DEV_SKIP_LAMBDA=1 times the iteration kernel alone on stale 1 / lambda)
+      static const bool skip = std::getenv("CTF_DEV_SKIP_LAMBDA") != nullptr;
+      if (!skip || c->done < 2) launch_lambda<Real>(c, m0, m1, st);
+      sp.invl_g = c->invl.p + (size_t)m0 * c->FL * c->N * c->T * c->real_size;
+      sp.logsum_g = c->logsum.p + (size_t)m0 * c->FL;
     }
     c->sv.gfn<<<dim3(c->FL, nm), c->NT, c->sweep_smem, st>>>(sp, c->gtab.p);
     if (c->has_fb) {  // the bins the Gram form handed over, in the frame domain
@@ -1359,6 +1418,15 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host,
   c->V.alloc(((size_t)c->B * c->SK * c->T + 4096) * rs);  // zero tail: the sweep reads V up to frame TP
   CK(cudaMemsetAsync(c->V.p, 0, c->V.n, c->stream));
   c->E.alloc((size_t)c->B * c->N * c->FL * c->T * rs);
+  // lambda ahead of the covariance-domain kernel (the variants compiled without a lambda phase)
+  c->lam_pre = c->sv.kind == 4 && c->sv.lpre != 0;
+  if (c->lam_pre) {
+    c->invl.alloc((size_t)c->B * c->FL * c->N * c->T * rs);
+    c->logsum.alloc((size_t)c->B * c->FL);
+  } else {
+    c->invl.free();
+    c->logsum.free();
+  }
   c->part.alloc((size_t)c->nchunk * c->B * 2 * c->SK * c->T * rs);
   c->packed.alloc(c->collective() ? (size_t)c->B * 2 * c->SK * c->T * rs : 16);
   c->rowpow.alloc((size_t)c->B * c->FL * c->R);
@@ -1902,7 +1970,7 @@ int ctf_describe(ctf_ctx* c, char* buf, int len) {
                 "\"smem_bytes\": %zu, \"grid\": [%d, %d], \"muv_chunks\": %d, \"bins\": [%d, %d], "
                 "\"world\": %d, \"rank\": %d, \"collective\": \"%s\", \"cluster\": %d, "
                 "\"gram_fallback\": %s, \"fallback_theta\": %g, \"fallback_kernel\": \"sweep_kernel<RMAX=%d,FT=%d,RREG=%d,NT=%d>\", "
-                "\"mix_chunks\": %d, \"exchange\": \"%s\"}",
+                "\"mix_chunks\": %d, \"exchange\": \"%s\", \"lambda_ahead\": %s}",
                 c->sv.kind == 5 ? "fsplit_kernel" : c->sv.kind == 4 ? "gram_kernel" : c->sv.kind == 3 ? "cluster_kernel" : c->sv.kind == 2 ? "stream_kernel" : c->sv.kind ? "rowwarp_kernel" : "sweep_kernel",
                 c->real_size == 4 ? "f32" : "f64", c->sv.rmax, c->sv.ft,
                 c->sv.kind == 4 ? "M" : (c->sv.kind == 3 || c->sv.kind == 5) ? "RREG" : c->sv.kind == 2 ? "RG" : c->sv.kind ? "WPR" : "RREG", c->sv.rreg, c->sv.maxt, c->sv.exact, c->NT,
@@ -1910,7 +1978,8 @@ int ctf_describe(ctf_ctx* c, char* buf, int len) {
                 c->group ? "host-group" : c->comm ? "nccl" : "none",
                 (c->sv.kind == 3 || c->sv.kind == 5) ? c->cluster_size : 1, c->has_fb ? "true" : "false",
                 c->fb_theta, c->fbv.rmax, c->fbv.ft, c->fbv.rreg, c->fbv.maxt, c->nmc,
-                c->sv.kind != 5 ? "none" : c->sv.pair ? "all-gather, step pairs" : c->sv.ag ? "all-gather" : "owner");
+                c->sv.kind != 5 ? "none" : c->sv.pair ? "all-gather, step pairs" : c->sv.ag ? "all-gather" : "owner",
+                c->lam_pre ? "true" : "false");
   return CTF_OK;
 }
 

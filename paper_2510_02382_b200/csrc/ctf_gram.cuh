@@ -34,6 +34,13 @@
 #ifndef CTF_LAMV
 #define CTF_LAMV 20
 #endif
+// Where 1 / lambda comes from: 1 = always from lambda_kernel (run by the host
+// ahead of the iteration kernel, which then has no lambda phase of its own),
+// 0 = always the kernel's own lambda phase, 2 (default) = per variant by
+// gram_lpre() below (measured on B200, tools/lam_ab.sh)
+#ifndef CTF_GRAM_LPRE
+#define CTF_GRAM_LPRE 2
+#endif
 #ifndef CTF_LAMV3  // the same for the 3-CTA/SM (80-register) cfg1 variant
 #define CTF_LAMV3 10
 #endif
@@ -132,11 +139,7 @@ __device__ __forceinline__ void gram_block(const typename Cplx<Real>::T* __restr
   if (u < u1) gram_step<Real, CNT, NS, UB, true>(x1, x2, w0, lp, u, u1, wv, acc);
 }
 
-// The objective's log term: MUFU-based in fp32 (abs. error ~1e-6, far inside
-// the fp32 cost tolerance), exact in fp64 (rcp_rn: ctf_kernels.cuh).
-__device__ __forceinline__ float log_fast(float x) { return __logf(x); }
-__device__ __forceinline__ double log_fast(double x) { return log(x); }
-
+// (log_fast, the objective's log term, and rcp_rn: ctf_kernels.cuh)
 // Sources accumulated per Gram pass: all of them in fp32 (the conj products
 // are shared); one at a time in fp64 (register budget, half the partials).
 #ifndef CTF_GRAM_NS64
@@ -175,6 +178,17 @@ template <typename Real, int NT, int R, int FT = 4> constexpr int gram_min_block
   return R > 16 ? 1
          : std::is_same<Real, float>::value ? (NT <= 256 ? (FT >= 8 ? 2 : 3) : 1)
                                             : (NT <= 256 ? CTF_GRAM_MINB64 : NT <= 384 ? 2 : 1);
+}
+
+// lambda ahead of the kernel pays where the kernel's own lambda phase (K
+// dependent V loads per frame, a reciprocal and a log per element) is poorly
+// hidden: fp64 and the variants below three CTAs per SM. At three CTAs per SM
+// (cfg1 fp32) the phase hides behind the other CTAs and the extra kernel with
+// its 1 / lambda round trip through HBM costs more than it saves.
+template <typename Real, int NT, int R, int FT> constexpr bool gram_lpre() {
+  return CTF_GRAM_LPRE == 1   ? true
+         : CTF_GRAM_LPRE == 0 ? false
+                              : (!std::is_same<Real, float>::value || gram_min_blocks<Real, NT, R, FT>() < 3);
 }
 
 // Tensor-core Gram (TC = true, fp32): the lag correlations as one real GEMM
@@ -301,6 +315,29 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L, FT>())
     }
   }
   const bool lam4 = (T % 4 == 0 && 4 * NT >= T);
+  // lambda phase done ahead by lambda_kernel (uniform over the launch)
+  constexpr int LVEC = 16 / (int)sizeof(Real);
+  constexpr int LV = (N * FT + LVEC - 1) / LVEC;  // >= (N*T/LVEC) / NT since T <= FT*NT
+  constexpr bool lpre = gram_lpre<Real, NT, M * L, FT>();
+  if (lpre && tid == 0 && p.pf_stride > 0) {
+    const size_t w = tile + p.pf_stride;
+    if (w < (size_t)p.nmix * p.FL)
+      prefetch_l2(reinterpret_cast<const Real*>(p.invl_g) + w * (size_t)N * T, (unsigned)((size_t)N * T * sizeof(Real)));
+  }
+  // 1 / lambda of the bin from lambda_kernel (one contiguous [N][T] block):
+  // 16-byte loads in flight together with the x tile's
+  const Real* lgs = reinterpret_cast<const Real*>(p.invl_g) + tile * (size_t)N * T;
+  const bool lvec = lpre && T % LVEC == 0;
+  float4 lv[LV];
+  const int nl16 = N * T / LVEC;
+  if (lvec) {
+    const float4* lg = reinterpret_cast<const float4*>(lgs);
+#pragma unroll
+    for (int i = 0; i < LV; ++i) {
+      const int e = tid + i * NT;
+      if (e < nl16) lv[i] = __ldg(lg + e);
+    }
+  }
   // ---- prologue: zero-padded x tile, W and B with the pending rescale
   if ((T * M) % CPB == 0) {
     // the bin's T x M complex block is contiguous: 16-byte loads, all in
@@ -336,6 +373,27 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L, FT>())
       R2 z;
       z.x = z.y = Real(0);
       xs[i] = (t >= 0 && t < T) ? xg[(size_t)t * M + m] : z;
+    }
+  }
+  if (lvec) {
+    for (int i = tid; i < N * p.lp; i += NT) {
+      const int s = i % p.lp - p.loff;
+      if (s < 0 || s >= T) invl[i] = Real(0);
+    }
+#pragma unroll
+    for (int i = 0; i < LV; ++i) {
+      const int e = tid + i * NT;
+      if (e < nl16) {
+        const int f = LVEC * e, n = f / T, t = f - n * T;
+        const Real* c = reinterpret_cast<const Real*>(&lv[i]);
+#pragma unroll
+        for (int h = 0; h < LVEC; ++h) invl[n * p.lp + p.loff + t + h] = c[h];
+      }
+    }
+  } else if (lpre) {
+    for (int i = tid; i < N * p.lp; i += NT) {
+      const int n = i / p.lp, s = i - n * p.lp - p.loff;
+      invl[i] = (s >= 0 && s < T) ? __ldg(lgs + (size_t)n * T + s) : Real(0);
     }
   }
   // pending rescale (estimator.cpp:399-411): W rows / mu_r, B_n / mu_row0^2
@@ -417,6 +475,9 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L, FT>())
   // ---- lambda = max(B V, floor) -> 1/lambda (zero outside [0, T)), log term
   double logsum = 0.0;
   const int t4 = tid * 4;
+  if (lpre) {
+    if (tid == 0 && p.has_prev) logsum = p.logsum_g[tile];
+  } else {
   for (int n = 0; n < N; ++n) {
     Real* il = invl + n * p.lp;
     for (int i = tid; i < p.lp; i += NT) {
@@ -499,6 +560,7 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L, FT>())
     }
   }
   __syncthreads();
+  }
   CTF_PHASE(2);
 
   // ---- virtual tail frames j in [T, T+L-1): y_r(j) = sum_c W[r,c] x~_c(j)

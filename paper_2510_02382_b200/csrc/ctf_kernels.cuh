@@ -90,6 +90,10 @@ struct SweepParams {
   // mixture-chunk launch gets every per-mixture pointer offset to its first
   // mixture and indexes mixtures by blockIdx.y
   int nmix;
+  // covariance-domain kernel: 1 / lambda and the objective's log term computed
+  // ahead by lambda_kernel (nullptr: the kernel's own lambda phase)
+  const void* invl_g;       // Real [mix][FL][N][T]
+  const double* logsum_g;   // [mix][FL]
 };
 
 // L2 prefetch of a contiguous block (bulk async, no registers or smem).
@@ -1145,6 +1149,194 @@ __global__ void __launch_bounds__(32) logdet_kernel(const void* W, double* logde
   const int st = warp_logdet<Real>(A, R, threadIdx.x & 31, out);
   if (threadIdx.x == 0) logdet[b] = st == 4 ? -INFINITY : out;
 }
+// The objective's log term: MUFU-based in fp32 (abs. error ~1e-6, far inside
+// the fp32 cost tolerance), exact in fp64.
+__device__ __forceinline__ float log_fast(float x) { return __logf(x); }
+__device__ __forceinline__ double log_fast(double x) { return log(x); }
+
+// ---------------------------------------------------------------------------
+// PSD of the next loop body, ahead of the covariance-domain kernel
+// (compute_psd model.cpp:210-215 with the pending rescale of B,
+// estimator.cpp:399-411): 1 / lambda_n(f, t) = 1 / max(sum_k B V, floor) for
+// every (bin, source, frame) of the launch's mixtures, written per bin as one
+// contiguous [N][T] block (the iteration kernel copies it with 16-byte loads
+// next to its x tile instead of running K dependent V loads per frame), and
+// the log term of the previous iteration's objective (estimator.cpp:55-77),
+// sum_n sum_t min(L_n, T - t) log lambda_n(t) per bin. lambda is formed in the
+// same fma order as everywhere else; fp64 divides exactly, fp32 takes the
+// MUFU reciprocal with one Newton step (~1 ulp). fp64 takes one log per group
+// of equally weighted frames: log prod(mantissas) + ln 2 sum(exponents).
+struct LambdaParams {
+  const void* Bf;           // Real [mix][FL][SK] (before the pending rescale)
+  const void* V;            // Real [mix][SK][T]
+  void* invl;               // Real [mix][FL][N][T]
+  double* logsum;           // [mix][FL]
+  const double* mu;         // [mix][R] pending rescale, or nullptr
+  const double* floor_abs;  // [mix]
+  int FL, T, N, SK, R, has_prev;
+  int koff[kMaxSources + 1], ntaps[kMaxSources], row0[kMaxSources];
+};
+
+constexpr int kLambdaBins = 8;  // bins per CTA (they share the V loads)
+template <typename Real, int KMAX, int VEC>
+__global__ void __launch_bounds__(256) lambda_kernel(const LambdaParams p) {
+  constexpr int BB = kLambdaBins, NT = 256, KP = (KMAX + 3) / 4 * 4, PV = 16 / (int)sizeof(Real);
+  constexpr bool F32 = std::is_same<Real, float>::value;
+  static_assert(VEC == 1 || VEC == PV, "one 16-byte vector of frames per thread, or one frame");
+  extern __shared__ __align__(16) unsigned char smem[];
+  Real* Bs = reinterpret_cast<Real*>(smem);  // [BB][N][KP], zero-padded
+  __shared__ double lred[NT / 32][BB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int mix = blockIdx.y, bin0 = blockIdx.x * BB, nb = min(BB, p.FL - bin0);
+  const Real floor_abs = (Real)p.floor_abs[mix];
+  const double* mu = p.mu ? p.mu + (size_t)mix * p.R : nullptr;
+  const Real* Bg = reinterpret_cast<const Real*>(p.Bf) + ((size_t)mix * p.FL + bin0) * p.SK;
+  for (int e = tid; e < BB * p.N * KP; e += NT) {
+    const int q = e % KP, bn = e / KP, n = bn % p.N, b = bn / p.N;
+    const int k = p.koff[n] + q;
+    Real v = Real(0);
+    if (b < nb && k < p.koff[n + 1]) {
+      v = Bg[(size_t)b * p.SK + k];
+      const double mb = mu ? mu[p.row0[n]] : 0.0;
+      if (mb != 0.0) {  // estimator.cpp:405-406: silent row, no rescale
+        if constexpr (F32) {
+          const float im = (float)(1.0 / mb);
+          v = fmaxf(v * (im * im), floor_abs);
+        } else {
+          v = fmax(v / (mb * mb), (double)floor_abs);
+        }
+      }
+    }
+    Bs[e] = v;
+  }
+  __syncthreads();
+  double ls[BB];
+#pragma unroll
+  for (int b = 0; b < BB; ++b) ls[b] = 0.0;
+  const Real* Vg = reinterpret_cast<const Real*>(p.V) + (size_t)mix * p.SK * p.T;
+  Real* out = reinterpret_cast<Real*>(p.invl) + ((size_t)mix * p.FL + bin0) * p.N * p.T;
+  for (int n = 0; n < p.N; ++n) {
+    const int k0 = p.koff[n], K = p.koff[n + 1] - k0, Ln = p.ntaps[n];
+    double prod[BB];
+    int esum[BB];
+#pragma unroll
+    for (int b = 0; b < BB; ++b) {
+      prod[b] = 1.0;
+      esum[b] = 0;
+    }
+    int pass = 0;
+    for (int t0 = tid * VEC; t0 < p.T; t0 += NT * VEC, ++pass) {
+      Real v[KMAX][VEC];
+#pragma unroll
+      for (int q = 0; q < KMAX; ++q) {
+        if (q < K) {
+          const Real* vr = Vg + (size_t)(k0 + q) * p.T + t0;
+          if constexpr (VEC == 1) {
+            v[q][0] = __ldg(vr);
+          } else {
+            const float4 raw = __ldg(reinterpret_cast<const float4*>(vr));
+            const Real* c = reinterpret_cast<const Real*>(&raw);
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) v[q][i] = c[i];
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < VEC; ++i) v[q][i] = Real(0);
+        }
+      }
+      // every frame of the vector carries weight L_n and its log goes the
+      // fast way (uniform per thread and pass; the last L_n - 1 frames do not)
+      const bool full = t0 + VEC - 1 + Ln <= p.T;
+      const int lmode = !p.has_prev ? 0 : full ? 1 : 2;
+#pragma unroll
+      for (int b = 0; b < BB; ++b) {
+        if (b >= nb) continue;
+        const float4* b4 = reinterpret_cast<const float4*>(Bs + (b * p.N + n) * KP);
+        Real bq[KP];
+#pragma unroll
+        for (int j = 0; j < KP / PV; ++j) {
+          const float4 raw = b4[j];
+          const Real* c = reinterpret_cast<const Real*>(&raw);
+#pragma unroll
+          for (int i = 0; i < PV; ++i) bq[j * PV + i] = c[i];
+        }
+        Real lam[VEC];
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) lam[i] = Real(0);
+#pragma unroll
+        for (int q = 0; q < KMAX; ++q)
+#pragma unroll
+          for (int i = 0; i < VEC; ++i) lam[i] = fma(bq[q], v[q][i], lam[i]);
+        Real il[VEC];
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) {
+          lam[i] = fmax(lam[i], floor_abs);
+          il[i] = rcp_fast(lam[i]);  // fp32: MUFU + one Newton step (~1 ulp); fp64: exact
+        }
+        if (lmode == 1) {
+          if constexpr (F32) {
+            float fsum = 0.f;
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) fsum += log_fast(lam[i]);
+            ls[b] += (double)Ln * (double)fsum;
+          } else {
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) {
+              const long long bits = __double_as_longlong(lam[i]);
+              const int ex = (int)((bits >> 52) & 0x7ff);
+              if (ex != 0 && ex != 0x7ff) {
+                prod[b] *= __longlong_as_double((bits & 0x800fffffffffffffLL) | 0x3ff0000000000000LL);
+                esum[b] += ex - 1023;
+              } else {
+                ls[b] += (double)Ln * log(lam[i]);
+              }
+            }
+          }
+        } else if (lmode == 2) {
+#pragma unroll
+          for (int i = 0; i < VEC; ++i)
+            if (t0 + i < p.T) ls[b] += (double)min(Ln, p.T - t0 - i) * (double)log_fast(lam[i]);
+        }
+        Real* o = out + ((size_t)b * p.N + n) * p.T + t0;
+        if constexpr (VEC == 1) {
+          o[0] = il[0];
+        } else {
+          float4 raw;
+          Real* c = reinterpret_cast<Real*>(&raw);
+#pragma unroll
+          for (int i = 0; i < VEC; ++i) c[i] = il[i];
+          *reinterpret_cast<float4*>(o) = raw;
+        }
+      }
+      if (!F32 && (pass & 63) == 63) {  // keep the mantissa products far from overflow
+#pragma unroll
+        for (int b = 0; b < BB; ++b) {
+          ls[b] += (double)Ln * (log(prod[b]) + (double)esum[b] * 0.693147180559945309417);
+          prod[b] = 1.0;
+          esum[b] = 0;
+        }
+      }
+    }
+    if (!F32 && p.has_prev) {
+#pragma unroll
+      for (int b = 0; b < BB; ++b)
+        ls[b] += (double)Ln * (log(prod[b]) + (double)esum[b] * 0.693147180559945309417);
+    }
+  }
+  if (!p.has_prev) return;
+#pragma unroll
+  for (int b = 0; b < BB; ++b) {
+    const double s = warp_sum(ls[b]);
+    if (lane == 0) lred[warp][b] = s;
+  }
+  __syncthreads();
+  if (tid < nb) {
+    double s = 0.0;
+    for (int w = 0; w < NT / 32; ++w) s += lred[w][tid];
+    p.logsum[(size_t)mix * p.FL + bin0 + tid] = s;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // MU-V (estimator.cpp:348-382): partial numerator/denominator over a chunk
 // of this rank's bins, for one source and a tile of frames. lambda' is

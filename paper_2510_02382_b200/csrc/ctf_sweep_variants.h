@@ -31,7 +31,12 @@ struct SweepVariant {
   int ag = 0;   // kind 5: all-gather exchange (every CTA derives every z)
   int tc = 0;   // kind 4: tensor-core (tcgen05) Gram
   int pair = 0; // kind 5: two ISS steps per pass and exchange (all-gather only)
+  int lpre = 0; // kind 4: compiled without its own lambda phase (the host runs lambda_kernel ahead)
 };
+inline SweepVariant with_lpre(SweepVariant v, bool lpre) {
+  v.lpre = lpre ? 1 : 0;
+  return v;
+}
 #define CTF_V(REAL, PREC, RMAX, FT, RREG, NT, EX) \
   SweepVariant { PREC, RMAX, FT, RREG, NT, EX, sweep_kernel<REAL, RMAX, FT, RREG, NT, EX> }
 // equal-taps variants: LT taps per source (row P = (P / LT, P % LT))
@@ -71,20 +76,19 @@ struct SweepVariant {
 #define CTF_CL(REAL, PREC, RB, FT, RREG, NT) \
   SweepVariant { PREC, RB, FT, RREG, NT, 0, nullptr, 3, 0, nullptr, cluster_kernel<REAL, RB, FT, RREG, NT> }
 // gram_kernel: covariance-domain steps, M mics = N sources, L taps
-#define CTF_GR(REAL, PREC, M, L, NT, FT)                                                                 \
-  SweepVariant {                                                                                         \
-    PREC, (M) * (L), FT, M, NT, 1, nullptr, 4, L, nullptr, nullptr, 0, gram_kernel<REAL, M, L, NT, FT>   \
-  }
+#define CTF_GR(REAL, PREC, M, L, NT, FT)                                                                  \
+  with_lpre(SweepVariant{PREC, (M) * (L), FT, M, NT, 1, nullptr, 4, L, nullptr, nullptr, 0,               \
+                         gram_kernel<REAL, M, L, NT, FT>},                                                \
+            gram_lpre<REAL, NT, (M) * (L), FT>())
 // gram_kernel with the tcgen05 Gram (fp32)
-#define CTF_GRT(REAL, PREC, M, L, NT, FT)                                                                        \
-  SweepVariant {                                                                                                \
-    PREC, (M) * (L), FT, M, NT, 1, nullptr, 4, L, nullptr, nullptr, 0, gram_kernel<REAL, M, L, NT, FT, false, true>, \
-        0, 0, nullptr, 0, 1                                                                                     \
-  }
-#define CTF_GRI(REAL, PREC, M, L, NT, FT)                                                                   \
-  SweepVariant {                                                                                            \
-    PREC, (M) * (L), FT, M, NT, 1, nullptr, 4, L, nullptr, nullptr, 0, gram_kernel<REAL, M, L, NT, FT, true>, 1 \
-  }
+#define CTF_GRT(REAL, PREC, M, L, NT, FT)                                                                 \
+  with_lpre(SweepVariant{PREC, (M) * (L), FT, M, NT, 1, nullptr, 4, L, nullptr, nullptr, 0,               \
+                         gram_kernel<REAL, M, L, NT, FT, false, true>, 0, 0, nullptr, 0, 1},              \
+            gram_lpre<REAL, NT, (M) * (L), FT>())
+#define CTF_GRI(REAL, PREC, M, L, NT, FT)                                                                 \
+  with_lpre(SweepVariant{PREC, (M) * (L), FT, M, NT, 1, nullptr, 4, L, nullptr, nullptr, 0,               \
+                         gram_kernel<REAL, M, L, NT, FT, true>, 1},                                       \
+            gram_lpre<REAL, NT, (M) * (L), FT>())
 // fsplit_kernel: R = M * L stacked rows, frames split over a cluster of CS CTAs
 #define CTF_FS(REAL, PREC, R, L, FT, NT, CS, RREG, RG, MINB)                                               \
   SweepVariant {                                                                                         \
