@@ -220,6 +220,7 @@ struct ctf_ctx {
   DevBuf<double2> stft_spec;
   // timing
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_sweep, ev_mu, ev_fin;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_lam;  // dev (CTF_DEV_TIME_LAMBDA): around lambda_kernel
   std::vector<cudaEvent_t> ev_rs;  // per iteration: between MU-V and the reduce/apply kernel (null when chunked)
   std::vector<cudaEvent_t> ev_pool;
   ctf_timing timing{};
@@ -1157,7 +1158,18 @@ void launch_sweep(ctf_ctx* c, bool do_sweep, int m0, int m1, int k, cudaStream_t
     if (c->lam_pre) {
       // (dev: CTF_DEV_SKIP_LAMBDA=1 times the iteration kernel alone on stale 1 / lambda)
       static const bool skip = std::getenv("CTF_DEV_SKIP_LAMBDA") != nullptr;
+      static const bool tim = std::getenv("CTF_DEV_TIME_LAMBDA") != nullptr;  // dev: event-timed in the stream
+      cudaEvent_t t0 = nullptr, t1 = nullptr;
+      if (tim) {
+        t0 = take_event(c);
+        t1 = take_event(c);
+        CK(cudaEventRecord(t0, st));
+      }
       if (!skip || c->done < 2) launch_lambda<Real>(c, m0, m1, st);
+      if (tim) {
+        CK(cudaEventRecord(t1, st));
+        c->ev_lam.push_back({t0, t1});
+      }
       sp.invl_g = c->invl.p + (size_t)m0 * c->FL * c->N * c->T * c->real_size;
       sp.logsum_g = c->logsum.p + (size_t)m0 * c->FL;
     }
@@ -1324,6 +1336,12 @@ void collect_timing(ctf_ctx* c) {
   c->ev_mu.clear();
   c->ev_rs.clear();
   drain(c->ev_fin, c->timing.finalize_ms);
+  if (!c->ev_lam.empty()) {
+    double lam_ms = 0.0;
+    const size_t nl = c->ev_lam.size();
+    drain(c->ev_lam, lam_ms);
+    std::fprintf(stderr, "[ctf dev] lambda_kernel: %.3f ms over %zu launches (%.3f ms each)\n", lam_ms, nl, lam_ms / nl);
+  }
 }
 
 void iterate_impl(ctf_ctx* c, int n, bool finalize) {

@@ -34,6 +34,9 @@
 #ifndef CTF_LAMV
 #define CTF_LAMV 20
 #endif
+#ifndef CTF_GRAM_CHAIN  // 1: mbarrier-chained ISS steps on the narrow tiles (0: one CTA barrier per step)
+#define CTF_GRAM_CHAIN 1
+#endif
 // Where 1 / lambda comes from: 1 = always from lambda_kernel (run by the host
 // ahead of the iteration kernel, which then has no lambda phase of its own),
 // 0 = always the kernel's own lambda phase, 2 (default) = per variant by
@@ -1102,16 +1105,72 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L, FT>())
     __syncthreads();
   } else {
   // ---- R covariance-domain ISS steps (estimator.cpp:556-579, 275-302)
-  R2* piv = zs;     // 2 x (D + LT1): pivot W row and tail, double-buffered by step parity
+  // Narrow tiles (CTF_GRAM_CHAIN): no CTA barrier per step. Every pivot has its
+  // own buffer (R x (D + LT1), in the Gram partial region, free between the
+  // Gram reduction and the |y|^2 rows) and its own mbarrier: the half-warp of
+  // row r + 1 publishes its updated row as soon as its step-r update is done
+  // and arrives; the warps wait only on the pivot they are about to read. The
+  // pivot's own scale (a division and a square root) runs after the publish, so
+  // the dependent chain of the sweep is load -> matvec -> reduce -> one
+  // reciprocal -> update -> publish per step.
+  constexpr bool CHAIN = !WIDE && CTF_GRAM_CHAIN;
+  R2* piv = CHAIN ? reinterpret_cast<R2*>(smem + p.off_e) : zs;  // !CHAIN: 2 x (D + LT1), double-buffered by step parity
   Real* fac = fac_s;  // (1 - z_r) per row, multiplied in row order at the end
   constexpr int PV = D + LT1;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(piv + R * PV);
   if (rowk[0] == 0) {
     if (hl < D) piv[hl] = wreg[0];
     if (hl < LT1) piv[D + hl] = yreg[0];
   }
+  if (CHAIN && tid < R) tc::mbar_init(&mbar[tid], 1);
   __syncthreads();
   CTF_PHASE(5);
   const bool wrows = (tid / 32) * (32 / LPR) < R;  // warp-uniform: this warp owns at least one row
+  if constexpr (CHAIN) {
+    if (wrows) {
+      const int row = rowk[0];
+      for (int r = 0; r < R; ++r) {
+        const R2* pv = piv + r * PV;
+        if (r > 0) tc::mbar_wait(&mbar[r], 0);
+        Real nre, nim, den;
+        row_sums(0, pv, 1, pv + D, nre, nim, den);
+        const bool ok = rowvk[0] && den > Real(0) && isfinite(den);  // estimator.cpp:451-454
+        if (rowvk[0] && !ok && hl == 0) atomicMin(&s_badrow, r * 64 + row);
+        R2 z;
+        z.x = z.y = Real(0);
+        if (ok && row != r) {  // every row but the pivot first: the next pivot is among them
+          Real inv;
+          if constexpr (F32) inv = __frcp_rn(den);
+          else inv = 1.0 / den;
+          z.x = nre * inv;
+          z.y = nim * inv;
+        }
+        // iss_apply (estimator.cpp:298-302) on the own row and its tail
+        if (hl < D) cmsub(wreg[0], z, pv[hl]);
+        if (hl < LT1) cmsub(yreg[0], z, pv[D + hl]);
+        if (r + 1 < R) {
+          if (row == r + 1) {
+            R2* nx = piv + (r + 1) * PV;
+            if (hl < D) nx[hl] = wreg[0];
+            if (hl < LT1) nx[D + hl] = yreg[0];
+          }
+          __syncwarp();
+          if (row == r + 1 && hl == 0) tc::mbar_arrive(&mbar[r + 1]);
+        }
+        if (ok && row == r) {  // the pivot's own scale: w_r (1 - z_r), off the chain
+          R2 zp;
+          zp.y = Real(0);
+          if constexpr (F32) zp.x = 1.f - sqrtf((float)T) * rsqrtf(den);
+          else zp.x = 1.0 - sqrt((double)T / den);
+          if (hl == 0) fac[row] = Real(1) - zp.x;
+          if (hl < D) cmsub(wreg[0], zp, pv[hl]);
+          if (hl < LT1) cmsub(yreg[0], zp, pv[D + hl]);
+        }
+      }
+    }
+    __syncthreads();
+    if (tid < R) tc::mbar_inval(&mbar[tid]);  // the region is plain data again below
+  } else {
   for (int r = 0; r < R; ++r) {
     const R2* pv = piv + (r & 1) * PV;
 #pragma unroll
@@ -1158,6 +1217,7 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L, FT>())
       }
     }
     __syncthreads();
+  }
   }
   if (s_badrow != kNoRow) {
     if (tid == 0) record_err<Real>(p.err, mix, err_key(p.iteration, kPhSweep, gbin, s_badrow >> 6, s_badrow & 63));

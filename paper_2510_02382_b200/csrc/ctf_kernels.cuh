@@ -144,6 +144,25 @@ __device__ __forceinline__ float rcp_fast(float x) {
   return fmaf(r, fmaf(-x, r, 1.f), r);
 }
 __device__ __forceinline__ double rcp_fast(double x) { return 1.0 / x; }
+// fp64 1/x for the MU-V weights (x = lambda' >= floor > 0, normal): the
+// MUFU.RCP64H seed (2^-23) and two Newton steps, ~1 ulp, branch-free and half
+// the dependent chain of the IEEE division (its correction steps and slow path)
+#ifndef CTF_MUV_RCPNR
+#define CTF_MUV_RCPNR 1
+#endif
+__device__ __forceinline__ double rcp_muv(double x) {
+#if CTF_MUV_RCPNR
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+#else
+  return 1.0 / x;
+#endif
+}
+__device__ __forceinline__ float rcp_muv(float x) { return rcp_fast(x); }
 template <typename V> __device__ __forceinline__ auto cnorm(V a) -> decltype(a.x) { return fma(a.x, a.x, a.y * a.y); }
 template <typename V> __device__ __forceinline__ bool cfinite(V a) { return isfinite(a.x) && isfinite(a.y); }
 template <typename Real> __device__ __forceinline__ typename Cplx<Real>::T czero() {
@@ -1227,10 +1246,13 @@ __global__ void __launch_bounds__(256) lambda_kernel(const LambdaParams p) {
     int pass = 0;
     for (int t0 = tid * VEC; t0 < p.T; t0 += NT * VEC, ++pass) {
       Real v[KMAX][VEC];
+      const Real* vbase = Vg + (size_t)k0 * p.T + t0;
+      Real* o = out + (size_t)n * p.T + t0;  // bin b of the CTA: + b * N * T
+      const size_t ostride = (size_t)p.N * p.T;
 #pragma unroll
       for (int q = 0; q < KMAX; ++q) {
         if (q < K) {
-          const Real* vr = Vg + (size_t)(k0 + q) * p.T + t0;
+          const Real* vr = vbase + (size_t)q * p.T;
           if constexpr (VEC == 1) {
             v[q][0] = __ldg(vr);
           } else {
@@ -1270,7 +1292,7 @@ __global__ void __launch_bounds__(256) lambda_kernel(const LambdaParams p) {
         Real il[VEC];
 #pragma unroll
         for (int i = 0; i < VEC; ++i) {
-          lam[i] = fmax(lam[i], floor_abs);
+          lam[i] = lam[i] > floor_abs ? lam[i] : floor_abs;  // = fmax (a NaN takes the floor)
           il[i] = rcp_fast(lam[i]);  // fp32: MUFU + one Newton step (~1 ulp); fp64: exact
         }
         if (lmode == 1) {
@@ -1297,15 +1319,14 @@ __global__ void __launch_bounds__(256) lambda_kernel(const LambdaParams p) {
           for (int i = 0; i < VEC; ++i)
             if (t0 + i < p.T) ls[b] += (double)min(Ln, p.T - t0 - i) * (double)log_fast(lam[i]);
         }
-        Real* o = out + ((size_t)b * p.N + n) * p.T + t0;
         if constexpr (VEC == 1) {
-          o[0] = il[0];
+          o[(size_t)b * ostride] = il[0];
         } else {
           float4 raw;
           Real* c = reinterpret_cast<Real*>(&raw);
 #pragma unroll
           for (int i = 0; i < VEC; ++i) c[i] = il[i];
-          *reinterpret_cast<float4*>(o) = raw;
+          *reinterpret_cast<float4*>(o + (size_t)b * ostride) = raw;
         }
       }
       if (!F32 && (pass & 63) == 63) {  // keep the mantissa products far from overflow
@@ -1359,8 +1380,18 @@ struct MuvParams {
 // bases over the two half-warps (lanes l and l ^ 16 share the frame): each
 // forms lambda' over its half and the halves are exchanged by one shuffle
 // (the sum is the same on both lanes), halving the v / num / den registers.
+// fp64 with K <= 10 (BASELINE cfg0 / cfg1): registers capped for four CTAs per
+// SM (128; a few spilled values) and the Newton reciprocal. Measured on cfg1
+// (ms per iteration, tools/muv_ab.sh): IEEE division at 1 / 3 / 4 CTAs per SM
+// 0.413 / 0.384 / 0.446, Newton 0.561 / 0.404 / 0.368 (five CTAs: 1.1, spills).
+#ifndef CTF_MUV_MINB64
+#define CTF_MUV_MINB64 4
+#endif
+// (the other variants: no occupancy target below K = 16, one CTA from there: fp32
+// cfg1 0.218 vs 0.244 ms with the explicit 1, cfg2 1.104 vs 1.136 ms per 32 mixtures)
+template <typename Real, int KMAX> constexpr bool muv_tight() { return sizeof(Real) == 8 && KMAX <= 10; }
 template <typename Real, int KMAX, int KS = 1>
-__global__ void __launch_bounds__(128) muv_partial_kernel(const MuvParams p) {
+__global__ void __launch_bounds__(128, muv_tight<Real, KMAX>() ? CTF_MUV_MINB64 : KMAX >= 16 ? 1 : 0) muv_partial_kernel(const MuvParams p) {
   constexpr int G = 8;
   constexpr int KPT = KMAX / KS;  // bases per thread
   static_assert(KS == 1 || (KS == 2 && KMAX % 2 == 0), "k split");
@@ -1426,9 +1457,10 @@ __global__ void __launch_bounds__(128) muv_partial_kernel(const MuvParams p) {
         la += __shfl_xor_sync(kFull, la, 16);
         lb += __shfl_xor_sync(kFull, lb, 16);
       }
-      // (the MUFU form measured faster at K = 20, slower at K = 10)
-      const Real ila = KMAX >= 16 ? rcp_fast(fmax(la, floor_abs)) : rcp_rn(fmax(la, floor_abs));
-      const Real ilb = KMAX >= 16 ? rcp_fast(fmax(lb, floor_abs)) : rcp_rn(fmax(lb, floor_abs));
+      // (fp32: the MUFU form measured faster at K = 20, slower at K = 10)
+      constexpr bool NR = muv_tight<Real, KMAX>() || (sizeof(Real) == 4 && KMAX >= 16);
+      const Real ila = NR ? rcp_muv(fmax(la, floor_abs)) : rcp_rn(fmax(la, floor_abs));
+      const Real ilb = NR ? rcp_muv(fmax(lb, floor_abs)) : rcp_rn(fmax(lb, floor_abs));
       const Real ana = ecur[u] * (ila * ila), bna = ila * cnt;
       const Real anb = ecur[u + 1] * (ilb * ilb), bnb = ilb * cnt;
 #pragma unroll
