@@ -974,7 +974,49 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L, FT>())
     }
   };
   double logdet = p.logdet[tile] - s_logmu;
-  if (p.has_prev) {
+  // Narrow ISS tiles (CTF_GRAM_CHAIN): the steps below run without a CTA
+  // barrier per step: every pivot has its own buffer (R x (D + LT1), in the
+  // Gram partial region, free between the Gram reduction and the |y|^2 rows)
+  // and its own mbarrier. The objective / conditioning phase, the first
+  // pivot's publish and the mbarrier initialisation share ONE barrier.
+  constexpr bool CHAIN = !WIDE && !IP && CTF_GRAM_CHAIN;
+  constexpr int PV = D + LT1;
+  R2* piv = CHAIN ? reinterpret_cast<R2*>(smem + p.off_e) : zs;  // !CHAIN: 2 x PV, double-buffered by step parity
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(piv + R * PV);
+  if constexpr (CHAIN) {
+    if (p.has_prev || p.fb_mode == 1) {
+      // quadratic term of the previous iteration's objective (estimator.cpp:55-77):
+      // sum_r w_r^T C_r conj(w_r) of the rescaled W under the new lambda
+      Real nre, nim, den;
+      const int rr = rowvk[0] ? rowk[0] : 0;
+      row_sums(0, Wb + rr, R, Yt + rr * LT1, nre, nim, den);
+      if (p.has_prev && hl == 0 && rowvk[0]) red[rowk[0]] = den;
+      cond_check(0, rr, den);
+    }
+    if (p.has_prev) {
+      const double ws = warp_sum(logsum);
+      if (lane == 0) dred[warp] = ws;
+    }
+    if (rowk[0] == 0) {  // pivot 0 (published even when the CTA returns below)
+      if (hl < D) piv[hl] = wreg[0];
+      if (hl < LT1) piv[D + hl] = yreg[0];
+    }
+    if (tid < R) tc::mbar_init(&mbar[tid], 1);
+    __syncthreads();
+    if (p.has_prev) {
+      const int det_status = isnan(logdet) || logdet == -INFINITY ? 4 : (logdet < log(1e-300) ? 5 : 0);
+      if (det_status) {  // estimator.cpp:45-51
+        if (tid == 0) record_err<Real>(p.err, mix, err_key(prev_it, kPhDet, gbin, 0, det_status));
+        return;
+      }
+      if (tid == 0) {
+        double quad = 0.0, ls = 0.0;
+        for (int r = 0; r < R; ++r) quad += (double)red[r];
+        for (int w = 0; w < NW; ++w) ls += dred[w];
+        p.objbin[tile] = ls + quad - 2.0 * (double)T * logdet;
+      }
+    }
+  } else if (p.has_prev) {
     // objective of the previous iteration (estimator.cpp:55-77): quadratic
     // term sum_r w_r^T C_r conj(w_r) of the rescaled W under the new lambda
 #pragma unroll
@@ -1105,25 +1147,20 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L, FT>())
     __syncthreads();
   } else {
   // ---- R covariance-domain ISS steps (estimator.cpp:556-579, 275-302)
-  // Narrow tiles (CTF_GRAM_CHAIN): no CTA barrier per step. Every pivot has its
-  // own buffer (R x (D + LT1), in the Gram partial region, free between the
-  // Gram reduction and the |y|^2 rows) and its own mbarrier: the half-warp of
-  // row r + 1 publishes its updated row as soon as its step-r update is done
-  // and arrives; the warps wait only on the pivot they are about to read. The
-  // pivot's own scale (a division and a square root) runs after the publish, so
-  // the dependent chain of the sweep is load -> matvec -> reduce -> one
-  // reciprocal -> update -> publish per step.
-  constexpr bool CHAIN = !WIDE && CTF_GRAM_CHAIN;
-  R2* piv = CHAIN ? reinterpret_cast<R2*>(smem + p.off_e) : zs;  // !CHAIN: 2 x (D + LT1), double-buffered by step parity
+  // CHAIN: the half-warp of row r + 1 publishes its updated row as soon as its
+  // step-r update is done and arrives on that pivot's mbarrier; the warps wait
+  // only on the pivot they are about to read. The pivot's own scale (a division
+  // and a square root) runs after the publish, so the dependent chain of the
+  // sweep is load -> matvec -> reduce -> one reciprocal -> update -> publish per
+  // step. (Pivot 0 and the mbarriers: set up before the barrier above.)
   Real* fac = fac_s;  // (1 - z_r) per row, multiplied in row order at the end
-  constexpr int PV = D + LT1;
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(piv + R * PV);
-  if (rowk[0] == 0) {
-    if (hl < D) piv[hl] = wreg[0];
-    if (hl < LT1) piv[D + hl] = yreg[0];
+  if constexpr (!CHAIN) {
+    if (rowk[0] == 0) {
+      if (hl < D) piv[hl] = wreg[0];
+      if (hl < LT1) piv[D + hl] = yreg[0];
+    }
+    __syncthreads();
   }
-  if (CHAIN && tid < R) tc::mbar_init(&mbar[tid], 1);
-  __syncthreads();
   CTF_PHASE(5);
   const bool wrows = (tid / 32) * (32 / LPR) < R;  // warp-uniform: this warp owns at least one row
   if constexpr (CHAIN) {
