@@ -98,7 +98,12 @@ struct SweepParams {
 
 // L2 prefetch of a contiguous block (bulk async, no registers or smem).
 __device__ __forceinline__ void prefetch_l2(const void* ptr, unsigned bytes) {
-  bytes &= ~15u;
+  // the bulk prefetch wants a 16-byte aligned address and size: start at the
+  // aligned address below (a tile of an odd number of complex64 values, e.g.
+  // W at R = D = 9, starts 8 bytes off on every other bin)
+  const unsigned off = (unsigned)(reinterpret_cast<uintptr_t>(ptr) & 15u);
+  ptr = reinterpret_cast<const unsigned char*>(ptr) - off;
+  bytes = (bytes + off) & ~15u;
   if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
 }
 // The CTAs resident after this one start roughly pf_stride work items later:
@@ -1390,8 +1395,21 @@ struct MuvParams {
 // (the other variants: no occupancy target below K = 16, one CTA from there: fp32
 // cfg1 0.218 vs 0.244 ms with the explicit 1, cfg2 1.104 vs 1.136 ms per 32 mixtures)
 template <typename Real, int KMAX> constexpr bool muv_tight() { return sizeof(Real) == 8 && KMAX <= 10; }
+// fp32, K < 16 (cfg0 / cfg1), measured on cfg1 (MU ms per iteration, tools/muv_ab.sh): unguarded
+// clamped E loads + MUFU reciprocal + registers capped for four CTAs per SM 0.189; without
+// the clamp 0.291, with the exact reciprocal 0.257, without the cap (134 registers) 0.320;
+// all three off (the previous kernel, 108 registers) 0.217. fp64: 0.367 -> 0.363.
+#ifndef CTF_MUV_MINB32  // fp32, K < 16: resident CTAs per SM the register allocation aims at (0: none)
+#define CTF_MUV_MINB32 4
+#endif
+#ifndef CTF_MUV_ECLAMP
+#define CTF_MUV_ECLAMP 1
+#endif
+#ifndef CTF_MUV_RCPF32
+#define CTF_MUV_RCPF32 1
+#endif
 template <typename Real, int KMAX, int KS = 1>
-__global__ void __launch_bounds__(128, muv_tight<Real, KMAX>() ? CTF_MUV_MINB64 : KMAX >= 16 ? 1 : 0) muv_partial_kernel(const MuvParams p) {
+__global__ void __launch_bounds__(128, muv_tight<Real, KMAX>() ? CTF_MUV_MINB64 : KMAX >= 16 ? 1 : CTF_MUV_MINB32) muv_partial_kernel(const MuvParams p) {
   constexpr int G = 8;
   constexpr int KPT = KMAX / KS;  // bases per thread
   static_assert(KS == 1 || (KS == 2 && KMAX % 2 == 0), "k split");
@@ -1406,6 +1424,7 @@ __global__ void __launch_bounds__(128, muv_tight<Real, KMAX>() ? CTF_MUV_MINB64 
   extern __shared__ __align__(16) unsigned char smem[];
   Real* Bsh = reinterpret_cast<Real*>(smem);  // [k][bin] (bins padded to nbp)
   const Real* Bg = reinterpret_cast<const Real*>(p.Bf) + (size_t)mix * p.FL * p.SK;
+  // (a warp per bin reading its K consecutive bases measured slower: cfg1 MU 0.238 vs 0.189 ms fp32)
   for (int e = threadIdx.x; e < KMAX * nbp; e += blockDim.x) {
     const int k = e / nbp, i = e - k * nbp;
     Bsh[e] = (k < K && i < nb) ? Bg[(size_t)(i0 + i) * p.SK + k0 + k] : Real(0);
@@ -1427,11 +1446,23 @@ __global__ void __launch_bounds__(128, muv_tight<Real, KMAX>() ? CTF_MUV_MINB64 
   const Real* Eg = reinterpret_cast<const Real*>(p.E) + (((size_t)mix * p.N + n) * p.FL) * p.T + tc;
   const Real* Bk = Bsh + kb0 * nbp;
   Real ecur[G], enext[G];
+  // K < 16: unguarded loads: bins past the chunk re-read its last bin (their B
+  // row is zero, so they add exactly 0); a lane past T reads frame 0 and stores
+  // nothing. (K = 20 measured slower that way: cfg2 MU 1.138 vs 1.105 ms.)
+  constexpr bool ECL = CTF_MUV_ECLAMP && KMAX < 16;
+  const Real* Ec = Eg + (size_t)i0 * p.T;
+  const int lastb = nb - 1;
 #pragma unroll
-  for (int u = 0; u < G; ++u) ecur[u] = (valid && u < nb) ? Eg[(size_t)(i0 + u) * p.T] : Real(0);
+  for (int u = 0; u < G; ++u) {
+    if constexpr (ECL) ecur[u] = __ldg(Ec + (size_t)min(u, lastb) * p.T);
+    else ecur[u] = (valid && u < nb) ? Eg[(size_t)(i0 + u) * p.T] : Real(0);
+  }
   for (int g = 0; g < nbp; g += G) {
 #pragma unroll
-    for (int u = 0; u < G; ++u) enext[u] = (valid && g + G + u < nb) ? Eg[(size_t)(i0 + g + G + u) * p.T] : Real(0);
+    for (int u = 0; u < G; ++u) {
+      if constexpr (ECL) enext[u] = __ldg(Ec + (size_t)min(g + G + u, lastb) * p.T);
+      else enext[u] = (valid && g + G + u < nb) ? Eg[(size_t)(i0 + g + G + u) * p.T] : Real(0);
+    }
 #pragma unroll
     for (int u = 0; u < G; u += 2) {
       // keep the B reads of one bin pair from being hoisted across the group
@@ -1458,7 +1489,7 @@ __global__ void __launch_bounds__(128, muv_tight<Real, KMAX>() ? CTF_MUV_MINB64 
         lb += __shfl_xor_sync(kFull, lb, 16);
       }
       // (fp32: the MUFU form measured faster at K = 20, slower at K = 10)
-      constexpr bool NR = muv_tight<Real, KMAX>() || (sizeof(Real) == 4 && KMAX >= 16);
+      constexpr bool NR = muv_tight<Real, KMAX>() || (sizeof(Real) == 4 && (CTF_MUV_RCPF32 || KMAX >= 16));
       const Real ila = NR ? rcp_muv(fmax(la, floor_abs)) : rcp_rn(fmax(la, floor_abs));
       const Real ilb = NR ? rcp_muv(fmax(lb, floor_abs)) : rcp_rn(fmax(lb, floor_abs));
       const Real ana = ecur[u] * (ila * ila), bna = ila * cnt;

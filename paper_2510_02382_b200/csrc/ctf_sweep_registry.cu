@@ -17,6 +17,8 @@ std::vector<SweepVariant> sweep_variants_check_f32();
 std::vector<SweepVariant> sweep_variants_gram_f32();
 std::vector<SweepVariant> sweep_variants_gram_f64();
 std::vector<SweepVariant> sweep_variants_gram_ip();
+std::vector<SweepVariant> sweep_variants_gram_more_f32();
+std::vector<SweepVariant> sweep_variants_gram_more_f64();
 std::vector<SweepVariant> sweep_variants_check_f64();
 std::vector<SweepVariant> sweep_variants_fsplit_f32();
 std::vector<SweepVariant> sweep_variants_ip_frame();
@@ -37,6 +39,8 @@ const std::vector<SweepVariant>& sweep_variants_f32() {
     a.insert(a.end(), ck.begin(), ck.end());
     auto gr = sweep_variants_gram_f32();
     a.insert(a.end(), gr.begin(), gr.end());
+    auto gm = sweep_variants_gram_more_f32();
+    a.insert(a.end(), gm.begin(), gm.end());
     for (const auto& v : sweep_variants_gram_ip())
       if (v.prec == 1) a.push_back(v);
     for (const auto& v : sweep_variants_ip_frame())
@@ -64,6 +68,8 @@ const std::vector<SweepVariant>& sweep_variants_f64() {
     a.insert(a.end(), ck.begin(), ck.end());
     auto gr = sweep_variants_gram_f64();
     a.insert(a.end(), gr.begin(), gr.end());
+    auto gm = sweep_variants_gram_more_f64();
+    a.insert(a.end(), gm.begin(), gm.end());
     for (const auto& v : sweep_variants_gram_ip())
       if (v.prec == 0) a.push_back(v);
     for (const auto& v : sweep_variants_ip_frame())

@@ -150,6 +150,48 @@ def test_fp32_trajectory_cfg_geometries(M, L, T, K, rho):
     assert final <= 1e-3, final
 
 
+@pytest.mark.parametrize("M,L", [(2, 4), (2, 8), (3, 2), (3, 3), (3, 5), (4, 2), (4, 3), (4, 4)])
+@pytest.mark.parametrize("precision,tol", [("f64", 1e-9), ("f32", 1e-4)])
+def test_more_stacked_shapes_on_the_covariance_kernel(M, L, precision, tol):
+    """The additional compiled (mics, taps) pairs of the covariance-domain
+    kernel (ctf_sweep_gram_more.cu, R = M*L <= 16, T <= 1024): every iteration
+    against the oracle's run() (estimator.cpp:513-657) on the stacked
+    observation; fp64 1e-9, fp32 1e-4 relative L2."""
+    F, T, K, iters, seed = 9, 300, 4, 8, 21
+    raw = synth_mixtures(1, F, T, M, M, L, K, 0.6, 400 + 10 * M + L)
+    ref = O.run(O.config([L] * M, [K] * M, iterations=iters, seed=seed, threads=NPROC),
+                O.stack_observation(raw[0], L), history=True)
+    xin = raw if precision == "f64" else raw.astype(np.complex64)
+    s = Session(xin, [L] * M, [K] * M, stack_taps=L, iterations=iters, precision=precision, seed=seed)
+    kern = json.loads(s.describe())["sweep_kernel"]
+    s.close()
+    if not (precision == "f64" and (M, L) == (4, 2)):  # (measured slower there: not compiled in fp64)
+        assert kern.startswith("gram_kernel"), kern
+    hist = gpu_history(xin, [L] * M, [K] * M, iters, precision, seed, L)
+    for it, (W, B, V, obj, _) in enumerate(hist):
+        e = max(rel(W[0], ref["hist_W"][it].reshape(F, -1)), rel(B[0], ref["hist_B"][it]),
+                rel(V[0], ref["hist_V"][it]))
+        eo = abs(obj[0, it] - ref["objective"][it]) / abs(ref["objective"][it])
+        assert max(e, eo if precision == "f64" else 0.0) <= tol, f"{kern} it={it + 1}: {e:.2e} obj {eo:.2e}"
+
+
+def test_odd_tile_sizes_with_the_l2_prefetch_active():
+    """fp32 tiles of an odd number of complex values (W at R = D = 9: 648
+    bytes per bin) start 8 bytes off a 16-byte boundary on every other bin; the
+    L2 prefetch of the tile a resident-CTA-count ahead must not fault (it did:
+    'misaligned address') once the batch has more tiles than resident CTAs."""
+    M, L, F, T, K, B, iters = 3, 3, 129, 200, 4, 8, 2
+    raw = synth_mixtures(B, F, T, M, M, L, K, 0.6, 77).astype(np.complex64)
+    s = Session(raw, [L] * M, [K] * M, stack_taps=L, iterations=iters, precision="f32", seed=3)
+    s.iterate(iters)
+    W, Bf, V, obj = s.download_raw()
+    s.close()
+    assert np.isfinite(W).all() and np.isfinite(obj).all()
+    ref = O.run(O.config([L] * M, [K] * M, iterations=iters, seed=3 + B - 1, threads=NPROC),
+                O.stack_observation(raw[B - 1].astype(np.complex128), L))
+    assert rel(W[B - 1], ref["W"].reshape(F, -1)) <= 1e-4
+
+
 def test_one_step_parity_from_oracle_state():
     """Restart the GPU from the oracle's state after 4 iterations (cfg1 shape,
     reduced F): one GPU iteration equals one oracle iteration (no trajectory
