@@ -173,13 +173,16 @@ template <typename Real, int N, int R> constexpr int gram_nsg() {
 #ifndef CTF_GRAM_MINB64
 #define CTF_GRAM_MINB64 2
 #endif
+#ifndef CTF_GRAM_MINB32  // fp32 short-frame variants at <= 256 threads: CTAs per SM (80 registers at 3)
+#define CTF_GRAM_MINB32 3
+#endif
 // fp32 long-frame variants (FT >= 8, BASELINE cfg2 T = 2000) at 256 threads:
 // two CTAs per SM (EREG energies + one-source partial buffer keep them under
 // half the shared memory)
 template <typename Real> constexpr bool gram_ereg(int FT) { return std::is_same<Real, float>::value && FT >= 8; }
 template <typename Real, int NT, int R, int FT = 4> constexpr int gram_min_blocks() {
   return R > 16 ? 1
-         : std::is_same<Real, float>::value ? (NT <= 256 ? (FT >= 8 ? 2 : 3) : 1)
+         : std::is_same<Real, float>::value ? (NT <= 256 ? (FT >= 8 ? 2 : CTF_GRAM_MINB32) : 1)
                                             : (NT <= 256 ? CTF_GRAM_MINB64 : NT <= 384 ? 2 : 1);
 }
 
