@@ -1130,6 +1130,11 @@ void launch_sweep(ctf_ctx* c, bool do_sweep, int m0, int m1, int k, cudaStream_t
     lc.numAttrs = 1;
     CK(cudaLaunchKernelEx(&lc, c->sv.cfn, cl));
   } else if (c->sv.kind == 5) {
+    if (c->lam_pre) {
+      launch_lambda<Real>(c, m0, m1, st);
+      sp.invl_g = c->invl.p + (size_t)m0 * c->FL * c->N * c->T * c->real_size;
+      sp.logsum_g = c->logsum.p + (size_t)m0 * c->FL;
+    }
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(c->FL * c->cluster_size, nm);
     lc.blockDim = dim3(c->NT);
@@ -1436,8 +1441,8 @@ void setup_impl(ctf_ctx* c, const ctf_problem* prob, const void* x_host,
   c->V.alloc(((size_t)c->B * c->SK * c->T + 4096) * rs);  // zero tail: the sweep reads V up to frame TP
   CK(cudaMemsetAsync(c->V.p, 0, c->V.n, c->stream));
   c->E.alloc((size_t)c->B * c->N * c->FL * c->T * rs);
-  // lambda ahead of the covariance-domain kernel (the variants compiled without a lambda phase)
-  c->lam_pre = c->sv.kind == 4 && c->sv.lpre != 0;
+  // lambda ahead of the covariance-domain / frame-split kernels (the variants compiled without a lambda phase)
+  c->lam_pre = (c->sv.kind == 4 || c->sv.kind == 5) && c->sv.lpre != 0;
   if (c->lam_pre) {
     c->invl.alloc((size_t)c->B * c->FL * c->N * c->T * rs);
     c->logsum.alloc((size_t)c->B * c->FL);

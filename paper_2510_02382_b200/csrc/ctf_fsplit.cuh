@@ -43,6 +43,12 @@
 #ifndef CTF_FS_LAMKB
 #define CTF_FS_LAMKB 20
 #endif
+// 1: 1 / lambda and the objective's log term come from lambda_kernel, run by
+// the host ahead of the kernel (SweepVariant::lpre); 0: the kernel's own
+// lambda phase (dev builds, A/B)
+#ifndef CTF_FS_LPRE
+#define CTF_FS_LPRE 1
+#endif
 namespace ctf {
 
 template <typename Real, int R, int L, int FT, int NT, int CS, int RREG, int RG, bool AG = false, bool PAIR = false>
@@ -330,6 +336,26 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
   CTF_FPHASE(1);
   // ---- lambda = max(B V, floor) -> 1/lambda over the frames j0 - LOFF .. j0 + TC
   double logsum = 0.0;
+  if constexpr (CTF_FS_LPRE != 0) {
+    // computed ahead by lambda_kernel (ctf_kernels.cuh) for the whole bin: this
+    // CTA copies its frame slice with the halo (all loads independent: one L2
+    // round trip instead of K dependent V loads per frame at one CTA per SM);
+    // the objective's log term of the bin goes in through cluster CTA 0
+    const Real* lg = reinterpret_cast<const Real*>(p.invl_g) + tile * (size_t)N * T;
+    constexpr int IT = (N * LP + NT - 1) / NT;
+    Real lv[IT];
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int e = tid + it * NT, n = e / LP, i = e - n * LP, tau = j0 + i - LOFF;
+      lv[it] = (e < N * LP && tau >= 0 && tau < T) ? __ldg(lg + (size_t)n * T + tau) : Real(0);
+    }
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int e = tid + it * NT;
+      if (e < N * LP) invl[e] = lv[it];
+    }
+    if (p.has_prev && c == 0 && tid == 0) logsum = p.logsum_g[tile];
+  } else {
   for (int n = 0; n < N; ++n) {
     const int k0 = p.koff[n], k1 = p.koff[n + 1];
     // ITB of the thread's IT frames x KB columns in flight at once (all IT
@@ -371,6 +397,7 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
         }
       }
     }
+  }
   }
   __syncthreads();
   CTF_FPHASE(2);

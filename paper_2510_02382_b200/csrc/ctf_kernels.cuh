@@ -1399,6 +1399,9 @@ template <typename Real, int KMAX> constexpr bool muv_tight() { return sizeof(Re
 // clamped E loads + MUFU reciprocal + registers capped for four CTAs per SM 0.189; without
 // the clamp 0.291, with the exact reciprocal 0.257, without the cap (134 registers) 0.320;
 // all three off (the previous kernel, 108 registers) 0.217. fp64: 0.367 -> 0.363.
+#ifndef CTF_MUV_G64  // fp64, K <= 10: bins per E prefetch group
+#define CTF_MUV_G64 4  // (cfg1 MU 0.355 vs 0.363 ms at 8; no spills)
+#endif
 #ifndef CTF_MUV_MINB32  // fp32, K < 16: resident CTAs per SM the register allocation aims at (0: none)
 #define CTF_MUV_MINB32 4
 #endif
@@ -1410,7 +1413,7 @@ template <typename Real, int KMAX> constexpr bool muv_tight() { return sizeof(Re
 #endif
 template <typename Real, int KMAX, int KS = 1>
 __global__ void __launch_bounds__(128, muv_tight<Real, KMAX>() ? CTF_MUV_MINB64 : KMAX >= 16 ? 1 : CTF_MUV_MINB32) muv_partial_kernel(const MuvParams p) {
-  constexpr int G = 8;
+  constexpr int G = muv_tight<Real, KMAX>() ? CTF_MUV_G64 : 8;  // bins per E prefetch group
   constexpr int KPT = KMAX / KS;  // bases per thread
   static_assert(KS == 1 || (KS == 2 && KMAX % 2 == 0), "k split");
   const int lane = threadIdx.x & 31, half = KS == 2 ? lane >> 4 : 0;

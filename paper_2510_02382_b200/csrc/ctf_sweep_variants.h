@@ -91,21 +91,21 @@ inline SweepVariant with_lpre(SweepVariant v, bool lpre) {
             gram_lpre<REAL, NT, (M) * (L), FT>())
 // fsplit_kernel: R = M * L stacked rows, frames split over a cluster of CS CTAs
 #define CTF_FS(REAL, PREC, R, L, FT, NT, CS, RREG, RG, MINB)                                               \
-  SweepVariant {                                                                                         \
+  with_lpre(SweepVariant {                                                                                         \
     PREC, R, FT, RREG, NT, 1, fsplit_kernel<REAL, R, L, FT, NT, CS, RREG, RG, MINB>, 5, L, nullptr, nullptr, 0, \
         nullptr, 0, CS, &FsplitLayout<REAL, R, L, FT, NT, CS, RREG, RG>::bytes                             \
-  }
+  }, CTF_FS_LPRE != 0)
 #define CTF_FSA(REAL, PREC, R, L, FT, NT, CS, RREG, RG, MINB)                                                  \
-  SweepVariant {                                                                                                \
+  with_lpre(SweepVariant {                                                                                                \
     PREC, R, FT, RREG, NT, 1, fsplit_kernel<REAL, R, L, FT, NT, CS, RREG, RG, MINB, true>, 5, L, nullptr, nullptr, 0, \
         nullptr, 0, CS, &FsplitLayout<REAL, R, L, FT, NT, CS, RREG, RG, true>::bytes, 1                         \
-  }
+  }, CTF_FS_LPRE != 0)
 // frame-split, all-gather, two ISS steps per pass / exchange (step pairs)
 #define CTF_FSP(REAL, PREC, R, L, FT, NT, CS, RREG, RG, MINB)                                                       \
-  SweepVariant {                                                                                                    \
+  with_lpre(SweepVariant {                                                                                                    \
     PREC, R, FT, RREG, NT, 1, fsplit_kernel<REAL, R, L, FT, NT, CS, RREG, RG, MINB, true, true>, 5, L, nullptr,       \
         nullptr, 0, nullptr, 0, CS, &FsplitLayout<REAL, R, L, FT, NT, CS, RREG, RG, true, true>::bytes, 1, 0, 1      \
-  }
+  }, CTF_FS_LPRE != 0)
 // rowwarp_kernel: R = NT / (32 * WPR) rows, FT frames per lane
 #define CTF_RW(REAL, PREC, FT, WPR, NT) \
   SweepVariant { PREC, (NT) / (32 * (WPR)), FT, WPR, NT, 1, rowwarp_kernel<REAL, FT, WPR, NT>, 1, 0 }
