@@ -1075,6 +1075,32 @@ void launch_lambda(ctf_ctx* c, int m0, int m1, cudaStream_t st) {
   c->timing.launches += 1;
 }
 
+// MU-B of mixtures [m0, m1) after an iteration kernel compiled without it
+// (SweepVariant::mubout): B <- max(B sqrt(num / den), floor) from E and 1/lambda.
+template <class Real>
+void launch_mub(ctf_ctx* c, int m0, int m1, cudaStream_t st) {
+  ctf::MubParams mp{};
+  const size_t mz = (size_t)m0, rs = c->real_size;
+  mp.Bf = c->Bf.p + mz * c->FL * c->SK * rs;
+  mp.V = c->V.p + mz * c->SK * c->T * rs;
+  mp.E = c->E.p + mz * c->N * c->FL * c->T * rs;
+  mp.invl = c->invl.p + mz * c->FL * c->N * c->T * rs;
+  mp.floor_abs = c->floor_abs.p + mz;
+  mp.err = c->err.p + mz;
+  mp.FL = c->FL;
+  mp.T = c->T;
+  mp.N = c->N;
+  mp.SK = c->SK;
+  for (int n = 0; n <= c->N; ++n) mp.koff[n] = c->koff[n];
+  for (int n = 0; n < c->N; ++n) mp.ntaps[n] = c->taps[n];
+  constexpr int VEC = 16 / (int)sizeof(Real);
+  const dim3 grid((c->FL + 7) / 8, c->N, m1 - m0);
+  if (c->T % VEC == 0) ctf::mub_kernel<Real, VEC><<<grid, 256, 0, st>>>(mp);
+  else ctf::mub_kernel<Real, 1><<<grid, 256, 0, st>>>(mp);
+  CK(cudaGetLastError());
+  c->timing.launches += 1;
+}
+
 template <class Real>
 void launch_sweep(ctf_ctx* c, bool do_sweep, int m0, int m1, int k, cudaStream_t st) {
   ctf::SweepParams sp = c->sp;
@@ -1148,6 +1174,7 @@ void launch_sweep(ctf_ctx* c, bool do_sweep, int m0, int m1, int k, cudaStream_t
     lc.attrs = at;
     lc.numAttrs = 1;
     CK(cudaLaunchKernelEx(&lc, c->sv.fn, sp));
+    if (do_sweep && c->lam_pre && c->sv.mubout) launch_mub<Real>(c, m0, m1, st);
   } else if (c->sv.kind == 2) {  // persistent over all work items (never chunked)
     ctf::StreamParams stp{};
     stp.s = sp;

@@ -49,6 +49,11 @@
 #ifndef CTF_FS_LPRE
 #define CTF_FS_LPRE 1
 #endif
+// 1: MU-B runs in mub_kernel after this kernel (needs CTF_FS_LPRE: 1/lambda in
+// HBM; SweepVariant::mubout tells the host); 0: the in-kernel MU-B passes
+#ifndef CTF_FS_MUBOUT
+#define CTF_FS_MUBOUT 1
+#endif
 namespace ctf {
 
 template <typename Real, int R, int L, int FT, int NT, int CS, int RREG, int RG, bool AG = false, bool PAIR = false>
@@ -203,6 +208,7 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
   static_assert(!PAIR || (AG && R % 2 == 0 && std::is_same<Real, float>::value),
                 "step pairs: all-gather exchange, even R, fp32");
   constexpr int N = LY::M, M = LY::M, NW = LY::NW, TC = LY::TC, XP = LY::XP, XOFF = LY::XOFF;
+  constexpr bool MUBOUT = CTF_FS_LPRE != 0 && CTF_FS_MUBOUT != 0;
   constexpr int LP = LY::LP, LOFF = LY::LOFF, RC = LY::RC, DC = LY::DC, NG = LY::NG, VP = LY::VP;
   constexpr int VM = VP / 32, HL = LY::HL, CH = LY::CH, RS = R - RREG;
   static_assert(R % L == 0 && R <= 64 && R >= CS && RREG <= R, "stacked equal-taps tiles, one owner per row");
@@ -1025,6 +1031,9 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
   });
 
   // MU-B partials (estimator.cpp:313-346) over the own frames, 16 bases per pass
+  // (CTF_FS_MUBOUT: left to mub_kernel, which runs after this kernel on E and
+  // 1/lambda from HBM; this kernel then writes back the rescaled B)
+  if constexpr (!MUBOUT)
   for (int n = 0; n < N; ++n) {
     const int k0 = p.koff[n], k1 = p.koff[n + 1];
     const Real* il = invl + n * LP + LOFF;
@@ -1090,7 +1099,8 @@ __global__ void __launch_bounds__(NT, MINB) fsplit_kernel(const SweepParams p) {
         num += dsmem_ld_f64(dsmem_map(smem_u32addr(exmub + 2 * k), (uint32_t)q));
         den += dsmem_ld_f64(dsmem_map(smem_u32addr(exmub + 2 * k + 1), (uint32_t)q));
       }
-      Bg[k] = fmax(Bs[k] * (Real)sqrt(num / den), floor_abs);
+      if constexpr (MUBOUT) Bg[k] = Bs[k];
+      else Bg[k] = fmax(Bs[k] * (Real)sqrt(num / den), floor_abs);
     }
     for (int row = tid; row < R; row += NT) {
       double s = 0.0;

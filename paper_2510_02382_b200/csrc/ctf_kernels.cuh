@@ -1364,6 +1364,99 @@ __global__ void __launch_bounds__(256) lambda_kernel(const LambdaParams p) {
 }
 
 // ---------------------------------------------------------------------------
+// MU-B (estimator.cpp:313-346) outside the iteration kernel, for the kernels
+// that run at one CTA per SM (the frame-split cluster kernel): there the
+// K x T dependent V loads of the in-kernel MU-B passes are fully exposed (10 %
+// of cfg3's kernel), while E and 1/lambda already sit in HBM (lambda ahead).
+// One warp per (mixture, source, bin): the lanes stride over the frames (VEC
+// consecutive frames per lane, 16-byte loads of E, 1/lambda and the V rows,
+// which the warps of a CTA share through L1), KW bases per pass
+// (numerators at [0, KW), denominators at [16, 16 + KW) of the 32 values of a
+// warp reduce-scatter), then B <- max(B sqrt(num / den), floor) on the
+// rescaled B the iteration kernel left in place.
+struct MubParams {
+  void* Bf;                 // Real [mix][FL][SK], rescaled, updated in place
+  const void* V;            // Real [mix][SK][T]
+  const void* E;            // Real [mix][N][FL][T]
+  const void* invl;         // Real [mix][FL][N][T]
+  const double* floor_abs;  // [mix]
+  const unsigned long long* err;  // [mix] error words (all ones: none): a failed mixture is left alone
+  int FL, T, N, SK;
+  int koff[kMaxSources + 1], ntaps[kMaxSources];
+};
+
+template <typename Real, int VEC>
+__global__ void __launch_bounds__(256) mub_kernel(const MubParams p) {
+  constexpr int PV = 16 / (int)sizeof(Real);
+  static_assert(VEC == 1 || VEC == PV, "one 16-byte vector of frames per lane, or one frame");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int bin = blockIdx.x * (blockDim.x >> 5) + warp, n = blockIdx.y, mix = blockIdx.z;
+  if (bin >= p.FL || p.err[mix] != ~0ull) return;
+  const int T = p.T, k0 = p.koff[n], k1 = p.koff[n + 1], Ln = p.ntaps[n];
+  const Real floor_abs = (Real)p.floor_abs[mix];
+  const Real* Eg = reinterpret_cast<const Real*>(p.E) + (((size_t)mix * p.N + n) * p.FL + bin) * T;
+  const Real* Il = reinterpret_cast<const Real*>(p.invl) + (((size_t)mix * p.FL + bin) * p.N + n) * T;
+  const Real* Vg = reinterpret_cast<const Real*>(p.V) + (size_t)mix * p.SK * T;
+  Real* Bg = reinterpret_cast<Real*>(p.Bf) + ((size_t)mix * p.FL + bin) * p.SK;
+  auto pass = [&](auto kw) {
+    constexpr int KW = decltype(kw)::value;
+    for (int kb = k0; kb < k1; kb += KW) {
+      Real a[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) a[i] = Real(0);
+      for (int t0 = lane * VEC; t0 < T; t0 += 32 * VEC) {
+        Real e[VEC], il[VEC];
+        if constexpr (VEC == 1) {
+          e[0] = __ldg(Eg + t0);
+          il[0] = __ldg(Il + t0);
+        } else {
+          const float4 er = __ldg(reinterpret_cast<const float4*>(Eg + t0));
+          const float4 ir = __ldg(reinterpret_cast<const float4*>(Il + t0));
+#pragma unroll
+          for (int i = 0; i < VEC; ++i) {
+            e[i] = reinterpret_cast<const Real*>(&er)[i];
+            il[i] = reinterpret_cast<const Real*>(&ir)[i];
+          }
+        }
+        Real an[VEC], bn[VEC];
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) {
+          an[i] = e[i] * (il[i] * il[i]);
+          bn[i] = il[i] * (Real)min(Ln, T - t0 - i);
+        }
+#pragma unroll
+        for (int q = 0; q < KW; ++q) {
+          const Real* vr = Vg + (size_t)min(kb + q, k1 - 1) * T + t0;
+          Real v[VEC];
+          if constexpr (VEC == 1) {
+            v[0] = __ldg(vr);
+          } else {
+            const float4 raw = __ldg(reinterpret_cast<const float4*>(vr));
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) v[i] = reinterpret_cast<const Real*>(&raw)[i];
+          }
+#pragma unroll
+          for (int i = 0; i < VEC; ++i) {
+            a[q] = fma(an[i], v[i], a[q]);
+            a[16 + q] = fma(bn[i], v[i], a[16 + q]);
+          }
+        }
+      }
+      warp_reduce_scatter(a, lane);  // lane i holds the warp's sum of value i
+      const Real den = __shfl_sync(kFull, a[0], (lane + 16) & 31);
+      if (lane < KW && kb + lane < k1) {
+        const Real b = Bg[kb + lane];
+        Bg[kb + lane] = fmax(b * (Real)sqrt((double)a[0] / (double)den), floor_abs);
+      }
+    }
+  };
+  if ((k1 - k0) % 10 == 0)
+    pass(std::integral_constant<int, 10>{});
+  else
+    pass(std::integral_constant<int, 16>{});
+}
+
+// ---------------------------------------------------------------------------
 // MU-V (estimator.cpp:348-382): partial numerator/denominator over a chunk
 // of this rank's bins, for one source and a tile of frames. lambda' is
 // recomputed with the updated bases; all taps contribute (:356-368).

@@ -31,10 +31,12 @@ struct SweepVariant {
   int ag = 0;   // kind 5: all-gather exchange (every CTA derives every z)
   int tc = 0;   // kind 4: tensor-core (tcgen05) Gram
   int pair = 0; // kind 5: two ISS steps per pass and exchange (all-gather only)
-  int lpre = 0; // kind 4: compiled without its own lambda phase (the host runs lambda_kernel ahead)
+  int lpre = 0; // kinds 4, 5: compiled without its own lambda phase (the host runs lambda_kernel ahead)
+  int mubout = 0; // kind 5: compiled without MU-B (the host runs mub_kernel after it)
 };
-inline SweepVariant with_lpre(SweepVariant v, bool lpre) {
+inline SweepVariant with_lpre(SweepVariant v, bool lpre, bool mubout = false) {
   v.lpre = lpre ? 1 : 0;
+  v.mubout = mubout ? 1 : 0;
   return v;
 }
 #define CTF_V(REAL, PREC, RMAX, FT, RREG, NT, EX) \
@@ -94,18 +96,18 @@ inline SweepVariant with_lpre(SweepVariant v, bool lpre) {
   with_lpre(SweepVariant {                                                                                         \
     PREC, R, FT, RREG, NT, 1, fsplit_kernel<REAL, R, L, FT, NT, CS, RREG, RG, MINB>, 5, L, nullptr, nullptr, 0, \
         nullptr, 0, CS, &FsplitLayout<REAL, R, L, FT, NT, CS, RREG, RG>::bytes                             \
-  }, CTF_FS_LPRE != 0)
+  }, CTF_FS_LPRE != 0, CTF_FS_LPRE != 0 && CTF_FS_MUBOUT != 0)
 #define CTF_FSA(REAL, PREC, R, L, FT, NT, CS, RREG, RG, MINB)                                                  \
   with_lpre(SweepVariant {                                                                                                \
     PREC, R, FT, RREG, NT, 1, fsplit_kernel<REAL, R, L, FT, NT, CS, RREG, RG, MINB, true>, 5, L, nullptr, nullptr, 0, \
         nullptr, 0, CS, &FsplitLayout<REAL, R, L, FT, NT, CS, RREG, RG, true>::bytes, 1                         \
-  }, CTF_FS_LPRE != 0)
+  }, CTF_FS_LPRE != 0, CTF_FS_LPRE != 0 && CTF_FS_MUBOUT != 0)
 // frame-split, all-gather, two ISS steps per pass / exchange (step pairs)
 #define CTF_FSP(REAL, PREC, R, L, FT, NT, CS, RREG, RG, MINB)                                                       \
   with_lpre(SweepVariant {                                                                                                    \
     PREC, R, FT, RREG, NT, 1, fsplit_kernel<REAL, R, L, FT, NT, CS, RREG, RG, MINB, true, true>, 5, L, nullptr,       \
         nullptr, 0, nullptr, 0, CS, &FsplitLayout<REAL, R, L, FT, NT, CS, RREG, RG, true, true>::bytes, 1, 0, 1      \
-  }, CTF_FS_LPRE != 0)
+  }, CTF_FS_LPRE != 0, CTF_FS_LPRE != 0 && CTF_FS_MUBOUT != 0)
 // rowwarp_kernel: R = NT / (32 * WPR) rows, FT frames per lane
 #define CTF_RW(REAL, PREC, FT, WPR, NT) \
   SweepVariant { PREC, (NT) / (32 * (WPR)), FT, WPR, NT, 1, rowwarp_kernel<REAL, FT, WPR, NT>, 1, 0 }
