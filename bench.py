@@ -392,8 +392,9 @@ def main():
                             "bytes_per_tfbin": bpt, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"}}
         if desc.get("lambda_ahead"):
             roofline["kernel_ms_note"] = ("event-timed sweep phase of one iteration: lambda_kernel (1/lambda and the "
-                                          "objective's log term, ahead) + the covariance-domain kernel; traffic is "
-                                          "the sum of both kernels' DRAM bytes")
+                                          "objective's log term, ahead) + the iteration kernel (+ mub_kernel, MU-B "
+                                          "after the frame-split cluster kernel); traffic, where given, is the sum "
+                                          "of lambda_kernel's and the iteration kernel's DRAM bytes")
         out = {"value": value, "ms_per_step": ms / args.steps, "roofline": roofline, "inputs": inputs,
                "gpu_launches": int(timing.launches), "clocks": clk.summary(),
                "kernels": {"sweep_ms_per_iteration": sweep_ms, "mu_ms_per_iteration": timing.mu_ms / args.steps,
