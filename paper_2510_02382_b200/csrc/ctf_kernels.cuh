@@ -1385,9 +1385,15 @@ struct MubParams {
   int koff[kMaxSources + 1], ntaps[kMaxSources];
 };
 
+#ifndef CTF_MUB_UNROLL  // frame-loop iterations in flight per lane
+#define CTF_MUB_UNROLL 1  // (2 and 4 measured slower on cfg3: 37.31 / 37.51 vs 37.05 ms per 16 mixtures)
+#endif
+#ifndef CTF_MUB_MINB
+#define CTF_MUB_MINB 2
+#endif
 template <typename Real, int VEC>
-__global__ void __launch_bounds__(256) mub_kernel(const MubParams p) {
-  constexpr int PV = 16 / (int)sizeof(Real);
+__global__ void __launch_bounds__(256, CTF_MUB_MINB) mub_kernel(const MubParams p) {
+  constexpr int PV = 16 / (int)sizeof(Real), UNR = CTF_MUB_UNROLL;
   static_assert(VEC == 1 || VEC == PV, "one 16-byte vector of frames per lane, or one frame");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int bin = blockIdx.x * (blockDim.x >> 5) + warp, n = blockIdx.y, mix = blockIdx.z;
@@ -1404,6 +1410,7 @@ __global__ void __launch_bounds__(256) mub_kernel(const MubParams p) {
       Real a[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) a[i] = Real(0);
+#pragma unroll UNR
       for (int t0 = lane * VEC; t0 < T; t0 += 32 * VEC) {
         Real e[VEC], il[VEC];
         if constexpr (VEC == 1) {
