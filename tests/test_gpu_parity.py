@@ -634,6 +634,35 @@ def test_odd_shapes(case):
     assert np.max(np.abs(obj[0] - ref["objective"]) / np.abs(ref["objective"])) <= tol
 
 
+@pytest.mark.parametrize("M,L,T,K,prec,kernel", [
+    (2, 5, 201, 4, "f64", "gram_kernel"),     # T odd: lambda_kernel one frame per thread, scalar 1/lambda copy
+    (3, 4, 1030, 5, "f32", "gram_kernel"),    # the T > 1024 fp32 variant (two CTAs per SM), T % 4 == 2
+    (4, 8, 998, 5, "f32", "fsplit_kernel"),   # frame-split + lambda_kernel + mub_kernel, T % 4 == 2
+])
+def test_lambda_ahead_unaligned_frame_counts(M, L, T, K, prec, kernel):
+    """The kernels that take 1/lambda from lambda_kernel (and, frame-split, leave
+    MU-B to mub_kernel) on frame counts that rule out the 16-byte vector paths:
+    every iteration against the oracle (compute_psd model.cpp:210-215, MU-B
+    estimator.cpp:313-346, objective :55-77)."""
+    F, iters, seed = 5, 4, 9
+    tol = 1e-9 if prec == "f64" else 1e-4
+    raw = synth_mixtures(2, F, T, M, M, L, K, 0.6, 900 + T)
+    xin = raw if prec == "f64" else raw.astype(np.complex64)
+    s = Session(xin, [L] * M, [K] * M, stack_taps=L, iterations=iters, precision=prec, seed=seed)
+    d = json.loads(s.describe())
+    s.close()
+    assert d["sweep_kernel"].startswith(kernel) and d["lambda_ahead"], d
+    hist = gpu_history(xin, [L] * M, [K] * M, iters, prec, seed, L)
+    for b in range(2):
+        ref = O.run(O.config([L] * M, [K] * M, iterations=iters, seed=seed + b, threads=NPROC),
+                    O.stack_observation(raw[b], L), history=True)
+        for it, (W, B, V, obj, _) in enumerate(hist):
+            e = max(rel(W[b], ref["hist_W"][it].reshape(F, -1)), rel(B[b], ref["hist_B"][it]),
+                    rel(V[b], ref["hist_V"][it]))
+            eo = abs(obj[b, it] - ref["objective"][it]) / abs(ref["objective"][it])
+            assert e <= tol and eo <= (tol if prec == "f64" else 1e-3), f"mixture {b} it={it + 1}: {e:.2e} obj {eo:.2e}"
+
+
 @pytest.mark.parametrize("B,iters,precision", [(3, 5, "f64"), (9, 2, "f64"), (11, 6, "f32"), (2, 1, "f32")])
 def test_ctf_run_end_to_end_matches_device_resident_path(B, iters, precision):
     """ctf_run (host buffers in, host buffers out) == setup + iterate + download,
