@@ -1187,8 +1187,8 @@ __device__ __forceinline__ double log_fast(double x) { return log(x); }
 // next to its x tile instead of running K dependent V loads per frame), and
 // the log term of the previous iteration's objective (estimator.cpp:55-77),
 // sum_n sum_t min(L_n, T - t) log lambda_n(t) per bin. lambda is formed in the
-// same fma order as everywhere else; fp64 divides exactly, fp32 takes the
-// MUFU reciprocal with one Newton step (~1 ulp). fp64 takes one log per group
+// same fma order as everywhere else; the reciprocal is the MUFU seed with one
+// (fp32) or two (fp64) Newton steps, ~1 ulp. fp64 takes one log per group
 // of equally weighted frames: log prod(mantissas) + ln 2 sum(exponents).
 struct LambdaParams {
   const void* Bf;           // Real [mix][FL][SK] (before the pending rescale)
@@ -1201,7 +1201,13 @@ struct LambdaParams {
   int koff[kMaxSources + 1], ntaps[kMaxSources], row0[kMaxSources];
 };
 
-constexpr int kLambdaBins = 8;  // bins per CTA (they share the V loads)
+#ifndef CTF_LAM_RCPNR  // fp64: Newton reciprocal (rcp_muv, ~1 ulp) instead of the IEEE division:
+#define CTF_LAM_RCPNR 1  // lambda_kernel 0.403 -> 0.377 ms in the stream on cfg1 (16 bins per CTA: 0.905, 4: 0.401)
+#endif
+#ifndef CTF_LAM_BINS
+#define CTF_LAM_BINS 8
+#endif
+constexpr int kLambdaBins = CTF_LAM_BINS;  // bins per CTA (they share the V loads)
 template <typename Real, int KMAX, int VEC>
 __global__ void __launch_bounds__(256) lambda_kernel(const LambdaParams p) {
   constexpr int BB = kLambdaBins, NT = 256, KP = (KMAX + 3) / 4 * 4, PV = 16 / (int)sizeof(Real);
@@ -1298,7 +1304,8 @@ __global__ void __launch_bounds__(256) lambda_kernel(const LambdaParams p) {
 #pragma unroll
         for (int i = 0; i < VEC; ++i) {
           lam[i] = lam[i] > floor_abs ? lam[i] : floor_abs;  // = fmax (a NaN takes the floor)
-          il[i] = rcp_fast(lam[i]);  // fp32: MUFU + one Newton step (~1 ulp); fp64: exact
+          // fp32: MUFU + one Newton step (~1 ulp); fp64: MUFU.RCP64H + two Newton steps (~1 ulp)
+          il[i] = CTF_LAM_RCPNR ? rcp_muv(lam[i]) : rcp_fast(lam[i]);
         }
         if (lmode == 1) {
           if constexpr (F32) {
