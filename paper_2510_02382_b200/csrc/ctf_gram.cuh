@@ -34,6 +34,15 @@
 #ifndef CTF_LAMV
 #define CTF_LAMV 20
 #endif
+#ifndef CTF_GRAM_RCPNR  // fp64 chained steps: Newton reciprocal (~1 ulp, 5 dependent operations) for z = num / den
+#define CTF_GRAM_RCPNR 1
+#endif
+#ifndef CTF_GRAM_RCPNR32  // the same in fp32: MUFU + one Newton step instead of __frcp_rn
+#define CTF_GRAM_RCPNR32 1
+#endif
+#ifndef CTF_GRAM_SPIN  // 1: poll the pivot's mbarrier (test_wait) instead of the suspending try_wait
+#define CTF_GRAM_SPIN 0
+#endif
 #ifndef CTF_GRAM_CHAIN  // 1: mbarrier-chained ISS steps on the narrow tiles (0: one CTA barrier per step)
 #define CTF_GRAM_CHAIN 1
 #endif
@@ -1171,7 +1180,10 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L, FT>())
       const int row = rowk[0];
       for (int r = 0; r < R; ++r) {
         const R2* pv = piv + r * PV;
-        if (r > 0) tc::mbar_wait(&mbar[r], 0);
+        if (r > 0) {
+          if constexpr (CTF_GRAM_SPIN != 0) tc::mbar_spin(&mbar[r], 0);
+          else tc::mbar_wait(&mbar[r], 0);
+        }
         Real nre, nim, den;
         row_sums(0, pv, 1, pv + D, nre, nim, den);
         const bool ok = rowvk[0] && den > Real(0) && isfinite(den);  // estimator.cpp:451-454
@@ -1180,8 +1192,9 @@ __global__ void __launch_bounds__(NT, gram_min_blocks<Real, NT, M * L, FT>())
         z.x = z.y = Real(0);
         if (ok && row != r) {  // every row but the pivot first: the next pivot is among them
           Real inv;
-          if constexpr (F32) inv = __frcp_rn(den);
-          else inv = 1.0 / den;
+          // (on the dependent chain of every step)
+          if constexpr (F32) inv = CTF_GRAM_RCPNR32 ? rcp_fast(den) : __frcp_rn(den);
+          else inv = CTF_GRAM_RCPNR ? rcp_muv(den) : 1.0 / den;
           z.x = nre * inv;
           z.y = nim * inv;
         }

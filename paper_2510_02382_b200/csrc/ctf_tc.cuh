@@ -60,6 +60,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// pure polling (mbarrier.test_wait never suspends the warp): measurement aid
+__device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
 // one arrival (release at CTA scope: the arriving thread's earlier shared-memory writes
 // are visible to a thread whose wait on the phase succeeded)
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
